@@ -1,0 +1,192 @@
+/*
+ * acct.h -- C ABI of libacct_sm100.so, the B200 (sm_100a) execution library
+ * behind the tuner's `gpu:` evaluator.
+ *
+ * The reference (acctuner) has no native interface: its only boundary on this
+ * path is the Python callable `evaluate(bits) -> Measurement` consumed by
+ * `run_ga` (pkg/src/acctuner/ga.py:170-217) and built by `build_evaluator`
+ * (pkg/src/acctuner/pipeline.py:151-163); the offloaded loops themselves were
+ * compiled by PGI from `#pragma acc kernels` regions.  This
+ * header is what those regions become on B200: one entry point per Darknet
+ * loop kind that a gene can offload, the transfer primitive the data
+ * directives (`#pragma acc data copyin/copyout/copy`, pkg/src/acctuner/
+ * emitter.py:41-49) execute as, the transfer counters whose contract is
+ * `directive_exec_counts` (pkg/src/acctuner/transfer.py:161-165), and a
+ * native runner for a compiled offload pattern.
+ *
+ * Conventions
+ *   - plain C types only; `acct_stream_t` is a `cudaStream_t` (NULL = legacy
+ *     default stream);
+ *   - every int-returning call returns 0 on success or a cudaError_t / ACCT_E*
+ *     code; the message is available from acct_last_error_string();
+ *   - stream-ordered and asynchronous unless stated; the caller owns every
+ *     device and host buffer (the library allocates only its own scratch);
+ *   - 2-D arrays are row-major [rows][cols] with a row pitch `ld` in ELEMENTS
+ *     (device arrays are allocated with ld rounded up to 32 so rows start on
+ *     128-byte boundaries, which TMA needs); 1-D arrays are dense;
+ *   - thread-safe: one host thread per device, each with its own streams.
+ */
+#ifndef ACCT_H
+#define ACCT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *acct_stream_t;
+
+enum {
+  ACCT_OK = 0,
+  ACCT_EINVAL = 1001,       /* bad argument (shape, pointer, enum) */
+  ACCT_ENOTSUP = 1002,      /* shape/mode not supported by this kernel */
+  ACCT_ETIMEOUT = 1003      /* schedule exceeded its wall-clock budget */
+};
+
+/* activation kinds (darknet ACTIVATION) */
+enum { ACCT_ACT_LINEAR = 0, ACCT_ACT_LEAKY = 1 };
+
+/* gemm_nn implementation modes */
+enum {
+  ACCT_GEMM_AUTO = 0,       /* tcgen05 3xTF32 where it applies, else SIMT FP32 */
+  ACCT_GEMM_SIMT = 1,       /* FP32 FMA on CUDA cores (the recompiled-loop baseline) */
+  ACCT_GEMM_TC3XTF32 = 2    /* TMA + tcgen05.mma kind::tf32, hi/lo split, TMEM accumulators */
+};
+
+/* ---------------------------------------------------------------- kernels --
+ * One entry per offloadable Darknet loop.  Each replaces the body of the
+ * corresponding `#pragma acc kernels` loop of the C-subset program
+ * (paper_1811_03882_b200/nets.py emits those loops).                        */
+
+/* fill_cpu: Y[r][c] = value for r < rows, c < cols */
+int acct_fill_f32(float *Y, int64_t rows, int64_t cols, int64_t ldy, float value,
+                  acct_stream_t stream);
+
+/* copy_cpu: Y[r][c] = X[r][c] */
+int acct_copy_f32(const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t rows,
+                  int64_t cols, acct_stream_t stream);
+
+/* im2col_cpu: col[c][h*ow+w] = im[c/(k*k)][(c/k%k + h*s - pad)*width + c%k + w*s - pad]
+ * or 0 outside the image; col has channels*k*k rows and oh*ow columns.      */
+int acct_im2col_f32(const float *im, int64_t ld_im, int channels, int height, int width,
+                    int ksize, int stride, int pad, float *col, int64_t ld_col,
+                    acct_stream_t stream);
+
+/* gemm_nn: C[M][N] = beta*C + alpha * A[M][K] . B[K][N]  (darknet gemm_nn is
+ * beta = 1 after fill_cpu).  `epilogue` optionally fuses the following
+ * add_bias (bias != NULL) and activation (act) of the same output array.   */
+int acct_gemm_nn_f32(int M, int N, int K, float alpha, const float *A, int64_t lda,
+                     const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
+                     const float *bias, int act, int mode, acct_stream_t stream);
+
+/* add_bias: out[r][c] += bias[r] */
+int acct_add_bias_f32(float *out, int64_t ld, const float *bias, int rows, int64_t cols,
+                      acct_stream_t stream);
+
+/* activate_array: leaky: x = x < 0 ? (float)(0.1 * (double)x) : x; linear: x */
+int acct_activate_f32(float *X, int64_t ld, int64_t rows, int64_t cols, int act,
+                      acct_stream_t stream);
+
+/* forward_maxpool (batch 1): out[c][i*ow+j] = max over the size x size window
+ * at (i*stride - off, j*stride - off), out-of-image = -FLT_MAX, strict '>'
+ * in (n, m) order; idx = c*height*width + row*width + col of the max.      */
+int acct_maxpool_f32(const float *in, int64_t ld_in, int channels, int height, int width,
+                     int size, int stride, int off, int out_h, int out_w, float *out,
+                     int64_t ld_out, int32_t *idx, int64_t ld_idx, acct_stream_t stream);
+
+/* ------------------------------------------------------------- transfers --
+ * Direction: 1 = host->device, 2 = device->host.  Pitched 2-D copy of
+ * `rows` rows of `row_bytes` bytes.  Counts calls and bytes per direction.  */
+int acct_memcpy2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t row_bytes,
+                  size_t rows, int direction, acct_stream_t stream);
+
+typedef struct {
+  int64_t directive_execs;   /* executions of data directives (transfer.py:161-165) */
+  int64_t var_transfers;     /* sum over executions of |vars| (x2 for copy)        */
+  int64_t h2d_calls, d2h_calls;
+  int64_t h2d_bytes, d2h_bytes;
+  int64_t kernel_launches;   /* device kernels launched by this library */
+  int64_t host_ops;          /* CPU-side loop executions (genes set to 0) */
+} acct_counters_t;
+
+/* counters are per calling host thread (one thread drives one device) */
+void acct_counters_get(acct_counters_t *out);
+void acct_counters_reset(void);
+const char *acct_last_error_string(void);
+
+/* ------------------------------------------------------------ host loops --
+ * The CPU side of a genome: the same loops run natively on host buffers when
+ * their gene is 0 (dense row-major, same argument meaning as above).       */
+int acct_host_fill_f32(float *Y, int64_t rows, int64_t cols, int64_t ldy, float value);
+int acct_host_copy_f32(const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t rows,
+                       int64_t cols);
+int acct_host_im2col_f32(const float *im, int64_t ld_im, int channels, int height, int width,
+                         int ksize, int stride, int pad, float *col, int64_t ld_col);
+int acct_host_gemm_nn_f32(int M, int N, int K, float alpha, const float *A, int64_t lda,
+                          const float *B, int64_t ldb, float *C, int64_t ldc);
+int acct_host_add_bias_f32(float *out, int64_t ld, const float *bias, int rows, int64_t cols);
+int acct_host_activate_f32(float *X, int64_t ld, int64_t rows, int64_t cols, int act);
+int acct_host_maxpool_f32(const float *in, int64_t ld_in, int channels, int height, int width,
+                          int size, int stride, int off, int out_h, int out_w, float *out,
+                          int64_t ld_out, int32_t *idx, int64_t ld_idx);
+
+/* --------------------------------------------------------- schedule runner --
+ * A genome's offload pattern compiled to a flat action list
+ * (paper_1811_03882_b200/executor.py builds it from the transfer plan).
+ * Arrays are referenced by slot index into `arrays`.                        */
+enum {
+  ACCT_A_LOOP_BEGIN = 1,   /* i[0]=trip count; host-side counted loop (the image loop) */
+  ACCT_A_LOOP_END = 2,     /* i[0]=index of the matching LOOP_BEGIN */
+  ACCT_A_DIRECTIVE = 3,    /* count one directive execution: i[0]=|vars|, i[1]=is_copy */
+  ACCT_A_H2D = 4,          /* slot a[0]: host -> device (pitched) */
+  ACCT_A_D2H = 5,          /* slot a[0]: device -> host (pitched) */
+  ACCT_A_BIND = 6,         /* slot a[0].host (i[2]=0) or .dev (i[2]=1) = base + loopvar(i[0]) * i[1]
+                              bytes: load_input / per-image output slots */
+  ACCT_A_STORE = 7,        /* memcpy(base + loopvar(i[0]) * i[1], slot a[0].host) (store_output) */
+  ACCT_A_KERNEL = 8,       /* device op: i[0]=op kind, operands a[], ints i[1..] */
+  ACCT_A_HOST = 9,         /* host op: same encoding, runs on host buffers */
+  ACCT_A_SYNC = 10         /* drain the stream (before host ops / end) */
+};
+
+enum {
+  ACCT_K_FILL = 1, ACCT_K_COPY = 2, ACCT_K_IM2COL = 3, ACCT_K_GEMM = 4,
+  ACCT_K_ADD_BIAS = 5, ACCT_K_LEAKY = 6, ACCT_K_LINEAR = 7, ACCT_K_MAXPOOL = 8
+};
+
+typedef struct {
+  void *host;          /* current host buffer (dense, rows x cols x 4 bytes) */
+  void *dev;           /* device buffer (rows x ld x 4 bytes) */
+  int64_t rows, cols;  /* logical 2-D shape (1-D arrays: rows = 1) */
+  int64_t ld_dev;      /* device row pitch in elements */
+} acct_array_t;
+
+typedef struct {
+  int32_t kind;        /* ACCT_A_* */
+  int32_t a[4];        /* array slots */
+  int64_t i[14];       /* integer operands */
+  void *base;          /* BIND/STORE: host base pointer */
+} acct_action_t;
+
+/* Run `n` actions on `stream`.  `host_base_loop` selects which loop counter
+ * BIND/STORE use.  Returns when all work is complete (synchronises the
+ * stream).  `timeout_s` > 0 aborts with ACCT_ETIMEOUT between actions.     */
+int acct_run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *actions,
+                      int n_actions, int gemm_mode, double timeout_s, acct_stream_t stream);
+
+/* Same, recording a CUDA event pair around every KERNEL action on `stream`;
+ * kernel_ms[k] receives the summed device milliseconds of action k over all
+ * its executions (0 for non-kernel actions).  Used by bench.py's roofline. */
+int acct_run_schedule_profiled(acct_array_t *arrays, int n_arrays, const acct_action_t *actions,
+                               int n_actions, int gemm_mode, double timeout_s,
+                               acct_stream_t stream, float *kernel_ms);
+
+/* library/device facts */
+int acct_device_sm_count(int device);
+const char *acct_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ACCT_H */

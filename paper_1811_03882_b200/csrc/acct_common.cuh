@@ -1,0 +1,52 @@
+// Shared plumbing for libacct_sm100.so: error reporting, counters, launch
+// geometry.  See include/acct.h for the ABI contract.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "acct.h"
+
+namespace acct {
+
+// ---- error reporting (per host thread) ----
+void set_error(const std::string &msg);
+int fail(int code, const char *what);
+int check_cuda(cudaError_t err, const char *what);
+
+// ---- process-wide counters (atomics; the library has no other globals) ----
+struct Counters {
+  std::atomic<int64_t> directive_execs{0}, var_transfers{0};
+  std::atomic<int64_t> h2d_calls{0}, d2h_calls{0}, h2d_bytes{0}, d2h_bytes{0};
+  std::atomic<int64_t> kernel_launches{0}, host_ops{0};
+};
+Counters &counters();
+
+inline int note_launch(const char *what) {
+  counters().kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  return check_cuda(cudaGetLastError(), what);
+}
+
+// grid for a grid-stride kernel: enough CTAs to cover `work` items, capped at
+// `per_sm` resident CTAs per SM over the whole chip (multiple of the SM count)
+int sm_count();
+inline unsigned grid_for(int64_t work, int block, int per_sm = 8) {
+  int64_t need = (work + block - 1) / block;
+  int64_t cap = (int64_t)sm_count() * per_sm;
+  if (need > cap) need = cap;
+  if (need < 1) need = 1;
+  return (unsigned)need;
+}
+
+inline cudaStream_t as_stream(acct_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace acct
+
+// leaky as darknet computes it: `.1*x` is a double product rounded to float
+__host__ __device__ __forceinline__ float acct_leaky(float v) {
+  return v < 0.0f ? (float)(0.1 * (double)v) : v;
+}

@@ -1,0 +1,184 @@
+// gemm_nn on CUDA cores (FP32 FMA): the `mode = SIMT` path and the kernels
+// for shapes the tensor-core path does not take (M < 64, or K % 4 / pitch
+// misalignment that TMA cannot describe).
+//
+//   C[M][N] = beta*C + alpha*(A . B)  (+ bias[row]) (leaky)
+//
+// Two kernels:
+//   * tile kernel: 128x128 CTA tile, BK = 8, 256 threads, 8x8 outputs per
+//     thread, register-staged double buffering through shared memory;
+//   * skinny kernel (M <= 32): one thread per output column keeps all M
+//     accumulators in registers and streams B once -- the first conv layer
+//     (M = 16, K = 27, N = 173056) is a pure HBM stream of B and C.
+// Both accumulate each output in k order within a thread (the tile kernel
+// in BK chunks), so results differ from the host i-k-j loop only by FMA
+// contraction; parity is checked to the 1e-4 relative tolerance.
+
+#include "acct_common.cuh"
+
+namespace {
+
+__device__ __forceinline__ float epilogue(float acc, float alpha, float beta, const float *cptr,
+                                          const float *bias, int row, int act) {
+  float v = alpha * acc;
+  if (beta != 0.0f) v = beta * (*cptr) + v;
+  if (bias) v += __ldg(bias + row);
+  if (act == ACCT_ACT_LEAKY) v = acct_leaky(v);
+  return v;
+}
+
+constexpr int BM = 128, BN = 128, BK = 8, TM = 8, TN = 8;
+
+__global__ void __launch_bounds__(256)
+gemm_tile_kernel(int M, int N, int K, float alpha, const float *__restrict__ A, int64_t lda,
+                 const float *__restrict__ B, int64_t ldb, float beta, float *__restrict__ C,
+                 int64_t ldc, const float *__restrict__ bias, int act) {
+  __shared__ float As[2][BK][BM + 4];
+  __shared__ float Bs[2][BK][BN];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+
+  // loaders: A tile 128x8 -> each thread 4 elems (row = tid/2, k = (tid%2)*4 ..+3)
+  const int a_row = tid / 2, a_k = (tid % 2) * 4;
+  // B tile 8x128 -> each thread 4 elems (k = tid/32, col = (tid%32)*4 ..+3)
+  const int b_k = tid / 32, b_col = (tid % 32) * 4;
+
+  float ra[4], rb[4];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int gr = m0 + a_row, gk = k0 + a_k + e;
+      ra[e] = (gr < M && gk < K) ? __ldg(A + (int64_t)gr * lda + gk) : 0.0f;
+      int bk = k0 + b_k, bc = n0 + b_col + e;
+      rb[e] = (bk < K && bc < N) ? __ldg(B + (int64_t)bk * ldb + bc) : 0.0f;
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) As[buf][a_k + e][a_row] = ra[e];
+    *reinterpret_cast<float4 *>(&Bs[buf][b_k][b_col]) = make_float4(rb[0], rb[1], rb[2], rb[3]);
+  };
+
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
+
+  load(0);
+  stash(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    const bool more = k0 + BK < K;
+    if (more) load(k0 + BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[TM], b[TN];
+      float4 a0 = *reinterpret_cast<const float4 *>(&As[buf][kk][ty * 4]);
+      float4 a1 = *reinterpret_cast<const float4 *>(&As[buf][kk][64 + ty * 4]);
+      float4 b0 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][tx * 4]);
+      float4 b1 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][64 + tx * 4]);
+      a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+      a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+      b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    if (more) {
+      stash(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int r = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int c = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+      if (c >= N) continue;
+      float *cp = C + (int64_t)r * ldc + c;
+      *cp = epilogue(acc[i][j], alpha, beta, cp, bias, r, act);
+    }
+  }
+}
+
+// M <= MAXM: A (M x K) staged whole in shared memory (dynamic), one thread per
+// output column.
+template <int MAXM>
+__global__ void __launch_bounds__(128)
+gemm_skinny_kernel(int M, int N, int K, float alpha, const float *__restrict__ A, int64_t lda,
+                   const float *__restrict__ B, int64_t ldb, float beta, float *__restrict__ C,
+                   int64_t ldc, const float *__restrict__ bias, int act) {
+  extern __shared__ float As[];  // [K][MAXM]
+  for (int t = threadIdx.x; t < K * MAXM; t += blockDim.x) {
+    int k = t / MAXM, m = t % MAXM;
+    As[t] = m < M ? A[(int64_t)m * lda + k] : 0.0f;
+  }
+  __syncthreads();
+  for (int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; col < N;
+       col += (int64_t)gridDim.x * blockDim.x) {
+    float acc[MAXM];
+#pragma unroll
+    for (int m = 0; m < MAXM; ++m) acc[m] = 0.0f;
+    const float *bp = B + col;
+    for (int k = 0; k < K; ++k) {
+      const float b = __ldcs(bp + (int64_t)k * ldb);
+      const float4 *ak = reinterpret_cast<const float4 *>(As + k * MAXM);
+#pragma unroll
+      for (int q = 0; q < MAXM / 4; ++q) {
+        float4 a = ak[q];
+        acc[4 * q + 0] = fmaf(a.x, b, acc[4 * q + 0]);
+        acc[4 * q + 1] = fmaf(a.y, b, acc[4 * q + 1]);
+        acc[4 * q + 2] = fmaf(a.z, b, acc[4 * q + 2]);
+        acc[4 * q + 3] = fmaf(a.w, b, acc[4 * q + 3]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MAXM; ++m) {
+      if (m < M) {
+        float *cp = C + (int64_t)m * ldc + col;
+        __stcs(cp, epilogue(acc[m], alpha, beta, cp, bias, m, act));
+      }
+    }
+  }
+}
+
+}  // namespace
+
+namespace acct {
+
+int gemm_simt(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
+              int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
+              cudaStream_t s) {
+  if (M <= 32 && (int64_t)K * 32 * 4 <= 200 * 1024) {
+    const int block = 128;
+    const size_t smem = (size_t)K * 32 * sizeof(float);
+    const int maxm = M <= 16 ? 16 : 32;
+    unsigned grid = grid_for(N, block, 4);
+    if (maxm == 16) {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(gemm_skinny_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      gemm_skinny_kernel<16><<<grid, block, (size_t)K * 16 * sizeof(float), s>>>(
+          M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act);
+    } else {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(gemm_skinny_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      gemm_skinny_kernel<32><<<grid, block, smem, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C,
+                                                       ldc, bias, act);
+    }
+    return note_launch("gemm_skinny");
+  }
+  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
+  gemm_tile_kernel<<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act);
+  return note_launch("gemm_tile");
+}
+
+}  // namespace acct

@@ -1,0 +1,390 @@
+// Runtime half of libacct_sm100.so: errors, counters, counted transfers, the
+// gemm_nn mode dispatcher and the native schedule runner that executes a
+// genome's compiled offload pattern (include/acct.h).
+//
+// The runner is the B200 analogue of running the emitted OpenACC program:
+// `#pragma acc data` lines become counted pitched cudaMemcpy2DAsync calls at
+// exactly the loops they precede (pkg/src/acctuner/emitter.py:41-84),
+// `#pragma acc kernels` loops become kernel launches, every other loop runs
+// natively on the host.  One stream per device; the stream is drained before
+// any host loop touches host buffers, which keeps the OpenACC data-region
+// ordering without extra events.
+
+#include <chrono>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "acct_common.cuh"
+
+namespace acct {
+
+static thread_local std::string g_error;
+
+void set_error(const std::string &msg) { g_error = msg; }
+
+int fail(int code, const char *what) {
+  set_error(std::string(what) + " (code " + std::to_string(code) + ")");
+  return code;
+}
+
+int check_cuda(cudaError_t err, const char *what) {
+  if (err == cudaSuccess) return ACCT_OK;
+  set_error(std::string(what) + ": " + cudaGetErrorName(err) + ": " + cudaGetErrorString(err));
+  return (int)err;
+}
+
+// per host thread: one thread drives one device, so a run's counters are
+// exactly the calling thread's
+Counters &counters() {
+  static thread_local Counters c;
+  return c;
+}
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cached[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cached[dev] = n;
+  }
+  return cached[dev];
+}
+
+int gemm_simt(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
+              int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
+              cudaStream_t s);
+int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
+            int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
+            cudaStream_t s);
+
+}  // namespace acct
+
+using namespace acct;
+
+extern "C" const char *acct_last_error_string(void) { return g_error.c_str(); }
+
+extern "C" void acct_counters_get(acct_counters_t *out) {
+  if (!out) return;
+  Counters &c = counters();
+  out->directive_execs = c.directive_execs.load();
+  out->var_transfers = c.var_transfers.load();
+  out->h2d_calls = c.h2d_calls.load();
+  out->d2h_calls = c.d2h_calls.load();
+  out->h2d_bytes = c.h2d_bytes.load();
+  out->d2h_bytes = c.d2h_bytes.load();
+  out->kernel_launches = c.kernel_launches.load();
+  out->host_ops = c.host_ops.load();
+}
+
+extern "C" void acct_counters_reset(void) {
+  Counters &c = counters();
+  c.directive_execs = 0;
+  c.var_transfers = 0;
+  c.h2d_calls = 0;
+  c.d2h_calls = 0;
+  c.h2d_bytes = 0;
+  c.d2h_bytes = 0;
+  c.kernel_launches = 0;
+  c.host_ops = 0;
+}
+
+extern "C" int acct_device_sm_count(int device) {
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  return n;
+}
+
+extern "C" const char *acct_build_info(void) {
+  return "libacct_sm100: sm_100a (tcgen05/TMA 3xTF32 gemm_nn, vectorized HBM kernels), CUDA "
+#ifdef __CUDACC_VER_MAJOR__
+      "12.x"
+#endif
+      ;
+}
+
+extern "C" int acct_memcpy2d(void *dst, size_t dpitch, const void *src, size_t spitch,
+                             size_t row_bytes, size_t rows, int direction, acct_stream_t stream) {
+  if (direction != 1 && direction != 2) return fail(ACCT_EINVAL, "memcpy2d: direction");
+  if (rows == 0 || row_bytes == 0) return ACCT_OK;
+  cudaMemcpyKind kind = direction == 1 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  cudaError_t err;
+  if (dpitch == row_bytes && spitch == row_bytes)
+    err = cudaMemcpyAsync(dst, src, row_bytes * rows, kind, as_stream(stream));
+  else
+    err = cudaMemcpy2DAsync(dst, dpitch, src, spitch, row_bytes, rows, kind, as_stream(stream));
+  Counters &c = counters();
+  if (direction == 1) {
+    c.h2d_calls.fetch_add(1);
+    c.h2d_bytes.fetch_add((int64_t)(row_bytes * rows));
+  } else {
+    c.d2h_calls.fetch_add(1);
+    c.d2h_bytes.fetch_add((int64_t)(row_bytes * rows));
+  }
+  return check_cuda(err, "memcpy2d");
+}
+
+extern "C" int acct_gemm_nn_f32(int M, int N, int K, float alpha, const float *A, int64_t lda,
+                                const float *B, int64_t ldb, float beta, float *C, int64_t ldc,
+                                const float *bias, int act, int mode, acct_stream_t stream) {
+  if (M < 0 || N < 0 || K < 0 || lda < K || ldb < N || ldc < N)
+    return fail(ACCT_EINVAL, "gemm_nn: bad shape/pitch");
+  if (act != -1 && act != ACCT_ACT_LINEAR && act != ACCT_ACT_LEAKY)
+    return fail(ACCT_EINVAL, "gemm_nn: bad activation");
+  if ((int64_t)M * N == 0) return ACCT_OK;
+  cudaStream_t s = as_stream(stream);
+  if (mode == ACCT_GEMM_TC3XTF32 || mode == ACCT_GEMM_AUTO) {
+    int rc = gemm_tc(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+    if (rc != ACCT_ENOTSUP || mode == ACCT_GEMM_TC3XTF32) return rc;
+  } else if (mode != ACCT_GEMM_SIMT) {
+    return fail(ACCT_EINVAL, "gemm_nn: unknown mode");
+  }
+  return gemm_simt(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+}
+
+// ------------------------------------------------------------ schedule runner
+
+namespace {
+
+struct LoopFrame {
+  int begin;
+  int64_t counter, trip;
+};
+
+inline float bits_to_float(int64_t v) {
+  uint32_t u = (uint32_t)v;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+int device_op(const acct_action_t &a, acct_array_t *arr, int gemm_mode, cudaStream_t s) {
+  const int64_t *I = a.i;
+  auto D = [&](int k) { return reinterpret_cast<float *>(arr[a.a[k]].dev); };
+  auto LD = [&](int k) { return arr[a.a[k]].ld_dev; };
+  acct_stream_t st = reinterpret_cast<acct_stream_t>(s);
+  switch ((int)I[0]) {
+    case ACCT_K_FILL:
+      return acct_fill_f32(D(0), I[1], I[2], LD(0), bits_to_float(I[3]), st);
+    case ACCT_K_COPY:
+      return acct_copy_f32(D(0), LD(0), D(1), LD(1), I[1], I[2], st);
+    case ACCT_K_IM2COL:
+      return acct_im2col_f32(D(0), LD(0), (int)I[1], (int)I[2], (int)I[3], (int)I[4], (int)I[5],
+                             (int)I[6], D(1), LD(1), st);
+    case ACCT_K_GEMM: {
+      const float *bias = a.a[3] >= 0 ? D(3) : nullptr;
+      return acct_gemm_nn_f32((int)I[1], (int)I[2], (int)I[3], 1.0f, D(0), LD(0), D(1), LD(1),
+                              I[4] ? 1.0f : 0.0f, D(2), LD(2), bias, (int)I[5], gemm_mode, st);
+    }
+    case ACCT_K_ADD_BIAS:
+      return acct_add_bias_f32(D(0), LD(0), D(1), (int)I[1], I[2], st);
+    case ACCT_K_LEAKY:
+      return acct_activate_f32(D(0), LD(0), I[1], I[2], ACCT_ACT_LEAKY, st);
+    case ACCT_K_LINEAR:
+      return acct_activate_f32(D(0), LD(0), I[1], I[2], ACCT_ACT_LINEAR, st);
+    case ACCT_K_MAXPOOL:
+      return acct_maxpool_f32(D(0), LD(0), (int)I[1], (int)I[2], (int)I[3], (int)I[4], (int)I[5],
+                              (int)I[6], (int)I[7], (int)I[8], D(1), LD(1),
+                              reinterpret_cast<int32_t *>(arr[a.a[2]].dev), LD(2), st);
+  }
+  return fail(ACCT_EINVAL, "schedule: unknown device op");
+}
+
+int host_op(const acct_action_t &a, acct_array_t *arr) {
+  const int64_t *I = a.i;
+  auto H = [&](int k) { return reinterpret_cast<float *>(arr[a.a[k]].host); };
+  auto LD = [&](int k) { return arr[a.a[k]].cols; };
+  int rc = ACCT_EINVAL;
+  switch ((int)I[0]) {
+    case ACCT_K_FILL: rc = acct_host_fill_f32(H(0), I[1], I[2], LD(0), bits_to_float(I[3])); break;
+    case ACCT_K_COPY: rc = acct_host_copy_f32(H(0), LD(0), H(1), LD(1), I[1], I[2]); break;
+    case ACCT_K_IM2COL:
+      rc = acct_host_im2col_f32(H(0), LD(0), (int)I[1], (int)I[2], (int)I[3], (int)I[4], (int)I[5],
+                                (int)I[6], H(1), LD(1));
+      break;
+    case ACCT_K_GEMM:
+      rc = acct_host_gemm_nn_f32((int)I[1], (int)I[2], (int)I[3], 1.0f, H(0), LD(0), H(1), LD(1),
+                                 H(2), LD(2));
+      break;
+    case ACCT_K_ADD_BIAS: rc = acct_host_add_bias_f32(H(0), LD(0), H(1), (int)I[1], I[2]); break;
+    case ACCT_K_LEAKY: rc = acct_host_activate_f32(H(0), LD(0), I[1], I[2], ACCT_ACT_LEAKY); break;
+    case ACCT_K_LINEAR: rc = acct_host_activate_f32(H(0), LD(0), I[1], I[2], ACCT_ACT_LINEAR); break;
+    case ACCT_K_MAXPOOL:
+      rc = acct_host_maxpool_f32(H(0), LD(0), (int)I[1], (int)I[2], (int)I[3], (int)I[4], (int)I[5],
+                                 (int)I[6], (int)I[7], (int)I[8], H(1), LD(1),
+                                 reinterpret_cast<int32_t *>(arr[a.a[2]].host), LD(2));
+      break;
+  }
+  if (rc != ACCT_OK) return fail(rc, "schedule: host op failed");
+  counters().host_ops.fetch_add(1);
+  return ACCT_OK;
+}
+
+}  // namespace
+
+namespace {
+
+// Optional per-action device timing: an event pair around every KERNEL
+// action execution, resolved after the final drain.
+struct Profiler {
+  float *out_ms = nullptr;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<int, size_t>> marks;  // (action index, first event of the pair)
+  size_t used = 0;
+  cudaEvent_t next() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  ~Profiler() {
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  }
+};
+
+int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *actions, int n_actions,
+                 int gemm_mode, double timeout_s, acct_stream_t stream, Profiler *prof);
+
+}  // namespace
+
+extern "C" int acct_run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *actions,
+                                 int n_actions, int gemm_mode, double timeout_s,
+                                 acct_stream_t stream) {
+  return run_schedule(arrays, n_arrays, actions, n_actions, gemm_mode, timeout_s, stream, nullptr);
+}
+
+extern "C" int acct_run_schedule_profiled(acct_array_t *arrays, int n_arrays,
+                                          const acct_action_t *actions, int n_actions,
+                                          int gemm_mode, double timeout_s, acct_stream_t stream,
+                                          float *kernel_ms) {
+  if (!kernel_ms) return fail(ACCT_EINVAL, "profiled schedule: null output");
+  for (int k = 0; k < n_actions; ++k) kernel_ms[k] = 0.0f;
+  Profiler prof;
+  prof.out_ms = kernel_ms;
+  int rc = run_schedule(arrays, n_arrays, actions, n_actions, gemm_mode, timeout_s, stream, &prof);
+  if (rc != ACCT_OK) return rc;
+  for (auto &m : prof.marks) {
+    float ms = 0.0f;
+    rc = check_cuda(cudaEventElapsedTime(&ms, prof.pool[m.second], prof.pool[m.second + 1]),
+                    "profiled schedule: elapsed");
+    if (rc) return rc;
+    kernel_ms[m.first] += ms;
+  }
+  return ACCT_OK;
+}
+
+namespace {
+
+int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *actions, int n_actions,
+                 int gemm_mode, double timeout_s, acct_stream_t stream, Profiler *prof) {
+  cudaStream_t s = as_stream(stream);
+  std::vector<LoopFrame> loops;
+  bool pending = false;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto drain = [&]() -> int {
+    if (!pending) return ACCT_OK;
+    pending = false;
+    return check_cuda(cudaStreamSynchronize(s), "schedule: stream sync");
+  };
+  auto check_slot = [&](int k) { return k >= 0 && k < n_arrays; };
+  Counters &cnt = counters();
+  int pc = 0;
+  while (pc < n_actions) {
+    const acct_action_t &a = actions[pc];
+    int rc = ACCT_OK;
+    switch (a.kind) {
+      case ACCT_A_LOOP_BEGIN:
+        if (a.i[0] <= 0) {
+          pc = (int)a.i[1] + 1;  // skip to after LOOP_END
+          continue;
+        }
+        loops.push_back({pc, 0, a.i[0]});
+        break;
+      case ACCT_A_LOOP_END: {
+        if (loops.empty()) return fail(ACCT_EINVAL, "schedule: unbalanced loop");
+        LoopFrame &f = loops.back();
+        if (++f.counter < f.trip) {
+          pc = f.begin + 1;
+          if (timeout_s > 0) {
+            double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if (el > timeout_s) {
+              cudaStreamSynchronize(s);
+              return fail(ACCT_ETIMEOUT, "schedule: timeout");
+            }
+          }
+          continue;
+        }
+        loops.pop_back();
+        break;
+      }
+      case ACCT_A_DIRECTIVE:
+        cnt.directive_execs.fetch_add(1, std::memory_order_relaxed);
+        cnt.var_transfers.fetch_add(a.i[0] * (a.i[1] ? 2 : 1), std::memory_order_relaxed);
+        break;
+      case ACCT_A_H2D:
+      case ACCT_A_D2H: {
+        if (!check_slot(a.a[0])) return fail(ACCT_EINVAL, "schedule: bad slot");
+        acct_array_t &x = arrays[a.a[0]];
+        size_t row = (size_t)x.cols * 4, dp = (size_t)x.ld_dev * 4;
+        if (a.kind == ACCT_A_H2D)
+          rc = acct_memcpy2d(x.dev, dp, x.host, row, row, (size_t)x.rows, 1, stream);
+        else
+          rc = acct_memcpy2d(x.host, row, x.dev, dp, row, (size_t)x.rows, 2, stream);
+        pending = true;
+        break;
+      }
+      case ACCT_A_BIND: {
+        if (!check_slot(a.a[0]) || a.i[0] >= (int64_t)loops.size()) return fail(ACCT_EINVAL, "schedule: bad bind");
+        int64_t lv = loops[(size_t)a.i[0]].counter;
+        void *p = static_cast<char *>(a.base) + lv * a.i[1];
+        if (a.i[2]) arrays[a.a[0]].dev = p;
+        else arrays[a.a[0]].host = p;
+        break;
+      }
+      case ACCT_A_STORE: {
+        if (!check_slot(a.a[0]) || a.i[0] >= (int64_t)loops.size()) return fail(ACCT_EINVAL, "schedule: bad store");
+        rc = drain();
+        if (rc) return rc;
+        int64_t lv = loops[(size_t)a.i[0]].counter;
+        char *dst = static_cast<char *>(a.base) + lv * a.i[1];
+        if (dst != arrays[a.a[0]].host) memcpy(dst, arrays[a.a[0]].host, (size_t)a.i[2]);
+        break;
+      }
+      case ACCT_A_KERNEL:
+        if (prof) {
+          size_t first = prof->used;
+          cudaEvent_t e0 = prof->next(), e1 = prof->next();
+          cudaEventRecord(e0, s);
+          rc = device_op(a, arrays, gemm_mode, s);
+          cudaEventRecord(e1, s);
+          prof->marks.emplace_back(pc, first);
+        } else {
+          rc = device_op(a, arrays, gemm_mode, s);
+        }
+        pending = true;
+        break;
+      case ACCT_A_HOST:
+        rc = drain();
+        if (rc) return rc;
+        rc = host_op(a, arrays);
+        break;
+      case ACCT_A_SYNC:
+        rc = drain();
+        break;
+      /* LOOP_END timeout check above; H2D/D2H/KERNEL set `pending` */
+      default:
+        return fail(ACCT_EINVAL, "schedule: unknown action");
+    }
+    if (rc != ACCT_OK) return rc;
+    ++pc;
+  }
+  return drain();  // host-only schedules never touch the CUDA runtime
+}
+
+}  // namespace

@@ -1,0 +1,487 @@
+"""Execute a genome's offload pattern on one B200.
+
+`PatternExecutor(net)` owns, for one device, a pinned host buffer and a
+device buffer for every array of the net's C-subset program, the seeded
+weights, a pinned batch of input images and a pinned batch of output slots.
+`compile(bits)` turns the genome plus its transfer plan into the flat action
+list of `acct_run_schedule` (include/acct.h); `run(...)` executes it
+natively and returns wall-clock seconds and the transfer/launch counters.
+
+Semantics follow the emitted OpenACC program (reference emitter
+`pkg/src/acctuner/emitter.py:41-84`, planner `transfer.py:82-158`):
+
+* the image loop `for (b ...)` runs on the host; `load_input(x)` binds the
+  host copy of `x` to image b of the pinned input batch, `store_output(y)`
+  makes the host copy of `y` image b's output slot;
+* every `#pragma acc data` directive executes once per arrival at its
+  target loop (the count contract of `directive_exec_counts`): its
+  copyin/copy variables go host->device before the loop, its copyout/copy
+  variables device->host after it.  Several directives moving the same
+  variable in the same direction at the same point issue one memcpy (the
+  emitter merges them into one line too) but each directive is counted;
+* a loop whose gene is 1 is one kernel launch on device buffers; a loop
+  whose gene is 0 runs natively (acct_host_*) on host buffers, after the
+  stream is drained.
+
+B200-specific choices, none of which changes observable results:
+
+* device arrays are pitched (row pitch rounded up to 32 floats = 128 B) so
+  every row is TMA- and float4-aligned; transfers are pitched 2-D copies;
+* with `fuse=True`, a run of consecutive offloaded ops on one conv output
+  -- fill, gemm_nn, add_bias, activation -- becomes ONE gemm launch with
+  beta=0 and a bias/leaky epilogue, provided no transfer of that output
+  sits between them (the intermediate states are then unobservable); the
+  arithmetic is the same float ops in the same order as the separate
+  kernels, so outputs are bit-identical to `fuse=False`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import struct
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import kernels as K
+from .errors import DeviceError, InvalidGenome
+from .legality import build_genome_map, check_all_parallelizable, profile_from_dict
+from .loopnest import build_loop_tree, extract_accesses
+from .nets import NetProgram, input_images, weight_data
+from .planner import (COPY, COPYIN, COPYOUT, TransferPlan, directive_exec_counts,
+                      plan_transfers, selected_loops)
+from .syntax import parse
+
+PITCH_ALIGN = 32  # elements (128 bytes)
+
+
+def _pitch(cols: int) -> int:
+    return -(-cols // PITCH_ALIGN) * PITCH_ALIGN
+
+
+def _f32_bits(v: float) -> int:
+    return struct.unpack("<I", struct.pack("<f", v))[0]
+
+
+@dataclass
+class Schedule:
+    genome: str
+    actions: object                       # ctypes Action array
+    n_actions: int
+    plan: TransferPlan
+    expected: dict                        # counters the run must reproduce
+    fused_groups: list = field(default_factory=list)
+    device_ops: int = 0
+    host_ops: int = 0
+
+
+@dataclass
+class RunResult:
+    seconds: float
+    counters: dict
+    status: str = "measured"
+    kernel_ms: list | None = None
+
+
+class PatternExecutor:
+    def __init__(self, net: NetProgram, device=0, seed: int = 1, fuse: bool = True,
+                 gemm_mode: int = K.GEMM_AUTO):
+        import torch
+        self.torch = torch
+        K.lib()  # fail loudly without the kernel library
+        # device=None: host-only executor (every gene 0) -- the CPU half of
+        # the runner, usable without a GPU
+        self.host_only = device is None
+        if not self.host_only and not torch.cuda.is_available():
+            raise DeviceError("PatternExecutor needs a CUDA device (sm_100a)")
+        self.net = net
+        self.fuse = fuse
+        self.gemm_mode = gemm_mode
+        if self.host_only:
+            self.device = None
+        else:
+            self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        self.program = parse(net.source)
+        self.tree = build_loop_tree(self.program)
+        self.accesses = extract_accesses(self.program)
+        self.genome_map = build_genome_map(check_all_parallelizable(self.tree, self.accesses))
+        self.profile = profile_from_dict(net.profile_dict(), net.spec.name, self.tree)
+        if list(self.genome_map.loop_ids) != [op.loop_id for op in net.ops]:
+            raise DeviceError("net program genes do not line up with its op manifest")
+        self.images = net.spec.images
+
+        pin = not self.host_only
+        if pin:
+            with torch.cuda.device(self.device):
+                self.stream = torch.cuda.Stream(self.device)
+        else:
+            self.stream = None
+        self.slot_of: dict[str, int] = {}
+        self.dev: dict[str, object] = {}
+        self.host: dict[str, object] = {}
+        slots = (K.ArraySlot * len(net.arrays))()
+        for k, spec in enumerate(net.arrays.values()):
+            rows, cols = (spec.shape if len(spec.shape) == 2 else (1, spec.shape[0]))
+            ld = _pitch(cols)
+            dt = torch.float32 if spec.dtype == "float" else torch.int32
+            d = None if self.host_only else torch.zeros(rows * ld, dtype=dt, device=self.device)
+            h = torch.zeros(rows * cols, dtype=dt, pin_memory=pin)
+            self.dev[spec.name], self.host[spec.name] = d, h
+            self.slot_of[spec.name] = k
+            slots[k].host = h.data_ptr()
+            slots[k].dev = None if d is None else d.data_ptr()
+            slots[k].rows, slots[k].cols, slots[k].ld_dev = rows, cols, ld
+        self.slots = slots
+        self._pristine = [(slots[k].host, slots[k].dev) for k in range(len(net.arrays))]
+        for spec in net.arrays.values():
+            if spec.role in ("weight", "bias"):
+                self.host[spec.name].copy_(torch.from_numpy(weight_data(net, spec.name, seed).ravel()))
+        xs = net.arrays[net.input_name]
+        self.input_batch = torch.from_numpy(
+            input_images(net, seed, 0, self.images).reshape(self.images, -1))
+        if pin:
+            self.input_batch = self.input_batch.pin_memory()
+        ys = net.arrays[net.output_name]
+        self.output_batch = torch.zeros((self.images, ys.numel), dtype=torch.float32,
+                                        pin_memory=pin)
+        self.image_bytes = xs.numel * 4
+        self.output_bytes = ys.numel * 4
+        self._cache: dict[str, Schedule] = {}
+
+    # ------------------------------------------------------------ compile
+    def compile(self, genome_bits: str, resident: bool = False) -> Schedule:
+        key = ("R" if resident else "E") + genome_bits
+        if key in self._cache:
+            return self._cache[key]
+        plan = plan_transfers(self.program, self.tree, self.accesses, genome_bits, self.genome_map)
+        chosen = selected_loops(genome_bits, self.genome_map)
+        if resident:
+            sched = self._compile_resident(genome_bits, plan, chosen)
+        else:
+            sched = self._compile_full(genome_bits, plan, chosen)
+        self._cache[key] = sched
+        return sched
+
+    def _compile_full(self, bits: str, plan: TransferPlan, chosen: set) -> Schedule:
+        net = self.net
+        acts: list[tuple] = []
+        at_target: dict[int, list] = {}
+        for d in plan.directives:
+            at_target.setdefault(d.target_loop, []).append(d)
+
+        def moves(target: int, clauses) -> list[str]:
+            names = set()
+            for d in at_target.get(target, ()):
+                if d.clause in clauses:
+                    names.update(v for v in d.vars if v in self.slot_of)
+            return sorted(names)
+
+        def entry(target: int):
+            for d in at_target.get(target, ()):
+                acts.append((K.A_DIRECTIVE, (), (len(d.vars), int(d.clause == COPY))))
+            for v in moves(target, (COPYIN, COPY)):
+                acts.append((K.A_H2D, (self.slot_of[v],), ()))
+
+        def leave(target: int):
+            for v in moves(target, (COPYOUT, COPY)):
+                acts.append((K.A_D2H, (self.slot_of[v],), ()))
+
+        img = net.image_loop
+        entry(img)
+        begin = len(acts)
+        acts.append([K.A_LOOP_BEGIN, (), (self.images, -1)])
+        x_slot, y_slot = self.slot_of[net.input_name], self.slot_of[net.output_name]
+        acts.append((K.A_BIND, (x_slot,), (0, self.image_bytes, 0), "in"))
+        # store_output(y) targets y's slot; binding y to it up front is exact
+        # because every iteration overwrites y completely before reading it
+        acts.append((K.A_BIND, (y_slot,), (0, self.output_bytes, 0), "out"))
+
+        plan_f = self._fusion_plan(plan, chosen) if self.fuse else {}
+        device_ops = host_ops = 0
+        for n, op in enumerate(net.ops):
+            role = plan_f.get(n)
+            if role is None:
+                entry(op.loop_id)
+                on_gpu = op.loop_id in chosen
+                acts.append(self._op_action(op, K.A_KERNEL if on_gpu else K.A_HOST))
+                if on_gpu:
+                    device_ops += op.kind != "linear"
+                else:
+                    host_ops += 1
+                leave(op.loop_id)
+            elif role[0] == "absorbed_before":      # fill: subsumed by beta = 0
+                entry(op.loop_id)
+                leave(op.loop_id)
+            elif role[0] == "anchor":               # gemm (+ later bias/act)
+                members = role[1]
+                for m in members:
+                    entry(net.ops[m].loop_id)
+                acts.append(self._fused_gemm_action([net.ops[m] for m in role[2]]))
+                for m in members:
+                    leave(net.ops[m].loop_id)
+                device_ops += 1
+            # role "absorbed_after": handled by its anchor
+        acts.append((K.A_STORE, (y_slot,), (0, self.output_bytes, self.output_bytes), "out"))
+        acts.append((K.A_LOOP_END, (), (begin,)))
+        end = len(acts) - 1
+        acts[begin] = (K.A_LOOP_BEGIN, (), (self.images, end))
+        leave(img)
+        acts.append((K.A_SYNC, (), ()))
+        expected = self._expected_counters(plan, acts)
+        sched = self._pack(bits, acts, plan, expected)
+        sched.fused_groups = sorted((n, r[2]) for n, r in plan_f.items() if r[0] == "anchor")
+        sched.device_ops, sched.host_ops = device_ops * self.images, host_ops * self.images
+        return sched
+
+    def _compile_resident(self, bits: str, plan: TransferPlan, chosen: set) -> Schedule:
+        """Kernels only, inputs already in HBM (one device batch of images):
+        the `value` leg of the benchmark.  Requires every op on the GPU."""
+        if len(chosen) != len(self.net.ops):
+            raise InvalidGenome("resident schedules need the all-offload genome")
+        if not hasattr(self, "device_batch"):
+            xs = self.net.arrays[self.net.input_name]
+            rows, cols = xs.shape
+            ld = _pitch(cols)
+            db = self.torch.zeros((self.images, rows, ld), dtype=self.torch.float32,
+                                  device=self.device)
+            db[:, :, :cols].copy_(self.input_batch.view(self.images, rows, cols))
+            self.device_batch = db
+        acts: list[tuple] = []
+        acts.append([K.A_LOOP_BEGIN, (), (self.images, -1)])
+        x_slot = self.slot_of[self.net.input_name]
+        rows, cols = self.net.arrays[self.net.input_name].shape
+        acts.append((K.A_BIND, (x_slot,), (0, rows * _pitch(cols) * 4, 1), "devin"))
+        plan_f = self._fusion_plan(plan, chosen) if self.fuse else {}
+        for n, op in enumerate(self.net.ops):
+            role = plan_f.get(n)
+            if role is None:
+                acts.append(self._op_action(op, K.A_KERNEL))
+            elif role[0] == "anchor":
+                acts.append(self._fused_gemm_action([self.net.ops[m] for m in role[2]]))
+        acts.append((K.A_LOOP_END, (), (0,)))
+        acts[0] = (K.A_LOOP_BEGIN, (), (self.images, len(acts) - 1))
+        acts.append((K.A_SYNC, (), ()))
+        return self._pack(bits, acts, plan, {})
+
+    def _fusion_plan(self, plan: TransferPlan, chosen: set) -> dict:
+        """Per conv layer, fuse offloaded fill -> gemm -> add_bias -> activation
+        of one output array into a single gemm launch.
+
+        Returns {op index: role}: ("absorbed_before",) for a fused fill,
+        ("anchor", [ops whose directives execute around the launch],
+        [fused op indices]) for the gemm, ("absorbed_after",) for a fused
+        bias/activation.  A member joins only if it is offloaded and no
+        directive moves the output array at any loop boundary strictly
+        inside the fused span (so its intermediate values are unobservable);
+        ops in between that do not touch the output (im2col) run unchanged.
+        """
+        moved: dict[int, set] = {}
+        for d in plan.directives:
+            moved.setdefault(d.target_loop, set()).update(d.vars)
+        ops = self.net.ops
+        on = [op.loop_id in chosen for op in ops]
+        roles: dict[int, tuple] = {}
+        for g, op in enumerate(ops):
+            if op.kind != "gemm" or not on[g]:
+                continue
+            out = op.arrays["C"]
+            touches = lambda i: out in ops[i].arrays.values()  # noqa: E731
+            blocked = lambda i: out in moved.get(ops[i].loop_id, set())  # noqa: E731
+            # backwards: the layer's fill, across ops that never touch `out`
+            fill = None
+            i = g - 1
+            while i >= 0 and not touches(i):
+                i -= 1
+            if i >= 0 and ops[i].kind == "fill" and ops[i].arrays["Y"] == out and on[i] \
+                    and not any(blocked(j) for j in range(i, g + 1)):
+                fill = i
+            after = []
+            j = g + 1
+            for kind in ("add_bias", "act"):
+                if j < len(ops) and on[j] and ops[j].arrays.get("Y") == out and \
+                        (ops[j].kind == kind or (kind == "act" and ops[j].kind in ("leaky", "linear"))):
+                    if blocked(j - 1) or blocked(j):
+                        break
+                    # the previous member's exit must not move `out` either
+                    after.append(j)
+                    j += 1
+                else:
+                    break
+            if after and blocked(g):
+                after = []
+            fused = ([fill] if fill is not None else []) + [g] + after
+            if len(fused) < 2:
+                continue
+            if fill is not None:
+                roles[fill] = ("absorbed_before",)
+            roles[g] = ("anchor", [g] + after, fused)
+            for j in after:
+                roles[j] = ("absorbed_after",)
+        return roles
+
+    def _fused_gemm_action(self, members):
+        kinds = [m.kind for m in members]
+        g = next(m for m in members if m.kind == "gemm")
+        p, a = g.params, g.arrays
+        bias_slot = -1
+        act = K.ACT_NONE
+        for m in members:
+            if m.kind == "add_bias":
+                bias_slot = self.slot_of[m.arrays["bias"]]
+            elif m.kind == "leaky":
+                act = K.ACT_LEAKY
+            elif m.kind == "linear":
+                act = K.ACT_LINEAR
+        beta_one = 0 if "fill" in kinds else 1
+        return (K.A_KERNEL, (self.slot_of[a["A"]], self.slot_of[a["B"]], self.slot_of[a["C"]],
+                             bias_slot),
+                (K.K_GEMM, p["M"], p["N"], p["K"], beta_one, act))
+
+    def _op_action(self, op, where: int):
+        s, p, a = self.slot_of, op.params, op.arrays
+        kind = op.kind
+        if kind == "fill":
+            return (where, (s[a["Y"]],), (K.K_FILL, p["M"], p["N"], _f32_bits(0.0)))
+        if kind == "copy":
+            return (where, (s[a["X"]], s[a["Y"]]), (K.K_COPY, p["M"], p["N"]))
+        if kind == "im2col":
+            return (where, (s[a["X"]], s[a["Y"]]),
+                    (K.K_IM2COL, p["c"], p["h"], p["w"], p["ksize"], p["stride"], p["pad"]))
+        if kind == "gemm":
+            return (where, (s[a["A"]], s[a["B"]], s[a["C"]], -1),
+                    (K.K_GEMM, p["M"], p["N"], p["K"], 1, K.ACT_NONE))
+        if kind == "add_bias":
+            return (where, (s[a["Y"]], s[a["bias"]]), (K.K_ADD_BIAS, p["M"], p["N"]))
+        if kind in ("leaky", "linear"):
+            return (where, (s[a["Y"]],),
+                    (K.K_LEAKY if kind == "leaky" else K.K_LINEAR, p["M"], p["N"]))
+        if kind == "maxpool":
+            return (where, (s[a["X"]], s[a["Y"]], s[a["I"]]),
+                    (K.K_MAXPOOL, p["c"], p["h"], p["w"], p["size"], p["stride"], p["off"],
+                     p["oh"], p["ow"]))
+        raise KeyError(kind)
+
+    def _expected_counters(self, plan: TransferPlan, acts) -> dict:
+        counts = directive_exec_counts(plan, self.tree, self.profile)
+        execs = sum(counts.values())
+        var_xfers = sum(n * len(d.vars) * (2 if d.clause == COPY else 1) for d, n in counts.items())
+        # memcpy calls: actions inside the image loop run `images` times
+        inside = False
+        h2d = d2h = h2d_b = d2h_b = 0
+        for act in acts:
+            kind = act[0]
+            if kind == K.A_LOOP_BEGIN:
+                inside = True
+            elif kind == K.A_LOOP_END:
+                inside = False
+            elif kind in (K.A_H2D, K.A_D2H):
+                spec = list(self.net.arrays.values())[act[1][0]]
+                reps = self.images if inside else 1
+                if kind == K.A_H2D:
+                    h2d += reps
+                    h2d_b += reps * spec.nbytes
+                else:
+                    d2h += reps
+                    d2h_b += reps * spec.nbytes
+        return {"directive_execs": execs, "var_transfers": var_xfers, "h2d_calls": h2d,
+                "d2h_calls": d2h, "h2d_bytes": h2d_b, "d2h_bytes": d2h_b}
+
+    def _pack(self, bits, acts, plan, expected) -> Schedule:
+        arr = (K.Action * len(acts))()
+        for n, act in enumerate(acts):
+            kind, slots, ints = act[0], act[1], act[2]
+            arr[n].kind = kind
+            for j in range(4):
+                arr[n].a[j] = slots[j] if j < len(slots) else -1
+            for j, v in enumerate(ints):
+                arr[n].i[j] = int(v)
+            if len(act) > 3:
+                arr[n].base = {"in": self.input_batch.data_ptr(),
+                               "out": self.output_batch.data_ptr(),
+                               "devin": getattr(self, "device_batch", None).data_ptr()
+                               if act[3] == "devin" else 0}[act[3]]
+        return Schedule(bits, arr, len(acts), plan, expected)
+
+    # ------------------------------------------------------------ run
+    def _restore_slots(self):
+        for k, (h, d) in enumerate(self._pristine):
+            self.slots[k].host, self.slots[k].dev = h, d
+
+    def run(self, schedule: Schedule | str, timeout_s: float = 0.0, resident: bool = False,
+            profile: bool = False) -> RunResult:
+        """Execute a compiled pattern.  With `profile=True` the result's
+        `kernel_ms` holds the summed device milliseconds of every kernel
+        action (CUDA events on the launch stream)."""
+        if isinstance(schedule, str):
+            schedule = self.compile(schedule, resident=resident)
+        if self.host_only and "1" in schedule.genome:
+            raise DeviceError("host-only executor can only run the all-zero genome")
+        lib = K.lib()
+        self._restore_slots()
+        K.reset_counters()
+        kernel_ms = (C.c_float * schedule.n_actions)() if profile else None
+
+        def go(stream):
+            t0 = time.perf_counter()
+            if profile:
+                rc = lib.acct_run_schedule_profiled(
+                    self.slots, len(self.net.arrays), schedule.actions, schedule.n_actions,
+                    self.gemm_mode, float(timeout_s), C.c_void_p(stream), kernel_ms)
+            else:
+                rc = lib.acct_run_schedule(self.slots, len(self.net.arrays), schedule.actions,
+                                           schedule.n_actions, self.gemm_mode, float(timeout_s),
+                                           C.c_void_p(stream))
+            return rc, time.perf_counter() - t0
+
+        if self.host_only:
+            rc, seconds = go(0)
+        else:
+            with self.torch.cuda.device(self.device):
+                rc, seconds = go(self.stream.cuda_stream)
+        self._restore_slots()
+        if rc == K.ETIMEOUT:
+            return RunResult(seconds, K.counters(), "timeout")
+        K.check(rc, f"acct_run_schedule({schedule.genome})")
+        res = RunResult(seconds, K.counters())
+        if profile:
+            res.kernel_ms = list(kernel_ms)
+        return res
+
+    def action_op(self, schedule: Schedule, k: int) -> dict:
+        """Describe KERNEL action k: op kind, shape ints and the algorithmic
+        bytes / flops one execution of it performs."""
+        a = schedule.actions[k]
+        kind = int(a.i[0])
+        ops = [op for op in self.net.ops]
+        name = {v: n for n, v in K.OP_KIND.items()}[kind]
+        i = [int(a.i[j]) for j in range(14)]
+        slots = list(self.net.arrays.values())
+        if kind == K.K_GEMM:
+            M, N, Kd = i[1], i[2], i[3]
+            c_bytes = (4 if i[4] else 0) + 4        # read C only when beta = 1
+            bias = 4 * M if a.a[3] >= 0 else 0
+            byts = 4 * (M * Kd + Kd * N) + c_bytes * M * N + bias
+            op = next(o for o in ops if o.kind == "gemm" and o.arrays["C"] == slots[a.a[2]].name)
+            return {"kind": "gemm", "layer": op.layer, "M": M, "N": N, "K": Kd,
+                    "flops": 2 * M * N * Kd, "bytes": byts, "fused": a.a[3] >= 0 or i[4] == 0}
+        target = slots[a.a[0]].name
+        op = next(o for o in ops if o.kind == name and target in o.arrays.values())
+        return {"kind": name, "layer": op.layer, "flops": 0, "bytes": op.algorithmic_bytes(),
+                "fused": False}
+
+    def outputs(self) -> np.ndarray:
+        """(images, C, H*W) copy of the output slots after a run."""
+        spec = self.net.arrays[self.net.output_name]
+        return self.output_batch.numpy().reshape((self.images,) + spec.shape).copy()
+
+    def device_array(self, name: str) -> np.ndarray:
+        """Logical (unpitched) contents of a device array."""
+        spec = self.net.arrays[name]
+        rows, cols = spec.shape if len(spec.shape) == 2 else (1, spec.shape[0])
+        d = self.dev[name].view(rows, _pitch(cols))[:, :cols]
+        return d.cpu().numpy().reshape(spec.shape)
+
+    def host_array(self, name: str) -> np.ndarray:
+        spec = self.net.arrays[name]
+        return self.host[name].numpy().reshape(spec.shape).copy()

@@ -1,0 +1,163 @@
+"""The `gpu:<config.json>` evaluator: measure a genome by running its offload
+pattern on B200.
+
+Boundary contract (reference `pkg/src/acctuner/ga.py:170-217`,
+`pipeline.py:151-163`, `evaluation.py:162-196`):
+
+* `evaluate(bits) -> Measurement`, called only for valid uncached genomes,
+  possibly concurrently from the GA's thread pool (`workers > 1`);
+* status `measured` with wall-clock seconds > 0 of the program run; a run
+  over `timeout_seconds` -> `Measurement(penalty, "timeout")`;
+* infrastructure failures (CUDA errors, missing library) raise
+  `DeviceError` -- never a penalty, as `SpawnError` in the reference.
+
+Config file (all keys optional except `net`):
+
+    {"net": "yolov2-tiny", "images": 16, "devices": [0, 1] | "all",
+     "seed": 1, "warmup": 1, "repeats": 3, "fuse": true,
+     "gemm": "auto" | "simt" | "tc", "timeout_seconds": 180,
+     "penalty_seconds": 1000}
+
+The program handed to `build_evaluator` must be the configured net's
+source (write it with `python -m paper_1811_03882_b200.nets <net> <dir>`).
+
+Multi-GPU: one `PatternExecutor` per device and a queue of idle devices; a
+GA with `workers = len(devices)` measures one individual per GPU at a time.
+Fitness values are gathered by the GA's order-preserving `pool.map`, so the
+search stays deterministic given the measurements.  No collective is needed
+(nothing crosses between GPUs).
+"""
+
+from __future__ import annotations
+
+import json
+import queue
+import statistics
+import threading
+from dataclasses import dataclass, field
+from pathlib import Path
+
+from . import kernels as K
+from .errors import ModelError
+from .measure import MEASURED, TIMEOUT, Measurement
+from .nets import NETS, build_net
+
+_GEMM_MODES = {"auto": K.GEMM_AUTO, "simt": K.GEMM_SIMT, "tc": K.GEMM_TC3XTF32}
+
+
+@dataclass
+class GpuEvaluatorConfig:
+    net: str = "yolov2-tiny"
+    images: int | None = None
+    devices: object = field(default_factory=lambda: [0])
+    seed: int = 1
+    warmup: int = 1
+    repeats: int = 3
+    fuse: bool = True
+    gemm: str = "auto"
+    timeout_seconds: float = 180.0
+    penalty_seconds: float = 1000.0
+
+    def __post_init__(self):
+        if self.net not in NETS:
+            raise ModelError(f"gpu evaluator: unknown net {self.net!r} (known: {sorted(NETS)})")
+        if self.gemm not in _GEMM_MODES:
+            raise ModelError(f"gpu evaluator: gemm must be one of {sorted(_GEMM_MODES)}")
+        if self.repeats < 1 or self.warmup < 0:
+            raise ModelError("gpu evaluator: repeats >= 1 and warmup >= 0 required")
+
+
+def load_gpu_config(path) -> GpuEvaluatorConfig:
+    try:
+        doc = json.loads(Path(path).read_text())
+    except (OSError, json.JSONDecodeError) as exc:
+        raise ModelError(f"cannot read gpu evaluator config {path}: {exc}") from exc
+    if not isinstance(doc, dict):
+        raise ModelError(f"gpu evaluator config {path}: expected an object")
+    try:
+        return GpuEvaluatorConfig(**doc)
+    except TypeError as exc:
+        raise ModelError(f"gpu evaluator config {path}: {exc}") from exc
+
+
+def resolve_devices(spec) -> list[int]:
+    import torch
+    n = torch.cuda.device_count()
+    if spec == "all":
+        return list(range(n))
+    ids = [int(d) for d in (spec if isinstance(spec, (list, tuple)) else [spec])]
+    bad = [d for d in ids if d < 0 or d >= n]
+    if bad or not ids:
+        raise ModelError(f"gpu evaluator: devices {ids} not available ({n} visible)")
+    return ids
+
+
+class DevicePool:
+    """One PatternExecutor per device; `measure(bits)` borrows an idle one."""
+
+    def __init__(self, cfg: GpuEvaluatorConfig):
+        from .executor import PatternExecutor
+        self.cfg = cfg
+        self.net = build_net(cfg.net, images=cfg.images)
+        self.devices = resolve_devices(cfg.devices)
+        self.executors = {}
+        for d in self.devices:
+            self.executors[d] = PatternExecutor(self.net, device=d, seed=cfg.seed, fuse=cfg.fuse,
+                                                gemm_mode=_GEMM_MODES[cfg.gemm])
+        self.idle: queue.Queue = queue.Queue()
+        for d in self.devices:
+            self.idle.put(d)
+        self.log_lock = threading.Lock()
+        self.log: list[dict] = []
+
+    def measure(self, bits: str) -> Measurement:
+        dev = self.idle.get()
+        try:
+            ex = self.executors[dev]
+            sched = ex.compile(bits)
+            for _ in range(self.cfg.warmup):
+                r = ex.run(sched, timeout_s=self.cfg.timeout_seconds)
+                if r.status == TIMEOUT:
+                    return self._record(bits, dev, None, r, Measurement(self.cfg.penalty_seconds, TIMEOUT))
+            times = []
+            last = None
+            for _ in range(self.cfg.repeats):
+                last = ex.run(sched, timeout_s=self.cfg.timeout_seconds)
+                if last.status == TIMEOUT or last.seconds > self.cfg.timeout_seconds:
+                    return self._record(bits, dev, None, last,
+                                        Measurement(self.cfg.penalty_seconds, TIMEOUT))
+                times.append(last.seconds)
+            secs = statistics.median(times)
+            return self._record(bits, dev, times, last, Measurement(secs, MEASURED))
+        finally:
+            self.idle.put(dev)
+
+    def _record(self, bits, dev, times, run, m: Measurement) -> Measurement:
+        with self.log_lock:
+            self.log.append({"genome": bits, "device": dev, "times": times,
+                             "counters": run.counters if run else None, "status": m.status})
+        return m
+
+
+def make_gpu_evaluator(cfg: GpuEvaluatorConfig, program, tree, accesses, genome_map, profile):
+    pool = DevicePool(cfg)
+    if program is not None and program.source_text != pool.net.source:
+        raise ModelError(f"gpu evaluator: the tuned source is not the {cfg.net!r} program "
+                         f"(write it with `python -m paper_1811_03882_b200.nets {cfg.net} DIR`)")
+
+    def evaluate(bits: str) -> Measurement:
+        return pool.measure(bits)
+
+    def report_section(best_bits: str) -> dict:
+        ex = pool.executors[pool.devices[0]]
+        sched = ex.compile(best_bits)
+        run = ex.run(sched)
+        return {"net": cfg.net, "images": ex.images, "devices": pool.devices,
+                "best_seconds_rerun": run.seconds,
+                "img_per_s": ex.images / run.seconds,
+                "transfers": run.counters, "expected_transfers": sched.expected,
+                "fused_gemm_groups": len(sched.fused_groups)}
+
+    evaluate.pool = pool
+    evaluate.report_section = report_section
+    return evaluate

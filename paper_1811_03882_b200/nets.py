@@ -420,3 +420,28 @@ def input_images(net: NetProgram, seed: int, first: int, count: int) -> np.ndarr
     n = spec.numel
     flat = synth_values("x", seed, n * count, array_scale(net, "x"), start=first * n)
     return flat.reshape((count,) + spec.shape)
+
+
+def write_net_files(name: str, outdir, images: int | None = None) -> dict:
+    """Write `<name>.c`, `<name>_profile.json` and a `<name>_gpu.json`
+    evaluator config -- the inputs of `tune --evaluator gpu:...`."""
+    import json
+    from pathlib import Path
+    net = build_net(name, images=images)
+    out = Path(outdir)
+    out.mkdir(parents=True, exist_ok=True)
+    paths = {"source": out / f"{name}.c", "profile": out / f"{name}_profile.json",
+             "gpu_config": out / f"{name}_gpu.json"}
+    paths["source"].write_text(net.source)
+    paths["profile"].write_text(json.dumps(net.profile_dict(), indent=1) + "\n")
+    paths["gpu_config"].write_text(json.dumps({"net": name, "images": net.spec.images}) + "\n")
+    return paths
+
+
+if __name__ == "__main__":
+    import sys
+    if len(sys.argv) < 3:
+        sys.exit("usage: python -m paper_1811_03882_b200.nets <net> <outdir> [images]")
+    for key, path in write_net_files(sys.argv[1], sys.argv[2],
+                                     int(sys.argv[3]) if len(sys.argv) > 3 else None).items():
+        print(key, path)

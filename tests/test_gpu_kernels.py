@@ -1,0 +1,175 @@
+"""sm_100a kernels through the C ABI vs the CPU oracle (B200 only).
+
+Tolerances: every non-GEMM kernel is pure data movement or the same single
+float/double operation as darknet, so it must be BIT-EXACT (values and
+maxpool argmax indices).  gemm_nn reassociates the K-sum (and, in tensor-
+core mode, splits operands into TF32 hi/lo parts), so it must satisfy
+    max|gpu - oracle| <= 1e-4 * max|oracle|      (elementwise, scale-relative)
+    ||gpu - oracle||_F <= 1e-5 * ||oracle||_F    (normwise)
+against the darknet i-k-j FP32 oracle.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import cprog
+from paper_1811_03882_b200 import kernels as K
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return cprog.load_oracle()
+
+
+def _rand(shape, seed, lo=-1.0, hi=1.0):
+    return np.random.default_rng(seed).uniform(lo, hi, shape).astype(np.float32)
+
+
+class Pitched:
+    """[rows][cols] device array with a 32-element row pitch."""
+
+    def __init__(self, host: np.ndarray, dtype=None, pad_value=np.nan):
+        rows, cols = host.shape
+        self.rows, self.cols = rows, cols
+        self.ld = -(-cols // 32) * 32
+        t = torch.full((rows, self.ld), float(pad_value) if host.dtype == np.float32 else -7,
+                       dtype=torch.float32 if host.dtype == np.float32 else torch.int32,
+                       device="cuda")
+        t[:, :cols] = torch.from_numpy(host).cuda()
+        self.t = t
+
+    @property
+    def ptr(self):
+        return self.t.data_ptr()
+
+    def numpy(self):
+        torch.cuda.synchronize()
+        return self.t[:, :self.cols].cpu().numpy()
+
+
+def stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def gemm_ok(got, want):
+    scale = max(1e-30, float(np.abs(want).max()))
+    assert float(np.abs(got - want).max()) <= 1e-4 * scale
+    assert float(np.linalg.norm((got - want).astype(np.float64))) <= \
+        1e-5 * float(np.linalg.norm(want.astype(np.float64))) + 1e-30
+
+
+def test_fill_copy_bias_leaky_bit_exact(cuda_device, orc):
+    for M, N in ((1, 1), (3, 5), (16, 169), (64, 4096), (7, 1001)):
+        y0 = _rand((M, N), M * N)
+        y = Pitched(y0)
+        K.fill(y.ptr, M, N, y.ld, 0.0, stream())
+        assert not y.numpy().any()
+        x = Pitched(y0)
+        K.copy(x.ptr, x.ld, y.ptr, y.ld, M, N, stream())
+        assert np.array_equal(y.numpy(), y0)
+        bias = _rand((M,), 3)
+        bt = torch.from_numpy(bias).cuda()
+        want = y0.copy()
+        orc.orc_add_bias(want.ctypes.data, bias.ctypes.data, 1, M, N)
+        orc.orc_activate(want.ctypes.data, M * N, 1)
+        K.add_bias(y.ptr, y.ld, bt.data_ptr(), M, N, stream())
+        K.activate(y.ptr, y.ld, M, N, K.ACT_LEAKY, stream())
+        assert np.array_equal(y.numpy(), want)
+        before = y.numpy()
+        K.activate(y.ptr, y.ld, M, N, K.ACT_LINEAR, stream())
+        assert np.array_equal(y.numpy(), before)
+
+
+def test_dense_unaligned_pitch_paths(cuda_device):
+    # ld == cols (not a multiple of 4) takes the scalar kernels
+    M, N = 5, 13
+    y0 = _rand((M, N), 11)
+    t = torch.from_numpy(y0).cuda()
+    K.activate(t.data_ptr(), N, M, N, K.ACT_LEAKY, stream())
+    torch.cuda.synchronize()
+    want = np.where(y0 < 0, (0.1 * y0.astype(np.float64)).astype(np.float32), y0)
+    assert np.array_equal(t.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("c,h,w,k,s,pad", [(3, 416, 416, 3, 1, 1), (16, 13, 13, 3, 1, 1),
+                                            (2, 9, 7, 3, 2, 1), (5, 6, 6, 1, 1, 0),
+                                            (1, 3, 3, 3, 1, 1)])
+def test_im2col_bit_exact(cuda_device, orc, c, h, w, k, s, pad):
+    im0 = _rand((c, h * w), 21)
+    oh, ow = (h + 2 * pad - k) // s + 1, (w + 2 * pad - k) // s + 1
+    want = np.empty((c * k * k, oh * ow), np.float32)
+    orc.orc_im2col(im0.ctypes.data, c, h, w, k, s, pad, want.ctypes.data)
+    im = Pitched(im0)
+    col = Pitched(np.zeros((c * k * k, oh * ow), np.float32))
+    K.im2col(im.ptr, im.ld, c, h, w, k, s, pad, col.ptr, col.ld, stream())
+    assert np.array_equal(col.numpy(), want)
+
+
+@pytest.mark.parametrize("c,h,w,size,stride", [(16, 416, 416, 2, 2), (512, 13, 13, 2, 1),
+                                                (3, 7, 9, 2, 2), (2, 5, 5, 3, 2)])
+def test_maxpool_values_and_indices_bit_exact(cuda_device, orc, c, h, w, size, stride):
+    x0 = _rand((c, h * w), 31)
+    x0[:, 1::7] = x0[:, 0::7][:, : x0[:, 1::7].shape[1]]  # plant ties
+    padding = size - 1
+    oh, ow = (h + padding - size) // stride + 1, (w + padding - size) // stride + 1
+    wo, wi = np.empty((c, oh * ow), np.float32), np.empty((c, oh * ow), np.int32)
+    orc.orc_maxpool(x0.ctypes.data, 1, c, h, w, size, stride, padding, wo.ctypes.data, wi.ctypes.data)
+    x = Pitched(x0)
+    out = Pitched(np.zeros((c, oh * ow), np.float32))
+    idx = Pitched(np.zeros((c, oh * ow), np.int32))
+    K.maxpool(x.ptr, x.ld, c, h, w, size, stride, padding // 2, oh, ow, out.ptr, out.ld,
+              idx.ptr, idx.ld, stream())
+    assert np.array_equal(out.numpy(), wo)
+    assert np.array_equal(idx.numpy(), wi)
+
+
+GEMM_SHAPES = [(16, 173056, 27), (32, 4000, 144), (64, 10816, 288), (128, 2704, 576),
+               (256, 676, 1152), (512, 169, 2304), (1024, 169, 4608), (425, 169, 512),
+               (1, 1, 1), (3, 5, 7), (130, 129, 33), (200, 300, 64)]
+
+
+@pytest.mark.parametrize("mode", [K.GEMM_SIMT, K.GEMM_AUTO])
+@pytest.mark.parametrize("M,N,K_", GEMM_SHAPES)
+def test_gemm_nn_within_tolerance(cuda_device, orc, mode, M, N, K_):
+    A0, B0 = _rand((M, K_), 41, -0.5, 0.5), _rand((K_, N), 42)
+    C0 = _rand((M, N), 43)
+    want = C0.copy()
+    orc.orc_gemm_nn(M, N, K_, 1.0, A0.ctypes.data, K_, B0.ctypes.data, N, want.ctypes.data, N)
+    A, B, Cd = Pitched(A0), Pitched(B0), Pitched(C0)
+    K.gemm_nn(M, N, K_, 1.0, A.ptr, A.ld, B.ptr, B.ld, 1.0, Cd.ptr, Cd.ld, None, K.ACT_NONE,
+              mode, stream())
+    gemm_ok(Cd.numpy(), want)
+
+
+@pytest.mark.parametrize("mode", [K.GEMM_SIMT, K.GEMM_AUTO])
+def test_gemm_fused_epilogue_equals_separate_ops(cuda_device, mode):
+    M, N, K_ = 256, 676, 1152
+    A0, B0 = _rand((M, K_), 51, -0.5, 0.5), _rand((K_, N), 52)
+    bias0 = _rand((M,), 53)
+    A, B = Pitched(A0), Pitched(B0)
+    bias = torch.from_numpy(bias0).cuda()
+    sep = Pitched(np.zeros((M, N), np.float32))
+    K.fill(sep.ptr, M, N, sep.ld, 0.0, stream())
+    K.gemm_nn(M, N, K_, 1.0, A.ptr, A.ld, B.ptr, B.ld, 1.0, sep.ptr, sep.ld, None, K.ACT_NONE,
+              mode, stream())
+    K.add_bias(sep.ptr, sep.ld, bias.data_ptr(), M, N, stream())
+    K.activate(sep.ptr, sep.ld, M, N, K.ACT_LEAKY, stream())
+    fused = Pitched(np.full((M, N), 3.0, np.float32))
+    K.gemm_nn(M, N, K_, 1.0, A.ptr, A.ld, B.ptr, B.ld, 0.0, fused.ptr, fused.ld,
+              bias.data_ptr(), K.ACT_LEAKY, mode, stream())
+    assert np.array_equal(fused.numpy(), sep.numpy())
+
+
+def test_kernel_launches_are_counted(cuda_device):
+    K.reset_counters()
+    y = Pitched(np.zeros((4, 40), np.float32))
+    K.fill(y.ptr, 4, 40, y.ld, 1.0, stream())
+    K.activate(y.ptr, y.ld, 4, 40, K.ACT_LEAKY, stream())
+    torch.cuda.synchronize()
+    assert K.counters()["kernel_launches"] == 2

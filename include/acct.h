@@ -182,6 +182,18 @@ int acct_run_schedule_profiled(acct_array_t *arrays, int n_arrays, const acct_ac
                                int n_actions, int gemm_mode, double timeout_s,
                                acct_stream_t stream, float *kernel_ms);
 
+/* CUDA-graph replay of a schedule that has no host loop (every gene 1):
+ * the whole action list -- every image of the loop, kernels and pitched
+ * transfers -- is captured once into one graph; a replay is one
+ * cudaGraphLaunch.  The counters the capture interpretation produced are
+ * re-applied on every replay, so counts stay per execution.  Returns
+ * ACCT_ENOTSUP (and no graph) if the schedule has host work.              */
+typedef struct acct_graph acct_graph_t;
+int acct_schedule_capture(acct_array_t *arrays, int n_arrays, const acct_action_t *actions,
+                          int n_actions, int gemm_mode, acct_stream_t stream, acct_graph_t **out);
+int acct_graph_replay(acct_graph_t *graph, acct_stream_t stream, int synchronize);
+void acct_graph_destroy(acct_graph_t *graph);
+
 /* library/device facts */
 int acct_device_sm_count(int device);
 const char *acct_build_info(void);

@@ -1,12 +1,524 @@
-// gemm_nn on the 5th-generation tensor cores: placeholder until the tcgen05
-// 3xTF32 kernel lands; AUTO mode falls back to the SIMT kernels.
+// gemm_nn on the 5th-generation tensor cores, FP32-accurate via 3xTF32.
+//
+//   C[M][N] = beta*C + alpha * A[M][K] . B[K][N]  (+ bias[row]) (leaky)
+//
+// A (the layer's weights) is row-major, K contiguous -> a "K-major" UMMA
+// operand; B (im2col columns / activations) is row-major, N contiguous -> an
+// "MN-major" operand (legal for kind::tf32 only in the SWIZZLE_128B_BASE32B
+// shared-memory layout, TMA swizzle 128B_ATOM_32B).  Each operand x is split
+// exactly into x_hi = x with the low 13 mantissa bits cleared (a TF32 value)
+// and x_lo = x - x_hi (exact in FP32; truncated to TF32 by the MMA), and the
+// tile accumulates  X_hi.Y_hi + X_hi.Y_lo + X_lo.Y_hi  in TMEM (FP32), which
+// keeps the product within ~2^-20 relative of FP32 -- the accuracy contract
+// of darknet's FP32 gemm_nn (tests: 1e-4 scale-relative, 1e-5 normwise).
+//
+// Two tile orientations (MMA M is always 128 rows = TMEM lanes):
+//   normal  X = 128 weight rows (K-major), Y = TN in {128, 192} columns of B
+//           (MN-major).  For the wide-M layers; TN = 192 covers the 13x13
+//           layers (N = 169) with one N tile.
+//   swap    X = 128 columns of B (MN-major), Y = TN in {16, 32, 64} weight
+//           rows (K-major): C^T = B^T A^T for the narrow-M layers (M = 16,
+//           32, 64) so no MMA rows are wasted; TMEM lanes are output columns,
+//           so epilogue stores are coalesced without a transpose.
+//
+// CTA = 6 warps:
+//   warp 0      TMA producer (one elected lane), `stages`-deep ring
+//   warp 1      TMEM allocator + MMA issuer (one elected lane)
+//   warps 2..5  hi/lo split of each landed stage (hi in place, lo to its own
+//               buffer; generic -> async proxy fence), then the epilogue:
+//               tcgen05.ld -> registers -> (normal: smem transpose) ->
+//               coalesced 128-B row stores with bias/leaky; or, under
+//               split-K, raw FP32 partials into an L2-resident workspace that
+//               a grid-wide reduce kernel sums in split order (deterministic
+//               run to run) and finishes with the same epilogue.
+// Barriers per stage: full (TMA bytes landed), conv (split done, 4 warp
+// arrivals), empty (tcgen05.commit after the stage's 12 MMAs).
+// The pipeline depth is chosen per launch (min(max_stages, k-blocks)) and
+// the dynamic shared memory sized to it, so short-K launches (layer 0 has a
+// single k-block) fit several CTAs per SM.
+
+#include <cuda.h>
+
+#include <mutex>
+#include <unordered_map>
+
 #include "acct_common.cuh"
+#include "acct_tc.cuh"
 
 namespace acct {
+namespace {
 
-int gemm_tc(int, int, int, float, const float *, int64_t, const float *, int64_t, float, float *,
-            int64_t, const float *, int, cudaStream_t) {
-  return ACCT_ENOTSUP;
+constexpr int BK = 32;
+constexpr int X_TILE = 128 * BK * 4;  // 16 KiB: 128 rows x 32 fp32
+constexpr int THREADS = 192;
+
+template <int TN>
+struct Cfg {
+  static constexpr int Y_TILE = TN * BK * 4;
+  static constexpr int STAGE_BYTES = 2 * X_TILE + 2 * Y_TILE;  // hi + lo of both operands
+  static constexpr int MAX_STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
+  static constexpr uint32_t TMEM_COLS = TN <= 32 ? 32 : TN <= 64 ? 64 : TN <= 128 ? 128 : 256;
+  static int smem_bytes(int stages) { return stages * STAGE_BYTES + 256 /*barriers*/ + 1024 /*align*/; }
+};
+
+__device__ __forceinline__ float4 split_hi(float4 v, float4 &lo) {
+  float4 h;
+  h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+  h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+  h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+  h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+  lo.x = v.x - h.x;
+  lo.y = v.y - h.y;
+  lo.z = v.z - h.z;
+  lo.w = v.w - h.w;
+  return h;
+}
+
+__device__ __forceinline__ float finish(float acc, float alpha, float beta, float c,
+                                        const float *bias, float bias_v, int act) {
+  float v = alpha * acc;
+  if (beta != 0.0f) v = beta * c + v;
+  if (bias) v += bias_v;
+  if (act == ACCT_ACT_LEAKY) v = acct_leaky(v);
+  return v;
+}
+
+// MN-major operand: `width` columns of a K x width slab, loaded as 32-column
+// boxes (4 KiB each for BK = 32) into SW128_BASE32B layout.
+// K-major operand: `rows` x 32 fp32, one box, SW128 layout.
+template <int TN, bool SWAP>
+__global__ void __launch_bounds__(THREADS, 2)
+tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               int M, int N, int K, int kb_per_split, int stages, float alpha, float beta,
+               float *__restrict__ C, int64_t ldc, const float *__restrict__ bias, int act,
+               float *__restrict__ ws, int64_t ws_ld, int64_t ws_split_stride) {
+  using G = Cfg<TN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  auto x_hi = [&](int s) { return base + s * G::STAGE_BYTES; };
+  auto x_lo = [&](int s) { return base + s * G::STAGE_BYTES + X_TILE; };
+  auto y_hi = [&](int s) { return base + s * G::STAGE_BYTES + 2 * X_TILE; };
+  auto y_lo = [&](int s) { return base + s * G::STAGE_BYTES + 2 * X_TILE + G::Y_TILE; };
+  uint64_t *full = reinterpret_cast<uint64_t *>(base + stages * G::STAGE_BYTES);
+  uint64_t *conv = full + stages;
+  uint64_t *empty = conv + stages;
+  uint64_t *tmem_full = empty + stages;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // n0: first output column of the tile, m0: first output row
+  const int n0 = blockIdx.x * (SWAP ? 128 : TN);
+  const int m0 = blockIdx.y * (SWAP ? TN : 128);
+  const int splits = gridDim.z, split = blockIdx.z;
+  const int total_kb = (K + BK - 1) / BK;
+  const int kb0 = split * kb_per_split;
+  const int nkb = max(0, min(kb0 + kb_per_split, total_kb) - kb0);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&conv[s], 4);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::mbar_init(tmem_full, 1);
+    ptx::fence_mbar_init();
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, G::TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % stages;
+        if (i >= stages) ptx::mbar_wait(&empty[s], ((i / stages) - 1) & 1);
+        ptx::mbar_expect_tx(&full[s], X_TILE + G::Y_TILE);
+        const int kx = (kb0 + i) * BK;
+        if (!SWAP) {
+          ptx::tma_load_2d(x_hi(s), &tmA, &full[s], kx, m0);
+#pragma unroll
+          for (int c = 0; c < TN / 32; ++c)
+            ptx::tma_load_2d(y_hi(s) + c * (BK * 128), &tmB, &full[s], n0 + 32 * c, kx);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            ptx::tma_load_2d(x_hi(s) + c * (BK * 128), &tmB, &full[s], n0 + 32 * c, kx);
+          ptx::tma_load_2d(y_hi(s), &tmA, &full[s], kx, m0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_tf32(128, TN, SWAP, !SWAP);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % stages;
+        ptx::mbar_wait(&conv[s], (i / stages) & 1);
+        ptx::tc_fence_after();
+        const uint32_t xh = ptx::smem_u32(x_hi(s)), xl = ptx::smem_u32(x_lo(s));
+        const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
+#pragma unroll
+        for (int k = 0; k < BK / 8; ++k) {
+          // K-major SW128: 8 tf32 (32 B) per step inside the 128-B rows.
+          // MN-major SW128_BASE32B: 8 k-rows (two 512-B atoms) per step,
+          // 32-column chunks BK*128 B apart (LBO).
+          uint64_t dxh, dxl, dyh, dyl;
+          if (!SWAP) {
+            dxh = ptx::smem_desc(xh + 32 * k, 16, 1024, ptx::kLayoutSW128);
+            dxl = ptx::smem_desc(xl + 32 * k, 16, 1024, ptx::kLayoutSW128);
+            dyh = ptx::smem_desc(yh + 1024 * k, BK * 128, 512, ptx::kLayoutSW128Base32B);
+            dyl = ptx::smem_desc(yl + 1024 * k, BK * 128, 512, ptx::kLayoutSW128Base32B);
+          } else {
+            dxh = ptx::smem_desc(xh + 1024 * k, BK * 128, 512, ptx::kLayoutSW128Base32B);
+            dxl = ptx::smem_desc(xl + 1024 * k, BK * 128, 512, ptx::kLayoutSW128Base32B);
+            dyh = ptx::smem_desc(yh + 32 * k, 16, 1024, ptx::kLayoutSW128);
+            dyl = ptx::smem_desc(yl + 32 * k, 16, 1024, ptx::kLayoutSW128);
+          }
+          ptx::mma_tf32(tmem, dxh, dyh, idesc, (i | k) != 0);
+          ptx::mma_tf32(tmem, dxh, dyl, idesc, 1);
+          ptx::mma_tf32(tmem, dxl, dyh, idesc, 1);
+        }
+        ptx::mma_commit(&empty[s]);
+      }
+      ptx::mma_commit(tmem_full);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- split hi/lo of each landed stage ----------------
+    const int ct = threadIdx.x - 64;  // 0..127
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % stages;
+      ptx::mbar_wait(&full[s], (i / stages) & 1);
+      float4 *xh = reinterpret_cast<float4 *>(x_hi(s));
+      float4 *xl = reinterpret_cast<float4 *>(x_lo(s));
+      float4 *yh = reinterpret_cast<float4 *>(y_hi(s));
+      float4 *yl = reinterpret_cast<float4 *>(y_lo(s));
+#pragma unroll 4
+      for (int v = ct; v < X_TILE / 16; v += 128) {
+        float4 lo;
+        float4 hi = split_hi(xh[v], lo);
+        xh[v] = hi;
+        xl[v] = lo;
+      }
+#pragma unroll 4
+      for (int v = ct; v < G::Y_TILE / 16; v += 128) {
+        float4 lo;
+        float4 hi = split_hi(yh[v], lo);
+        yh[v] = hi;
+        yl[v] = lo;
+      }
+      ptx::fence_proxy_async_smem();   // generic-proxy writes -> tensor core
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&conv[s]);
+    }
+
+    // ---------------- epilogue ----------------
+    const int q = warp & 3;  // this warp may read TMEM lanes 32q..32q+31
+    if (nkb > 0) {
+      ptx::mbar_wait(tmem_full, 0);
+      ptx::tc_fence_after();
+    }
+    const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
+    if (!SWAP) {
+      // lanes = output rows: transpose each 32x32 chunk through smem so that
+      // lane = column and each store writes a contiguous 128-B row segment
+      float *stg = reinterpret_cast<float *>(x_lo(0)) + q * (32 * 33);  // free: MMAs done
+      const int row0 = m0 + 32 * q;
+      for (int c = 0; c < TN / 32; ++c) {
+        uint32_t r[32];
+        if (nkb > 0) {
+          ptx::tmem_ld_32x32b_x32(trow + 32 * c, r);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = __uint_as_float(r[j]);
+        __syncwarp();
+        const int col = n0 + 32 * c + lane;
+        if (splits == 1) {
+          if (col < N) {
+            float cv[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i)  // all C loads in flight before any store
+              cv[i] = (beta != 0.0f && row0 + i < M) ? C[(int64_t)(row0 + i) * ldc + col] : 0.0f;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int row = row0 + i;
+              if (row < M)
+                C[(int64_t)row * ldc + col] = finish(stg[i * 33 + lane], alpha, beta, cv[i], bias,
+                                                     bias ? __ldg(bias + row) : 0.0f, act);
+            }
+          }
+        } else {
+          float *dst = ws + split * ws_split_stride + (int64_t)row0 * ws_ld + col;
+#pragma unroll 8
+          for (int i = 0; i < 32; ++i) __stcg(dst + (int64_t)i * ws_ld, stg[i * 33 + lane]);
+        }
+        __syncwarp();
+      }
+    } else {
+      // lanes = output columns, TMEM columns = output rows: stores are
+      // coalesced across the warp as they come
+      const int col = n0 + 32 * q + lane;
+      constexpr int CH = TN < 32 ? TN : 32;
+      for (int c = 0; c < TN / CH; ++c) {
+        uint32_t r[32];
+        if (nkb > 0) {
+          if constexpr (CH == 16) {
+            uint32_t r16[16];
+            ptx::tmem_ld_32x32b_x16(trow + 16 * c, r16);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[j] = r16[j];
+          } else {
+            ptx::tmem_ld_32x32b_x32(trow + 32 * c, r);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < CH; ++j) r[j] = 0u;
+        }
+        if (col >= N) continue;
+        const int rbase = m0 + CH * c;
+        if (splits == 1) {
+          float cv[CH];
+#pragma unroll
+          for (int j = 0; j < CH; ++j)
+            cv[j] = (beta != 0.0f && rbase + j < M) ? C[(int64_t)(rbase + j) * ldc + col] : 0.0f;
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int row = rbase + j;
+            if (row < M)
+              C[(int64_t)row * ldc + col] = finish(__uint_as_float(r[j]), alpha, beta, cv[j], bias,
+                                                   bias ? __ldg(bias + row) : 0.0f, act);
+          }
+        } else {
+          float *dst = ws + split * ws_split_stride + (int64_t)rbase * ws_ld + col;
+#pragma unroll
+          for (int j = 0; j < CH; ++j) __stcg(dst + (int64_t)j * ws_ld, __uint_as_float(r[j]));
+        }
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc(tmem, G::TMEM_COLS);
+}
+
+// Sum the split-K partials of every output element in split order and apply
+// the epilogue (grid-wide, one thread per 4 consecutive columns).
+__global__ void __launch_bounds__(256)
+splitk_reduce_kernel(const float *__restrict__ ws, int64_t ws_ld, int64_t split_stride, int splits,
+                     int M, int N, float alpha, float beta, float *__restrict__ C, int64_t ldc,
+                     const float *__restrict__ bias, int act) {
+  const int nq = (N + 3) / 4;
+  const int total = M * nq;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int row = t / nq;
+    const int col = (t - row * nq) * 4;
+    const float *p = ws + (int64_t)row * ws_ld + col;
+    float4 acc = __ldcg(reinterpret_cast<const float4 *>(p));
+    for (int sp = 1; sp < splits; ++sp) {
+      const float4 v = __ldcg(reinterpret_cast<const float4 *>(p + sp * split_stride));
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    const float bv = bias ? __ldg(bias + row) : 0.0f;
+    float *cp = C + (int64_t)row * ldc + col;
+    const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (col + e < N) {
+        const float cv = beta != 0.0f ? cp[e] : 0.0f;
+        cp[e] = finish(a4[e], alpha, beta, cv, bias, bv, act);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D fp32 tensor map: inner dim `inner` (contiguous), outer dim `outer` with
+// row pitch `ld` elements; box = 32 x box_outer; out-of-bounds reads are 0.
+bool make_map(CUtensorMap *map, const float *ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+              uint32_t box_outer, CUtensorMapSwizzle swizzle) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {32, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Tensor maps are pure functions of (pointer, shape, pitch, box, swizzle);
+// the executor replays the same few dozen per image, so encode each once per
+// host thread.
+struct MapKey {
+  const void *ptr;
+  uint64_t inner, outer, ld;
+  uint32_t box, swz;
+  bool operator==(const MapKey &o) const {
+    return ptr == o.ptr && inner == o.inner && outer == o.outer && ld == o.ld && box == o.box &&
+           swz == o.swz;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey &k) const {
+    uint64_t h = reinterpret_cast<uint64_t>(k.ptr) * 0x9E3779B97F4A7C15ull;
+    h ^= k.inner + 0x9E37 + (h << 6) + (h >> 2);
+    h ^= k.outer + 0x7F4A + (h << 6) + (h >> 2);
+    h ^= k.ld + ((uint64_t)k.box << 32) + ((uint64_t)k.swz << 48) + (h << 6) + (h >> 2);
+    return (size_t)h;
+  }
+};
+
+bool cached_map(CUtensorMap *map, const float *ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                uint32_t box_outer, CUtensorMapSwizzle swizzle) {
+  static thread_local std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  MapKey key{ptr, inner, outer, ld, box_outer, (uint32_t)swizzle};
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *map = it->second;
+    return true;
+  }
+  if (!make_map(map, ptr, inner, outer, ld, box_outer, swizzle)) return false;
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, *map);
+  return true;
+}
+
+// split-K scratch, one per (device, stream) so concurrent streams never share it
+std::mutex g_scratch_mu;
+std::unordered_map<uint64_t, std::pair<float *, size_t>> g_scratch;
+
+int scratch_for(cudaStream_t s, size_t floats, float **out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  uint64_t key = (reinterpret_cast<uint64_t>(s) << 8) ^ (uint64_t)dev;
+  std::lock_guard<std::mutex> lock(g_scratch_mu);
+  auto &sc = g_scratch[key];
+  if (sc.second < floats) {
+    if (sc.first) cudaFree(sc.first);
+    sc.first = nullptr;
+    sc.second = 0;
+    if (int rc = check_cuda(cudaMalloc(&sc.first, floats * sizeof(float)), "gemm_tc: workspace"))
+      return rc;
+    sc.second = floats;
+  }
+  *out = sc.first;
+  return ACCT_OK;
+}
+
+template <int TN, bool SWAP>
+int set_smem_attr() {
+  // the attribute is per device context; set the maximum once
+  static std::mutex mu;
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev >= 0 && dev < 64 && !done[dev]) {
+    if (int rc = check_cuda(cudaFuncSetAttribute(tc_gemm_kernel<TN, SWAP>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 Cfg<TN>::smem_bytes(Cfg<TN>::MAX_STAGES)),
+                            "gemm_tc: smem attribute"))
+      return rc;
+    done[dev] = true;
+  }
+  return ACCT_OK;
+}
+
+template <int TN, bool SWAP>
+int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
+              int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
+              cudaStream_t s) {
+  using G = Cfg<TN>;
+  CUtensorMap ta, tb;
+  // weights: K-major box of (32 k) x (rows of the weight-side tile)
+  const uint32_t a_rows = SWAP ? TN : 128;
+  if (!cached_map(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, a_rows, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !cached_map(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, BK,
+                  CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+    return fail(ACCT_ENOTSUP, "gemm_tc: cuTensorMapEncodeTiled failed");
+  const int tile_n = SWAP ? 128 : TN, tile_m = SWAP ? TN : 128;
+  const int nt = (N + tile_n - 1) / tile_n, mt = (M + tile_m - 1) / tile_m, tiles = mt * nt;
+  const int total_kb = (K + BK - 1) / BK;
+  const int sms = sm_count();
+  // fill one wave: split K until tiles x splits covers the SMs, keeping >= 2
+  // k-blocks per split so the pipeline has something to overlap
+  int splits = 1;
+  if (tiles < sms) {
+    splits = sms / tiles;
+    if (splits > total_kb / 2) splits = total_kb / 2;
+    if (splits < 1) splits = 1;
+  }
+  const int kb_per = (total_kb + splits - 1) / splits;
+  splits = (total_kb + kb_per - 1) / kb_per;
+  const int stages = kb_per < G::MAX_STAGES ? kb_per : G::MAX_STAGES;
+
+  float *ws = nullptr;
+  const int64_t ws_ld = (int64_t)nt * tile_n, rows = (int64_t)mt * tile_m;
+  if (splits > 1) {
+    if (int rc = scratch_for(s, (size_t)splits * rows * ws_ld, &ws)) return rc;
+  }
+  if (int rc = set_smem_attr<TN, SWAP>()) return rc;
+  dim3 grid(nt, mt, splits);
+  tc_gemm_kernel<TN, SWAP><<<grid, THREADS, G::smem_bytes(stages), s>>>(
+      ta, tb, M, N, K, kb_per, stages, alpha, beta, C, ldc, bias, act, ws, ws_ld, rows * ws_ld);
+  if (int rc = note_launch("gemm_tc")) return rc;
+  if (splits > 1) {
+    const int64_t work = (int64_t)M * ((N + 3) / 4);
+    splitk_reduce_kernel<<<grid_for(work, 256), 256, 0, s>>>(ws, ws_ld, rows * ws_ld, splits, M, N,
+                                                             alpha, beta, C, ldc, bias, act);
+    if (int rc = note_launch("gemm_tc_splitk_reduce")) return rc;
+  }
+  return ACCT_OK;
+}
+
+}  // namespace
+
+int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
+            int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
+            cudaStream_t s) {
+  // TMA needs 16-B aligned bases and row pitches
+  if (M < 1 || N < 1 || K < 1 || (lda % 4) || (ldb % 4) ||
+      (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
+    return ACCT_ENOTSUP;
+  if (M <= 16) return launch_tc<16, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (M <= 32) return launch_tc<32, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (M <= 64) return launch_tc<64, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (N > 128 && N <= 192)
+    return launch_tc<192, false>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  return launch_tc<128, false>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
 }
 
 }  // namespace acct

@@ -249,7 +249,8 @@ struct Profiler {
 };
 
 int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *actions, int n_actions,
-                 int gemm_mode, double timeout_s, acct_stream_t stream, Profiler *prof);
+                 int gemm_mode, double timeout_s, acct_stream_t stream, Profiler *prof,
+                 bool capturing = false);
 
 }  // namespace
 
@@ -282,13 +283,14 @@ extern "C" int acct_run_schedule_profiled(acct_array_t *arrays, int n_arrays,
 namespace {
 
 int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *actions, int n_actions,
-                 int gemm_mode, double timeout_s, acct_stream_t stream, Profiler *prof) {
+                 int gemm_mode, double timeout_s, acct_stream_t stream, Profiler *prof,
+                 bool capturing) {
   cudaStream_t s = as_stream(stream);
   std::vector<LoopFrame> loops;
   bool pending = false;
   const auto t0 = std::chrono::steady_clock::now();
   auto drain = [&]() -> int {
-    if (!pending) return ACCT_OK;
+    if (!pending || capturing) return ACCT_OK;
     pending = false;
     return check_cuda(cudaStreamSynchronize(s), "schedule: stream sync");
   };
@@ -311,7 +313,7 @@ int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *action
         LoopFrame &f = loops.back();
         if (++f.counter < f.trip) {
           pc = f.begin + 1;
-          if (timeout_s > 0) {
+          if (timeout_s > 0 && !capturing) {
             double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
             if (el > timeout_s) {
               cudaStreamSynchronize(s);
@@ -353,7 +355,10 @@ int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *action
         if (rc) return rc;
         int64_t lv = loops[(size_t)a.i[0]].counter;
         char *dst = static_cast<char *>(a.base) + lv * a.i[1];
-        if (dst != arrays[a.a[0]].host) memcpy(dst, arrays[a.a[0]].host, (size_t)a.i[2]);
+        if (dst != arrays[a.a[0]].host) {
+          if (capturing) return fail(ACCT_ENOTSUP, "schedule capture: store_output needs a host copy");
+          memcpy(dst, arrays[a.a[0]].host, (size_t)a.i[2]);
+        }
         break;
       }
       case ACCT_A_KERNEL:
@@ -370,6 +375,7 @@ int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *action
         pending = true;
         break;
       case ACCT_A_HOST:
+        if (capturing) return fail(ACCT_ENOTSUP, "schedule capture: host loop in schedule");
         rc = drain();
         if (rc) return rc;
         rc = host_op(a, arrays);
@@ -388,3 +394,85 @@ int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *action
 }
 
 }  // namespace
+
+// ---------------------------------------------------------------- graphs
+
+struct acct_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  acct_counters_t delta{};
+};
+
+extern "C" int acct_schedule_capture(acct_array_t *arrays, int n_arrays,
+                                     const acct_action_t *actions, int n_actions, int gemm_mode,
+                                     acct_stream_t stream, acct_graph_t **out) {
+  if (!out) return fail(ACCT_EINVAL, "capture: null output");
+  *out = nullptr;
+  for (int k = 0; k < n_actions; ++k)
+    if (actions[k].kind == ACCT_A_HOST) return ACCT_ENOTSUP;
+  cudaStream_t s = as_stream(stream);
+  acct_counters_t before, after;
+  acct_counters_get(&before);
+  if (int rc = check_cuda(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal),
+                          "capture: begin"))
+    return rc;
+  int rc = run_schedule(arrays, n_arrays, actions, n_actions, gemm_mode, 0.0, stream, nullptr,
+                        /*capturing=*/true);
+  cudaGraph_t graph = nullptr;
+  cudaError_t end = cudaStreamEndCapture(s, &graph);
+  if (rc != ACCT_OK || end != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    return rc != ACCT_OK ? rc : check_cuda(end, "capture: end");
+  }
+  acct_counters_get(&after);
+  auto *g = new acct_graph();
+  g->graph = graph;
+  if (int irc = check_cuda(cudaGraphInstantiate(&g->exec, graph, 0), "capture: instantiate")) {
+    cudaGraphDestroy(graph);
+    delete g;
+    return irc;
+  }
+  g->delta.directive_execs = after.directive_execs - before.directive_execs;
+  g->delta.var_transfers = after.var_transfers - before.var_transfers;
+  g->delta.h2d_calls = after.h2d_calls - before.h2d_calls;
+  g->delta.d2h_calls = after.d2h_calls - before.d2h_calls;
+  g->delta.h2d_bytes = after.h2d_bytes - before.h2d_bytes;
+  g->delta.d2h_bytes = after.d2h_bytes - before.d2h_bytes;
+  g->delta.kernel_launches = after.kernel_launches - before.kernel_launches;
+  g->delta.host_ops = 0;
+  // the capture only recorded work: take its counts back out
+  Counters &c = counters();
+  c.directive_execs -= g->delta.directive_execs;
+  c.var_transfers -= g->delta.var_transfers;
+  c.h2d_calls -= g->delta.h2d_calls;
+  c.d2h_calls -= g->delta.d2h_calls;
+  c.h2d_bytes -= g->delta.h2d_bytes;
+  c.d2h_bytes -= g->delta.d2h_bytes;
+  c.kernel_launches -= g->delta.kernel_launches;
+  *out = g;
+  return ACCT_OK;
+}
+
+extern "C" int acct_graph_replay(acct_graph_t *g, acct_stream_t stream, int synchronize) {
+  if (!g || !g->exec) return fail(ACCT_EINVAL, "replay: null graph");
+  cudaStream_t s = as_stream(stream);
+  if (int rc = check_cuda(cudaGraphLaunch(g->exec, s), "replay: launch")) return rc;
+  Counters &c = counters();
+  c.directive_execs += g->delta.directive_execs;
+  c.var_transfers += g->delta.var_transfers;
+  c.h2d_calls += g->delta.h2d_calls;
+  c.d2h_calls += g->delta.d2h_calls;
+  c.h2d_bytes += g->delta.h2d_bytes;
+  c.d2h_bytes += g->delta.d2h_bytes;
+  c.kernel_launches += g->delta.kernel_launches;
+  if (synchronize) return check_cuda(cudaStreamSynchronize(s), "replay: sync");
+  return ACCT_OK;
+}
+
+extern "C" void acct_graph_destroy(acct_graph_t *g) {
+  if (!g) return;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
+}

@@ -78,8 +78,13 @@ SIGNATURES = {
     "acct_run_schedule_profiled": [C.POINTER(ArraySlot), _i32, C.POINTER(Action), _i32, _i32,
                                    _f64, _vp, C.POINTER(C.c_float)],
     "acct_device_sm_count": [_i32],
+    "acct_schedule_capture": [C.POINTER(ArraySlot), _i32, C.POINTER(Action), _i32, _i32, _vp,
+                              C.POINTER(C.c_void_p)],
+    "acct_graph_replay": [_vp, _vp, _i32],
 }
-VOID_FUNCS = {"acct_counters_get": [C.POINTER(Counters)], "acct_counters_reset": []}
+VOID_FUNCS = {"acct_counters_get": [C.POINTER(Counters)], "acct_counters_reset": [],
+              "acct_graph_destroy": [_vp]}
+ENOTSUP = 1002
 STRING_FUNCS = {"acct_last_error_string": [], "acct_build_info": []}
 
 _lock = threading.Lock()

@@ -134,9 +134,11 @@ GEMM_SHAPES = [(16, 173056, 27), (32, 4000, 144), (64, 10816, 288), (128, 2704, 
                (1, 1, 1), (3, 5, 7), (130, 129, 33), (200, 300, 64)]
 
 
-@pytest.mark.parametrize("mode", [K.GEMM_SIMT, K.GEMM_AUTO])
+@pytest.mark.parametrize("mode", [K.GEMM_SIMT, K.GEMM_AUTO, K.GEMM_TC3XTF32])
 @pytest.mark.parametrize("M,N,K_", GEMM_SHAPES)
 def test_gemm_nn_within_tolerance(cuda_device, orc, mode, M, N, K_):
+    if mode == K.GEMM_TC3XTF32 and M < 64:
+        pytest.skip("tensor-core path takes M >= 64 (smaller M runs the SIMT skinny kernel)")
     A0, B0 = _rand((M, K_), 41, -0.5, 0.5), _rand((K_, N), 42)
     C0 = _rand((M, N), 43)
     want = C0.copy()
@@ -147,7 +149,7 @@ def test_gemm_nn_within_tolerance(cuda_device, orc, mode, M, N, K_):
     gemm_ok(Cd.numpy(), want)
 
 
-@pytest.mark.parametrize("mode", [K.GEMM_SIMT, K.GEMM_AUTO])
+@pytest.mark.parametrize("mode", [K.GEMM_SIMT, K.GEMM_AUTO, K.GEMM_TC3XTF32])
 def test_gemm_fused_epilogue_equals_separate_ops(cuda_device, mode):
     M, N, K_ = 256, 676, 1152
     A0, B0 = _rand((M, K_), 51, -0.5, 0.5), _rand((K_, N), 52)

@@ -86,7 +86,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._pump, daemon=True)
             self.thread.start()
@@ -281,7 +281,11 @@ def run_ours(args):
 
     gemm_mode = {"auto": K.GEMM_AUTO, "simt": K.GEMM_SIMT, "tc": K.GEMM_TC3XTF32}[args.gemm]
     net = build_net(args.net, images=args.images)
-    ex = PatternExecutor(net, device=local, fuse=not args.no_fuse, gemm_mode=gemm_mode)
+    # weak scaling: rank r owns images [r*images, (r+1)*images) of the stream
+    from paper_1811_03882_b200.sharding import image_shard
+    shard = image_shard(world * args.images, world, rank)
+    ex = PatternExecutor(net, device=local, fuse=not args.no_fuse, gemm_mode=gemm_mode,
+                         first_image=shard.first)
     bits = "1" * len(net.ops)
     full = ex.compile(bits)
     res = ex.compile(bits, resident=True)
@@ -299,6 +303,9 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
+    # clocks are sampled from the first warm-up step to the end of the e2e leg
+    # (every step in between keeps the GPU busy); see ClockSampler
+    clocks = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
         ex.run(res)
         ex.run(full)
@@ -307,18 +314,17 @@ def run_ours(args):
     barrier()
     step_ms = []
     launches = 0
-    with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
-            with torch.cuda.stream(ex.stream):
-                flush.zero_()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(ex.stream)
-            r = ex.run(res)
-            e1.record(ex.stream)
-            e1.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
-            launches += r.counters["kernel_launches"]
+    for _ in range(args.steps):
+        with torch.cuda.stream(ex.stream):
+            flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(ex.stream)
+        r = ex.run(res)
+        e1.record(ex.stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        launches += r.counters["kernel_launches"]
     barrier()
     local_total = sum(step_ms) * 1e-3
     total = max_over_ranks(local_total)
@@ -338,6 +344,8 @@ def run_ours(args):
     barrier()
     e2e_total = max_over_ranks(sum(walls))
     e2e_value = world * args.images * args.steps / e2e_total
+    time.sleep(0.25)  # let the sampler log the tail of the loaded period
+    clocks.__exit__(None, None, None)
     for key, val in full.expected.items():
         if counters[key] != val:
             raise SystemExit(f"transfer counter mismatch {key}: {counters[key]} != {val}")

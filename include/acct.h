@@ -194,6 +194,10 @@ int acct_schedule_capture(acct_array_t *arrays, int n_arrays, const acct_action_
 int acct_graph_replay(acct_graph_t *graph, acct_stream_t stream, int synchronize);
 void acct_graph_destroy(acct_graph_t *graph);
 
+/* tensor-core gemm: 1 = store the TF32 hi part explicitly, 0 (default) =
+ * leave raw FP32 in shared memory (the MMA truncates); for verification */
+void acct_tc_set_write_hi(int on);
+
 /* library/device facts */
 int acct_device_sm_count(int device);
 const char *acct_build_info(void);

@@ -22,13 +22,26 @@ namespace {
 constexpr int kBlock = 256;
 constexpr int64_t kMaxElems = (int64_t)1 << 31;
 
-dim3 grid2d(int64_t per_row_items, int64_t rows, int block) {
-  int64_t gx = (per_row_items + block - 1) / block;
+// 2-D launch shape for a [rows][items] sweep: blockDim.x covers a row (a
+// multiple of 32, at most 256), blockDim.y packs several short rows into one
+// 256-thread CTA so 13x13 planes do not leave 80% of the threads idle.
+struct Shape2 {
+  dim3 grid, block;
+};
+
+Shape2 shape2d(int64_t per_row_items, int64_t rows) {
+  int bx = (int)((per_row_items + 31) / 32 * 32);
+  if (bx > kBlock) bx = kBlock;
+  if (bx < 32) bx = 32;
+  int by = kBlock / bx;
+  if (by > rows) by = (int)rows;
+  int64_t gx = (per_row_items + bx - 1) / bx;
+  const int64_t gy = (rows + by - 1) / by;
   const int64_t cap = (int64_t)acct::sm_count() * 8;
   // keep x * y within ~8 resident CTAs per SM when rows are many
-  if (gx * rows > cap) gx = (cap + rows - 1) / rows;
+  if (gx * gy > cap) gx = (cap + gy - 1) / gy;
   if (gx < 1) gx = 1;
-  return dim3((unsigned)gx, (unsigned)rows);
+  return {dim3((unsigned)gx, (unsigned)gy), dim3((unsigned)bx, (unsigned)by)};
 }
 
 __device__ __forceinline__ float4 leaky4(float4 v) {
@@ -42,8 +55,9 @@ __device__ __forceinline__ float4 leaky4(float4 v) {
 // op: 0 fill, 1 copy, 2 bias add, 3 leaky
 template <int OP>
 __global__ void rows_vec(const float4 *__restrict__ x, int ldxv, float4 *__restrict__ y, int ldyv,
-                         int nvec, float value, const float *__restrict__ bias) {
-  const int r = blockIdx.y;
+                         int rows, int nvec, float value, const float *__restrict__ bias) {
+  const int r = blockIdx.y * blockDim.y + threadIdx.y;
+  if (r >= rows) return;
   const float b = OP == 2 ? __ldg(bias + r) : 0.0f;
   const float4 *xr = x + (int64_t)r * ldxv;
   float4 *yr = y + (int64_t)r * ldyv;
@@ -68,8 +82,9 @@ __global__ void rows_vec(const float4 *__restrict__ x, int ldxv, float4 *__restr
 
 template <int OP>
 __global__ void rows_scalar(const float *__restrict__ x, int ldx, float *__restrict__ y, int ldy,
-                            int cols, float value, const float *__restrict__ bias) {
-  const int r = blockIdx.y;
+                            int rows, int cols, float value, const float *__restrict__ bias) {
+  const int r = blockIdx.y * blockDim.y + threadIdx.y;
+  if (r >= rows) return;
   const float *xr = x + (int64_t)r * ldx;
   float *yr = y + (int64_t)r * ldy;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
@@ -84,9 +99,10 @@ __global__ void rows_scalar(const float *__restrict__ x, int ldx, float *__restr
 // blockIdx.y = col row c = (channel, kh, kw); a warp covers 128 consecutive
 // pixels of an output row band, so its input reads walk image rows.
 __global__ void im2col_kernel(const float *__restrict__ im, int64_t ld_im, int height, int width,
-                              int ksize, int stride, int pad, int out_w, int npix,
+                              int ksize, int stride, int pad, int out_w, int npix, int krows,
                               float *__restrict__ col, int64_t ld_col, bool vec) {
-  const int c = blockIdx.y;
+  const int c = blockIdx.y * blockDim.y + threadIdx.y;
+  if (c >= krows) return;
   const int kw = c % ksize, kh = (c / ksize) % ksize;
   const float *src = im + (int64_t)(c / (ksize * ksize)) * ld_im;
   float *dst_row = col + (int64_t)c * ld_col;
@@ -122,10 +138,11 @@ __global__ void im2col_kernel(const float *__restrict__ im, int64_t ld_im, int h
 
 // ---- forward_maxpool: blockIdx.y = channel, one thread per output pixel ----
 __global__ void maxpool_kernel(const float *__restrict__ in, int64_t ld_in, int height, int width,
-                               int size, int stride, int off, int out_h, int out_w,
+                               int size, int stride, int off, int out_h, int out_w, int channels,
                                float *__restrict__ out, int64_t ld_out, int32_t *__restrict__ idx,
                                int64_t ld_idx) {
-  const int c = blockIdx.y;
+  const int c = blockIdx.y * blockDim.y + threadIdx.y;
+  if (c >= channels) return;
   const float *src = in + (int64_t)c * ld_in;
   const int per = out_h * out_w;
   const int plane = height * width;
@@ -159,17 +176,19 @@ bool vec_ok(const void *p, int64_t ld, int64_t cols) {
 template <int OP>
 int launch_rows(const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t rows, int64_t cols,
                 float value, const float *bias, cudaStream_t s, const char *what) {
-  if (rows > 65535 || rows * (ldy > ldx ? ldy : ldx) >= kMaxElems)
+  if (rows > 65535 * 8 || rows * (ldy > ldx ? ldy : ldx) >= kMaxElems)
     return acct::fail(ACCT_ENOTSUP, what);
   const bool vec = vec_ok(Y, ldy, cols) && (OP != 1 || vec_ok(X, ldx, cols));
   if (vec) {
     const int nvec = (int)((cols + 3) / 4);
-    rows_vec<OP><<<grid2d(nvec, rows, kBlock), kBlock, 0, s>>>(
+    const Shape2 g = shape2d(nvec, rows);
+    rows_vec<OP><<<g.grid, g.block, 0, s>>>(
         reinterpret_cast<const float4 *>(X), (int)(ldx / 4), reinterpret_cast<float4 *>(Y),
-        (int)(ldy / 4), nvec, value, bias);
+        (int)(ldy / 4), (int)rows, nvec, value, bias);
   } else {
-    rows_scalar<OP><<<grid2d(cols, rows, kBlock), kBlock, 0, s>>>(X, (int)ldx, Y, (int)ldy,
-                                                                  (int)cols, value, bias);
+    const Shape2 g = shape2d(cols, rows);
+    rows_scalar<OP><<<g.grid, g.block, 0, s>>>(X, (int)ldx, Y, (int)ldy, (int)rows, (int)cols,
+                                               value, bias);
   }
   return acct::note_launch(what);
 }
@@ -221,8 +240,9 @@ extern "C" int acct_im2col_f32(const float *im, int64_t ld_im, int channels, int
     return fail(ACCT_ENOTSUP, "im2col: too large for 32-bit indexing");
   const bool vec = vec_ok(col, ld_col, npix);
   const int64_t nq = (npix + 3) / 4;
-  im2col_kernel<<<grid2d(nq, krows, kBlock), kBlock, 0, as_stream(stream)>>>(
-      im, ld_im, height, width, ksize, stride, pad, out_w, (int)npix, col, ld_col, vec);
+  const Shape2 g = shape2d(nq, krows);
+  im2col_kernel<<<g.grid, g.block, 0, as_stream(stream)>>>(
+      im, ld_im, height, width, ksize, stride, pad, out_w, (int)npix, (int)krows, col, ld_col, vec);
   return note_launch("im2col");
 }
 
@@ -236,7 +256,8 @@ extern "C" int acct_maxpool_f32(const float *in, int64_t ld_in, int channels, in
     return fail(ACCT_EINVAL, "maxpool: pitch too small");
   if (channels > 65535 || (int64_t)channels * ld_in >= kMaxElems)
     return fail(ACCT_ENOTSUP, "maxpool: too large for 32-bit indexing");
-  maxpool_kernel<<<grid2d(per, channels, kBlock), kBlock, 0, as_stream(stream)>>>(
-      in, ld_in, height, width, size, stride, off, out_h, out_w, out, ld_out, idx, ld_idx);
+  const Shape2 g = shape2d(per, channels);
+  maxpool_kernel<<<g.grid, g.block, 0, as_stream(stream)>>>(
+      in, ld_in, height, width, size, stride, off, out_h, out_w, channels, out, ld_out, idx, ld_idx);
   return note_launch("maxpool");
 }

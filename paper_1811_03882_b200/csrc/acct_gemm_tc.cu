@@ -24,8 +24,9 @@
 // CTA = 6 warps:
 //   warp 0      TMA producer (one elected lane), `stages`-deep ring
 //   warp 1      TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..5  hi/lo split of each landed stage (hi in place, lo to its own
-//               buffer; generic -> async proxy fence), then the epilogue:
+//   warps 2..5  hi/lo split of each landed stage (the raw value stays as hi --
+//               the MMA truncates to TF32 itself; lo to its own buffer;
+//               generic -> async proxy fence), then the epilogue:
 //               tcgen05.ld -> registers -> (normal: smem transpose) ->
 //               coalesced 128-B row stores with bias/leaky; or, under
 //               split-K, raw FP32 partials into an L2-resident workspace that
@@ -51,6 +52,13 @@ namespace {
 constexpr int BK = 32;
 constexpr int X_TILE = 128 * BK * 4;  // 16 KiB: 128 rows x 32 fp32
 constexpr int THREADS = 192;
+
+// 1: store x_hi explicitly; 0 (default): leave the raw FP32 value in place --
+// tcgen05 kind::tf32 reads only the TF32 bits of each operand (truncation),
+// measured bit-identical to the explicit x_hi on B200 (tools/tf32_trunc_check.py,
+// tests/test_gpu_kernels.py::test_tf32_operand_truncation) -- saving a third
+// of the split pass's shared-memory stores.
+int g_write_hi = 0;
 
 template <int TN>
 struct Cfg {
@@ -89,7 +97,7 @@ __device__ __forceinline__ float finish(float acc, float alpha, float beta, floa
 template <int TN, bool SWAP>
 __global__ void __launch_bounds__(THREADS, 2)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               int M, int N, int K, int kb_per_split, int stages, float alpha, float beta,
+               int M, int N, int K, int kb_per_split, int stages, int write_hi, float alpha, float beta,
                float *__restrict__ C, int64_t ldc, const float *__restrict__ bias, int act,
                float *__restrict__ ws, int64_t ws_ld, int64_t ws_split_stride) {
   using G = Cfg<TN>;
@@ -203,14 +211,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       for (int v = ct; v < X_TILE / 16; v += 128) {
         float4 lo;
         float4 hi = split_hi(xh[v], lo);
-        xh[v] = hi;
+        if (write_hi) xh[v] = hi;
         xl[v] = lo;
       }
 #pragma unroll 4
       for (int v = ct; v < G::Y_TILE / 16; v += 128) {
         float4 lo;
         float4 hi = split_hi(yh[v], lo);
-        yh[v] = hi;
+        if (write_hi) yh[v] = hi;
         yl[v] = lo;
       }
       ptx::fence_proxy_async_smem();   // generic-proxy writes -> tensor core
@@ -493,7 +501,7 @@ int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, con
   if (int rc = set_smem_attr<TN, SWAP>()) return rc;
   dim3 grid(nt, mt, splits);
   tc_gemm_kernel<TN, SWAP><<<grid, THREADS, G::smem_bytes(stages), s>>>(
-      ta, tb, M, N, K, kb_per, stages, alpha, beta, C, ldc, bias, act, ws, ws_ld, rows * ws_ld);
+      ta, tb, M, N, K, kb_per, stages, g_write_hi, alpha, beta, C, ldc, bias, act, ws, ws_ld, rows * ws_ld);
   if (int rc = note_launch("gemm_tc")) return rc;
   if (splits > 1) {
     const int64_t work = (int64_t)M * ((N + 3) / 4);
@@ -522,3 +530,5 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
 }
 
 }  // namespace acct
+
+extern "C" void acct_tc_set_write_hi(int on) { acct::g_write_hi = on ? 1 : 0; }

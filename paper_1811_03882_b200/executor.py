@@ -89,7 +89,7 @@ class RunResult:
 
 class PatternExecutor:
     def __init__(self, net: NetProgram, device=0, seed: int = 1, fuse: bool = True,
-                 gemm_mode: int = K.GEMM_AUTO, graphs: bool = True):
+                 gemm_mode: int = K.GEMM_AUTO, graphs: bool = True, first_image: int = 0):
         import torch
         self.torch = torch
         K.lib()  # fail loudly without the kernel library
@@ -143,7 +143,8 @@ class PatternExecutor:
                 self.host[spec.name].copy_(torch.from_numpy(weight_data(net, spec.name, seed).ravel()))
         xs = net.arrays[net.input_name]
         self.input_batch = torch.from_numpy(
-            input_images(net, seed, 0, self.images).reshape(self.images, -1))
+            input_images(net, seed, first_image, self.images).reshape(self.images, -1))
+        self.first_image = first_image
         if pin:
             self.input_batch = self.input_batch.pin_memory()
         ys = net.arrays[net.output_name]

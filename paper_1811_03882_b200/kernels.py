@@ -83,7 +83,7 @@ SIGNATURES = {
     "acct_graph_replay": [_vp, _vp, _i32],
 }
 VOID_FUNCS = {"acct_counters_get": [C.POINTER(Counters)], "acct_counters_reset": [],
-              "acct_graph_destroy": [_vp]}
+              "acct_graph_destroy": [_vp], "acct_tc_set_write_hi": [_i32]}
 ENOTSUP = 1002
 STRING_FUNCS = {"acct_last_error_string": [], "acct_build_info": []}
 

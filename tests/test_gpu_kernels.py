@@ -168,6 +168,26 @@ def test_gemm_fused_epilogue_equals_separate_ops(cuda_device, mode):
     assert np.array_equal(fused.numpy(), sep.numpy())
 
 
+@pytest.mark.parametrize("M,N,K_", [(128, 128, 64), (1024, 169, 4608), (16, 4096, 27)])
+def test_tf32_operand_truncation(cuda_device, M, N, K_):
+    """The tensor-core gemm leaves raw FP32 in shared memory as the TF32 hi
+    part, relying on tcgen05 kind::tf32 truncating operands; this pins that
+    hardware behaviour: results must be bit-identical to storing the
+    explicitly masked hi values."""
+    A, B = Pitched(_rand((M, K_), 61, -0.5, 0.5)), Pitched(_rand((K_, N), 62))
+    outs = []
+    try:
+        for explicit in (1, 0):
+            K.lib().acct_tc_set_write_hi(explicit)
+            Cd = Pitched(np.zeros((M, N), np.float32))
+            K.gemm_nn(M, N, K_, 1.0, A.ptr, A.ld, B.ptr, B.ld, 0.0, Cd.ptr, Cd.ld, None,
+                      K.ACT_NONE, K.GEMM_TC3XTF32, stream())
+            outs.append(Cd.numpy())
+    finally:
+        K.lib().acct_tc_set_write_hi(0)
+    assert np.array_equal(outs[0], outs[1])
+
+
 def test_kernel_launches_are_counted(cuda_device):
     K.reset_counters()
     y = Pitched(np.zeros((4, 40), np.float32))

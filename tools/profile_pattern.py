@@ -28,7 +28,27 @@ def main():
     ap.add_argument("--resident", action="store_true")
     ap.add_argument("--gemm", default="auto", choices=("auto", "simt", "tc"))
     ap.add_argument("--no-fuse", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="1 plain run, then graph capture + replays (ncu: skip the first run's "
+                         "launches); prints device ms per replay")
     args = ap.parse_args()
+    if args.graph:
+        import torch
+        mode = {"auto": K.GEMM_AUTO, "simt": K.GEMM_SIMT, "tc": K.GEMM_TC3XTF32}[args.gemm]
+        net = build_net(args.net, images=args.images)
+        ex = PatternExecutor(net, device=0, gemm_mode=mode, fuse=not args.no_fuse)
+        sched = ex.compile("1" * len(net.ops), resident=args.resident)
+        ex.run(sched)
+        for _ in range(args.runs):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ex.stream)
+            r = ex.run(sched)
+            e1.record(ex.stream)
+            e1.synchronize()
+            print(f"replay: {e0.elapsed_time(e1):.3f} ms device, {r.seconds * 1e3:.3f} ms wall, "
+                  f"{args.images} images, launches {r.counters['kernel_launches']}, "
+                  f"graph={'yes' if sched.graph is not None else 'no'}")
+        return
     mode = {"auto": K.GEMM_AUTO, "simt": K.GEMM_SIMT, "tc": K.GEMM_TC3XTF32}[args.gemm]
     net = build_net(args.net, images=args.images)
     ex = PatternExecutor(net, device=0, gemm_mode=mode, fuse=not args.no_fuse)

@@ -11,32 +11,38 @@
 // tile accumulates  X_hi.Y_hi + X_hi.Y_lo + X_lo.Y_hi  in TMEM (FP32), which
 // keeps the product within ~2^-20 relative of FP32 -- the accuracy contract
 // of darknet's FP32 gemm_nn (tests: 1e-4 scale-relative, 1e-5 normwise).
+// tcgen05 kind::tf32 truncates FP32 operands itself (measured bit-identical,
+// tests/test_gpu_kernels.py::test_tf32_operand_truncation), so the raw value
+// stays in shared memory as x_hi and only x_lo is written.
 //
 // Two tile orientations (MMA M is always 128 rows = TMEM lanes):
 //   normal  X = 128 weight rows (K-major), Y = TN in {128, 192} columns of B
-//           (MN-major).  For the wide-M layers; TN = 192 covers the 13x13
-//           layers (N = 169) with one N tile.
+//           (MN-major): the wide-M layers; TN = 192 covers the 13x13 layers
+//           (N = 169) with one N tile.
 //   swap    X = 128 columns of B (MN-major), Y = TN in {16, 32, 64} weight
-//           rows (K-major): C^T = B^T A^T for the narrow-M layers (M = 16,
-//           32, 64) so no MMA rows are wasted; TMEM lanes are output columns,
-//           so epilogue stores are coalesced without a transpose.
+//           rows (K-major): C^T = B^T A^T for the narrow-M layers (M = 16, 32,
+//           64), so no MMA rows are wasted; TMEM lanes are output columns and
+//           epilogue stores coalesce as they come.
 //
-// CTA = 6 warps:
-//   warp 0      TMA producer (one elected lane), `stages`-deep ring
-//   warp 1      TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..5  hi/lo split of each landed stage (the raw value stays as hi --
-//               the MMA truncates to TF32 itself; lo to its own buffer;
-//               generic -> async proxy fence), then the epilogue:
-//               tcgen05.ld -> registers -> (normal: smem transpose) ->
-//               coalesced 128-B row stores with bias/leaky; or, under
-//               split-K, raw FP32 partials into an L2-resident workspace that
-//               a grid-wide reduce kernel sums in split order (deterministic
-//               run to run) and finishes with the same epilogue.
-// Barriers per stage: full (TMA bytes landed), conv (split done, 4 warp
-// arrivals), empty (tcgen05.commit after the stage's 12 MMAs).
-// The pipeline depth is chosen per launch (min(max_stages, k-blocks)) and
-// the dynamic shared memory sized to it, so short-K launches (layer 0 has a
-// single k-block) fit several CTAs per SM.
+// Persistent, warp-specialized CTA (one per SM, 10 warps) looping over work
+// units (tile x K-split) round-robin:
+//   warp 0      TMA producer (one elected lane): a continuous `stages`-deep
+//               ring of k-blocks that runs across unit boundaries
+//   warp 1      TMEM allocator + MMA issuer (one elected lane); two TMEM
+//               accumulators so unit j+1 accumulates while unit j drains
+//   warps 2..5  hi/lo split of each landed stage (lo to its own buffer;
+//               generic -> async proxy fence before the release)
+//   warps 6..9  epilogue: tcgen05.ld -> registers -> (normal tiles: smem
+//               transpose) -> coalesced 128-B row stores with beta*C, bias and
+//               leaky fused; under split-K, raw FP32 partials to an L2-resident
+//               workspace summed in split order by a grid-wide kernel
+//               (deterministic run to run)
+// Barriers: per stage full (TMA bytes landed) / conv (split done, 4 warp
+// arrivals) / empty (tcgen05.commit after the stage's MMAs); per accumulator
+// acc_full (commit after a unit's last k-block) / acc_empty (4 epilogue warps).
+// BK is the k depth of one stage: 32 (128-B K-major rows, SWIZZLE_128B) or 16
+// (64-B rows, SWIZZLE_64B) so the 80-KB/stage TN=192 tile still gets a deep
+// ring.
 
 #include <cuda.h>
 
@@ -49,37 +55,45 @@
 namespace acct {
 namespace {
 
-constexpr int BK = 32;
-constexpr int X_TILE = 128 * BK * 4;  // 16 KiB: 128 rows x 32 fp32
-constexpr int THREADS = 192;
+// warps: 0 TMA, 1 MMA, 2-5 split, 6-9 and 10-13 two epilogue groups that take
+// alternate work units (one group's drain overlaps the other's)
+constexpr int EPI_GROUPS = 2;
+constexpr int THREADS = 32 * (6 + 4 * EPI_GROUPS);
+constexpr int STAGING_BYTES = EPI_GROUPS * 4 * 32 * 33 * 4;  // normal-tile epilogue transpose
 
-// 1: store x_hi explicitly; 0 (default): leave the raw FP32 value in place --
-// tcgen05 kind::tf32 reads only the TF32 bits of each operand (truncation),
-// measured bit-identical to the explicit x_hi on B200 (tools/tf32_trunc_check.py,
-// tests/test_gpu_kernels.py::test_tf32_operand_truncation) -- saving a third
-// of the split pass's shared-memory stores.
+// bit 0: store x_hi explicitly (default 0: leave the raw FP32 value in place --
+// tcgen05 kind::tf32 reads only the TF32 bits of each operand).  Bits 1-3 are
+// profiling knobs that skip the split / MMA / epilogue work (results are then
+// wrong; tools/gemm_bench.py only).
 int g_write_hi = 0;
 
-template <int TN>
+template <int TN, int BK>
 struct Cfg {
+  static constexpr int X_TILE = 128 * BK * 4;
   static constexpr int Y_TILE = TN * BK * 4;
-  static constexpr int STAGE_BYTES = 2 * X_TILE + 2 * Y_TILE;  // hi + lo of both operands
-  static constexpr int MAX_STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
-  static constexpr uint32_t TMEM_COLS = TN <= 32 ? 32 : TN <= 64 ? 64 : TN <= 128 ? 128 : 256;
-  static int smem_bytes(int stages) { return stages * STAGE_BYTES + 256 /*barriers*/ + 1024 /*align*/; }
+  static constexpr int STAGE_BYTES = 2 * X_TILE + 2 * Y_TILE;  // raw(hi) + lo of both operands
+  static constexpr int BUDGET = 220 * 1024 - STAGING_BYTES - 512 - 1024;
+  static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 512 + 1024;
+  // TMEM accumulator ring: 4 buffers when they fit in 512 columns, else 2
+  static constexpr int NACC = 4 * TN <= 512 ? 4 : 2;
+  static constexpr uint32_t TMEM_COLS = NACC * TN <= 32 ? 32 : NACC * TN <= 64 ? 64
+                                       : NACC * TN <= 128 ? 128 : NACC * TN <= 256 ? 256 : 512;
+  // K-major operand (rows x BK fp32)
+  static constexpr uint32_t KROW = BK * 4;                    // 128 or 64 bytes
+  static constexpr uint32_t K_LAYOUT = BK == 32 ? ptx::kLayoutSW128 : 4u /*SWIZZLE_64B*/;
+  static constexpr uint32_t K_SBO = 8 * KROW;                 // 8-row swizzle atom
+  // MN-major operand (BK rows x 32-column chunks)
+  static constexpr uint32_t MN_CHUNK = BK * 128;              // LBO between 32-col chunks
+  static_assert(STAGES >= 2, "tile does not fit shared memory");
 };
 
-__device__ __forceinline__ float4 split_hi(float4 v, float4 &lo) {
-  float4 h;
-  h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-  h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-  h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-  h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-  lo.x = v.x - h.x;
-  lo.y = v.y - h.y;
-  lo.z = v.z - h.z;
-  lo.w = v.w - h.w;
-  return h;
+__device__ __forceinline__ float4 split_lo(float4 v, float4 &hi) {
+  hi.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+  hi.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+  hi.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+  hi.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+  return make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
 }
 
 __device__ __forceinline__ float finish(float acc, float alpha, float beta, float c,
@@ -91,45 +105,62 @@ __device__ __forceinline__ float finish(float acc, float alpha, float beta, floa
   return v;
 }
 
-// MN-major operand: `width` columns of a K x width slab, loaded as 32-column
-// boxes (4 KiB each for BK = 32) into SW128_BASE32B layout.
-// K-major operand: `rows` x 32 fp32, one box, SW128 layout.
-template <int TN, bool SWAP>
-__global__ void __launch_bounds__(THREADS, 2)
+struct Unit {
+  int n0, m0, split, kb0, nkb;
+};
+
+template <int TN, bool SWAP, int BK>
+__device__ __forceinline__ Unit unit_of(int u, int nt, int tiles, int kb_per, int total_kb) {
+  Unit w;
+  w.split = u / tiles;
+  const int t = u - w.split * tiles;
+  const int tm = t / nt, tn = t - tm * nt;
+  w.n0 = tn * (SWAP ? 128 : TN);
+  w.m0 = tm * (SWAP ? TN : 128);
+  w.kb0 = w.split * kb_per;
+  w.nkb = min(w.kb0 + kb_per, total_kb) - w.kb0;
+  return w;
+}
+
+template <int TN, bool SWAP, int BK>
+__global__ void __launch_bounds__(THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               int M, int N, int K, int kb_per_split, int stages, int write_hi, float alpha, float beta,
-               float *__restrict__ C, int64_t ldc, const float *__restrict__ bias, int act,
-               float *__restrict__ ws, int64_t ws_ld, int64_t ws_split_stride) {
-  using G = Cfg<TN>;
+               int M, int N, int K, int nt, int mt, int splits, int kb_per, int write_hi,
+               float alpha, float beta, float *__restrict__ C, int64_t ldc,
+               const float *__restrict__ bias, int act, float *__restrict__ ws, int64_t ws_ld,
+               int64_t ws_split_stride) {
+  using G = Cfg<TN, BK>;
+  constexpr int S = G::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
   auto x_hi = [&](int s) { return base + s * G::STAGE_BYTES; };
-  auto x_lo = [&](int s) { return base + s * G::STAGE_BYTES + X_TILE; };
-  auto y_hi = [&](int s) { return base + s * G::STAGE_BYTES + 2 * X_TILE; };
-  auto y_lo = [&](int s) { return base + s * G::STAGE_BYTES + 2 * X_TILE + G::Y_TILE; };
-  uint64_t *full = reinterpret_cast<uint64_t *>(base + stages * G::STAGE_BYTES);
-  uint64_t *conv = full + stages;
-  uint64_t *empty = conv + stages;
-  uint64_t *tmem_full = empty + stages;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+  auto x_lo = [&](int s) { return base + s * G::STAGE_BYTES + G::X_TILE; };
+  auto y_hi = [&](int s) { return base + s * G::STAGE_BYTES + 2 * G::X_TILE; };
+  auto y_lo = [&](int s) { return base + s * G::STAGE_BYTES + 2 * G::X_TILE + G::Y_TILE; };
+  float *staging = reinterpret_cast<float *>(base + S * G::STAGE_BYTES);
+  uint64_t *full = reinterpret_cast<uint64_t *>(base + S * G::STAGE_BYTES + STAGING_BYTES);
+  uint64_t *conv = full + S;
+  uint64_t *empty = conv + S;
+  constexpr int NACC = G::NACC;
+  uint64_t *acc_full = empty + S;
+  uint64_t *acc_empty = acc_full + NACC;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + NACC);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // n0: first output column of the tile, m0: first output row
-  const int n0 = blockIdx.x * (SWAP ? 128 : TN);
-  const int m0 = blockIdx.y * (SWAP ? TN : 128);
-  const int splits = gridDim.z, split = blockIdx.z;
+  const int tiles = nt * mt, units = tiles * splits;
   const int total_kb = (K + BK - 1) / BK;
-  const int kb0 = split * kb_per_split;
-  const int nkb = max(0, min(kb0 + kb_per_split, total_kb) - kb0);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) {
+    for (int s = 0; s < S; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&conv[s], 4);
       ptx::mbar_init(&empty[s], 1);
     }
-    ptx::mbar_init(tmem_full, 1);
+    for (int a = 0; a < NACC; ++a) {
+      ptx::mbar_init(&acc_full[a], 1);
+      ptx::mbar_init(&acc_empty[a], 4);
+    }
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
@@ -143,21 +174,25 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % stages;
-        if (i >= stages) ptx::mbar_wait(&empty[s], ((i / stages) - 1) & 1);
-        ptx::mbar_expect_tx(&full[s], X_TILE + G::Y_TILE);
-        const int kx = (kb0 + i) * BK;
-        if (!SWAP) {
-          ptx::tma_load_2d(x_hi(s), &tmA, &full[s], kx, m0);
+      int g = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit w = unit_of<TN, SWAP, BK>(u, nt, tiles, kb_per, total_kb);
+        for (int kb = 0; kb < w.nkb; ++kb, ++g) {
+          const int s = g % S;
+          if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
+          ptx::mbar_expect_tx(&full[s], G::X_TILE + G::Y_TILE);
+          const int kx = (w.kb0 + kb) * BK;
+          if (!SWAP) {
+            ptx::tma_load_2d(x_hi(s), &tmA, &full[s], kx, w.m0);
 #pragma unroll
-          for (int c = 0; c < TN / 32; ++c)
-            ptx::tma_load_2d(y_hi(s) + c * (BK * 128), &tmB, &full[s], n0 + 32 * c, kx);
-        } else {
+            for (int c = 0; c < TN / 32; ++c)
+              ptx::tma_load_2d(y_hi(s) + c * G::MN_CHUNK, &tmB, &full[s], w.n0 + 32 * c, kx);
+          } else {
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            ptx::tma_load_2d(x_hi(s) + c * (BK * 128), &tmB, &full[s], n0 + 32 * c, kx);
-          ptx::tma_load_2d(y_hi(s), &tmA, &full[s], kx, m0);
+            for (int c = 0; c < 4; ++c)
+              ptx::tma_load_2d(x_hi(s) + c * G::MN_CHUNK, &tmB, &full[s], w.n0 + 32 * c, kx);
+            ptx::tma_load_2d(y_hi(s), &tmA, &full[s], kx, w.m0);
+          }
         }
       }
     }
@@ -165,152 +200,166 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_tf32(128, TN, SWAP, !SWAP);
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % stages;
-        ptx::mbar_wait(&conv[s], (i / stages) & 1);
+      int g = 0, j = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+        const Unit w = unit_of<TN, SWAP, BK>(u, nt, tiles, kb_per, total_kb);
+        const int a = j % NACC;
+        if (j >= NACC) ptx::mbar_wait(&acc_empty[a], ((j / NACC) - 1) & 1);
         ptx::tc_fence_after();
-        const uint32_t xh = ptx::smem_u32(x_hi(s)), xl = ptx::smem_u32(x_lo(s));
-        const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
+        const uint32_t d = tmem + a * TN;
+        for (int kb = 0; kb < w.nkb; ++kb, ++g) {
+          const int s = g % S;
+          ptx::mbar_wait(&conv[s], (g / S) & 1);
+          ptx::tc_fence_after();
+          const uint32_t xh = ptx::smem_u32(x_hi(s)), xl = ptx::smem_u32(x_lo(s));
+          const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
 #pragma unroll
-        for (int k = 0; k < BK / 8; ++k) {
-          // K-major SW128: 8 tf32 (32 B) per step inside the 128-B rows.
-          // MN-major SW128_BASE32B: 8 k-rows (two 512-B atoms) per step,
-          // 32-column chunks BK*128 B apart (LBO).
-          uint64_t dxh, dxl, dyh, dyl;
-          if (!SWAP) {
-            dxh = ptx::smem_desc(xh + 32 * k, 16, 1024, ptx::kLayoutSW128);
-            dxl = ptx::smem_desc(xl + 32 * k, 16, 1024, ptx::kLayoutSW128);
-            dyh = ptx::smem_desc(yh + 1024 * k, BK * 128, 512, ptx::kLayoutSW128Base32B);
-            dyl = ptx::smem_desc(yl + 1024 * k, BK * 128, 512, ptx::kLayoutSW128Base32B);
-          } else {
-            dxh = ptx::smem_desc(xh + 1024 * k, BK * 128, 512, ptx::kLayoutSW128Base32B);
-            dxl = ptx::smem_desc(xl + 1024 * k, BK * 128, 512, ptx::kLayoutSW128Base32B);
-            dyh = ptx::smem_desc(yh + 32 * k, 16, 1024, ptx::kLayoutSW128);
-            dyl = ptx::smem_desc(yl + 32 * k, 16, 1024, ptx::kLayoutSW128);
+          for (int k = 0; k < BK / 8; ++k) {
+            // K-major: 8 tf32 (32 B) per step inside a row; MN-major
+            // SW128_BASE32B: 8 k-rows (two 512-B atoms) per step
+            uint64_t dxh, dxl, dyh, dyl;
+            if (!SWAP) {
+              dxh = ptx::smem_desc(xh + 32 * k, 16, G::K_SBO, G::K_LAYOUT);
+              dxl = ptx::smem_desc(xl + 32 * k, 16, G::K_SBO, G::K_LAYOUT);
+              dyh = ptx::smem_desc(yh + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
+              dyl = ptx::smem_desc(yl + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
+            } else {
+              dxh = ptx::smem_desc(xh + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
+              dxl = ptx::smem_desc(xl + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
+              dyh = ptx::smem_desc(yh + 32 * k, 16, G::K_SBO, G::K_LAYOUT);
+              dyl = ptx::smem_desc(yl + 32 * k, 16, G::K_SBO, G::K_LAYOUT);
+            }
+            if (write_hi & 4) continue;
+            ptx::mma_tf32(d, dxh, dyh, idesc, (kb | k) != 0);
+            ptx::mma_tf32(d, dxh, dyl, idesc, 1);
+            ptx::mma_tf32(d, dxl, dyh, idesc, 1);
           }
-          ptx::mma_tf32(tmem, dxh, dyh, idesc, (i | k) != 0);
-          ptx::mma_tf32(tmem, dxh, dyl, idesc, 1);
-          ptx::mma_tf32(tmem, dxl, dyh, idesc, 1);
+          ptx::mma_commit(&empty[s]);
         }
-        ptx::mma_commit(&empty[s]);
+        ptx::mma_commit(&acc_full[a]);
       }
-      ptx::mma_commit(tmem_full);
     }
     __syncwarp();
-  } else {
+  } else if (warp < 6) {
     // ---------------- split hi/lo of each landed stage ----------------
     const int ct = threadIdx.x - 64;  // 0..127
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % stages;
-      ptx::mbar_wait(&full[s], (i / stages) & 1);
-      float4 *xh = reinterpret_cast<float4 *>(x_hi(s));
-      float4 *xl = reinterpret_cast<float4 *>(x_lo(s));
-      float4 *yh = reinterpret_cast<float4 *>(y_hi(s));
-      float4 *yl = reinterpret_cast<float4 *>(y_lo(s));
+    int g = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit w = unit_of<TN, SWAP, BK>(u, nt, tiles, kb_per, total_kb);
+      for (int kb = 0; kb < w.nkb; ++kb, ++g) {
+        const int s = g % S;
+        ptx::mbar_wait(&full[s], (g / S) & 1);
+        float4 *xh = reinterpret_cast<float4 *>(x_hi(s));
+        float4 *xl = reinterpret_cast<float4 *>(x_lo(s));
+        float4 *yh = reinterpret_cast<float4 *>(y_hi(s));
+        float4 *yl = reinterpret_cast<float4 *>(y_lo(s));
+        if (!(write_hi & 2)) {
 #pragma unroll 4
-      for (int v = ct; v < X_TILE / 16; v += 128) {
-        float4 lo;
-        float4 hi = split_hi(xh[v], lo);
-        if (write_hi) xh[v] = hi;
-        xl[v] = lo;
-      }
+          for (int v = ct; v < G::X_TILE / 16; v += 128) {
+            float4 hi;
+            xl[v] = split_lo(xh[v], hi);
+            if (write_hi & 1) xh[v] = hi;
+          }
 #pragma unroll 4
-      for (int v = ct; v < G::Y_TILE / 16; v += 128) {
-        float4 lo;
-        float4 hi = split_hi(yh[v], lo);
-        if (write_hi) yh[v] = hi;
-        yl[v] = lo;
+          for (int v = ct; v < G::Y_TILE / 16; v += 128) {
+            float4 hi;
+            yl[v] = split_lo(yh[v], hi);
+            if (write_hi & 1) yh[v] = hi;
+          }
+        }
+        ptx::fence_proxy_async_smem();  // generic-proxy writes -> tensor core
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&conv[s]);
       }
-      ptx::fence_proxy_async_smem();   // generic-proxy writes -> tensor core
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&conv[s]);
     }
-
+  } else {
     // ---------------- epilogue ----------------
     const int q = warp & 3;  // this warp may read TMEM lanes 32q..32q+31
-    if (nkb > 0) {
-      ptx::mbar_wait(tmem_full, 0);
+    const int grp = (warp - 6) / 4;
+    float *stg = staging + (grp * 4 + q) * (32 * 33);
+    int j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      if ((j % EPI_GROUPS) != grp) continue;
+      const Unit w = unit_of<TN, SWAP, BK>(u, nt, tiles, kb_per, total_kb);
+      const int a = j % NACC;
+      ptx::mbar_wait(&acc_full[a], (j / NACC) & 1);
       ptx::tc_fence_after();
-    }
-    const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
-    if (!SWAP) {
-      // lanes = output rows: transpose each 32x32 chunk through smem so that
-      // lane = column and each store writes a contiguous 128-B row segment
-      float *stg = reinterpret_cast<float *>(x_lo(0)) + q * (32 * 33);  // free: MMAs done
-      const int row0 = m0 + 32 * q;
-      for (int c = 0; c < TN / 32; ++c) {
-        uint32_t r[32];
-        if (nkb > 0) {
+      const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * TN;
+      float *part = ws + w.split * ws_split_stride;
+      if (write_hi & 8) {
+        // debug: skip the epilogue body
+      } else if (!SWAP) {
+        // lanes = output rows: transpose each 32x32 chunk through smem so that
+        // lane = column and each store writes a contiguous 128-B row segment
+        const int row0 = w.m0 + 32 * q;
+        for (int c = 0; c < TN / 32; ++c) {
+          uint32_t r[32];
           ptx::tmem_ld_32x32b_x32(trow + 32 * c, r);
-        } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = 0u;
-        }
+          for (int jj = 0; jj < 32; ++jj) stg[lane * 33 + jj] = __uint_as_float(r[jj]);
+          __syncwarp();
+          const int col = w.n0 + 32 * c + lane;
+          if (splits == 1) {
+            // bias of row row0+i is loaded once by lane i, then broadcast
+            const float my_bias = (bias && row0 + lane < M) ? __ldg(bias + row0 + lane) : 0.0f;
+            float bv[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = __uint_as_float(r[j]);
-        __syncwarp();
-        const int col = n0 + 32 * c + lane;
-        if (splits == 1) {
-          if (col < N) {
-            float cv[32];
+            for (int i = 0; i < 32; ++i) bv[i] = __shfl_sync(0xffffffffu, my_bias, i);
+            if (col < N) {
+              float cv[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i)  // all C loads in flight before any store
-              cv[i] = (beta != 0.0f && row0 + i < M) ? C[(int64_t)(row0 + i) * ldc + col] : 0.0f;
+              for (int i = 0; i < 32; ++i)  // all C loads in flight before any store
+                cv[i] = (beta != 0.0f && row0 + i < M) ? C[(int64_t)(row0 + i) * ldc + col] : 0.0f;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const int row = row0 + i;
-              if (row < M)
-                C[(int64_t)row * ldc + col] = finish(stg[i * 33 + lane], alpha, beta, cv[i], bias,
-                                                     bias ? __ldg(bias + row) : 0.0f, act);
+              for (int i = 0; i < 32; ++i) {
+                const int row = row0 + i;
+                if (row < M)
+                  C[(int64_t)row * ldc + col] = finish(stg[i * 33 + lane], alpha, beta, cv[i],
+                                                       bias, bv[i], act);
+              }
             }
-          }
-        } else {
-          float *dst = ws + split * ws_split_stride + (int64_t)row0 * ws_ld + col;
-#pragma unroll 8
-          for (int i = 0; i < 32; ++i) __stcg(dst + (int64_t)i * ws_ld, stg[i * 33 + lane]);
-        }
-        __syncwarp();
-      }
-    } else {
-      // lanes = output columns, TMEM columns = output rows: stores are
-      // coalesced across the warp as they come
-      const int col = n0 + 32 * q + lane;
-      constexpr int CH = TN < 32 ? TN : 32;
-      for (int c = 0; c < TN / CH; ++c) {
-        uint32_t r[32];
-        if (nkb > 0) {
-          if constexpr (CH == 16) {
-            uint32_t r16[16];
-            ptx::tmem_ld_32x32b_x16(trow + 16 * c, r16);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) r[j] = r16[j];
           } else {
-            ptx::tmem_ld_32x32b_x32(trow + 32 * c, r);
+            float *dst = part + (int64_t)row0 * ws_ld + col;
+#pragma unroll 8
+            for (int i = 0; i < 32; ++i) __stcg(dst + (int64_t)i * ws_ld, stg[i * 33 + lane]);
           }
-        } else {
-#pragma unroll
-          for (int j = 0; j < CH; ++j) r[j] = 0u;
+          __syncwarp();
         }
-        if (col >= N) continue;
-        const int rbase = m0 + CH * c;
-        if (splits == 1) {
-          float cv[CH];
+      } else {
+        // lanes = output columns, TMEM columns = output rows
+        const int col = w.n0 + 32 * q + lane;
+        constexpr int CH = 16;  // 16 rows per TMEM load keeps the epilogue in registers
+        for (int c = 0; c < TN / CH; ++c) {
+          uint32_t r[CH];
+          ptx::tmem_ld_32x32b_x16(trow + CH * c, r);
+          if (col >= N) continue;
+          const int rbase = w.m0 + CH * c;
+          if (splits == 1) {
+            float cv[CH], bv[CH];
 #pragma unroll
-          for (int j = 0; j < CH; ++j)
-            cv[j] = (beta != 0.0f && rbase + j < M) ? C[(int64_t)(rbase + j) * ldc + col] : 0.0f;
+            for (int jj = 0; jj < CH; ++jj) {  // every load in flight before any store
+              const bool ok = rbase + jj < M;
+              cv[jj] = (beta != 0.0f && ok) ? C[(int64_t)(rbase + jj) * ldc + col] : 0.0f;
+              bv[jj] = (bias && ok) ? __ldg(bias + rbase + jj) : 0.0f;
+            }
 #pragma unroll
-          for (int j = 0; j < CH; ++j) {
-            const int row = rbase + j;
-            if (row < M)
-              C[(int64_t)row * ldc + col] = finish(__uint_as_float(r[j]), alpha, beta, cv[j], bias,
-                                                   bias ? __ldg(bias + row) : 0.0f, act);
+            for (int jj = 0; jj < CH; ++jj) {
+              const int row = rbase + jj;
+              if (row < M)
+                C[(int64_t)row * ldc + col] = finish(__uint_as_float(r[jj]), alpha, beta, cv[jj],
+                                                     bias, bv[jj], act);
+            }
+          } else {
+            float *dst = part + (int64_t)rbase * ws_ld + col;
+#pragma unroll
+            for (int jj = 0; jj < CH; ++jj) __stcg(dst + (int64_t)jj * ws_ld, __uint_as_float(r[jj]));
           }
-        } else {
-          float *dst = ws + split * ws_split_stride + (int64_t)rbase * ws_ld + col;
-#pragma unroll
-          for (int j = 0; j < CH; ++j) __stcg(dst + (int64_t)j * ws_ld, __uint_as_float(r[j]));
         }
       }
+      // accumulator a may be overwritten once all four warps have read it
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&acc_empty[a]);
     }
   }
 
@@ -373,14 +422,14 @@ EncodeTiledFn encode_fn() {
 }
 
 // 2-D fp32 tensor map: inner dim `inner` (contiguous), outer dim `outer` with
-// row pitch `ld` elements; box = 32 x box_outer; out-of-bounds reads are 0.
+// row pitch `ld` elements; box = box_inner x box_outer; out-of-bounds reads are 0.
 bool make_map(CUtensorMap *map, const float *ptr, uint64_t inner, uint64_t outer, uint64_t ld,
-              uint32_t box_outer, CUtensorMapSwizzle swizzle) {
+              uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swizzle) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {ld * 4};
-  cuuint32_t box[2] = {32, box_outer};
+  cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides, box,
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -393,10 +442,10 @@ bool make_map(CUtensorMap *map, const float *ptr, uint64_t inner, uint64_t outer
 struct MapKey {
   const void *ptr;
   uint64_t inner, outer, ld;
-  uint32_t box, swz;
+  uint32_t box, box_in, swz;
   bool operator==(const MapKey &o) const {
     return ptr == o.ptr && inner == o.inner && outer == o.outer && ld == o.ld && box == o.box &&
-           swz == o.swz;
+           box_in == o.box_in && swz == o.swz;
   }
 };
 struct MapKeyHash {
@@ -404,21 +453,22 @@ struct MapKeyHash {
     uint64_t h = reinterpret_cast<uint64_t>(k.ptr) * 0x9E3779B97F4A7C15ull;
     h ^= k.inner + 0x9E37 + (h << 6) + (h >> 2);
     h ^= k.outer + 0x7F4A + (h << 6) + (h >> 2);
-    h ^= k.ld + ((uint64_t)k.box << 32) + ((uint64_t)k.swz << 48) + (h << 6) + (h >> 2);
+    h ^= k.ld + ((uint64_t)k.box << 32) + ((uint64_t)k.swz << 48) + ((uint64_t)k.box_in << 56) +
+         (h << 6) + (h >> 2);
     return (size_t)h;
   }
 };
 
 bool cached_map(CUtensorMap *map, const float *ptr, uint64_t inner, uint64_t outer, uint64_t ld,
-                uint32_t box_outer, CUtensorMapSwizzle swizzle) {
+                uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swizzle) {
   static thread_local std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-  MapKey key{ptr, inner, outer, ld, box_outer, (uint32_t)swizzle};
+  MapKey key{ptr, inner, outer, ld, box_outer, box_inner, (uint32_t)swizzle};
   auto it = cache.find(key);
   if (it != cache.end()) {
     *map = it->second;
     return true;
   }
-  if (!make_map(map, ptr, inner, outer, ld, box_outer, swizzle)) return false;
+  if (!make_map(map, ptr, inner, outer, ld, box_inner, box_outer, swizzle)) return false;
   if (cache.size() > 4096) cache.clear();
   cache.emplace(key, *map);
   return true;
@@ -446,18 +496,18 @@ int scratch_for(cudaStream_t s, size_t floats, float **out) {
   return ACCT_OK;
 }
 
-template <int TN, bool SWAP>
+template <int TN, bool SWAP, int BK>
 int set_smem_attr() {
-  // the attribute is per device context; set the maximum once
+  // the attribute is per device context
   static std::mutex mu;
   static bool done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
   if (dev >= 0 && dev < 64 && !done[dev]) {
-    if (int rc = check_cuda(cudaFuncSetAttribute(tc_gemm_kernel<TN, SWAP>,
+    if (int rc = check_cuda(cudaFuncSetAttribute(tc_gemm_kernel<TN, SWAP, BK>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 Cfg<TN>::smem_bytes(Cfg<TN>::MAX_STAGES)),
+                                                 Cfg<TN, BK>::SMEM_BYTES),
                             "gemm_tc: smem attribute"))
       return rc;
     done[dev] = true;
@@ -465,24 +515,24 @@ int set_smem_attr() {
   return ACCT_OK;
 }
 
-template <int TN, bool SWAP>
+template <int TN, bool SWAP, int BK>
 int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
               int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
               cudaStream_t s) {
-  using G = Cfg<TN>;
+  using G = Cfg<TN, BK>;
   CUtensorMap ta, tb;
-  // weights: K-major box of (32 k) x (rows of the weight-side tile)
-  const uint32_t a_rows = SWAP ? TN : 128;
-  if (!cached_map(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, a_rows, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !cached_map(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, BK,
+  const uint32_t a_rows = SWAP ? TN : 128;  // weights: K-major box (BK k) x rows
+  const CUtensorMapSwizzle kswz = BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  if (!cached_map(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BK, a_rows, kswz) ||
+      !cached_map(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, 32, BK,
                   CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
     return fail(ACCT_ENOTSUP, "gemm_tc: cuTensorMapEncodeTiled failed");
   const int tile_n = SWAP ? 128 : TN, tile_m = SWAP ? TN : 128;
   const int nt = (N + tile_n - 1) / tile_n, mt = (M + tile_m - 1) / tile_m, tiles = mt * nt;
   const int total_kb = (K + BK - 1) / BK;
   const int sms = sm_count();
-  // fill one wave: split K until tiles x splits covers the SMs, keeping >= 2
-  // k-blocks per split so the pipeline has something to overlap
+  // fill the machine: split K until tiles x splits covers the SMs, keeping
+  // >= 2 k-blocks per split so the pipeline has something to overlap
   int splits = 1;
   if (tiles < sms) {
     splits = sms / tiles;
@@ -491,17 +541,18 @@ int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, con
   }
   const int kb_per = (total_kb + splits - 1) / splits;
   splits = (total_kb + kb_per - 1) / kb_per;
-  const int stages = kb_per < G::MAX_STAGES ? kb_per : G::MAX_STAGES;
+  const int units = tiles * splits;
 
   float *ws = nullptr;
   const int64_t ws_ld = (int64_t)nt * tile_n, rows = (int64_t)mt * tile_m;
   if (splits > 1) {
     if (int rc = scratch_for(s, (size_t)splits * rows * ws_ld, &ws)) return rc;
   }
-  if (int rc = set_smem_attr<TN, SWAP>()) return rc;
-  dim3 grid(nt, mt, splits);
-  tc_gemm_kernel<TN, SWAP><<<grid, THREADS, G::smem_bytes(stages), s>>>(
-      ta, tb, M, N, K, kb_per, stages, g_write_hi, alpha, beta, C, ldc, bias, act, ws, ws_ld, rows * ws_ld);
+  if (int rc = set_smem_attr<TN, SWAP, BK>()) return rc;
+  const int grid = units < sms ? units : sms;
+  tc_gemm_kernel<TN, SWAP, BK><<<grid, THREADS, G::SMEM_BYTES, s>>>(
+      ta, tb, M, N, K, nt, mt, splits, kb_per, g_write_hi, alpha, beta, C, ldc, bias, act, ws,
+      ws_ld, rows * ws_ld);
   if (int rc = note_launch("gemm_tc")) return rc;
   if (splits > 1) {
     const int64_t work = (int64_t)M * ((N + 3) / 4);
@@ -521,14 +572,14 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
   if (M < 1 || N < 1 || K < 1 || (lda % 4) || (ldb % 4) ||
       (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
     return ACCT_ENOTSUP;
-  if (M <= 16) return launch_tc<16, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
-  if (M <= 32) return launch_tc<32, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
-  if (M <= 64) return launch_tc<64, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (M <= 16) return launch_tc<16, true, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (M <= 32) return launch_tc<32, true, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (M <= 64) return launch_tc<64, true, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (N > 128 && N <= 192)
-    return launch_tc<192, false>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
-  return launch_tc<128, false>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+    return launch_tc<192, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  return launch_tc<128, false, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
 }
 
 }  // namespace acct
 
-extern "C" void acct_tc_set_write_hi(int on) { acct::g_write_hi = on ? 1 : 0; }
+extern "C" void acct_tc_set_write_hi(int on) { acct::g_write_hi = on; }

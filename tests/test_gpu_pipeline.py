@@ -1,0 +1,63 @@
+"""End to end through the reference-facing entry points with the gpu:
+evaluator (B200 only): `tune` CLI on the demo net (BASELINE configs[0]:
+pop 4 x 2 gens), the GA over a device pool, and the report's gpu section."""
+
+from __future__ import annotations
+
+import json
+
+import pytest
+
+import paper_1811_03882_b200 as at
+from paper_1811_03882_b200 import cli
+from paper_1811_03882_b200.nets import write_net_files
+
+pytestmark = pytest.mark.gpu
+
+
+def test_tune_cli_with_gpu_evaluator(cuda_device, tmp_path):
+    paths = write_net_files("demo", tmp_path)
+    code = cli.main(["tune", "--source", str(paths["source"]), "--profile",
+                     str(paths["profile"]), "--evaluator", f"gpu:{paths['gpu_config']}",
+                     "--pop", "4", "--gens", "2", "--seed", "1", "--out",
+                     str(tmp_path / "best.c"), "--report", str(tmp_path / "report.json")])
+    assert code == 0
+    report = json.loads((tmp_path / "report.json").read_text())
+    assert report["result"] == "ok"
+    assert report["best"]["status"] == "measured" and report["best"]["seconds"] > 0
+    gpu = report["gpu"]
+    for key, val in gpu["expected_transfers"].items():
+        assert gpu["transfers"][key] == val
+    annotated = (tmp_path / "best.c").read_text()
+    assert at.strip_annotations(at.AnnotatedSource(annotated, ())) is not None
+    assert "#pragma acc" in annotated or set(report["best"]["genome"]) == {"0"}
+
+
+def test_gpu_evaluator_rejects_foreign_source(cuda_device, tmp_path):
+    paths = write_net_files("demo", tmp_path)
+    program = at.parse("int main(){int i; float a[10]; for(i=0;i<10;i++){ a[i] = 1.0; }}")
+    tree = at.build_loop_tree(program)
+    acc = at.extract_accesses(program)
+    gm = at.build_genome_map(at.check_all_parallelizable(tree, acc))
+    with pytest.raises(at.ModelError):
+        at.build_evaluator(f"gpu:{paths['gpu_config']}", program, tree, acc, gm, None,
+                           at.GAConfig())
+
+
+def test_ga_over_gpu_pool_finds_faster_than_all_cpu(cuda_device, tmp_path):
+    from paper_1811_03882_b200.gpu_evaluator import GpuEvaluatorConfig, make_gpu_evaluator
+    from paper_1811_03882_b200.legality import profile_from_dict
+    from paper_1811_03882_b200.nets import build_net
+    net = build_net("demo")
+    prog = at.parse(net.source)
+    tree = at.build_loop_tree(prog)
+    acc = at.extract_accesses(prog)
+    gm = at.build_genome_map(at.check_all_parallelizable(tree, acc))
+    prof = profile_from_dict(net.profile_dict(), "demo", tree)
+    ev = make_gpu_evaluator(GpuEvaluatorConfig(net="demo", devices="all"), prog, tree, acc, gm,
+                            prof)
+    res = at.run_ga(at.GAConfig(population=6, generations=3, rng_seed=2,
+                                workers=len(ev.pool.devices)), gm, tree, ev)
+    all_cpu = ev("0" * len(gm)).seconds
+    assert res.best.status == "measured"
+    assert res.best.seconds <= all_cpu * 1.5

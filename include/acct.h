@@ -160,7 +160,15 @@ typedef struct {
   void *dev;           /* device buffer (rows x ld x 4 bytes) */
   int64_t rows, cols;  /* logical 2-D shape (1-D arrays: rows = 1) */
   int64_t ld_dev;      /* device row pitch in elements */
+  void *stage;         /* optional dense device staging buffer (>= rows x cols x 4
+                          bytes) for padded arrays: H2D is then one dense copy plus
+                          a repack kernel instead of a slow short-row 2-D copy */
 } acct_array_t;
+
+/* H2D of a padded array through a dense staging buffer: one contiguous copy
+ * (counted as one h2d call) + a repack kernel into the pitched layout.      */
+int acct_h2d_staged(void *dev, int64_t ld, const void *host, int64_t rows, int64_t cols,
+                    void *stage, acct_stream_t stream);
 
 typedef struct {
   int32_t kind;        /* ACCT_A_* */

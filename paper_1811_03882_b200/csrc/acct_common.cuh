@@ -18,7 +18,7 @@ void set_error(const std::string &msg);
 int fail(int code, const char *what);
 int check_cuda(cudaError_t err, const char *what);
 
-// ---- process-wide counters (atomics; the library has no other globals) ----
+// ---- per-thread counters (one host thread drives one device) ----
 struct Counters {
   std::atomic<int64_t> directive_execs{0}, var_transfers{0};
   std::atomic<int64_t> h2d_calls{0}, d2h_calls{0}, h2d_bytes{0}, d2h_bytes{0};
@@ -44,7 +44,35 @@ inline unsigned grid_for(int64_t work, int block, int per_sm = 8) {
 
 inline cudaStream_t as_stream(acct_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Programmatic dependent launch.  Every kernel of the library is launched
+// with programmaticStreamSerializationAllowed (so inside a CUDA graph the
+// next kernel's CTAs may be scheduled, and run their prologue, while this one
+// drains) and calls pdl_wait() before touching any global data a previous
+// kernel produced or may still read.  The attribute is opt-in (ACCT_PDL=1).
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                   Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 }  // namespace acct
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // leaky as darknet computes it: `.1*x` is a double product rounded to float
 __host__ __device__ __forceinline__ float acct_leaky(float v) {

@@ -56,6 +56,8 @@ __device__ __forceinline__ float4 leaky4(float4 v) {
 template <int OP>
 __global__ void rows_vec(const float4 *__restrict__ x, int ldxv, float4 *__restrict__ y, int ldyv,
                          int rows, int nvec, float value, const float *__restrict__ bias) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.y * blockDim.y + threadIdx.y;
   if (r >= rows) return;
   const float b = OP == 2 ? __ldg(bias + r) : 0.0f;
@@ -83,6 +85,8 @@ __global__ void rows_vec(const float4 *__restrict__ x, int ldxv, float4 *__restr
 template <int OP>
 __global__ void rows_scalar(const float *__restrict__ x, int ldx, float *__restrict__ y, int ldy,
                             int rows, int cols, float value, const float *__restrict__ bias) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.y * blockDim.y + threadIdx.y;
   if (r >= rows) return;
   const float *xr = x + (int64_t)r * ldx;
@@ -101,6 +105,8 @@ __global__ void rows_scalar(const float *__restrict__ x, int ldx, float *__restr
 __global__ void im2col_kernel(const float *__restrict__ im, int64_t ld_im, int height, int width,
                               int ksize, int stride, int pad, int out_w, int npix, int krows,
                               float *__restrict__ col, int64_t ld_col, bool vec) {
+  pdl_trigger();
+  pdl_wait();
   const int c = blockIdx.y * blockDim.y + threadIdx.y;
   if (c >= krows) return;
   const int kw = c % ksize, kh = (c / ksize) % ksize;
@@ -141,6 +147,8 @@ __global__ void maxpool_kernel(const float *__restrict__ in, int64_t ld_in, int 
                                int size, int stride, int off, int out_h, int out_w, int channels,
                                float *__restrict__ out, int64_t ld_out, int32_t *__restrict__ idx,
                                int64_t ld_idx) {
+  pdl_trigger();
+  pdl_wait();
   const int c = blockIdx.y * blockDim.y + threadIdx.y;
   if (c >= channels) return;
   const float *src = in + (int64_t)c * ld_in;
@@ -169,6 +177,119 @@ __global__ void maxpool_kernel(const float *__restrict__ in, int64_t ld_in, int 
   }
 }
 
+// ---- wide planes: 3-D grid (w-quads x output rows x col rows), no division ----
+// blockIdx.z = col row c, threadIdx.y/blockIdx.y = output row h, each thread 4
+// consecutive output pixels of that row: one input row, float4 store.
+__global__ void im2col_rows_kernel(const float *__restrict__ im, int64_t ld_im, int height,
+                                   int width, int ksize, int stride, int pad, int out_h, int out_w,
+                                   float *__restrict__ col, int64_t ld_col, bool vec) {
+  pdl_trigger();
+  pdl_wait();
+  const int c = blockIdx.z;
+  const int h = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h >= out_h) return;
+  const int kw = c % ksize, kh = (c / ksize) % ksize;
+  const int row = kh + h * stride - pad;
+  const bool row_ok = row >= 0 && row < height;
+  const float *srow = im + (int64_t)(c / (ksize * ksize)) * ld_im + (int64_t)row * width;
+  float *dst = col + (int64_t)c * ld_col + (int64_t)h * out_w;
+  for (int w0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4; w0 < out_w;
+       w0 += gridDim.x * blockDim.x * 4) {
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int cc = kw + (w0 + e) * stride - pad;
+      v[e] = (row_ok && cc >= 0 && cc < width && w0 + e < out_w) ? __ldg(srow + cc) : 0.0f;
+    }
+    if (vec) {
+      __stcs(reinterpret_cast<float4 *>(dst + w0), make_float4(v[0], v[1], v[2], v[3]));
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (w0 + e < out_w) dst[w0 + e] = v[e];
+    }
+  }
+}
+
+// ---- 3x3 / stride 1 / pad 1 (every 3x3 conv of the three nets) ----
+// blockIdx.z = input channel; a thread owns 4 consecutive output pixels of
+// one output row, loads the 3 x 6 input window once and writes the 9 col rows
+// (kh, kw) of that channel: 9 float4 stores per 18 loads.
+__global__ void im2col_k3s1_kernel(const float *__restrict__ im, int64_t ld_im, int height,
+                                   int width, int out_h, int out_w, float *__restrict__ col,
+                                   int64_t ld_col, bool vec) {
+  pdl_trigger();
+  pdl_wait();
+  const int ci = blockIdx.z;
+  const int h = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h >= out_h) return;
+  const float *src = im + (int64_t)ci * ld_im;
+  float *dst0 = col + (int64_t)(ci * 9) * ld_col + (int64_t)h * out_w;
+  for (int w0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4; w0 < out_w;
+       w0 += gridDim.x * blockDim.x * 4) {
+    float win[3][6];
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh) {
+      const int r = h + kh - 1;
+      const bool rok = r >= 0 && r < height;
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        const int cc = w0 + t - 1;
+        win[kh][t] = (rok && cc >= 0 && cc < width) ? __ldg(src + r * width + cc) : 0.0f;
+      }
+    }
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh) {
+#pragma unroll
+      for (int kw = 0; kw < 3; ++kw) {
+        float *dst = dst0 + (int64_t)(kh * 3 + kw) * ld_col + w0;
+        if (vec) {
+          __stcs(reinterpret_cast<float4 *>(dst),
+                 make_float4(win[kh][kw], win[kh][kw + 1], win[kh][kw + 2], win[kh][kw + 3]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (w0 + e < out_w) dst[e] = win[kh][kw + e];
+        }
+      }
+    }
+  }
+}
+
+// blockIdx.z = channel, (blockIdx.y, threadIdx.y) = output row, x = output column
+__global__ void maxpool_rows_kernel(const float *__restrict__ in, int64_t ld_in, int height,
+                                    int width, int size, int stride, int off, int out_h, int out_w,
+                                    float *__restrict__ out, int64_t ld_out,
+                                    int32_t *__restrict__ idx, int64_t ld_idx) {
+  pdl_trigger();
+  pdl_wait();
+  const int c = blockIdx.z;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= out_h) return;
+  const float *src = in + (int64_t)c * ld_in;
+  const int plane = height * width;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < out_w; j += gridDim.x * blockDim.x) {
+    float best = -FLT_MAX;
+    int32_t arg = -1;
+    for (int n = 0; n < size; ++n) {
+      const int r = i * stride + n - off;
+      if (r < 0 || r >= height) continue;
+      for (int m = 0; m < size; ++m) {
+        const int q = j * stride + m - off;
+        if (q >= 0 && q < width) {
+          const float v = __ldg(src + r * width + q);
+          if (v > best) {
+            best = v;
+            arg = c * plane + r * width + q;
+          }
+        }
+      }
+    }
+    __stcs(out + (int64_t)c * ld_out + i * out_w + j, best);
+    __stcs(idx + (int64_t)c * ld_idx + i * out_w + j, arg);
+  }
+}
+
 bool vec_ok(const void *p, int64_t ld, int64_t cols) {
   return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && ld % 4 == 0 && ld >= ((cols + 3) / 4) * 4;
 }
@@ -182,13 +303,13 @@ int launch_rows(const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t rows
   if (vec) {
     const int nvec = (int)((cols + 3) / 4);
     const Shape2 g = shape2d(nvec, rows);
-    rows_vec<OP><<<g.grid, g.block, 0, s>>>(
-        reinterpret_cast<const float4 *>(X), (int)(ldx / 4), reinterpret_cast<float4 *>(Y),
-        (int)(ldy / 4), (int)rows, nvec, value, bias);
+    acct::launch(rows_vec<OP>, g.grid, g.block, 0, s, reinterpret_cast<const float4 *>(X),
+                 (int)(ldx / 4), reinterpret_cast<float4 *>(Y), (int)(ldy / 4), (int)rows, nvec,
+                 value, bias);
   } else {
     const Shape2 g = shape2d(cols, rows);
-    rows_scalar<OP><<<g.grid, g.block, 0, s>>>(X, (int)ldx, Y, (int)ldy, (int)rows, (int)cols,
-                                               value, bias);
+    acct::launch(rows_scalar<OP>, g.grid, g.block, 0, s, X, (int)ldx, Y, (int)ldy, (int)rows,
+                 (int)cols, value, bias);
   }
   return acct::note_launch(what);
 }
@@ -238,11 +359,32 @@ extern "C" int acct_im2col_f32(const float *im, int64_t ld_im, int channels, int
   if (ld_im < (int64_t)height * width || ld_col < npix) return fail(ACCT_EINVAL, "im2col: pitch too small");
   if (krows > 65535 || krows * ld_col >= kMaxElems || (int64_t)channels * ld_im >= kMaxElems)
     return fail(ACCT_ENOTSUP, "im2col: too large for 32-bit indexing");
+  if (ksize == 3 && stride == 1 && pad == 1) {
+    const bool vec = out_w % 4 == 0 && ld_col % 4 == 0 && (reinterpret_cast<uintptr_t>(col) & 15) == 0;
+    const int quads = (out_w + 3) / 4;
+    const dim3 block(quads >= 32 ? 32 : (quads >= 16 ? 16 : (quads >= 8 ? 8 : 4)),
+                     quads >= 32 ? 4 : 16);
+    const dim3 grid((unsigned)((quads + block.x - 1) / block.x),
+                    (unsigned)((out_h + block.y - 1) / block.y), (unsigned)channels);
+    launch(im2col_k3s1_kernel, grid, block, 0, as_stream(stream), im, ld_im, height, width, out_h,
+           out_w, col, ld_col, vec);
+    return note_launch("im2col");
+  }
+  if (out_w >= 64) {
+    const bool vec = out_w % 4 == 0 && ld_col % 4 == 0 && (reinterpret_cast<uintptr_t>(col) & 15) == 0;
+    const int quads = (out_w + 3) / 4;
+    const dim3 block(quads >= 32 ? 32 : 16, 8);
+    const dim3 grid((unsigned)((quads + block.x - 1) / block.x), (unsigned)((out_h + 7) / 8),
+                    (unsigned)krows);
+    launch(im2col_rows_kernel, grid, block, 0, as_stream(stream), im, ld_im, height, width, ksize,
+           stride, pad, out_h, out_w, col, ld_col, vec);
+    return note_launch("im2col");
+  }
   const bool vec = vec_ok(col, ld_col, npix);
   const int64_t nq = (npix + 3) / 4;
   const Shape2 g = shape2d(nq, krows);
-  im2col_kernel<<<g.grid, g.block, 0, as_stream(stream)>>>(
-      im, ld_im, height, width, ksize, stride, pad, out_w, (int)npix, (int)krows, col, ld_col, vec);
+  launch(im2col_kernel, g.grid, g.block, 0, as_stream(stream), im, ld_im, height, width, ksize,
+         stride, pad, out_w, (int)npix, (int)krows, col, ld_col, vec);
   return note_launch("im2col");
 }
 
@@ -256,8 +398,15 @@ extern "C" int acct_maxpool_f32(const float *in, int64_t ld_in, int channels, in
     return fail(ACCT_EINVAL, "maxpool: pitch too small");
   if (channels > 65535 || (int64_t)channels * ld_in >= kMaxElems)
     return fail(ACCT_ENOTSUP, "maxpool: too large for 32-bit indexing");
+  if (out_w >= 32) {
+    const dim3 block(32, 8);
+    const dim3 grid((unsigned)((out_w + 31) / 32), (unsigned)((out_h + 7) / 8), (unsigned)channels);
+    launch(maxpool_rows_kernel, grid, block, 0, as_stream(stream), in, ld_in, height, width, size,
+           stride, off, out_h, out_w, out, ld_out, idx, ld_idx);
+    return note_launch("maxpool");
+  }
   const Shape2 g = shape2d(per, channels);
-  maxpool_kernel<<<g.grid, g.block, 0, as_stream(stream)>>>(
-      in, ld_in, height, width, size, stride, off, out_h, out_w, channels, out, ld_out, idx, ld_idx);
+  launch(maxpool_kernel, g.grid, g.block, 0, as_stream(stream), in, ld_in, height, width, size,
+         stride, off, out_h, out_w, channels, out, ld_out, idx, ld_idx);
   return note_launch("maxpool");
 }

@@ -33,6 +33,8 @@ __global__ void __launch_bounds__(256)
 gemm_tile_kernel(int M, int N, int K, float alpha, const float *__restrict__ A, int64_t lda,
                  const float *__restrict__ B, int64_t ldb, float beta, float *__restrict__ C,
                  int64_t ldc, const float *__restrict__ bias, int act) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float As[2][BK][BM + 4];
   __shared__ float Bs[2][BK][BN];
   const int tid = threadIdx.x;
@@ -118,6 +120,8 @@ gemm_skinny_kernel(int M, int N, int K, float alpha, const float *__restrict__ A
                    const float *__restrict__ B, int64_t ldb, float beta, float *__restrict__ C,
                    int64_t ldc, const float *__restrict__ bias, int act) {
   extern __shared__ float As[];  // [K][MAXM]
+  pdl_trigger();
+  pdl_wait();
   for (int t = threadIdx.x; t < K * MAXM; t += blockDim.x) {
     int k = t / MAXM, m = t % MAXM;
     As[t] = m < M ? A[(int64_t)m * lda + k] : 0.0f;
@@ -166,18 +170,19 @@ int gemm_simt(int M, int N, int K, float alpha, const float *A, int64_t lda, con
     if (maxm == 16) {
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(gemm_skinny_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      gemm_skinny_kernel<16><<<grid, block, (size_t)K * 16 * sizeof(float), s>>>(
-          M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act);
+      launch(gemm_skinny_kernel<16>, dim3(grid), dim3(block), (size_t)K * 16 * sizeof(float), s, M,
+             N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act);
     } else {
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(gemm_skinny_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      gemm_skinny_kernel<32><<<grid, block, smem, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C,
-                                                       ldc, bias, act);
+      launch(gemm_skinny_kernel<32>, dim3(grid), dim3(block), smem, s, M, N, K, alpha, A, lda, B,
+             ldb, beta, C, ldc, bias, act);
     }
     return note_launch("gemm_skinny");
   }
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
-  gemm_tile_kernel<<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act);
+  launch(gemm_tile_kernel, grid, dim3(256), 0, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias,
+         act);
   return note_launch("gemm_tile");
 }
 

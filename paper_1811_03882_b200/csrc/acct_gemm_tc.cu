@@ -170,6 +170,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // the prologue above overlaps the previous kernel's tail (PDL); operands
+  // and C are only touched after it has completed
+  pdl_trigger();
+  pdl_wait();
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -374,6 +378,8 @@ __global__ void __launch_bounds__(256)
 splitk_reduce_kernel(const float *__restrict__ ws, int64_t ws_ld, int64_t split_stride, int splits,
                      int M, int N, float alpha, float beta, float *__restrict__ C, int64_t ldc,
                      const float *__restrict__ bias, int act) {
+  pdl_trigger();
+  pdl_wait();
   const int nq = (N + 3) / 4;
   const int total = M * nq;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
@@ -550,14 +556,14 @@ int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, con
   }
   if (int rc = set_smem_attr<TN, SWAP, BK>()) return rc;
   const int grid = units < sms ? units : sms;
-  tc_gemm_kernel<TN, SWAP, BK><<<grid, THREADS, G::SMEM_BYTES, s>>>(
-      ta, tb, M, N, K, nt, mt, splits, kb_per, g_write_hi, alpha, beta, C, ldc, bias, act, ws,
-      ws_ld, rows * ws_ld);
+  launch(tc_gemm_kernel<TN, SWAP, BK>, dim3(grid), dim3(THREADS), G::SMEM_BYTES, s, ta, tb, M, N,
+         K, nt, mt, splits, kb_per, g_write_hi, alpha, beta, C, ldc, bias, act, ws, ws_ld,
+         rows * ws_ld);
   if (int rc = note_launch("gemm_tc")) return rc;
   if (splits > 1) {
     const int64_t work = (int64_t)M * ((N + 3) / 4);
-    splitk_reduce_kernel<<<grid_for(work, 256), 256, 0, s>>>(ws, ws_ld, rows * ws_ld, splits, M, N,
-                                                             alpha, beta, C, ldc, bias, act);
+    launch(splitk_reduce_kernel, dim3(grid_for(work, 256)), dim3(256), 0, s, (const float *)ws, ws_ld,
+           rows * ws_ld, splits, M, N, alpha, beta, C, ldc, bias, act);
     if (int rc = note_launch("gemm_tc_splitk_reduce")) return rc;
   }
   return ACCT_OK;

@@ -136,6 +136,14 @@ class PatternExecutor:
             slots[k].host = h.data_ptr()
             slots[k].dev = None if d is None else d.data_ptr()
             slots[k].rows, slots[k].cols, slots[k].ld_dev = rows, cols, ld
+        # dense staging for padded arrays: their H2D is one contiguous copy plus
+        # a repack kernel (short-row 2-D H2D copies run ~10x slower)
+        padded = [k for k in range(len(net.arrays)) if slots[k].ld_dev != slots[k].cols]
+        if padded and not self.host_only:
+            most = max(slots[k].rows * slots[k].cols for k in padded)
+            self.stage = torch.empty(most, dtype=torch.float32, device=self.device)
+            for k in padded:
+                slots[k].stage = self.stage.data_ptr()
         self.slots = slots
         self._pristine = [(slots[k].host, slots[k].dev) for k in range(len(net.arrays))]
         for spec in net.arrays.values():

@@ -45,7 +45,7 @@ class Counters(C.Structure):
 
 class ArraySlot(C.Structure):
     _fields_ = [("host", C.c_void_p), ("dev", C.c_void_p), ("rows", C.c_int64),
-                ("cols", C.c_int64), ("ld_dev", C.c_int64)]
+                ("cols", C.c_int64), ("ld_dev", C.c_int64), ("stage", C.c_void_p)]
 
 
 class Action(C.Structure):
@@ -66,6 +66,7 @@ SIGNATURES = {
     "acct_maxpool_f32": [_vp, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _i64,
                          _vp, _i64, _vp],
     "acct_memcpy2d": [_vp, _sz, _vp, _sz, _sz, _sz, _i32, _vp],
+    "acct_h2d_staged": [_vp, _i64, _vp, _i64, _i64, _vp, _vp],
     "acct_host_fill_f32": [_vp, _i64, _i64, _i64, _f32],
     "acct_host_copy_f32": [_vp, _i64, _vp, _i64, _i64, _i64],
     "acct_host_im2col_f32": [_vp, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _i64],

@@ -58,6 +58,9 @@ def parse_args():
     ap.add_argument("--images", type=int, default=16)
     ap.add_argument("--gemm", default="auto", choices=("auto", "simt", "tc"))
     ap.add_argument("--no-fuse", action="store_true")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="images per launch of the image loop's body (0 = all images of a "
+                         "step, 1 = image at a time)")
     ap.add_argument("--no-ga", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-images", type=int, default=2, help="images per CPU process per step")
@@ -212,9 +215,9 @@ def roofline(ex, sched, steps: int, flush, peaks: dict) -> dict:
             kind = info["kind"] + ("+epilogue" if info.get("fused") else "")
             per_kind_ms[kind] = per_kind_ms.get(kind, 0.0) + ms
             w = per_kind_work.setdefault(kind, {"flops": 0, "bytes": 0})
-            w["flops"] += info["flops"] * ex.images
-            w["bytes"] += info["bytes"] * ex.images
-            launches[kind] = launches.get(kind, 0) + ex.images
+            w["flops"] += info["flops"] * info["executions"]
+            w["bytes"] += info["bytes"] * info["executions"]
+            launches[kind] = launches.get(kind, 0) + info["executions"]
     total = sum(per_kind_ms.values())
     top = max(per_kind_ms, key=per_kind_ms.get)
     ms, work, n = per_kind_ms[top], per_kind_work[top], launches[top]
@@ -285,7 +288,7 @@ def run_ours(args):
     from paper_1811_03882_b200.sharding import image_shard
     shard = image_shard(world * args.images, world, rank)
     ex = PatternExecutor(net, device=local, fuse=not args.no_fuse, gemm_mode=gemm_mode,
-                         first_image=shard.first)
+                         first_image=shard.first, batch=args.batch or True)
     bits = "1" * len(net.ops)
     full = ex.compile(bits)
     res = ex.compile(bits, resident=True)
@@ -377,6 +380,7 @@ def run_ours(args):
                                f"({len(net.ops)} genes) with hoisted transfers",
                    "net": args.net, "images_per_step_per_gpu": args.images,
                    "genes": len(net.ops), "gemm": args.gemm, "fused_epilogues": not args.no_fuse,
+                   "images_per_launch": res.batch,
                    "l2": "flushed before every step (256 MiB write); per-step footprint "
                          f"{net.total_bytes_per_image() * args.images / 2**20:.0f} MiB",
                    "parallelism": f"images sharded, {world} GPU(s), no collective"},

@@ -96,6 +96,38 @@ int acct_maxpool_f32(const float *in, int64_t ld_in, int channels, int height, i
                      int size, int stride, int off, int out_h, int out_w, float *out,
                      int64_t ld_out, int32_t *idx, int64_t ld_idx, acct_stream_t stream);
 
+/* ---------------------------------------------------- image-batched forms --
+ * The same loops over `batch` images in one launch: image b's operand X is at
+ * X + b * x_stride (elements; 0 = one operand shared by every image, e.g. the
+ * weights).  This is how the image loop `for (b ...)` (nets.py) runs when
+ * every op of its body is offloaded: the loop's private arrays get one copy
+ * per image and each op becomes one launch over all images.
+ * The per-image arithmetic is exactly that of the single-image entries.    */
+int acct_fill_batched_f32(float *Y, int64_t rows, int64_t cols, int64_t ldy, int64_t y_stride,
+                          float value, int batch, acct_stream_t stream);
+int acct_copy_batched_f32(const float *X, int64_t ldx, int64_t x_stride, float *Y, int64_t ldy,
+                          int64_t y_stride, int64_t rows, int64_t cols, int batch,
+                          acct_stream_t stream);
+int acct_im2col_batched_f32(const float *im, int64_t ld_im, int64_t im_stride, int channels,
+                            int height, int width, int ksize, int stride, int pad, float *col,
+                            int64_t ld_col, int64_t col_stride, int batch, acct_stream_t stream);
+/* one gemm of N' = (batch-1)*s + N columns when A is shared and B, C are
+ * column-interleaved with the same stride s >= N; else `batch` gemms       */
+int acct_gemm_nn_batched_f32(int M, int N, int K, float alpha, const float *A, int64_t lda,
+                             int64_t a_stride, const float *B, int64_t ldb, int64_t b_stride,
+                             float beta, float *C, int64_t ldc, int64_t c_stride,
+                             const float *bias, int act, int batch, int mode,
+                             acct_stream_t stream);
+int acct_add_bias_batched_f32(float *out, int64_t ld, int64_t out_stride, const float *bias,
+                              int rows, int64_t cols, int batch, acct_stream_t stream);
+int acct_activate_batched_f32(float *X, int64_t ld, int64_t x_stride, int64_t rows, int64_t cols,
+                              int act, int batch, acct_stream_t stream);
+int acct_maxpool_batched_f32(const float *in, int64_t ld_in, int64_t in_stride, int channels,
+                             int height, int width, int size, int stride, int off, int out_h,
+                             int out_w, float *out, int64_t ld_out, int64_t out_stride,
+                             int32_t *idx, int64_t ld_idx, int64_t idx_stride, int batch,
+                             acct_stream_t stream);
+
 /* ------------------------------------------------------------- transfers --
  * Direction: 1 = host->device, 2 = device->host.  Pitched 2-D copy of
  * `rows` rows of `row_bytes` bytes.  Counts calls and bytes per direction.  */
@@ -139,13 +171,16 @@ int acct_host_maxpool_f32(const float *in, int64_t ld_in, int channels, int heig
 enum {
   ACCT_A_LOOP_BEGIN = 1,   /* i[0]=trip count; host-side counted loop (the image loop) */
   ACCT_A_LOOP_END = 2,     /* i[0]=index of the matching LOOP_BEGIN */
-  ACCT_A_DIRECTIVE = 3,    /* count one directive execution: i[0]=|vars|, i[1]=is_copy */
-  ACCT_A_H2D = 4,          /* slot a[0]: host -> device (pitched) */
-  ACCT_A_D2H = 5,          /* slot a[0]: device -> host (pitched) */
+  ACCT_A_DIRECTIVE = 3,    /* count directive executions: i[0]=|vars|, i[1]=is_copy,
+                              i[2]=executions this action stands for (0 = 1) */
+  ACCT_A_H2D = 4,          /* slot a[0]: host -> device (pitched); i[0]=first image,
+                              i[1]=images (0 = 1), i[2]=transfers counted (0 = 1) */
+  ACCT_A_D2H = 5,          /* slot a[0]: device -> host (pitched); same operands */
   ACCT_A_BIND = 6,         /* slot a[0].host (i[2]=0) or .dev (i[2]=1) = base + loopvar(i[0]) * i[1]
                               bytes: load_input / per-image output slots */
   ACCT_A_STORE = 7,        /* memcpy(base + loopvar(i[0]) * i[1], slot a[0].host) (store_output) */
-  ACCT_A_KERNEL = 8,       /* device op: i[0]=op kind, operands a[], ints i[1..] */
+  ACCT_A_KERNEL = 8,       /* device op: i[0]=op kind, operands a[], ints i[1..];
+                              i[13] = images per launch (image-batched loop, 0 = 1) */
   ACCT_A_HOST = 9,         /* host op: same encoding, runs on host buffers */
   ACCT_A_SYNC = 10         /* drain the stream (before host ops / end) */
 };
@@ -161,13 +196,22 @@ typedef struct {
   int64_t rows, cols;  /* logical 2-D shape (1-D arrays: rows = 1) */
   int64_t ld_dev;      /* device row pitch in elements */
   void *stage;         /* optional dense device staging buffer (>= rows x cols x 4
-                          bytes) for padded arrays: H2D is then one dense copy plus
-                          a repack kernel instead of a slow short-row 2-D copy */
+                          bytes x images moved at once) for padded arrays: H2D is then
+                          one dense copy plus a repack kernel, D2H a pack kernel plus
+                          one dense copy, instead of a slow short-row 2-D copy */
+  int64_t img_stride;  /* image-batched schedules: elements between the private copies
+                          of consecutive images (0 = one copy shared by all images).
+                          [rows][B*ld] interleaved copies have img_stride = ld / B-th of
+                          the pitch; image-major [B][rows][ld] copies rows * ld */
 } acct_array_t;
 
 /* H2D of a padded array through a dense staging buffer: one contiguous copy
  * (counted as one h2d call) + a repack kernel into the pitched layout.      */
 int acct_h2d_staged(void *dev, int64_t ld, const void *host, int64_t rows, int64_t cols,
+                    void *stage, acct_stream_t stream);
+/* D2H of a padded array through the staging buffer: a pack kernel + one
+ * contiguous copy (counted as one d2h call).                                */
+int acct_d2h_staged(void *host, const void *dev, int64_t ld, int64_t rows, int64_t cols,
                     void *stage, acct_stream_t stream);
 
 typedef struct {

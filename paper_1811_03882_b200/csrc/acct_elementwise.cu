@@ -54,15 +54,16 @@ __device__ __forceinline__ float4 leaky4(float4 v) {
 
 // op: 0 fill, 1 copy, 2 bias add, 3 leaky
 template <int OP>
-__global__ void rows_vec(const float4 *__restrict__ x, int ldxv, float4 *__restrict__ y, int ldyv,
-                         int rows, int nvec, float value, const float *__restrict__ bias) {
+__global__ void rows_vec(const float4 *__restrict__ x, int ldxv, int64_t xbs, float4 *__restrict__ y,
+                         int ldyv, int64_t ybs, int rows, int nvec, float value,
+                         const float *__restrict__ bias) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.y * blockDim.y + threadIdx.y;
   if (r >= rows) return;
   const float b = OP == 2 ? __ldg(bias + r) : 0.0f;
-  const float4 *xr = x + (int64_t)r * ldxv;
-  float4 *yr = y + (int64_t)r * ldyv;
+  const float4 *xr = x + blockIdx.z * xbs + (int64_t)r * ldxv;
+  float4 *yr = y + blockIdx.z * ybs + (int64_t)r * ldyv;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nvec; c += gridDim.x * blockDim.x) {
     float4 v;
     if (OP == 0) {
@@ -83,14 +84,15 @@ __global__ void rows_vec(const float4 *__restrict__ x, int ldxv, float4 *__restr
 }
 
 template <int OP>
-__global__ void rows_scalar(const float *__restrict__ x, int ldx, float *__restrict__ y, int ldy,
-                            int rows, int cols, float value, const float *__restrict__ bias) {
+__global__ void rows_scalar(const float *__restrict__ x, int ldx, int64_t xbs, float *__restrict__ y,
+                            int ldy, int64_t ybs, int rows, int cols, float value,
+                            const float *__restrict__ bias) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.y * blockDim.y + threadIdx.y;
   if (r >= rows) return;
-  const float *xr = x + (int64_t)r * ldx;
-  float *yr = y + (int64_t)r * ldy;
+  const float *xr = x + blockIdx.z * xbs + (int64_t)r * ldx;
+  float *yr = y + blockIdx.z * ybs + (int64_t)r * ldy;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
     if (OP == 0) yr[c] = value;
     else if (OP == 1) yr[c] = xr[c];
@@ -102,13 +104,16 @@ __global__ void rows_scalar(const float *__restrict__ x, int ldx, float *__restr
 // ---- im2col: one thread per 4 consecutive output pixels of one col row ----
 // blockIdx.y = col row c = (channel, kh, kw); a warp covers 128 consecutive
 // pixels of an output row band, so its input reads walk image rows.
-__global__ void im2col_kernel(const float *__restrict__ im, int64_t ld_im, int height, int width,
-                              int ksize, int stride, int pad, int out_w, int npix, int krows,
-                              float *__restrict__ col, int64_t ld_col, bool vec) {
+__global__ void im2col_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs,
+                              int height, int width, int ksize, int stride, int pad, int out_w,
+                              int npix, int krows, float *__restrict__ col, int64_t ld_col,
+                              int64_t col_bs, bool vec) {
   pdl_trigger();
   pdl_wait();
   const int c = blockIdx.y * blockDim.y + threadIdx.y;
   if (c >= krows) return;
+  im += blockIdx.z * im_bs;  // blockIdx.z = image of the batch
+  col += blockIdx.z * col_bs;
   const int kw = c % ksize, kh = (c / ksize) % ksize;
   const float *src = im + (int64_t)(c / (ksize * ksize)) * ld_im;
   float *dst_row = col + (int64_t)c * ld_col;
@@ -143,14 +148,18 @@ __global__ void im2col_kernel(const float *__restrict__ im, int64_t ld_im, int h
 }
 
 // ---- forward_maxpool: blockIdx.y = channel, one thread per output pixel ----
-__global__ void maxpool_kernel(const float *__restrict__ in, int64_t ld_in, int height, int width,
-                               int size, int stride, int off, int out_h, int out_w, int channels,
-                               float *__restrict__ out, int64_t ld_out, int32_t *__restrict__ idx,
-                               int64_t ld_idx) {
+__global__ void maxpool_kernel(const float *__restrict__ in, int64_t ld_in, int64_t in_bs,
+                               int height, int width, int size, int stride, int off, int out_h,
+                               int out_w, int channels, float *__restrict__ out, int64_t ld_out,
+                               int64_t out_bs, int32_t *__restrict__ idx, int64_t ld_idx,
+                               int64_t idx_bs) {
   pdl_trigger();
   pdl_wait();
   const int c = blockIdx.y * blockDim.y + threadIdx.y;
   if (c >= channels) return;
+  in += blockIdx.z * in_bs;  // blockIdx.z = image of the batch
+  out += blockIdx.z * out_bs;
+  idx += blockIdx.z * idx_bs;
   const float *src = in + (int64_t)c * ld_in;
   const int per = out_h * out_w;
   const int plane = height * width;
@@ -180,14 +189,17 @@ __global__ void maxpool_kernel(const float *__restrict__ in, int64_t ld_in, int 
 // ---- wide planes: 3-D grid (w-quads x output rows x col rows), no division ----
 // blockIdx.z = col row c, threadIdx.y/blockIdx.y = output row h, each thread 4
 // consecutive output pixels of that row: one input row, float4 store.
-__global__ void im2col_rows_kernel(const float *__restrict__ im, int64_t ld_im, int height,
-                                   int width, int ksize, int stride, int pad, int out_h, int out_w,
-                                   float *__restrict__ col, int64_t ld_col, bool vec) {
+__global__ void im2col_rows_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs,
+                                   int height, int width, int ksize, int stride, int pad,
+                                   int out_h, int out_w, int krows, float *__restrict__ col,
+                                   int64_t ld_col, int64_t col_bs, bool vec) {
   pdl_trigger();
   pdl_wait();
-  const int c = blockIdx.z;
+  const int img = blockIdx.z / krows, c = blockIdx.z - img * krows;
   const int h = blockIdx.y * blockDim.y + threadIdx.y;
   if (h >= out_h) return;
+  im += img * im_bs;
+  col += img * col_bs;
   const int kw = c % ksize, kh = (c / ksize) % ksize;
   const int row = kh + h * stride - pad;
   const bool row_ok = row >= 0 && row < height;
@@ -215,14 +227,17 @@ __global__ void im2col_rows_kernel(const float *__restrict__ im, int64_t ld_im, 
 // blockIdx.z = input channel; a thread owns 4 consecutive output pixels of
 // one output row, loads the 3 x 6 input window once and writes the 9 col rows
 // (kh, kw) of that channel: 9 float4 stores per 18 loads.
-__global__ void im2col_k3s1_kernel(const float *__restrict__ im, int64_t ld_im, int height,
-                                   int width, int out_h, int out_w, float *__restrict__ col,
-                                   int64_t ld_col, bool vec) {
+__global__ void im2col_k3s1_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs,
+                                   int height, int width, int out_h, int out_w, int channels,
+                                   float *__restrict__ col, int64_t ld_col, int64_t col_bs,
+                                   bool vec) {
   pdl_trigger();
   pdl_wait();
-  const int ci = blockIdx.z;
+  const int img = blockIdx.z / channels, ci = blockIdx.z - img * channels;
   const int h = blockIdx.y * blockDim.y + threadIdx.y;
   if (h >= out_h) return;
+  im += img * im_bs;
+  col += img * col_bs;
   const float *src = im + (int64_t)ci * ld_im;
   float *dst0 = col + (int64_t)(ci * 9) * ld_col + (int64_t)h * out_w;
   for (int w0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4; w0 < out_w;
@@ -257,15 +272,19 @@ __global__ void im2col_k3s1_kernel(const float *__restrict__ im, int64_t ld_im, 
 }
 
 // blockIdx.z = channel, (blockIdx.y, threadIdx.y) = output row, x = output column
-__global__ void maxpool_rows_kernel(const float *__restrict__ in, int64_t ld_in, int height,
-                                    int width, int size, int stride, int off, int out_h, int out_w,
-                                    float *__restrict__ out, int64_t ld_out,
-                                    int32_t *__restrict__ idx, int64_t ld_idx) {
+__global__ void maxpool_rows_kernel(const float *__restrict__ in, int64_t ld_in, int64_t in_bs,
+                                    int height, int width, int size, int stride, int off,
+                                    int out_h, int out_w, int channels, float *__restrict__ out,
+                                    int64_t ld_out, int64_t out_bs, int32_t *__restrict__ idx,
+                                    int64_t ld_idx, int64_t idx_bs) {
   pdl_trigger();
   pdl_wait();
-  const int c = blockIdx.z;
+  const int img = blockIdx.z / channels, c = blockIdx.z - img * channels;
   const int i = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= out_h) return;
+  in += img * in_bs;
+  out += img * out_bs;
+  idx += img * idx_bs;
   const float *src = in + (int64_t)c * ld_in;
   const int plane = height * width;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < out_w; j += gridDim.x * blockDim.x) {
@@ -294,22 +313,30 @@ bool vec_ok(const void *p, int64_t ld, int64_t cols) {
   return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && ld % 4 == 0 && ld >= ((cols + 3) / 4) * 4;
 }
 
+
+// batch b of a [rows][cols] op lives at base + b * stride (stride 0: shared)
+bool batch_ok(int batch, int64_t per_z) { return batch >= 1 && (int64_t)batch * per_z <= 65535; }
+
 template <int OP>
-int launch_rows(const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t rows, int64_t cols,
-                float value, const float *bias, cudaStream_t s, const char *what) {
-  if (rows > 65535 * 8 || rows * (ldy > ldx ? ldy : ldx) >= kMaxElems)
+int launch_rows(const float *X, int64_t ldx, int64_t xbs, float *Y, int64_t ldy, int64_t ybs,
+                int64_t rows, int64_t cols, int batch, float value, const float *bias,
+                cudaStream_t s, const char *what) {
+  if (rows > 65535 * 8 || rows * (ldy > ldx ? ldy : ldx) >= kMaxElems || !batch_ok(batch, 1))
     return acct::fail(ACCT_ENOTSUP, what);
-  const bool vec = vec_ok(Y, ldy, cols) && (OP != 1 || vec_ok(X, ldx, cols));
+  const bool vec = vec_ok(Y, ldy, cols) && ybs % 4 == 0 &&
+                   (OP != 1 || (vec_ok(X, ldx, cols) && xbs % 4 == 0));
   if (vec) {
     const int nvec = (int)((cols + 3) / 4);
-    const Shape2 g = shape2d(nvec, rows);
+    Shape2 g = shape2d(nvec, rows);
+    g.grid.z = (unsigned)batch;
     acct::launch(rows_vec<OP>, g.grid, g.block, 0, s, reinterpret_cast<const float4 *>(X),
-                 (int)(ldx / 4), reinterpret_cast<float4 *>(Y), (int)(ldy / 4), (int)rows, nvec,
-                 value, bias);
+                 (int)(ldx / 4), xbs / 4, reinterpret_cast<float4 *>(Y), (int)(ldy / 4), ybs / 4,
+                 (int)rows, nvec, value, bias);
   } else {
-    const Shape2 g = shape2d(cols, rows);
-    acct::launch(rows_scalar<OP>, g.grid, g.block, 0, s, X, (int)ldx, Y, (int)ldy, (int)rows,
-                 (int)cols, value, bias);
+    Shape2 g = shape2d(cols, rows);
+    g.grid.z = (unsigned)batch;
+    acct::launch(rows_scalar<OP>, g.grid, g.block, 0, s, X, (int)ldx, xbs, Y, (int)ldy, ybs,
+                 (int)rows, (int)cols, value, bias);
   }
   return acct::note_launch(what);
 }
@@ -318,39 +345,71 @@ int launch_rows(const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t rows
 
 using namespace acct;
 
+extern "C" int acct_fill_batched_f32(float *Y, int64_t rows, int64_t cols, int64_t ldy,
+                                     int64_t y_stride, float value, int batch,
+                                     acct_stream_t stream) {
+  if (rows < 0 || cols < 0 || ldy < cols || batch < 1 || (rows * cols > 0 && !Y))
+    return fail(ACCT_EINVAL, "fill: bad shape");
+  if (rows * cols == 0) return ACCT_OK;
+  return launch_rows<0>(Y, ldy, y_stride, Y, ldy, y_stride, rows, cols, batch, value, nullptr,
+                        as_stream(stream), "fill");
+}
+
 extern "C" int acct_fill_f32(float *Y, int64_t rows, int64_t cols, int64_t ldy, float value,
                              acct_stream_t stream) {
-  if (rows < 0 || cols < 0 || ldy < cols || (rows * cols > 0 && !Y)) return fail(ACCT_EINVAL, "fill: bad shape");
+  return acct_fill_batched_f32(Y, rows, cols, ldy, 0, value, 1, stream);
+}
+
+extern "C" int acct_copy_batched_f32(const float *X, int64_t ldx, int64_t x_stride, float *Y,
+                                     int64_t ldy, int64_t y_stride, int64_t rows, int64_t cols,
+                                     int batch, acct_stream_t stream) {
+  if (rows < 0 || cols < 0 || ldx < cols || ldy < cols || batch < 1)
+    return fail(ACCT_EINVAL, "copy: bad shape");
   if (rows * cols == 0) return ACCT_OK;
-  return launch_rows<0>(Y, ldy, Y, ldy, rows, cols, value, nullptr, as_stream(stream), "fill");
+  return launch_rows<1>(X, ldx, x_stride, Y, ldy, y_stride, rows, cols, batch, 0.0f, nullptr,
+                        as_stream(stream), "copy");
 }
 
 extern "C" int acct_copy_f32(const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t rows,
                              int64_t cols, acct_stream_t stream) {
-  if (rows < 0 || cols < 0 || ldx < cols || ldy < cols) return fail(ACCT_EINVAL, "copy: bad shape");
-  if (rows * cols == 0) return ACCT_OK;
-  return launch_rows<1>(X, ldx, Y, ldy, rows, cols, 0.0f, nullptr, as_stream(stream), "copy");
+  return acct_copy_batched_f32(X, ldx, 0, Y, ldy, 0, rows, cols, 1, stream);
+}
+
+extern "C" int acct_add_bias_batched_f32(float *out, int64_t ld, int64_t out_stride,
+                                         const float *bias, int rows, int64_t cols, int batch,
+                                         acct_stream_t stream) {
+  if (rows < 0 || cols < 0 || ld < cols || !bias || batch < 1)
+    return fail(ACCT_EINVAL, "add_bias: bad shape");
+  if ((int64_t)rows * cols == 0) return ACCT_OK;
+  return launch_rows<2>(out, ld, out_stride, out, ld, out_stride, rows, cols, batch, 0.0f, bias,
+                        as_stream(stream), "add_bias");
 }
 
 extern "C" int acct_add_bias_f32(float *out, int64_t ld, const float *bias, int rows, int64_t cols,
                                  acct_stream_t stream) {
-  if (rows < 0 || cols < 0 || ld < cols || !bias) return fail(ACCT_EINVAL, "add_bias: bad shape");
-  if ((int64_t)rows * cols == 0) return ACCT_OK;
-  return launch_rows<2>(out, ld, out, ld, rows, cols, 0.0f, bias, as_stream(stream), "add_bias");
+  return acct_add_bias_batched_f32(out, ld, 0, bias, rows, cols, 1, stream);
+}
+
+extern "C" int acct_activate_batched_f32(float *X, int64_t ld, int64_t x_stride, int64_t rows,
+                                         int64_t cols, int act, int batch, acct_stream_t stream) {
+  if (rows < 0 || cols < 0 || ld < cols || batch < 1) return fail(ACCT_EINVAL, "activate: bad shape");
+  if (act == ACCT_ACT_LINEAR || rows * cols == 0) return ACCT_OK;  // identity loop: no device work
+  if (act != ACCT_ACT_LEAKY) return fail(ACCT_EINVAL, "activate: unknown activation");
+  return launch_rows<3>(X, ld, x_stride, X, ld, x_stride, rows, cols, batch, 0.0f, nullptr,
+                        as_stream(stream), "activate");
 }
 
 extern "C" int acct_activate_f32(float *X, int64_t ld, int64_t rows, int64_t cols, int act,
                                  acct_stream_t stream) {
-  if (rows < 0 || cols < 0 || ld < cols) return fail(ACCT_EINVAL, "activate: bad shape");
-  if (act == ACCT_ACT_LINEAR || rows * cols == 0) return ACCT_OK;  // identity loop: no device work
-  if (act != ACCT_ACT_LEAKY) return fail(ACCT_EINVAL, "activate: unknown activation");
-  return launch_rows<3>(X, ld, X, ld, rows, cols, 0.0f, nullptr, as_stream(stream), "activate");
+  return acct_activate_batched_f32(X, ld, 0, rows, cols, act, 1, stream);
 }
 
-extern "C" int acct_im2col_f32(const float *im, int64_t ld_im, int channels, int height, int width,
-                               int ksize, int stride, int pad, float *col, int64_t ld_col,
-                               acct_stream_t stream) {
-  if (channels <= 0 || height <= 0 || width <= 0 || ksize <= 0 || stride <= 0 || pad < 0)
+extern "C" int acct_im2col_batched_f32(const float *im, int64_t ld_im, int64_t im_stride,
+                                       int channels, int height, int width, int ksize, int stride,
+                                       int pad, float *col, int64_t ld_col, int64_t col_stride,
+                                       int batch, acct_stream_t stream) {
+  if (channels <= 0 || height <= 0 || width <= 0 || ksize <= 0 || stride <= 0 || pad < 0 ||
+      batch < 1)
     return fail(ACCT_EINVAL, "im2col: bad geometry");
   const int out_h = (height + 2 * pad - ksize) / stride + 1;
   const int out_w = (width + 2 * pad - ksize) / stride + 1;
@@ -359,54 +418,79 @@ extern "C" int acct_im2col_f32(const float *im, int64_t ld_im, int channels, int
   if (ld_im < (int64_t)height * width || ld_col < npix) return fail(ACCT_EINVAL, "im2col: pitch too small");
   if (krows > 65535 || krows * ld_col >= kMaxElems || (int64_t)channels * ld_im >= kMaxElems)
     return fail(ACCT_ENOTSUP, "im2col: too large for 32-bit indexing");
-  if (ksize == 3 && stride == 1 && pad == 1) {
-    const bool vec = out_w % 4 == 0 && ld_col % 4 == 0 && (reinterpret_cast<uintptr_t>(col) & 15) == 0;
+  const bool col_vec = ld_col % 4 == 0 && col_stride % 4 == 0 &&
+                       (reinterpret_cast<uintptr_t>(col) & 15) == 0;
+  cudaStream_t s = as_stream(stream);
+  if (ksize == 3 && stride == 1 && pad == 1 && batch_ok(batch, channels)) {
+    const bool vec = out_w % 4 == 0 && col_vec;
     const int quads = (out_w + 3) / 4;
     const dim3 block(quads >= 32 ? 32 : (quads >= 16 ? 16 : (quads >= 8 ? 8 : 4)),
                      quads >= 32 ? 4 : 16);
     const dim3 grid((unsigned)((quads + block.x - 1) / block.x),
-                    (unsigned)((out_h + block.y - 1) / block.y), (unsigned)channels);
-    launch(im2col_k3s1_kernel, grid, block, 0, as_stream(stream), im, ld_im, height, width, out_h,
-           out_w, col, ld_col, vec);
+                    (unsigned)((out_h + block.y - 1) / block.y), (unsigned)(channels * batch));
+    launch(im2col_k3s1_kernel, grid, block, 0, s, im, ld_im, im_stride, height, width, out_h,
+           out_w, channels, col, ld_col, col_stride, vec);
     return note_launch("im2col");
   }
-  if (out_w >= 64) {
-    const bool vec = out_w % 4 == 0 && ld_col % 4 == 0 && (reinterpret_cast<uintptr_t>(col) & 15) == 0;
+  if (out_w >= 64 && batch_ok(batch, krows)) {
+    const bool vec = out_w % 4 == 0 && col_vec;
     const int quads = (out_w + 3) / 4;
     const dim3 block(quads >= 32 ? 32 : 16, 8);
     const dim3 grid((unsigned)((quads + block.x - 1) / block.x), (unsigned)((out_h + 7) / 8),
-                    (unsigned)krows);
-    launch(im2col_rows_kernel, grid, block, 0, as_stream(stream), im, ld_im, height, width, ksize,
-           stride, pad, out_h, out_w, col, ld_col, vec);
+                    (unsigned)(krows * batch));
+    launch(im2col_rows_kernel, grid, block, 0, s, im, ld_im, im_stride, height, width, ksize,
+           stride, pad, out_h, out_w, (int)krows, col, ld_col, col_stride, vec);
     return note_launch("im2col");
   }
-  const bool vec = vec_ok(col, ld_col, npix);
+  if (!batch_ok(batch, 1)) return fail(ACCT_ENOTSUP, "im2col: batch too large");
+  const bool vec = vec_ok(col, ld_col, npix) && col_stride % 4 == 0;
   const int64_t nq = (npix + 3) / 4;
-  const Shape2 g = shape2d(nq, krows);
-  launch(im2col_kernel, g.grid, g.block, 0, as_stream(stream), im, ld_im, height, width, ksize,
-         stride, pad, out_w, (int)npix, (int)krows, col, ld_col, vec);
+  Shape2 g = shape2d(nq, krows);
+  g.grid.z = (unsigned)batch;
+  launch(im2col_kernel, g.grid, g.block, 0, s, im, ld_im, im_stride, height, width, ksize, stride,
+         pad, out_w, (int)npix, (int)krows, col, ld_col, col_stride, vec);
   return note_launch("im2col");
 }
 
-extern "C" int acct_maxpool_f32(const float *in, int64_t ld_in, int channels, int height, int width,
-                                int size, int stride, int off, int out_h, int out_w, float *out,
-                                int64_t ld_out, int32_t *idx, int64_t ld_idx, acct_stream_t stream) {
-  if (channels <= 0 || size <= 0 || stride <= 0 || out_h <= 0 || out_w <= 0 || !idx)
+extern "C" int acct_im2col_f32(const float *im, int64_t ld_im, int channels, int height, int width,
+                               int ksize, int stride, int pad, float *col, int64_t ld_col,
+                               acct_stream_t stream) {
+  return acct_im2col_batched_f32(im, ld_im, 0, channels, height, width, ksize, stride, pad, col,
+                                 ld_col, 0, 1, stream);
+}
+
+extern "C" int acct_maxpool_batched_f32(const float *in, int64_t ld_in, int64_t in_stride,
+                                        int channels, int height, int width, int size, int stride,
+                                        int off, int out_h, int out_w, float *out, int64_t ld_out,
+                                        int64_t out_stride, int32_t *idx, int64_t ld_idx,
+                                        int64_t idx_stride, int batch, acct_stream_t stream) {
+  if (channels <= 0 || size <= 0 || stride <= 0 || out_h <= 0 || out_w <= 0 || !idx || batch < 1)
     return fail(ACCT_EINVAL, "maxpool: bad geometry");
   const int64_t per = (int64_t)out_h * out_w;
   if (ld_in < (int64_t)height * width || ld_out < per || ld_idx < per)
     return fail(ACCT_EINVAL, "maxpool: pitch too small");
   if (channels > 65535 || (int64_t)channels * ld_in >= kMaxElems)
     return fail(ACCT_ENOTSUP, "maxpool: too large for 32-bit indexing");
-  if (out_w >= 32) {
+  cudaStream_t s = as_stream(stream);
+  if (out_w >= 32 && batch_ok(batch, channels)) {
     const dim3 block(32, 8);
-    const dim3 grid((unsigned)((out_w + 31) / 32), (unsigned)((out_h + 7) / 8), (unsigned)channels);
-    launch(maxpool_rows_kernel, grid, block, 0, as_stream(stream), in, ld_in, height, width, size,
-           stride, off, out_h, out_w, out, ld_out, idx, ld_idx);
+    const dim3 grid((unsigned)((out_w + 31) / 32), (unsigned)((out_h + 7) / 8),
+                    (unsigned)(channels * batch));
+    launch(maxpool_rows_kernel, grid, block, 0, s, in, ld_in, in_stride, height, width, size,
+           stride, off, out_h, out_w, channels, out, ld_out, out_stride, idx, ld_idx, idx_stride);
     return note_launch("maxpool");
   }
-  const Shape2 g = shape2d(per, channels);
-  launch(maxpool_kernel, g.grid, g.block, 0, as_stream(stream), in, ld_in, height, width, size,
-         stride, off, out_h, out_w, channels, out, ld_out, idx, ld_idx);
+  if (!batch_ok(batch, 1)) return fail(ACCT_ENOTSUP, "maxpool: batch too large");
+  Shape2 g = shape2d(per, channels);
+  g.grid.z = (unsigned)batch;
+  launch(maxpool_kernel, g.grid, g.block, 0, s, in, ld_in, in_stride, height, width, size, stride,
+         off, out_h, out_w, channels, out, ld_out, out_stride, idx, ld_idx, idx_stride);
   return note_launch("maxpool");
+}
+
+extern "C" int acct_maxpool_f32(const float *in, int64_t ld_in, int channels, int height, int width,
+                                int size, int stride, int off, int out_h, int out_w, float *out,
+                                int64_t ld_out, int32_t *idx, int64_t ld_idx, acct_stream_t stream) {
+  return acct_maxpool_batched_f32(in, ld_in, 0, channels, height, width, size, stride, off, out_h,
+                                  out_w, out, ld_out, 0, idx, ld_idx, 0, 1, stream);
 }

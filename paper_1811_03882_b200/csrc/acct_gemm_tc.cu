@@ -66,6 +66,15 @@ constexpr int STAGING_BYTES = EPI_GROUPS * 4 * 32 * 33 * 4;  // normal-tile epil
 // profiling knobs that skip the split / MMA / epilogue work (results are then
 // wrong; tools/gemm_bench.py only).
 int g_write_hi = 0;
+// bits 8-15 of the same word: L2 prefetch distance in k-blocks (ACCT_TC_PF, default 8)
+int prefetch_distance() {
+  static const int pf = [] {
+    const char *e = getenv("ACCT_TC_PF");
+    int v = e ? atoi(e) : 8;
+    return v < 0 ? 0 : (v > 255 ? 255 : v);
+  }();
+  return pf;
+}
 
 template <int TN, int BK>
 struct Cfg {
@@ -178,11 +187,36 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
+      // L2 prefetch cursor: walks the same (unit, k-block) sequence as the
+      // loads, PF k-blocks ahead, so the ring's TMA loads hit L2 rather than
+      // paying HBM latency with only S small stages in flight.
+      int pu = blockIdx.x, pkb = 0;
+      Unit pw{};
+      if (pu < units) pw = unit_of<TN, SWAP, BK>(pu, nt, tiles, kb_per, total_kb);
+      auto prefetch_next = [&]() {
+        if (pu >= units) return;
+        const int kx = (pw.kb0 + pkb) * BK;
+        if (!SWAP) {
+          ptx::tma_prefetch_2d(&tmA, kx, pw.m0);
+          for (int c = 0; c < TN / 32; ++c) ptx::tma_prefetch_2d(&tmB, pw.n0 + 32 * c, kx);
+        } else {
+          for (int c = 0; c < 4; ++c) ptx::tma_prefetch_2d(&tmB, pw.n0 + 32 * c, kx);
+          ptx::tma_prefetch_2d(&tmA, kx, pw.m0);
+        }
+        if (++pkb == pw.nkb) {
+          pkb = 0;
+          pu += gridDim.x;
+          if (pu < units) pw = unit_of<TN, SWAP, BK>(pu, nt, tiles, kb_per, total_kb);
+        }
+      };
+      const int pf = (write_hi >> 8) & 0xff;
+      for (int i = 0; i < pf; ++i) prefetch_next();
       int g = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit w = unit_of<TN, SWAP, BK>(u, nt, tiles, kb_per, total_kb);
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
           const int s = g % S;
+          if (pf > 0) prefetch_next();
           if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
           ptx::mbar_expect_tx(&full[s], G::X_TILE + G::Y_TILE);
           const int kx = (w.kb0 + kb) * BK;
@@ -557,7 +591,7 @@ int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, con
   if (int rc = set_smem_attr<TN, SWAP, BK>()) return rc;
   const int grid = units < sms ? units : sms;
   launch(tc_gemm_kernel<TN, SWAP, BK>, dim3(grid), dim3(THREADS), G::SMEM_BYTES, s, ta, tb, M, N,
-         K, nt, mt, splits, kb_per, g_write_hi, alpha, beta, C, ldc, bias, act, ws, ws_ld,
+         K, nt, mt, splits, kb_per, g_write_hi | (prefetch_distance() << 8), alpha, beta, C, ldc, bias, act, ws, ws_ld,
          rows * ws_ld);
   if (int rc = note_launch("gemm_tc")) return rc;
   if (splits > 1) {

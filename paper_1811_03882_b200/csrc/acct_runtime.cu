@@ -133,6 +133,17 @@ __global__ void repack_kernel(const float *__restrict__ src, int64_t cols, float
       dst[r * ld + c] = __ldcs(src + r * cols + c);
 }
 
+// pitched [rows][ld] -> dense [rows][cols] (the D2H half of the staging)
+__global__ void pack_kernel(const float *__restrict__ src, int64_t ld, float *__restrict__ dst,
+                            int64_t cols, int64_t rows) {
+  pdl_trigger();
+  pdl_wait();
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cols;
+         c += (int64_t)gridDim.x * blockDim.x)
+      dst[r * cols + c] = __ldcs(src + r * ld + c);
+}
+
 }  // namespace
 
 extern "C" int acct_h2d_staged(void *dev, int64_t ld, const void *host, int64_t rows,
@@ -153,6 +164,25 @@ extern "C" int acct_h2d_staged(void *dev, int64_t ld, const void *host, int64_t 
   launch(repack_kernel, dim3(gx, gy), dim3(256), 0, s, static_cast<const float *>(stage), cols,
          static_cast<float *>(dev), ld, rows);
   return note_launch("h2d_staged repack");
+}
+
+extern "C" int acct_d2h_staged(void *host, const void *dev, int64_t ld, int64_t rows,
+                               int64_t cols, void *stage, acct_stream_t stream) {
+  if (!dev || !host || !stage || rows < 0 || cols < 0 || ld < cols)
+    return fail(ACCT_EINVAL, "d2h_staged: bad arguments");
+  if (rows * cols == 0) return ACCT_OK;
+  const size_t bytes = (size_t)rows * cols * 4;
+  cudaStream_t s = as_stream(stream);
+  const unsigned gx = (unsigned)((cols + 255) / 256 < 64 ? (cols + 255) / 256 : 64);
+  const unsigned gy = (unsigned)(rows < 1024 ? rows : 1024);
+  launch(pack_kernel, dim3(gx, gy), dim3(256), 0, s, static_cast<const float *>(dev), ld,
+         static_cast<float *>(stage), cols, rows);
+  if (int rc = note_launch("d2h_staged pack")) return rc;
+  Counters &c = counters();
+  c.d2h_calls.fetch_add(1);
+  c.d2h_bytes.fetch_add((int64_t)bytes);
+  return check_cuda(cudaMemcpyAsync(host, stage, bytes, cudaMemcpyDeviceToHost, s),
+                    "d2h_staged: copy");
 }
 
 extern "C" int acct_memcpy2d(void *dst, size_t dpitch, const void *src, size_t spitch,
@@ -194,6 +224,31 @@ extern "C" int acct_gemm_nn_f32(int M, int N, int K, float alpha, const float *A
   return gemm_simt(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
 }
 
+// Batched gemm over `batch` images, image b's operands at base + b * stride
+// (stride 0 = one shared operand, e.g. the weights).  When A is shared and B
+// and C are column-interleaved ([rows][batch * s] with image b at column
+// offset b * s, s >= N) the batch is ONE gemm of N' = (batch-1)*s + N
+// columns -- the padding columns between images are computed and never read.
+extern "C" int acct_gemm_nn_batched_f32(int M, int N, int K, float alpha, const float *A,
+                                        int64_t lda, int64_t a_stride, const float *B,
+                                        int64_t ldb, int64_t b_stride, float beta, float *C,
+                                        int64_t ldc, int64_t c_stride, const float *bias, int act,
+                                        int batch, int mode, acct_stream_t stream) {
+  if (batch < 1) return fail(ACCT_EINVAL, "gemm_nn: bad batch");
+  if (batch == 1)
+    return acct_gemm_nn_f32(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, mode, stream);
+  const int64_t span = (int64_t)(batch - 1) * b_stride + N;
+  if (a_stride == 0 && b_stride == c_stride && b_stride >= N && span <= ldb && span <= ldc &&
+      span < (int64_t)1 << 31)
+    return acct_gemm_nn_f32(M, (int)span, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, mode,
+                            stream);
+  for (int b = 0; b < batch; ++b)
+    if (int rc = acct_gemm_nn_f32(M, N, K, alpha, A + b * a_stride, lda, B + b * b_stride, ldb,
+                                  beta, C + b * c_stride, ldc, bias, act, mode, stream))
+      return rc;
+  return ACCT_OK;
+}
+
 // ------------------------------------------------------------ schedule runner
 
 namespace {
@@ -214,30 +269,34 @@ int device_op(const acct_action_t &a, acct_array_t *arr, int gemm_mode, cudaStre
   const int64_t *I = a.i;
   auto D = [&](int k) { return reinterpret_cast<float *>(arr[a.a[k]].dev); };
   auto LD = [&](int k) { return arr[a.a[k]].ld_dev; };
+  auto BS = [&](int k) { return arr[a.a[k]].img_stride; };  // per-image offset (0 = shared)
+  const int nb = I[13] > 1 ? (int)I[13] : 1;                 // images per launch
   acct_stream_t st = reinterpret_cast<acct_stream_t>(s);
   switch ((int)I[0]) {
     case ACCT_K_FILL:
-      return acct_fill_f32(D(0), I[1], I[2], LD(0), bits_to_float(I[3]), st);
+      return acct_fill_batched_f32(D(0), I[1], I[2], LD(0), BS(0), bits_to_float(I[3]), nb, st);
     case ACCT_K_COPY:
-      return acct_copy_f32(D(0), LD(0), D(1), LD(1), I[1], I[2], st);
+      return acct_copy_batched_f32(D(0), LD(0), BS(0), D(1), LD(1), BS(1), I[1], I[2], nb, st);
     case ACCT_K_IM2COL:
-      return acct_im2col_f32(D(0), LD(0), (int)I[1], (int)I[2], (int)I[3], (int)I[4], (int)I[5],
-                             (int)I[6], D(1), LD(1), st);
+      return acct_im2col_batched_f32(D(0), LD(0), BS(0), (int)I[1], (int)I[2], (int)I[3],
+                                     (int)I[4], (int)I[5], (int)I[6], D(1), LD(1), BS(1), nb, st);
     case ACCT_K_GEMM: {
       const float *bias = a.a[3] >= 0 ? D(3) : nullptr;
-      return acct_gemm_nn_f32((int)I[1], (int)I[2], (int)I[3], 1.0f, D(0), LD(0), D(1), LD(1),
-                              I[4] ? 1.0f : 0.0f, D(2), LD(2), bias, (int)I[5], gemm_mode, st);
+      return acct_gemm_nn_batched_f32((int)I[1], (int)I[2], (int)I[3], 1.0f, D(0), LD(0), BS(0),
+                                      D(1), LD(1), BS(1), I[4] ? 1.0f : 0.0f, D(2), LD(2), BS(2),
+                                      bias, (int)I[5], nb, gemm_mode, st);
     }
     case ACCT_K_ADD_BIAS:
-      return acct_add_bias_f32(D(0), LD(0), D(1), (int)I[1], I[2], st);
+      return acct_add_bias_batched_f32(D(0), LD(0), BS(0), D(1), (int)I[1], I[2], nb, st);
     case ACCT_K_LEAKY:
-      return acct_activate_f32(D(0), LD(0), I[1], I[2], ACCT_ACT_LEAKY, st);
+      return acct_activate_batched_f32(D(0), LD(0), BS(0), I[1], I[2], ACCT_ACT_LEAKY, nb, st);
     case ACCT_K_LINEAR:
-      return acct_activate_f32(D(0), LD(0), I[1], I[2], ACCT_ACT_LINEAR, st);
+      return acct_activate_batched_f32(D(0), LD(0), BS(0), I[1], I[2], ACCT_ACT_LINEAR, nb, st);
     case ACCT_K_MAXPOOL:
-      return acct_maxpool_f32(D(0), LD(0), (int)I[1], (int)I[2], (int)I[3], (int)I[4], (int)I[5],
-                              (int)I[6], (int)I[7], (int)I[8], D(1), LD(1),
-                              reinterpret_cast<int32_t *>(arr[a.a[2]].dev), LD(2), st);
+      return acct_maxpool_batched_f32(D(0), LD(0), BS(0), (int)I[1], (int)I[2], (int)I[3],
+                                      (int)I[4], (int)I[5], (int)I[6], (int)I[7], (int)I[8], D(1),
+                                      LD(1), BS(1), reinterpret_cast<int32_t *>(arr[a.a[2]].dev),
+                                      LD(2), BS(2), nb, st);
   }
   return fail(ACCT_EINVAL, "schedule: unknown device op");
 }
@@ -444,41 +503,60 @@ int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *action
         loops.pop_back();
         break;
       }
-      case ACCT_A_DIRECTIVE:
-        cnt.directive_execs.fetch_add(1, std::memory_order_relaxed);
-        cnt.var_transfers.fetch_add(a.i[0] * (a.i[1] ? 2 : 1), std::memory_order_relaxed);
+      case ACCT_A_DIRECTIVE: {
+        const int64_t reps = a.i[2] > 1 ? a.i[2] : 1;  // executions this action stands for
+        cnt.directive_execs.fetch_add(reps, std::memory_order_relaxed);
+        cnt.var_transfers.fetch_add(reps * a.i[0] * (a.i[1] ? 2 : 1), std::memory_order_relaxed);
         break;
+      }
       case ACCT_A_H2D:
       case ACCT_A_D2H: {
         if (!check_slot(a.a[0])) return fail(ACCT_EINVAL, "schedule: bad slot");
         acct_array_t &x = arrays[a.a[0]];
+        // images [first, first + n) of the slot: device view b at dev + b * img_stride,
+        // host images dense and consecutive; `reps` = transfers this action stands for
+        const int64_t first = a.i[0], n = a.i[1] > 1 ? a.i[1] : 1, reps = a.i[2] > 1 ? a.i[2] : 1;
         size_t row = (size_t)x.cols * 4, dp = (size_t)x.ld_dev * 4;
-        if (a.kind == ACCT_A_H2D) {
-          acct_stream_t on = stream;
-          if (defer && in_prefix) {
-            if (!forked) {
-              if ((rc = check_cuda(cudaEventRecord(side->fork, s), "side fork record"))) return rc;
-              if ((rc = check_cuda(cudaStreamWaitEvent(side->t, side->fork, 0), "side fork wait")))
-                return rc;
-              forked = true;
+        char *dev0 = static_cast<char *>(x.dev) + first * x.img_stride * 4;
+        // image-major copies ([n][rows][ld]) move as one block of n * rows rows
+        const bool block = n == 1 || x.img_stride == x.rows * x.ld_dev;
+        const int64_t rows = block ? n * x.rows : x.rows;
+        const bool staged = x.stage && x.ld_dev != x.cols;
+        const int64_t h2d0 = cnt.h2d_calls.load(), d2h0 = cnt.d2h_calls.load();
+        for (int64_t b = 0; b < (block ? 1 : n) && rc == ACCT_OK; ++b) {
+          char *dev = dev0 + b * x.img_stride * 4;
+          char *host = static_cast<char *>(x.host) + b * x.rows * x.cols * 4;
+          if (a.kind == ACCT_A_H2D) {
+            acct_stream_t on = stream;
+            if (defer && in_prefix) {
+              if (!forked) {
+                if ((rc = check_cuda(cudaEventRecord(side->fork, s), "side fork record"))) return rc;
+                if ((rc = check_cuda(cudaStreamWaitEvent(side->t, side->fork, 0), "side fork wait")))
+                  return rc;
+                forked = true;
+              }
+              on = reinterpret_cast<acct_stream_t>(side->t);
+            } else {
+              // the staging buffer is shared with the side stream's staged copies
+              if (staged && (rc = join_all())) return rc;
+              if ((rc = need(a.a[0]))) return rc;
             }
-            on = reinterpret_cast<acct_stream_t>(side->t);
+            rc = staged ? acct_h2d_staged(dev, x.ld_dev, host, rows, x.cols, x.stage, on)
+                        : acct_memcpy2d(dev, dp, host, row, row, (size_t)rows, 1, on);
+            if (rc == ACCT_OK && on != stream) {
+              rc = check_cuda(cudaEventRecord(side->ev[a.a[0]], side->t), "side event record");
+              waiting[a.a[0]] = 1;
+            }
           } else {
-            // the staging buffer is shared with the side stream's staged copies
-            if (x.stage && x.ld_dev != x.cols && (rc = join_all())) return rc;
             if ((rc = need(a.a[0]))) return rc;
+            if (staged && (rc = join_all())) return rc;
+            rc = staged ? acct_d2h_staged(host, dev, x.ld_dev, rows, x.cols, x.stage, stream)
+                        : acct_memcpy2d(host, row, dev, dp, row, (size_t)rows, 2, stream);
           }
-          rc = (x.stage && x.ld_dev != x.cols)
-                   ? acct_h2d_staged(x.dev, x.ld_dev, x.host, x.rows, x.cols, x.stage, on)
-                   : acct_memcpy2d(x.dev, dp, x.host, row, row, (size_t)x.rows, 1, on);
-          if (rc == ACCT_OK && on != stream) {
-            rc = check_cuda(cudaEventRecord(side->ev[a.a[0]], side->t), "side event record");
-            waiting[a.a[0]] = 1;
-          }
-        } else {
-          if ((rc = need(a.a[0]))) return rc;
-          rc = acct_memcpy2d(x.host, row, x.dev, dp, row, (size_t)x.rows, 2, stream);
         }
+        // count the transfers the action stands for, not the memcpy calls it took
+        if (a.kind == ACCT_A_H2D) cnt.h2d_calls.store(h2d0 + reps);
+        else cnt.d2h_calls.store(d2h0 + reps);
         pending = true;
         break;
       }

@@ -77,6 +77,17 @@ class Schedule:
     runs: int = 0
     graph: object = None                  # acct_graph_t* once captured (all-GPU schedules)
     graph_failed: bool = False
+    batch: int = 1                        # images per launch of the image loop's body
+    slots: object = None                  # slot table of a batched schedule (None = base)
+
+
+def _batched(act: tuple, nimg: int) -> tuple:
+    """KERNEL action over `nimg` images per launch (int operand 13)."""
+    if nimg <= 1:
+        return act
+    ints = list(act[2]) + [0] * (14 - len(act[2]))
+    ints[13] = nimg
+    return (act[0], act[1], tuple(ints)) + tuple(act[3:])
 
 
 @dataclass
@@ -89,7 +100,8 @@ class RunResult:
 
 class PatternExecutor:
     def __init__(self, net: NetProgram, device=0, seed: int = 1, fuse: bool = True,
-                 gemm_mode: int = K.GEMM_AUTO, graphs: bool = True, first_image: int = 0):
+                 gemm_mode: int = K.GEMM_AUTO, graphs: bool = True, first_image: int = 0,
+                 batch: int | bool = True, batch_bytes: int = 48 << 30):
         import torch
         self.torch = torch
         K.lib()  # fail loudly without the kernel library
@@ -101,6 +113,11 @@ class PatternExecutor:
         self.net = net
         self.fuse = fuse
         self.gemm_mode = gemm_mode
+        # image batching of the image loop (see _batch_plan): True = as many
+        # images per launch as divide the step and fit `batch_bytes` of
+        # private copies; an int caps the batch; False/1 = one image at a time
+        self.max_batch = (1 << 30) if batch is True else max(1, int(batch or 1))
+        self.batch_bytes = batch_bytes
         self.graphs = graphs and not self.host_only
         if self.host_only:
             self.device = None
@@ -146,6 +163,9 @@ class PatternExecutor:
                 slots[k].stage = self.stage.data_ptr()
         self.slots = slots
         self._pristine = [(slots[k].host, slots[k].dev) for k in range(len(net.arrays))]
+        self._tables: dict[int, tuple] = {1: (slots, self._pristine)}
+        self._bdev: dict[int, dict] = {}          # batch -> private device copies
+        self._last_table = 1
         for spec in net.arrays.values():
             if spec.role in ("weight", "bias"):
                 self.host[spec.name].copy_(torch.from_numpy(weight_data(net, spec.name, seed).ravel()))
@@ -169,19 +189,119 @@ class PatternExecutor:
             return self._cache[key]
         plan = plan_transfers(self.program, self.tree, self.accesses, genome_bits, self.genome_map)
         chosen = selected_loops(genome_bits, self.genome_map)
+        bp = self._batch_plan(plan, chosen)
         if resident:
-            sched = self._compile_resident(genome_bits, plan, chosen)
+            sched = self._compile_resident(genome_bits, plan, chosen, bp)
         else:
-            sched = self._compile_full(genome_bits, plan, chosen)
+            sched = self._compile_full(genome_bits, plan, chosen, bp)
         self._cache[key] = sched
         return sched
 
-    def _compile_full(self, bits: str, plan: TransferPlan, chosen: set) -> Schedule:
+    # ------------------------------------------------------------ batching
+    def _batch_plan(self, plan: TransferPlan, chosen: set):
+        """Image batching of the image loop `for (b ...)`.
+
+        Legal when every op of the loop body is offloaded (no host loop
+        inside it) and every array the body writes is private to an
+        iteration: its first access in the body is a full overwrite (fill,
+        im2col, copy or maxpool output; the input is rewritten by
+        load_input), so no value flows from image b to image b+1.  Each
+        private array then gets one device copy per image and consecutive
+        iterations run as ONE launch per op over P images -- loop
+        privatization + batching of an independent loop.  In-body transfers
+        may only move private arrays (the input before, the output after);
+        their copies are image-major so a batch moves as one block.
+        Directives still count once per image, hoisted transfers before the
+        loop fill image 0's copy and those after it read image P-1's copy
+        (the last iteration), so the counters and every host-visible value
+        equal the image-at-a-time run.  Returns None or
+        (P, {array: "im" | "il"}) -- image-major / column-interleaved.
+        """
+        if self.host_only or self.max_batch <= 1 or self.images <= 1:
+            return None
         net = self.net
+        if any(op.loop_id not in chosen for op in net.ops):
+            return None
+        full_write = {"fill": ("Y",), "im2col": ("Y",), "copy": ("Y",), "maxpool": ("Y", "I")}
+        first: dict[str, str] = {net.input_name: "w"}   # load_input(x) writes x first
+        written = {net.input_name, net.output_name}
+        for op in net.ops:
+            outs = full_write.get(op.kind, ())
+            for role, name in op.arrays.items():
+                is_write = role in outs or (op.kind == "gemm" and role == "C") or \
+                    (op.kind in ("add_bias", "leaky", "linear") and role == "Y")
+                if is_write:
+                    written.add(name)
+                if name not in first:
+                    first[name] = "w" if role in outs else "r"
+        if any(first.get(v) != "w" for v in written):
+            return None                                   # a value crosses iterations
+        inside = {lid for lid in net.loop_parent} - {net.image_loop}
+        moved_inside = set()
+        for d in plan.directives:
+            if d.target_loop in inside:
+                moved_inside.update(d.vars)
+        if not moved_inside <= written:
+            return None
+        layout = {v: ("im" if v in moved_inside or v == net.input_name else "il") for v in written}
+        per_image = 0
+        for v in written:
+            spec = net.arrays[v]
+            rows, cols = spec.shape if len(spec.shape) == 2 else (1, spec.shape[0])
+            per_image += rows * _pitch(cols) * 4
+        p = min(self.images, self.max_batch, max(1, self.batch_bytes // max(per_image, 1)))
+        while self.images % p:
+            p -= 1
+        return (p, layout) if p > 1 else None
+
+    def _batched_table(self, p: int, layout: dict):
+        """Slot table for P-image batches: private arrays get P copies
+        (image-major [P][rows][ld] or interleaved [rows][P*ld]); shared arrays
+        (weights, biases) keep their single buffer."""
+        if p in self._tables:
+            return self._tables[p][0]
+        torch = self.torch
+        n = len(self.net.arrays)
+        slots = (K.ArraySlot * n)()
+        keep = []
+        stage_need = 0
+        for k, spec in enumerate(self.net.arrays.values()):
+            base = self.slots[k]
+            slots[k].host, slots[k].rows, slots[k].cols = base.host, base.rows, base.cols
+            slots[k].ld_dev, slots[k].dev, slots[k].img_stride = base.ld_dev, base.dev, 0
+            rows, cols, ld = base.rows, base.cols, base.ld_dev
+            lay = layout.get(spec.name)
+            if lay is not None:
+                dt = torch.float32 if spec.dtype == "float" else torch.int32
+                d = torch.zeros(p * rows * ld, dtype=dt, device=self.device)
+                keep.append(d)
+                self._bdev.setdefault(p, {})[spec.name] = d
+                slots[k].dev = d.data_ptr()
+                if lay == "im":
+                    slots[k].img_stride = rows * ld
+                else:
+                    slots[k].ld_dev, slots[k].img_stride = p * ld, ld
+            if slots[k].ld_dev != cols:
+                stage_need = max(stage_need, rows * cols * (p if lay == "im" else 1))
+        if stage_need:
+            stage = torch.empty(stage_need, dtype=torch.float32, device=self.device)
+            keep.append(stage)
+            for k in range(n):
+                if slots[k].ld_dev != slots[k].cols:
+                    slots[k].stage = stage.data_ptr()
+        self._keep_alive = getattr(self, "_keep_alive", []) + keep
+        pristine = [(slots[k].host, slots[k].dev) for k in range(n)]
+        self._tables[p] = (slots, pristine)
+        return slots
+
+    def _compile_full(self, bits: str, plan: TransferPlan, chosen: set, bp=None) -> Schedule:
+        net = self.net
+        p = bp[0] if bp else 1
         acts: list[tuple] = []
         at_target: dict[int, list] = {}
         for d in plan.directives:
             at_target.setdefault(d.target_loop, []).append(d)
+        in_loop = [False]
 
         def moves(target: int, clauses) -> list[str]:
             names = set()
@@ -190,25 +310,34 @@ class PatternExecutor:
                     names.update(v for v in d.vars if v in self.slot_of)
             return sorted(names)
 
+        # transfers inside the loop move all P images of a batch; before it,
+        # image 0's copy; after it, image P-1's (the last iteration's values)
+        def xfer(kind, v, after=False):
+            if in_loop[0]:
+                return (kind, (self.slot_of[v],), (0, p, p))
+            return (kind, (self.slot_of[v],), (p - 1 if after else 0, 1, 1))
+
         def entry(target: int):
             for d in at_target.get(target, ()):
-                acts.append((K.A_DIRECTIVE, (), (len(d.vars), int(d.clause == COPY))))
+                acts.append((K.A_DIRECTIVE, (), (len(d.vars), int(d.clause == COPY),
+                                                  p if in_loop[0] else 1)))
             for v in moves(target, (COPYIN, COPY)):
-                acts.append((K.A_H2D, (self.slot_of[v],), ()))
+                acts.append(xfer(K.A_H2D, v))
 
         def leave(target: int):
             for v in moves(target, (COPYOUT, COPY)):
-                acts.append((K.A_D2H, (self.slot_of[v],), ()))
+                acts.append(xfer(K.A_D2H, v, after=not in_loop[0]))
 
         img = net.image_loop
         entry(img)
         begin = len(acts)
-        acts.append([K.A_LOOP_BEGIN, (), (self.images, -1)])
+        acts.append([K.A_LOOP_BEGIN, (), (self.images // p, -1)])
+        in_loop[0] = True
         x_slot, y_slot = self.slot_of[net.input_name], self.slot_of[net.output_name]
-        acts.append((K.A_BIND, (x_slot,), (0, self.image_bytes, 0), "in"))
+        acts.append((K.A_BIND, (x_slot,), (0, p * self.image_bytes, 0), "in"))
         # store_output(y) targets y's slot; binding y to it up front is exact
         # because every iteration overwrites y completely before reading it
-        acts.append((K.A_BIND, (y_slot,), (0, self.output_bytes, 0), "out"))
+        acts.append((K.A_BIND, (y_slot,), (0, p * self.output_bytes, 0), "out"))
 
         plan_f = self._fusion_plan(plan, chosen) if self.fuse else {}
         device_ops = host_ops = 0
@@ -217,7 +346,7 @@ class PatternExecutor:
             if role is None:
                 entry(op.loop_id)
                 on_gpu = op.loop_id in chosen
-                acts.append(self._op_action(op, K.A_KERNEL if on_gpu else K.A_HOST))
+                acts.append(self._op_action(op, K.A_KERNEL if on_gpu else K.A_HOST, p))
                 if on_gpu:
                     device_ops += op.kind != "linear"
                 else:
@@ -230,24 +359,28 @@ class PatternExecutor:
                 members = role[1]
                 for m in members:
                     entry(net.ops[m].loop_id)
-                acts.append(self._fused_gemm_action([net.ops[m] for m in role[2]]))
+                acts.append(self._fused_gemm_action([net.ops[m] for m in role[2]], p))
                 for m in members:
                     leave(net.ops[m].loop_id)
                 device_ops += 1
             # role "absorbed_after": handled by its anchor
-        acts.append((K.A_STORE, (y_slot,), (0, self.output_bytes, self.output_bytes), "out"))
+        acts.append((K.A_STORE, (y_slot,), (0, p * self.output_bytes, p * self.output_bytes), "out"))
         acts.append((K.A_LOOP_END, (), (begin,)))
         end = len(acts) - 1
-        acts[begin] = (K.A_LOOP_BEGIN, (), (self.images, end))
+        acts[begin] = (K.A_LOOP_BEGIN, (), (self.images // p, end))
+        in_loop[0] = False
         leave(img)
         acts.append((K.A_SYNC, (), ()))
         expected = self._expected_counters(plan, acts)
         sched = self._pack(bits, acts, plan, expected)
+        sched.batch = p
+        if bp:
+            sched.slots = self._batched_table(p, bp[1])
         sched.fused_groups = sorted((n, r[2]) for n, r in plan_f.items() if r[0] == "anchor")
         sched.device_ops, sched.host_ops = device_ops * self.images, host_ops * self.images
         return sched
 
-    def _compile_resident(self, bits: str, plan: TransferPlan, chosen: set) -> Schedule:
+    def _compile_resident(self, bits: str, plan: TransferPlan, chosen: set, bp=None) -> Schedule:
         """Kernels only, inputs already in HBM (one device batch of images):
         the `value` leg of the benchmark.  Requires every op on the GPU."""
         if len(chosen) != len(self.net.ops):
@@ -260,22 +393,27 @@ class PatternExecutor:
                                   device=self.device)
             db[:, :, :cols].copy_(self.input_batch.view(self.images, rows, cols))
             self.device_batch = db
+        p = bp[0] if bp else 1
         acts: list[tuple] = []
-        acts.append([K.A_LOOP_BEGIN, (), (self.images, -1)])
+        acts.append([K.A_LOOP_BEGIN, (), (self.images // p, -1)])
         x_slot = self.slot_of[self.net.input_name]
         rows, cols = self.net.arrays[self.net.input_name].shape
-        acts.append((K.A_BIND, (x_slot,), (0, rows * _pitch(cols) * 4, 1), "devin"))
+        acts.append((K.A_BIND, (x_slot,), (0, p * rows * _pitch(cols) * 4, 1), "devin"))
         plan_f = self._fusion_plan(plan, chosen) if self.fuse else {}
         for n, op in enumerate(self.net.ops):
             role = plan_f.get(n)
             if role is None:
-                acts.append(self._op_action(op, K.A_KERNEL))
+                acts.append(self._op_action(op, K.A_KERNEL, p))
             elif role[0] == "anchor":
-                acts.append(self._fused_gemm_action([self.net.ops[m] for m in role[2]]))
+                acts.append(self._fused_gemm_action([self.net.ops[m] for m in role[2]], p))
         acts.append((K.A_LOOP_END, (), (0,)))
-        acts[0] = (K.A_LOOP_BEGIN, (), (self.images, len(acts) - 1))
+        acts[0] = (K.A_LOOP_BEGIN, (), (self.images // p, len(acts) - 1))
         acts.append((K.A_SYNC, (), ()))
-        return self._pack(bits, acts, plan, {})
+        sched = self._pack(bits, acts, plan, {})
+        sched.batch = p
+        if bp:
+            sched.slots = self._batched_table(p, bp[1])
+        return sched
 
     def _fusion_plan(self, plan: TransferPlan, chosen: set) -> dict:
         """Per conv layer, fuse offloaded fill -> gemm -> add_bias -> activation
@@ -333,7 +471,7 @@ class PatternExecutor:
                 roles[j] = ("absorbed_after",)
         return roles
 
-    def _fused_gemm_action(self, members):
+    def _fused_gemm_action(self, members, nimg: int = 1):
         kinds = [m.kind for m in members]
         g = next(m for m in members if m.kind == "gemm")
         p, a = g.params, g.arrays
@@ -347,11 +485,14 @@ class PatternExecutor:
             elif m.kind == "linear":
                 act = K.ACT_LINEAR
         beta_one = 0 if "fill" in kinds else 1
-        return (K.A_KERNEL, (self.slot_of[a["A"]], self.slot_of[a["B"]], self.slot_of[a["C"]],
-                             bias_slot),
-                (K.K_GEMM, p["M"], p["N"], p["K"], beta_one, act))
+        return _batched((K.A_KERNEL, (self.slot_of[a["A"]], self.slot_of[a["B"]],
+                                      self.slot_of[a["C"]], bias_slot),
+                         (K.K_GEMM, p["M"], p["N"], p["K"], beta_one, act)), nimg)
 
-    def _op_action(self, op, where: int):
+    def _op_action(self, op, where: int, nimg: int = 1):
+        return _batched(self._op_action1(op, where), nimg)
+
+    def _op_action1(self, op, where: int):
         s, p, a = self.slot_of, op.params, op.arrays
         kind = op.kind
         if kind == "fill":
@@ -390,7 +531,9 @@ class PatternExecutor:
                 inside = False
             elif kind in (K.A_H2D, K.A_D2H):
                 spec = list(self.net.arrays.values())[act[1][0]]
-                reps = self.images if inside else 1
+                ints = act[2]
+                per = max(ints[2], 1) if len(ints) > 2 else 1   # transfers the action stands for
+                reps = (self.images // per) * per if inside else 1
                 if kind == K.A_H2D:
                     h2d += reps
                     h2d_b += reps * spec.nbytes
@@ -417,9 +560,15 @@ class PatternExecutor:
         return Schedule(bits, arr, len(acts), plan, expected)
 
     # ------------------------------------------------------------ run
-    def _restore_slots(self):
-        for k, (h, d) in enumerate(self._pristine):
-            self.slots[k].host, self.slots[k].dev = h, d
+    def _table(self, schedule: Schedule):
+        p = schedule.batch if schedule.slots is not None else 1
+        return self._tables[p][0], p
+
+    def _restore_slots(self, p: int = None):
+        for q in ([p] if p is not None else list(self._tables)):
+            slots, pristine = self._tables[q]
+            for k, (h, d) in enumerate(pristine):
+                slots[k].host, slots[k].dev = h, d
 
     def run(self, schedule: Schedule | str, timeout_s: float = 0.0, resident: bool = False,
             profile: bool = False) -> RunResult:
@@ -431,7 +580,9 @@ class PatternExecutor:
         if self.host_only and "1" in schedule.genome:
             raise DeviceError("host-only executor can only run the all-zero genome")
         lib = K.lib()
-        self._restore_slots()
+        slots, p = self._table(schedule)
+        self._last_table = p
+        self._restore_slots(p)
         K.reset_counters()
         kernel_ms = (C.c_float * schedule.n_actions)() if profile else None
 
@@ -439,10 +590,10 @@ class PatternExecutor:
             t0 = time.perf_counter()
             if profile:
                 rc = lib.acct_run_schedule_profiled(
-                    self.slots, len(self.net.arrays), schedule.actions, schedule.n_actions,
+                    slots, len(self.net.arrays), schedule.actions, schedule.n_actions,
                     self.gemm_mode, float(timeout_s), C.c_void_p(stream), kernel_ms)
             else:
-                rc = lib.acct_run_schedule(self.slots, len(self.net.arrays), schedule.actions,
+                rc = lib.acct_run_schedule(slots, len(self.net.arrays), schedule.actions,
                                            schedule.n_actions, self.gemm_mode, float(timeout_s),
                                            C.c_void_p(stream))
             return rc, time.perf_counter() - t0
@@ -455,7 +606,7 @@ class PatternExecutor:
                         and not schedule.graph_failed):
                     return self._replay(schedule, timeout_s)
                 rc, seconds = go(self.stream.cuda_stream)
-        self._restore_slots()
+        self._restore_slots(p)
         schedule.runs += 1
         if rc == K.ETIMEOUT:
             return RunResult(seconds, K.counters(), "timeout")
@@ -472,12 +623,13 @@ class PatternExecutor:
         the library per replay."""
         lib = K.lib()
         stream = C.c_void_p(self.stream.cuda_stream)
+        slots, p = self._table(schedule)
         if schedule.graph is None:
             handle = C.c_void_p()
-            rc = lib.acct_schedule_capture(self.slots, len(self.net.arrays), schedule.actions,
+            rc = lib.acct_schedule_capture(slots, len(self.net.arrays), schedule.actions,
                                            schedule.n_actions, self.gemm_mode, stream,
                                            C.byref(handle))
-            self._restore_slots()
+            self._restore_slots(p)
             if rc != 0 or not handle.value:
                 schedule.graph_failed = True
                 K.lib().acct_counters_reset()
@@ -503,18 +655,22 @@ class PatternExecutor:
         name = {v: n for n, v in K.OP_KIND.items()}[kind]
         i = [int(a.i[j]) for j in range(14)]
         slots = list(self.net.arrays.values())
+        nimg = max(i[13], 1)                       # images per launch
+        execs = self.images // nimg                # launches per run (body of the image loop)
         if kind == K.K_GEMM:
             M, N, Kd = i[1], i[2], i[3]
             c_bytes = (4 if i[4] else 0) + 4        # read C only when beta = 1
             bias = 4 * M if a.a[3] >= 0 else 0
-            byts = 4 * (M * Kd + Kd * N) + c_bytes * M * N + bias
+            # the weights are read once per launch, whatever the batch
+            byts = 4 * M * Kd + nimg * (4 * Kd * N + c_bytes * M * N) + bias
             op = next(o for o in ops if o.kind == "gemm" and o.arrays["C"] == slots[a.a[2]].name)
-            return {"kind": "gemm", "layer": op.layer, "M": M, "N": N, "K": Kd,
-                    "flops": 2 * M * N * Kd, "bytes": byts, "fused": a.a[3] >= 0 or i[4] == 0}
+            return {"kind": "gemm", "layer": op.layer, "M": M, "N": N, "K": Kd, "images": nimg,
+                    "executions": execs, "flops": 2 * M * N * Kd * nimg, "bytes": byts,
+                    "fused": a.a[3] >= 0 or i[4] == 0}
         target = slots[a.a[0]].name
         op = next(o for o in ops if o.kind == name and target in o.arrays.values())
-        return {"kind": name, "layer": op.layer, "flops": 0, "bytes": op.algorithmic_bytes(),
-                "fused": False}
+        return {"kind": name, "layer": op.layer, "images": nimg, "executions": execs, "flops": 0,
+                "bytes": op.algorithmic_bytes() * nimg, "fused": False}
 
     def outputs(self) -> np.ndarray:
         """(images, C, H*W) copy of the output slots after a run."""
@@ -525,8 +681,16 @@ class PatternExecutor:
         """Logical (unpitched) contents of a device array."""
         spec = self.net.arrays[name]
         rows, cols = spec.shape if len(spec.shape) == 2 else (1, spec.shape[0])
-        d = self.dev[name].view(rows, _pitch(cols))[:, :cols]
-        return d.cpu().numpy().reshape(spec.shape)
+        p = self._last_table
+        priv = self._bdev.get(p, {}).get(name)
+        if priv is None:
+            d = self.dev[name].view(rows, _pitch(cols))[:, :cols]
+            return d.cpu().numpy().reshape(spec.shape)
+        # batched schedule: the last image's private copy (what the
+        # image-at-a-time loop leaves in the array)
+        slot = self._tables[p][0][self.slot_of[name]]
+        view = priv[(p - 1) * slot.img_stride:].as_strided((rows, cols), (slot.ld_dev, 1))
+        return view.cpu().numpy().reshape(spec.shape)
 
     def host_array(self, name: str) -> np.ndarray:
         spec = self.net.arrays[name]

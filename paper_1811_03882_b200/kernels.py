@@ -45,7 +45,8 @@ class Counters(C.Structure):
 
 class ArraySlot(C.Structure):
     _fields_ = [("host", C.c_void_p), ("dev", C.c_void_p), ("rows", C.c_int64),
-                ("cols", C.c_int64), ("ld_dev", C.c_int64), ("stage", C.c_void_p)]
+                ("cols", C.c_int64), ("ld_dev", C.c_int64), ("stage", C.c_void_p),
+                ("img_stride", C.c_int64)]
 
 
 class Action(C.Structure):
@@ -67,6 +68,17 @@ SIGNATURES = {
                          _vp, _i64, _vp],
     "acct_memcpy2d": [_vp, _sz, _vp, _sz, _sz, _sz, _i32, _vp],
     "acct_h2d_staged": [_vp, _i64, _vp, _i64, _i64, _vp, _vp],
+    "acct_d2h_staged": [_vp, _vp, _i64, _i64, _i64, _vp, _vp],
+    "acct_fill_batched_f32": [_vp, _i64, _i64, _i64, _i64, _f32, _i32, _vp],
+    "acct_copy_batched_f32": [_vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _vp],
+    "acct_im2col_batched_f32": [_vp, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _i64,
+                                _i64, _i32, _vp],
+    "acct_gemm_nn_batched_f32": [_i32, _i32, _i32, _f32, _vp, _i64, _i64, _vp, _i64, _i64, _f32,
+                                 _vp, _i64, _i64, _vp, _i32, _i32, _i32, _vp],
+    "acct_add_bias_batched_f32": [_vp, _i64, _i64, _vp, _i32, _i64, _i32, _vp],
+    "acct_activate_batched_f32": [_vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp],
+    "acct_maxpool_batched_f32": [_vp, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
+                                 _vp, _i64, _i64, _vp, _i64, _i64, _i32, _vp],
     "acct_host_fill_f32": [_vp, _i64, _i64, _i64, _f32],
     "acct_host_copy_f32": [_vp, _i64, _vp, _i64, _i64, _i64],
     "acct_host_im2col_f32": [_vp, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _i64],

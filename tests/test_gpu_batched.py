@@ -1,0 +1,115 @@
+"""Image-batched execution of the image loop (B200 only).
+
+With every op of the loop body offloaded, the executor privatises the
+body's arrays per image and runs P images per launch (executor
+`_batch_plan`).  It must be unobservable: outputs match the oracle and the
+image-at-a-time run, the transfer counters equal the planner's
+(`directive_exec_counts`, pkg/src/acctuner/transfer.py:161-165) exactly, and
+arrays copied out after the loop hold the last image's values.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import cprog
+from paper_1811_03882_b200 import kernels as K
+from paper_1811_03882_b200.executor import PatternExecutor
+from paper_1811_03882_b200.nets import build_net
+
+pytestmark = pytest.mark.gpu
+
+
+def close(got, want):
+    scale = max(1e-30, float(np.abs(want).max()))
+    err = float(np.abs(got - want).max())
+    assert err <= 1e-4 * scale, (err, scale)
+
+
+@pytest.mark.parametrize("name,images,batch,expect", [
+    ("micro", 2, True, 2), ("demo", 8, True, 8), ("demo", 8, 3, 2), ("demo", 6, 4, 3),
+    ("yolov2-tiny", 2, True, 2)])
+def test_batched_all_offload_matches_oracle(cuda_device, name, images, batch, expect):
+    net = build_net(name, images=images)
+    ref = cprog.reference_forward(net)["outputs"]
+    ex = PatternExecutor(net, device=0, batch=batch)
+    bits = "1" * len(net.ops)
+    sched = ex.compile(bits)
+    assert sched.batch == expect
+    for _ in range(3):                       # plain run, graph capture, replay
+        r = ex.run(sched)
+        for key, val in sched.expected.items():
+            assert r.counters[key] == val, key
+        close(ex.outputs(), ref)
+
+
+@pytest.mark.parametrize("name", ["micro", "demo"])
+def test_batched_equals_image_at_a_time(cuda_device, name):
+    net = build_net(name)
+    a = PatternExecutor(net, device=0, batch=True)
+    b = PatternExecutor(net, device=0, batch=False)
+    bits = "1" * len(net.ops)
+    sa, sb = a.compile(bits), b.compile(bits)
+    assert sa.batch > 1 and sb.batch == 1
+    ra, rb = a.run(sa), b.run(sb)
+    assert ra.counters == {**rb.counters, "kernel_launches": ra.counters["kernel_launches"]}
+    close(a.outputs(), b.outputs())
+    # hoisted copyouts after the loop see the last image's arrays
+    for name_ in net.arrays:
+        close(a.host_array(name_), b.host_array(name_))
+        close(a.device_array(name_), b.device_array(name_))
+
+
+def test_partial_offload_is_not_batched(cuda_device):
+    net = build_net("demo")
+    ex = PatternExecutor(net, device=0)
+    bits = "1" * (len(net.ops) - 1) + "0"
+    assert ex.compile(bits).batch == 1
+
+
+def test_batched_resident_matches_full(cuda_device):
+    net = build_net("demo")
+    ex = PatternExecutor(net, device=0)
+    bits = "1" * len(net.ops)
+    ex.run(bits)
+    last = ex.device_array(net.output_name)
+    r = ex.run(bits, resident=True)
+    assert r.counters["h2d_calls"] == 0 and r.counters["d2h_calls"] == 0
+    assert np.array_equal(ex.device_array(net.output_name), last)
+
+
+def test_batched_kernel_entries_match_single(cuda_device):
+    """The *_batched C-ABI entries equal a loop of single-image calls."""
+    import torch
+    lib = K.lib()
+    P, c, h, w = 3, 4, 9, 11
+    ld_im = 128
+    im = torch.randn(P, c, ld_im, device="cuda")
+    krows, npix = c * 9, h * w
+    ldc = 128
+    col_b = torch.zeros(krows, P * ldc, device="cuda")
+    col_1 = torch.zeros(P, krows, ldc, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    assert lib.acct_im2col_batched_f32(im.data_ptr(), ld_im, c * ld_im, c, h, w, 3, 1, 1,
+                                       col_b.data_ptr(), P * ldc, ldc, P, s) == 0
+    for b in range(P):
+        assert lib.acct_im2col_f32(im[b].data_ptr(), ld_im, c, h, w, 3, 1, 1,
+                                   col_1[b].data_ptr(), ldc, s) == 0
+    torch.cuda.synchronize()
+    for b in range(P):
+        assert torch.equal(col_b[:, b * ldc:b * ldc + npix], col_1[b][:, :npix])
+    out_b = torch.zeros(c, P * 64, device="cuda")
+    idx_b = torch.zeros(c, P * 64, dtype=torch.int32, device="cuda")
+    out_1 = torch.zeros(P, c, 64, device="cuda")
+    idx_1 = torch.zeros(P, c, 64, dtype=torch.int32, device="cuda")
+    assert lib.acct_maxpool_batched_f32(im.data_ptr(), ld_im, c * ld_im, c, h, w, 2, 2, 0, 4, 5,
+                                        out_b.data_ptr(), P * 64, 64, idx_b.data_ptr(), P * 64,
+                                        64, P, s) == 0
+    for b in range(P):
+        assert lib.acct_maxpool_f32(im[b].data_ptr(), ld_im, c, h, w, 2, 2, 0, 4, 5,
+                                    out_1[b].data_ptr(), 64, idx_1[b].data_ptr(), 64, s) == 0
+    torch.cuda.synchronize()
+    for b in range(P):
+        assert torch.equal(out_b[:, b * 64:b * 64 + 20], out_1[b][:, :20])
+        assert torch.equal(idx_b[:, b * 64:b * 64 + 20], idx_1[b][:, :20])

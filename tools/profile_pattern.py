@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--resident", action="store_true")
     ap.add_argument("--gemm", default="auto", choices=("auto", "simt", "tc"))
     ap.add_argument("--no-fuse", action="store_true")
+    ap.add_argument("--batch", type=int, default=0, help="images per launch (0 = all)")
     ap.add_argument("--graph", action="store_true",
                     help="1 plain run, then graph capture + replays (ncu: skip the first run's "
                          "launches); prints device ms per replay")
@@ -36,7 +37,8 @@ def main():
         import torch
         mode = {"auto": K.GEMM_AUTO, "simt": K.GEMM_SIMT, "tc": K.GEMM_TC3XTF32}[args.gemm]
         net = build_net(args.net, images=args.images)
-        ex = PatternExecutor(net, device=0, gemm_mode=mode, fuse=not args.no_fuse)
+        ex = PatternExecutor(net, device=0, gemm_mode=mode, fuse=not args.no_fuse,
+                             batch=args.batch or True)
         sched = ex.compile("1" * len(net.ops), resident=args.resident)
         ex.run(sched)
         for _ in range(args.runs):
@@ -51,7 +53,8 @@ def main():
         return
     mode = {"auto": K.GEMM_AUTO, "simt": K.GEMM_SIMT, "tc": K.GEMM_TC3XTF32}[args.gemm]
     net = build_net(args.net, images=args.images)
-    ex = PatternExecutor(net, device=0, gemm_mode=mode, fuse=not args.no_fuse)
+    ex = PatternExecutor(net, device=0, gemm_mode=mode, fuse=not args.no_fuse,
+                             batch=args.batch or True)
     bits = "1" * len(net.ops)
     sched = ex.compile(bits, resident=args.resident)
     for _ in range(args.runs - 1):

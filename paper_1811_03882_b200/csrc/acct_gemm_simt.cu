@@ -155,13 +155,130 @@ gemm_skinny_kernel(int M, int N, int K, float alpha, const float *__restrict__ A
   }
 }
 
+// HBM-streaming gemm for M <= MT (the first conv layers: M = 16 / 32, K <= a
+// few hundred, N up to millions of pixels x images): the whole A (M x K) sits
+// in shared memory as [K][MT] so each k reads MT weights as broadcast float4s,
+// each thread owns 4 consecutive columns (one float4 of B per k, coalesced
+// 512-B warp rows), keeps 4 x MT accumulators in registers and issues KU
+// B loads before using any -- the kernel is a pure stream of B in and C out.
+// Per output the k loop runs in order (as the tile kernel), so results differ
+// from the host loop only by FMA contraction.
+template <int MT, int KU>
+__global__ void __launch_bounds__(128)
+gemm_stream_kernel(int M, int N, int K, float alpha, const float *__restrict__ A, int64_t lda,
+                   const float *__restrict__ B, int64_t ldb, float beta, float *__restrict__ C,
+                   int64_t ldc, const float *__restrict__ bias, int act) {
+  extern __shared__ float4 As4[];  // [K][MT/4]
+  float *As = reinterpret_cast<float *>(As4);
+  pdl_trigger();
+  pdl_wait();
+  for (int t = threadIdx.x; t < K * MT; t += blockDim.x) {
+    const int k = t / MT, m = t - k * MT;
+    As[t] = m < M ? A[(int64_t)m * lda + k] : 0.0f;
+  }
+  __syncthreads();
+  const int nq = (N + 3) >> 2;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+    const int col = q * 4;
+    const bool full = col + 4 <= N;
+    float acc[MT][4];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.0f;
+    const float *bp = B + col;
+    for (int k0 = 0; k0 < K; k0 += KU) {
+      float4 b[KU];
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const int k = k0 + u;
+        if (k < K) {
+          if (full) {
+            b[u] = __ldcs(reinterpret_cast<const float4 *>(bp + (int64_t)k * ldb));
+          } else {
+            const float *r = bp + (int64_t)k * ldb;
+            b[u] = make_float4(r[0], col + 1 < N ? r[1] : 0.0f, col + 2 < N ? r[2] : 0.0f, 0.0f);
+          }
+        } else {
+          b[u] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        if (k0 + u >= K) break;
+        const float4 *ak = As4 + (k0 + u) * (MT / 4);
+#pragma unroll
+        for (int g = 0; g < MT / 4; ++g) {
+          const float4 a = ak[g];
+          const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            acc[4 * g + e][0] = fmaf(av[e], b[u].x, acc[4 * g + e][0]);
+            acc[4 * g + e][1] = fmaf(av[e], b[u].y, acc[4 * g + e][1]);
+            acc[4 * g + e][2] = fmaf(av[e], b[u].z, acc[4 * g + e][2]);
+            acc[4 * g + e][3] = fmaf(av[e], b[u].w, acc[4 * g + e][3]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      if (m >= M) break;
+      float *cp = C + (int64_t)m * ldc + col;
+      if (full) {
+        float4 cv = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (beta != 0.0f) cv = *reinterpret_cast<const float4 *>(cp);
+        float4 o;
+        o.x = epilogue(acc[m][0], alpha, beta, &cv.x, bias, m, act);
+        o.y = epilogue(acc[m][1], alpha, beta, &cv.y, bias, m, act);
+        o.z = epilogue(acc[m][2], alpha, beta, &cv.z, bias, m, act);
+        o.w = epilogue(acc[m][3], alpha, beta, &cv.w, bias, m, act);
+        __stcs(reinterpret_cast<float4 *>(cp), o);
+      } else {
+        for (int e = 0; e < 4 && col + e < N; ++e)
+          cp[e] = epilogue(acc[m][e], alpha, beta, cp + e, bias, m, act);
+      }
+    }
+  }
+}
+
+template <int MT>
+int launch_stream(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
+                  int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
+                  cudaStream_t s) {
+  const size_t smem = (size_t)K * MT * sizeof(float);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(gemm_stream_kernel<MT, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  const int64_t nq = (N + 3) / 4;
+  const int block = 128;
+  unsigned grid = acct::grid_for(nq, block, MT <= 16 ? 8 : 4);
+  acct::launch(gemm_stream_kernel<MT, 8>, dim3(grid), dim3(block), smem, s, M, N, K, alpha, A, lda,
+               B, ldb, beta, C, ldc, bias, act);
+  return acct::note_launch("gemm_stream");
+}
+
 }  // namespace
 
 namespace acct {
 
+// M <= 16 with 16-B aligned rows: the streaming kernel (HBM-bound shapes; at
+// M = 32 the 128 accumulators per thread cost more occupancy than the stream
+// gains -- the tensor-core swap tile is faster there)
+int gemm_stream(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
+                int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
+                cudaStream_t s) {
+  if (M < 1 || M > 16 || N < 1 || K < 1 || (int64_t)K * 32 * 4 > 200 * 1024 || (ldb % 4) ||
+      (ldc % 4) || (reinterpret_cast<uintptr_t>(B) & 15) || (reinterpret_cast<uintptr_t>(C) & 15))
+    return ACCT_ENOTSUP;
+  return launch_stream<16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+}
+
 int gemm_simt(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
               int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
               cudaStream_t s) {
+  if (M <= 16) {
+    int rc = gemm_stream(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+    if (rc != ACCT_ENOTSUP) return rc;
+  }
   if (M <= 32 && (int64_t)K * 32 * 4 <= 200 * 1024) {
     const int block = 128;
     const size_t smem = (size_t)K * 32 * sizeof(float);

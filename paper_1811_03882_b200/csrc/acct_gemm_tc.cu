@@ -66,6 +66,10 @@ constexpr int STAGING_BYTES = EPI_GROUPS * 4 * 32 * 33 * 4;  // normal-tile epil
 // profiling knobs that skip the split / MMA / epilogue work (results are then
 // wrong; tools/gemm_bench.py only).
 int g_write_hi = 0;
+// bit 4: event trace of CTA 0's first kTrace stages (clock64 per role), read
+// back with acct_tc_trace -- pipeline analysis only (tools/tc_trace.py)
+constexpr int kTrace = 512;
+__device__ long long g_trace[8][kTrace];
 // bits 8-15 of the same word: L2 prefetch distance in k-blocks (ACCT_TC_PF, default 8)
 int prefetch_distance() {
   static const int pf = [] {
@@ -218,6 +222,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const int s = g % S;
           if (pf > 0) prefetch_next();
           if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
+          if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace) g_trace[0][g] = clock64();
           ptx::mbar_expect_tx(&full[s], G::X_TILE + G::Y_TILE);
           const int kx = (w.kb0 + kb) * BK;
           if (!SWAP) {
@@ -248,6 +253,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
           const int s = g % S;
           ptx::mbar_wait(&conv[s], (g / S) & 1);
+          if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace) g_trace[3][g] = clock64();
           ptx::tc_fence_after();
           const uint32_t xh = ptx::smem_u32(x_hi(s)), xl = ptx::smem_u32(x_lo(s));
           const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
@@ -273,6 +279,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             ptx::mma_tf32(d, dxl, dyh, idesc, 1);
           }
           ptx::mma_commit(&empty[s]);
+          if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace) g_trace[4][g] = clock64();
         }
         ptx::mma_commit(&acc_full[a]);
       }
@@ -287,40 +294,55 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       for (int kb = 0; kb < w.nkb; ++kb, ++g) {
         const int s = g % S;
         ptx::mbar_wait(&full[s], (g / S) & 1);
-        float4 *xh = reinterpret_cast<float4 *>(x_hi(s));
-        float4 *xl = reinterpret_cast<float4 *>(x_lo(s));
-        float4 *yh = reinterpret_cast<float4 *>(y_hi(s));
-        float4 *yl = reinterpret_cast<float4 *>(y_lo(s));
+        if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace && ct == 0) g_trace[1][g] = clock64();
+        const uint32_t xh = ptx::smem_u32(x_hi(s)), xl = ptx::smem_u32(x_lo(s));
+        const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
         if (!(write_hi & 2)) {
-#pragma unroll 4
-          for (int v = ct; v < G::X_TILE / 16; v += 128) {
+          // every load of the stage in flight before the first store
+          constexpr int NX = G::X_TILE / 16 / 128;
+          constexpr int NY = (G::Y_TILE / 16 + 127) / 128;
+          float4 rx[NX], ry[NY];
+#pragma unroll
+          for (int i = 0; i < NX; ++i) rx[i] = ptx::lds128(xh + 16 * (ct + 128 * i));
+#pragma unroll
+          for (int i = 0; i < NY; ++i)
+            if (ct + 128 * i < G::Y_TILE / 16) ry[i] = ptx::lds128(yh + 16 * (ct + 128 * i));
+          if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace && ct == 0)
+            g_trace[5][g] = clock64() + (long long)(rx[0].x * 0.0f) + (long long)(ry[0].x * 0.0f);
+#pragma unroll
+          for (int i = 0; i < NX; ++i) {
             float4 hi;
-            xl[v] = split_lo(xh[v], hi);
-            if (write_hi & 1) xh[v] = hi;
+            ptx::sts128(xl + 16 * (ct + 128 * i), split_lo(rx[i], hi));
+            if (write_hi & 1) ptx::sts128(xh + 16 * (ct + 128 * i), hi);
           }
-#pragma unroll 4
-          for (int v = ct; v < G::Y_TILE / 16; v += 128) {
-            float4 hi;
-            yl[v] = split_lo(yh[v], hi);
-            if (write_hi & 1) yh[v] = hi;
+#pragma unroll
+          for (int i = 0; i < NY; ++i) {
+            if (ct + 128 * i < G::Y_TILE / 16) {
+              float4 hi;
+              ptx::sts128(yl + 16 * (ct + 128 * i), split_lo(ry[i], hi));
+              if (write_hi & 1) ptx::sts128(yh + 16 * (ct + 128 * i), hi);
+            }
           }
         }
+        if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace && ct == 0) g_trace[6][g] = clock64();
         ptx::fence_proxy_async_smem();  // generic-proxy writes -> tensor core
+        if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace && ct == 0) g_trace[7][g] = clock64();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&conv[s]);
+        if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace && ct == 0) g_trace[2][g] = clock64();
       }
     }
   } else {
     // ---------------- epilogue ----------------
     const int q = warp & 3;  // this warp may read TMEM lanes 32q..32q+31
     const int grp = (warp - 6) / 4;
-    float *stg = staging + (grp * 4 + q) * (32 * 33);
+    const uint32_t stg_s = ptx::smem_u32(staging + (grp * 4 + q) * (32 * 33));
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       if ((j % EPI_GROUPS) != grp) continue;
       const Unit w = unit_of<TN, SWAP, BK>(u, nt, tiles, kb_per, total_kb);
       const int a = j % NACC;
-      ptx::mbar_wait(&acc_full[a], (j / NACC) & 1);
+      ptx::mbar_wait_sleepy(&acc_full[a], (j / NACC) & 1);
       ptx::tc_fence_after();
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * TN;
       float *part = ws + w.split * ws_split_stride;
@@ -334,7 +356,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           uint32_t r[32];
           ptx::tmem_ld_32x32b_x32(trow + 32 * c, r);
 #pragma unroll
-          for (int jj = 0; jj < 32; ++jj) stg[lane * 33 + jj] = __uint_as_float(r[jj]);
+          for (int jj = 0; jj < 32; ++jj) ptx::sts32(stg_s + 4 * (lane * 33 + jj), __uint_as_float(r[jj]));
           __syncwarp();
           const int col = w.n0 + 32 * c + lane;
           if (splits == 1) {
@@ -352,14 +374,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               for (int i = 0; i < 32; ++i) {
                 const int row = row0 + i;
                 if (row < M)
-                  C[(int64_t)row * ldc + col] = finish(stg[i * 33 + lane], alpha, beta, cv[i],
-                                                       bias, bv[i], act);
+                  C[(int64_t)row * ldc + col] = finish(ptx::lds32(stg_s + 4 * (i * 33 + lane)), alpha,
+                                                       beta, cv[i], bias, bv[i], act);
               }
             }
           } else {
             float *dst = part + (int64_t)row0 * ws_ld + col;
 #pragma unroll 8
-            for (int i = 0; i < 32; ++i) __stcg(dst + (int64_t)i * ws_ld, stg[i * 33 + lane]);
+            for (int i = 0; i < 32; ++i)
+              __stcg(dst + (int64_t)i * ws_ld, ptx::lds32(stg_s + 4 * (i * 33 + lane)));
           }
           __syncwarp();
         }
@@ -555,6 +578,30 @@ int set_smem_attr() {
   return ACCT_OK;
 }
 
+// fill the machine: split K until tiles x splits covers the SMs, keeping
+// >= 2 k-blocks per split so the pipeline has something to overlap
+void plan_splits(int tiles, int total_kb, int sms, int *splits_out, int *kb_per_out) {
+  int splits = 1;
+  if (tiles < sms) {
+    splits = sms / tiles;
+    if (splits > total_kb / 2) splits = total_kb / 2;
+    if (splits < 1) splits = 1;
+  }
+  const int kb_per = (total_kb + splits - 1) / splits;
+  *splits_out = (total_kb + kb_per - 1) / kb_per;
+  *kb_per_out = kb_per;
+}
+
+// critical-path estimate of a normal-orientation launch with TN-wide tiles:
+// waves x k-blocks per unit x TN (MMA time per k-block grows with TN)
+int64_t tile_cost(int M, int N, int K, int TN, int BK, int sms) {
+  const int tiles = ((M + 127) / 128) * ((N + TN - 1) / TN);
+  int splits, kb_per;
+  plan_splits(tiles, (K + BK - 1) / BK, sms, &splits, &kb_per);
+  const int64_t waves = ((int64_t)tiles * splits + sms - 1) / sms;
+  return waves * kb_per * BK * TN;
+}
+
 template <int TN, bool SWAP, int BK>
 int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
               int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
@@ -571,16 +618,8 @@ int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, con
   const int nt = (N + tile_n - 1) / tile_n, mt = (M + tile_m - 1) / tile_m, tiles = mt * nt;
   const int total_kb = (K + BK - 1) / BK;
   const int sms = sm_count();
-  // fill the machine: split K until tiles x splits covers the SMs, keeping
-  // >= 2 k-blocks per split so the pipeline has something to overlap
-  int splits = 1;
-  if (tiles < sms) {
-    splits = sms / tiles;
-    if (splits > total_kb / 2) splits = total_kb / 2;
-    if (splits < 1) splits = 1;
-  }
-  const int kb_per = (total_kb + splits - 1) / splits;
-  splits = (total_kb + kb_per - 1) / kb_per;
+  int splits, kb_per;
+  plan_splits(tiles, total_kb, sms, &splits, &kb_per);
   const int units = tiles * splits;
 
   float *ws = nullptr;
@@ -615,11 +654,28 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
   if (M <= 16) return launch_tc<16, true, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (M <= 32) return launch_tc<32, true, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (M <= 64) return launch_tc<64, true, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
-  if (N > 128 && N <= 192)
-    return launch_tc<192, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
-  return launch_tc<128, false, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  static const int force = [] {
+    const char *e = getenv("ACCT_TC_TILE");
+    return e ? atoi(e) : 0;
+  }();
+  if (force == 1) return launch_tc<192, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (force == 2) return launch_tc<128, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (force == 3) return launch_tc<128, false, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (force == 4) return launch_tc<256, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  // 128 x 192 or 128 x 256 tiles, BK = 16: whichever has the shorter critical
+  // path after wave quantisation and split-K (tools/gemm_bench.py: 192 wins
+  // when it fills the SMs without a split, 256 when both need splits)
+  const int sms = sm_count();
+  if (tile_cost(M, N, K, 256, 16, sms) < tile_cost(M, N, K, 192, 16, sms))
+    return launch_tc<256, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  return launch_tc<192, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
 }
 
 }  // namespace acct
 
 extern "C" void acct_tc_set_write_hi(int on) { acct::g_write_hi = on; }
+
+extern "C" int acct_tc_trace(long long *out) {
+  return acct::check_cuda(cudaMemcpyFromSymbol(out, acct::g_trace, sizeof(acct::g_trace)),
+                          "tc trace");
+}

@@ -73,6 +73,9 @@ int gemm_simt(int M, int N, int K, float alpha, const float *A, int64_t lda, con
 int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
             int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
             cudaStream_t s);
+int gemm_stream(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
+                int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
+                cudaStream_t s);
 
 }  // namespace acct
 
@@ -215,6 +218,12 @@ extern "C" int acct_gemm_nn_f32(int M, int N, int K, float alpha, const float *A
     return fail(ACCT_EINVAL, "gemm_nn: bad activation");
   if ((int64_t)M * N == 0) return ACCT_OK;
   cudaStream_t s = as_stream(stream);
+  // M <= 16 (the first conv layer): an HBM stream of B and C with ~0.2
+  // flop/byte -- CUDA cores near the HBM roofline beat 16-row MMA tiles
+  if (mode == ACCT_GEMM_AUTO && M <= 16) {
+    int rc = gemm_stream(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+    if (rc != ACCT_ENOTSUP) return rc;
+  }
   if (mode == ACCT_GEMM_TC3XTF32 || mode == ACCT_GEMM_AUTO) {
     int rc = gemm_tc(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
     if (rc != ACCT_ENOTSUP || mode == ACCT_GEMM_TC3XTF32) return rc;

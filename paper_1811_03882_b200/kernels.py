@@ -94,6 +94,7 @@ SIGNATURES = {
     "acct_schedule_capture": [C.POINTER(ArraySlot), _i32, C.POINTER(Action), _i32, _i32, _vp,
                               C.POINTER(C.c_void_p)],
     "acct_graph_replay": [_vp, _vp, _i32],
+    "acct_tc_trace": [_vp],
 }
 VOID_FUNCS = {"acct_counters_get": [C.POINTER(Counters)], "acct_counters_reset": [],
               "acct_graph_destroy": [_vp], "acct_tc_set_write_hi": [_i32]}

@@ -10,7 +10,9 @@ lib = K.lib()
 SHAPES = [(16, 173056, 27), (32, 43264, 144), (64, 10816, 288), (128, 2704, 576), (256, 676, 1152),
           (512, 169, 2304), (1024, 169, 4608), (512, 169, 9216), (425, 169, 512), (4096, 4096, 4096)]
 flag_sets = [int(f) for f in sys.argv[1].split(",")] if len(sys.argv) > 1 else [0]
-modes = {"tc": K.GEMM_TC3XTF32, "simt": K.GEMM_SIMT}
+if len(sys.argv) > 2:   # "MxNxK,MxNxK,..."
+    SHAPES = [tuple(int(v) for v in t.split("x")) for t in sys.argv[2].split(",")]
+modes = {"tc": K.GEMM_TC3XTF32, "simt": K.GEMM_SIMT, "auto": K.GEMM_AUTO}
 for (M, N, Kd) in SHAPES:
     ldA, ldB = -(-Kd // 32) * 32, -(-N // 32) * 32
     A = torch.rand(M, ldA, device="cuda") - 0.5

@@ -70,28 +70,41 @@ int g_write_hi = 0;
 // back with acct_tc_trace -- pipeline analysis only (tools/tc_trace.py)
 constexpr int kTrace = 512;
 __device__ long long g_trace[8][kTrace];
-// bits 8-15 of the same word: L2 prefetch distance in k-blocks (ACCT_TC_PF, default 8)
+// bits 8-15 of the same word: L2 prefetch distance in k-blocks (ACCT_TC_PF,
+// default 0: measured slower for every net shape -- the ring is not HBM-latency bound)
 int prefetch_distance() {
   static const int pf = [] {
     const char *e = getenv("ACCT_TC_PF");
-    int v = e ? atoi(e) : 8;
+    int v = e ? atoi(e) : 0;
     return v < 0 ? 0 : (v > 255 ? 255 : v);
   }();
   return pf;
 }
 
-template <int TN, int BK>
+// AT: the weight tile (MMA operand A) goes to TMEM -- the split warps read it
+// from shared memory once and store hi and lo with tcgen05.st, so the MMAs
+// read only B from shared memory.  Shared-memory bandwidth is the binding
+// limit of 3xTF32 on one SM (per 16-deep k-block: TMA 20 KB + split 40 KB +
+// MMA operand reads 60 KB vs 576 MMA cycles x 128 B/cycle), and AT cuts it
+// from 120 KB to 88 KB per k-block.
+template <int TN, int BK, bool AT>
 struct Cfg {
   static constexpr int X_TILE = 128 * BK * 4;
   static constexpr int Y_TILE = TN * BK * 4;
-  static constexpr int STAGE_BYTES = 2 * X_TILE + 2 * Y_TILE;  // raw(hi) + lo of both operands
+  // raw(hi) + lo of both operands; with AT the A lo lives in TMEM
+  static constexpr int STAGE_BYTES = (AT ? 1 : 2) * X_TILE + 2 * Y_TILE;
   static constexpr int BUDGET = 220 * 1024 - STAGING_BYTES - 512 - 1024;
-  static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 512 + 1024;
   // TMEM accumulator ring: 4 buffers when they fit in 512 columns, else 2
   static constexpr int NACC = 4 * TN <= 512 ? 4 : 2;
-  static constexpr uint32_t TMEM_COLS = NACC * TN <= 32 ? 32 : NACC * TN <= 64 ? 64
-                                       : NACC * TN <= 128 ? 128 : NACC * TN <= 256 ? 256 : 512;
+  static constexpr int SMEM_STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
+  // with AT each stage also holds 2 x BK TMEM columns (A hi, A lo)
+  static constexpr int TMEM_STAGES = AT ? (512 - NACC * TN) / (2 * BK) : 8;
+  static constexpr int STAGES = SMEM_STAGES < TMEM_STAGES ? SMEM_STAGES : TMEM_STAGES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 512 + 1024;
+  static constexpr int A_COL0 = NACC * TN;                    // first A-stage TMEM column
+  static constexpr int USED_COLS = NACC * TN + (AT ? STAGES * 2 * BK : 0);
+  static constexpr uint32_t TMEM_COLS = USED_COLS <= 32 ? 32 : USED_COLS <= 64 ? 64
+                                       : USED_COLS <= 128 ? 128 : USED_COLS <= 256 ? 256 : 512;
   // K-major operand (rows x BK fp32)
   static constexpr uint32_t KROW = BK * 4;                    // 128 or 64 bytes
   static constexpr uint32_t K_LAYOUT = BK == 32 ? ptx::kLayoutSW128 : 4u /*SWIZZLE_64B*/;
@@ -99,6 +112,13 @@ struct Cfg {
   // MN-major operand (BK rows x 32-column chunks)
   static constexpr uint32_t MN_CHUNK = BK * 128;              // LBO between 32-col chunks
   static_assert(STAGES >= 2, "tile does not fit shared memory");
+  static_assert(USED_COLS <= 512, "TMEM overflow");
+};
+
+template <int TN, bool SWAP, int BK>
+struct Pick {
+  static constexpr bool AT = (!SWAP && TN == 192 && BK == 16) || (SWAP && BK == 32);
+  using G = Cfg<TN, BK, AT>;
 };
 
 __device__ __forceinline__ float4 split_lo(float4 v, float4 &hi) {
@@ -142,15 +162,17 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                float alpha, float beta, float *__restrict__ C, int64_t ldc,
                const float *__restrict__ bias, int act, float *__restrict__ ws, int64_t ws_ld,
                int64_t ws_split_stride) {
-  using G = Cfg<TN, BK>;
+  using G = typename Pick<TN, SWAP, BK>::G;
+  constexpr bool AT = Pick<TN, SWAP, BK>::AT;
   constexpr int S = G::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
+  constexpr int XB = (AT ? 1 : 2) * G::X_TILE;  // x bytes per stage (AT: no x lo)
   auto x_hi = [&](int s) { return base + s * G::STAGE_BYTES; };
   auto x_lo = [&](int s) { return base + s * G::STAGE_BYTES + G::X_TILE; };
-  auto y_hi = [&](int s) { return base + s * G::STAGE_BYTES + 2 * G::X_TILE; };
-  auto y_lo = [&](int s) { return base + s * G::STAGE_BYTES + 2 * G::X_TILE + G::Y_TILE; };
+  auto y_hi = [&](int s) { return base + s * G::STAGE_BYTES + XB; };
+  auto y_lo = [&](int s) { return base + s * G::STAGE_BYTES + XB + G::Y_TILE; };
   float *staging = reinterpret_cast<float *>(base + S * G::STAGE_BYTES);
   uint64_t *full = reinterpret_cast<uint64_t *>(base + S * G::STAGE_BYTES + STAGING_BYTES);
   uint64_t *conv = full + S;
@@ -242,7 +264,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_tf32(128, TN, SWAP, !SWAP);
+      // operand A from TMEM has no major-ness (lane = row, column = k)
+      constexpr uint32_t idesc = ptx::idesc_tf32(128, TN, SWAP && !AT, !SWAP);
       int g = 0, j = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
         const Unit w = unit_of<TN, SWAP, BK>(u, nt, tiles, kb_per, total_kb);
@@ -257,6 +280,27 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           ptx::tc_fence_after();
           const uint32_t xh = ptx::smem_u32(x_hi(s)), xl = ptx::smem_u32(x_lo(s));
           const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
+          if constexpr (AT) {
+            // A hi / lo of this stage in TMEM columns, 8 per k step
+            const uint32_t at = tmem + G::A_COL0 + s * 2 * BK;
+#pragma unroll
+            for (int k = 0; k < BK / 8; ++k) {
+              // B: MN-major activations (normal) or K-major weights (swap)
+              const uint64_t dyh =
+                  SWAP ? ptx::smem_desc(yh + 32 * k, 16, G::K_SBO, G::K_LAYOUT)
+                       : ptx::smem_desc(yh + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
+              const uint64_t dyl =
+                  SWAP ? ptx::smem_desc(yl + 32 * k, 16, G::K_SBO, G::K_LAYOUT)
+                       : ptx::smem_desc(yl + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
+              if (write_hi & 4) continue;
+              ptx::mma_tf32_ts(d, at + 8 * k, dyh, idesc, (kb | k) != 0);
+              ptx::mma_tf32_ts(d, at + 8 * k, dyl, idesc, 1);
+              ptx::mma_tf32_ts(d, at + BK + 8 * k, dyh, idesc, 1);
+            }
+            ptx::mma_commit(&empty[s]);
+            if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace) g_trace[4][g] = clock64();
+            continue;
+          }
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {
             // K-major: 8 tf32 (32 B) per step inside a row; MN-major
@@ -297,7 +341,63 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace && ct == 0) g_trace[1][g] = clock64();
         const uint32_t xh = ptx::smem_u32(x_hi(s)), xl = ptx::smem_u32(x_lo(s));
         const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
-        if (!(write_hi & 2)) {
+        if (AT && !(write_hi & 2)) {
+          // operand A (the x tile) -> this stage's TMEM columns, hi then lo.
+          // Warp q may write TMEM lanes 32q..32q+31 = MMA rows 32q + lane:
+          //  normal: weight row r, its BK values from the SWIZZLE_64B K-major
+          //          tile (16-B chunk c of row r at r*64 + (c ^ (r/2 % 4))*16);
+          //  swap:   activation column n = 32q + lane of 32-column chunk q,
+          //          SWIZZLE_128B_BASE32B MN-major (k-row of 128 B, 32-B
+          //          pieces XOR k % 4): one conflict-free 128-B row per k.
+          const int q = warp & 3;
+          constexpr int NA = BK;  // A values per thread (one MMA row, BK deep)
+          uint32_t hi[NA], lo[NA];
+          if constexpr (!SWAP) {
+            const int row = 32 * q + lane;
+            float4 ra[NA / 4];
+#pragma unroll
+            for (int c = 0; c < NA / 4; ++c)
+              ra[c] = ptx::lds128(xh + row * 64 + ((c ^ ((row >> 1) & 3)) << 4));
+#pragma unroll
+            for (int c = 0; c < NA / 4; ++c) {
+              const float v[4] = {ra[c].x, ra[c].y, ra[c].z, ra[c].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const uint32_t h = __float_as_uint(v[e]) & 0xFFFFE000u;
+                hi[4 * c + e] = h;
+                lo[4 * c + e] = __float_as_uint(v[e] - __uint_as_float(h));
+              }
+            }
+          } else {
+            const uint32_t cb = xh + q * G::MN_CHUNK + ((lane & 7) << 2);
+            float va[NA];
+#pragma unroll
+            for (int k = 0; k < NA; ++k)
+              va[k] = ptx::lds32(cb + k * 128 + ((((lane >> 3) ^ k) & 3) << 5));
+#pragma unroll
+            for (int k = 0; k < NA; ++k) {
+              const uint32_t h = __float_as_uint(va[k]) & 0xFFFFE000u;
+              hi[k] = h;
+              lo[k] = __float_as_uint(va[k] - __uint_as_float(h));
+            }
+          }
+          constexpr int NY = (G::Y_TILE / 16 + 127) / 128;
+          float4 ry[NY];
+#pragma unroll
+          for (int i = 0; i < NY; ++i)
+            if (ct + 128 * i < G::Y_TILE / 16) ry[i] = ptx::lds128(yh + 16 * (ct + 128 * i));
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + G::A_COL0 + s * 2 * BK;
+          ptx::tmem_st_cols<NA>(ta, hi);
+          ptx::tmem_st_cols<NA>(ta + BK, lo);
+#pragma unroll
+          for (int i = 0; i < NY; ++i) {
+            if (ct + 128 * i < G::Y_TILE / 16) {
+              float4 h4;
+              ptx::sts128(yl + 16 * (ct + 128 * i), split_lo(ry[i], h4));
+            }
+          }
+          ptx::tmem_st_wait();
+        } else if (!(write_hi & 2)) {
           // every load of the stage in flight before the first store
           constexpr int NX = G::X_TILE / 16 / 128;
           constexpr int NY = (G::Y_TILE / 16 + 127) / 128;
@@ -326,6 +426,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
         if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace && ct == 0) g_trace[6][g] = clock64();
         ptx::fence_proxy_async_smem();  // generic-proxy writes -> tensor core
+        if (AT) ptx::tc_fence_before();  // tcgen05.st -> the MMA issuer's thread sync
         if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace && ct == 0) g_trace[7][g] = clock64();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&conv[s]);
@@ -570,7 +671,7 @@ int set_smem_attr() {
   if (dev >= 0 && dev < 64 && !done[dev]) {
     if (int rc = check_cuda(cudaFuncSetAttribute(tc_gemm_kernel<TN, SWAP, BK>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 Cfg<TN, BK>::SMEM_BYTES),
+                                                 Pick<TN, SWAP, BK>::G::SMEM_BYTES),
                             "gemm_tc: smem attribute"))
       return rc;
     done[dev] = true;
@@ -606,7 +707,7 @@ template <int TN, bool SWAP, int BK>
 int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
               int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
               cudaStream_t s) {
-  using G = Cfg<TN, BK>;
+  using G = typename Pick<TN, SWAP, BK>::G;
   CUtensorMap ta, tb;
   const uint32_t a_rows = SWAP ? TN : 128;  // weights: K-major box (BK k) x rows
   const CUtensorMapSwizzle kswz = BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;

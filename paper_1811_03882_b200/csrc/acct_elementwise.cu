@@ -309,6 +309,61 @@ __global__ void maxpool_rows_kernel(const float *__restrict__ in, int64_t ld_in,
   }
 }
 
+// 2x2 / stride 2 windows fully inside the image (even height and width,
+// off = 0 -- every pooling layer of the nets but the 13x13 stride-1 one): a
+// thread owns V consecutive outputs of one output row, reads its two input
+// rows as V/2 float4 each and writes V outputs + V int32 indexes as one
+// vector store each.  Same compare order and strict '>' as the scalar loop.
+template <int V>
+__global__ void maxpool2s2_kernel(const float *__restrict__ in, int64_t ld_in, int64_t in_bs,
+                                  int width, int out_h, int out_w, int channels,
+                                  float *__restrict__ out, int64_t ld_out, int64_t out_bs,
+                                  int32_t *__restrict__ idx, int64_t ld_idx, int64_t idx_bs,
+                                  int plane) {
+  pdl_trigger();
+  pdl_wait();
+  const int img = blockIdx.z / channels, c = blockIdx.z - img * channels;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= out_h) return;
+  const float *r0 = in + img * in_bs + (int64_t)c * ld_in + (int64_t)(2 * i) * width;
+  const float *r1 = r0 + width;
+  float *o = out + img * out_bs + (int64_t)c * ld_out + (int64_t)i * out_w;
+  int32_t *x = idx + img * idx_bs + (int64_t)c * ld_idx + (int64_t)i * out_w;
+  const int base0 = c * plane + 2 * i * width;
+  for (int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * V; j0 < out_w;
+       j0 += gridDim.x * blockDim.x * V) {
+    float a[2 * V], b[2 * V];
+#pragma unroll
+    for (int q = 0; q < V / 2; ++q) {
+      const float4 u = __ldcs(reinterpret_cast<const float4 *>(r0 + 2 * j0) + q);
+      const float4 w = __ldcs(reinterpret_cast<const float4 *>(r1 + 2 * j0) + q);
+      a[4 * q] = u.x; a[4 * q + 1] = u.y; a[4 * q + 2] = u.z; a[4 * q + 3] = u.w;
+      b[4 * q] = w.x; b[4 * q + 1] = w.y; b[4 * q + 2] = w.z; b[4 * q + 3] = w.w;
+    }
+    float best[V];
+    int32_t arg[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const int col = 2 * (j0 + e);
+      float m = -FLT_MAX;
+      int32_t k = -1;
+      if (a[2 * e] > m) { m = a[2 * e]; k = base0 + col; }
+      if (a[2 * e + 1] > m) { m = a[2 * e + 1]; k = base0 + col + 1; }
+      if (b[2 * e] > m) { m = b[2 * e]; k = base0 + width + col; }
+      if (b[2 * e + 1] > m) { m = b[2 * e + 1]; k = base0 + width + col + 1; }
+      best[e] = m;
+      arg[e] = k;
+    }
+    if (V == 4) {
+      __stcs(reinterpret_cast<float4 *>(o + j0), make_float4(best[0], best[1], best[2], best[3]));
+      __stcs(reinterpret_cast<int4 *>(x + j0), make_int4(arg[0], arg[1], arg[2], arg[3]));
+    } else {
+      __stcs(reinterpret_cast<float2 *>(o + j0), make_float2(best[0], best[1]));
+      __stcs(reinterpret_cast<int2 *>(x + j0), make_int2(arg[0], arg[1]));
+    }
+  }
+}
+
 bool vec_ok(const void *p, int64_t ld, int64_t cols) {
   return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && ld % 4 == 0 && ld >= ((cols + 3) / 4) * 4;
 }
@@ -472,6 +527,29 @@ extern "C" int acct_maxpool_batched_f32(const float *in, int64_t ld_in, int64_t 
   if (channels > 65535 || (int64_t)channels * ld_in >= kMaxElems)
     return fail(ACCT_ENOTSUP, "maxpool: too large for 32-bit indexing");
   cudaStream_t s = as_stream(stream);
+  auto aligned = [](const void *p, int64_t ld, int64_t bs, int a) {
+    return (reinterpret_cast<uintptr_t>(p) % (4 * a)) == 0 && ld % a == 0 && bs % a == 0;
+  };
+  if (size == 2 && stride == 2 && off == 0 && height == 2 * out_h && width == 2 * out_w &&
+      out_w % 2 == 0 && batch_ok(batch, channels) && aligned(in, ld_in, in_stride, 4) &&
+      width % 4 == 0) {
+    const int v = (out_w % 4 == 0 && aligned(out, ld_out, out_stride, 4) &&
+                   aligned(idx, ld_idx, idx_stride, 4)) ? 4 : 2;
+    if (v == 4 || (aligned(out, ld_out, out_stride, 2) && aligned(idx, ld_idx, idx_stride, 2))) {
+      const int groups = out_w / v;
+      const int bx = groups >= 32 ? 32 : (groups >= 16 ? 16 : 8);
+      const dim3 block(bx, 256 / bx);
+      const dim3 grid((unsigned)((groups + bx - 1) / bx), (unsigned)((out_h + block.y - 1) / block.y),
+                      (unsigned)(channels * batch));
+      if (v == 4)
+        launch(maxpool2s2_kernel<4>, grid, block, 0, s, in, ld_in, in_stride, width, out_h, out_w,
+               channels, out, ld_out, out_stride, idx, ld_idx, idx_stride, height * width);
+      else
+        launch(maxpool2s2_kernel<2>, grid, block, 0, s, in, ld_in, in_stride, width, out_h, out_w,
+               channels, out, ld_out, out_stride, idx, ld_idx, idx_stride, height * width);
+      return note_launch("maxpool");
+    }
+  }
   if (out_w >= 32 && batch_ok(batch, channels)) {
     const dim3 block(32, 8);
     const dim3 grid((unsigned)((out_w + 31) / 32), (unsigned)((out_h + 7) / 8),

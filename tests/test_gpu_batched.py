@@ -113,3 +113,20 @@ def test_batched_kernel_entries_match_single(cuda_device):
     for b in range(P):
         assert torch.equal(out_b[:, b * 64:b * 64 + 20], out_1[b][:, :20])
         assert torch.equal(idx_b[:, b * 64:b * 64 + 20], idx_1[b][:, :20])
+    # the vectorised 2x2/2 path (8x16 -> 4x8 per channel)
+    h2, w2, ld2 = 8, 16, 128
+    im2 = torch.randn(P, c, ld2, device="cuda")
+    ob = torch.zeros(c, P * 32, device="cuda")
+    ib = torch.zeros(c, P * 32, dtype=torch.int32, device="cuda")
+    o1 = torch.zeros(P, c, 32, device="cuda")
+    i1 = torch.zeros(P, c, 32, dtype=torch.int32, device="cuda")
+    assert lib.acct_maxpool_batched_f32(im2.data_ptr(), ld2, c * ld2, c, h2, w2, 2, 2, 0, 4, 8,
+                                        ob.data_ptr(), P * 32, 32, ib.data_ptr(), P * 32, 32, P,
+                                        s) == 0
+    for b in range(P):
+        assert lib.acct_maxpool_f32(im2[b].data_ptr(), ld2, c, h2, w2, 2, 2, 0, 4, 8,
+                                    o1[b].data_ptr(), 32, i1[b].data_ptr(), 32, s) == 0
+    torch.cuda.synchronize()
+    for b in range(P):
+        assert torch.equal(ob[:, b * 32:b * 32 + 32], o1[b])
+        assert torch.equal(ib[:, b * 32:b * 32 + 32], i1[b])

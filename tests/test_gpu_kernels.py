@@ -112,7 +112,9 @@ def test_im2col_bit_exact(cuda_device, orc, c, h, w, k, s, pad):
 
 
 @pytest.mark.parametrize("c,h,w,size,stride", [(16, 416, 416, 2, 2), (512, 13, 13, 2, 1),
-                                                (3, 7, 9, 2, 2), (2, 5, 5, 3, 2)])
+                                                (3, 7, 9, 2, 2), (2, 5, 5, 3, 2),
+                                                (32, 52, 52, 2, 2), (64, 104, 104, 2, 2),
+                                                (8, 26, 26, 2, 2), (4, 12, 20, 2, 2)])
 def test_maxpool_values_and_indices_bit_exact(cuda_device, orc, c, h, w, size, stride):
     x0 = _rand((c, h * w), 31)
     x0[:, 1::7] = x0[:, 0::7][:, : x0[:, 1::7].shape[1]]  # plant ties

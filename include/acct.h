@@ -176,7 +176,10 @@ enum {
                               i[2]=executions this action stands for (0 = 1) */
   ACCT_A_H2D = 4,          /* slot a[0]: host -> device (pitched); i[0]=first image,
                               i[1]=images (0 = 1), i[2]=transfers counted (0 = 1) */
-  ACCT_A_D2H = 5,          /* slot a[0]: device -> host (pitched); same operands */
+  ACCT_A_D2H = 5,          /* slot a[0]: device -> host (pitched); same operands, plus
+                              i[3] = 1: early copyout -- may run on a side stream
+                              concurrently with the actions that follow (the compiler
+                              places it after the array's last writer) */
   ACCT_A_BIND = 6,         /* slot a[0].host (i[2]=0) or .dev (i[2]=1) = base + loopvar(i[0]) * i[1]
                               bytes: load_input / per-image output slots */
   ACCT_A_STORE = 7,        /* memcpy(base + loopvar(i[0]) * i[1], slot a[0].host) (store_output) */
@@ -247,9 +250,14 @@ int acct_schedule_capture(acct_array_t *arrays, int n_arrays, const acct_action_
 int acct_graph_replay(acct_graph_t *graph, acct_stream_t stream, int synchronize);
 void acct_graph_destroy(acct_graph_t *graph);
 
-/* tensor-core gemm: 1 = store the TF32 hi part explicitly, 0 (default) =
- * leave raw FP32 in shared memory (the MMA truncates); for verification */
+/* tensor-core gemm debug word: bit 0 = store the TF32 hi part explicitly
+ * (default: leave raw FP32 in shared memory, the MMA truncates); bits 1-3
+ * skip the split / MMA / epilogue (timing only, results wrong); bit 4 =
+ * record CTA 0's pipeline events; for verification and tools/ only */
 void acct_tc_set_write_hi(int on);
+/* copy the event trace of the last bit-4 launch: 8 x 512 int64 clock64
+ * stamps (TMA issue, landed, split done, MMA in, commit, split parts) */
+int acct_tc_trace(long long *out);
 
 /* library/device facts */
 int acct_device_sm_count(int device);

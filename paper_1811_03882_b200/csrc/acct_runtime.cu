@@ -403,11 +403,32 @@ namespace {
 // main stream waits on an array's event only right before the first action
 // that touches that array -- so layer 12's weights stream in while layers
 // 0-11 compute.  One per host thread and device (thread_local).
+//
+// A second side stream `d` carries early copyouts (D2H actions flagged
+// i[3] = 1 by the compiler: the array's final value exists once its last
+// writer ran), so device->host traffic overlaps the remaining kernels and the
+// host->device stream (PCIe is full duplex).  Its staged copies use their own
+// scratch, `dstage`, never the arrays' shared staging buffer.
 struct SideXfer {
   int device = -1;
-  cudaStream_t t = nullptr;
-  cudaEvent_t fork = nullptr, done = nullptr;
+  cudaStream_t t = nullptr, d = nullptr;
+  cudaEvent_t fork = nullptr, done = nullptr, dfork = nullptr, ddone = nullptr;
   std::vector<cudaEvent_t> ev;
+  void *dstage = nullptr;
+  size_t dstage_bytes = 0;
+  int ensure_dstage(size_t bytes, bool capturing) {
+    if (bytes <= dstage_bytes) return ACCT_OK;
+    if (capturing) return fail(ACCT_ENOTSUP, "early copyout scratch grows during capture");
+    if (dstage) {
+      cudaDeviceSynchronize();
+      cudaFree(dstage);
+    }
+    dstage = nullptr;
+    dstage_bytes = 0;
+    if (int rc = check_cuda(cudaMalloc(&dstage, bytes), "early copyout scratch")) return rc;
+    dstage_bytes = bytes;
+    return ACCT_OK;
+  }
   int ensure(int n) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -416,15 +437,24 @@ struct SideXfer {
       ev.clear();
       cudaEventDestroy(fork);
       cudaEventDestroy(done);
+      cudaEventDestroy(dfork);
+      cudaEventDestroy(ddone);
       cudaStreamDestroy(t);
-      t = nullptr;
+      cudaStreamDestroy(d);
+      t = d = nullptr;
+      dstage = nullptr;  // belongs to the old device's context; not reused
+      dstage_bytes = 0;
     }
     if (!t) {
       device = dev;
       if (int rc = check_cuda(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking), "side stream"))
         return rc;
+      if (int rc = check_cuda(cudaStreamCreateWithFlags(&d, cudaStreamNonBlocking), "d2h stream"))
+        return rc;
       cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
       cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&dfork, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&ddone, cudaEventDisableTiming);
     }
     while ((int)ev.size() < n) {
       cudaEvent_t e;
@@ -474,8 +504,16 @@ int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *action
     return check_cuda(cudaStreamWaitEvent(s, side->ev[slot], 0), "side wait");
   };
 
+  bool dforked = false;  // early copyouts in flight on side->d
+  auto join_d2h = [&]() -> int {
+    if (!dforked) return ACCT_OK;
+    dforked = false;
+    if (int rc = check_cuda(cudaEventRecord(side->ddone, side->d), "d2h join record")) return rc;
+    return check_cuda(cudaStreamWaitEvent(s, side->ddone, 0), "d2h join wait");
+  };
   auto drain = [&]() -> int {
     if (int rc = join_all()) return rc;
+    if (int rc = join_d2h()) return rc;
     if (!pending || capturing) return ACCT_OK;
     pending = false;
     return check_cuda(cudaStreamSynchronize(s), "schedule: stream sync");
@@ -556,6 +594,18 @@ int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *action
               rc = check_cuda(cudaEventRecord(side->ev[a.a[0]], side->t), "side event record");
               waiting[a.a[0]] = 1;
             }
+          } else if (a.i[3] == 1 && defer) {
+            // early copyout on the d2h side stream, ordered after everything
+            // issued so far on the main stream
+            if ((rc = need(a.a[0]))) return rc;
+            if (staged && (rc = side->ensure_dstage((size_t)rows * x.cols * 4, capturing))) return rc;
+            if ((rc = check_cuda(cudaEventRecord(side->dfork, s), "d2h fork record"))) return rc;
+            if ((rc = check_cuda(cudaStreamWaitEvent(side->d, side->dfork, 0), "d2h fork wait")))
+              return rc;
+            dforked = true;
+            acct_stream_t on = reinterpret_cast<acct_stream_t>(side->d);
+            rc = staged ? acct_d2h_staged(host, dev, x.ld_dev, rows, x.cols, side->dstage, on)
+                        : acct_memcpy2d(host, row, dev, dp, row, (size_t)rows, 2, on);
           } else {
             if ((rc = need(a.a[0]))) return rc;
             if (staged && (rc = join_all())) return rc;

@@ -372,6 +372,8 @@ class PatternExecutor:
         leave(img)
         acts.append((K.A_SYNC, (), ()))
         expected = self._expected_counters(plan, acts)
+        if bp and host_ops == 0:
+            acts = self._overlap_transfers(acts, single_pass=self.images // p == 1)
         sched = self._pack(bits, acts, plan, expected)
         sched.batch = p
         if bp:
@@ -414,6 +416,73 @@ class PatternExecutor:
         if bp:
             sched.slots = self._batched_table(p, bp[1])
         return sched
+
+    @staticmethod
+    def _written_slots(act) -> tuple:
+        """Array slots a KERNEL action writes."""
+        kind, slots = act[2][0], act[1]
+        if kind in (K.K_FILL, K.K_ADD_BIAS, K.K_LEAKY, K.K_LINEAR):
+            return (slots[0],)
+        if kind in (K.K_COPY, K.K_IM2COL):
+            return (slots[1],)
+        if kind == K.K_GEMM:
+            return (slots[2],)
+        if kind == K.K_MAXPOOL:
+            return (slots[1], slots[2])
+        return ()
+
+    def _overlap_transfers(self, acts: list, single_pass: bool) -> list:
+        """Reorder the transfers of an all-device schedule for overlap; the
+        set of transfers, their directions and counts are unchanged.
+
+        * hoisted copyins in front of the image loop (all at one program
+          point, so their mutual order is free) go out in order of first use
+          in the loop body -- the runner streams them on a side stream and
+          each kernel waits only for its own operands;
+        * when the loop body runs once (one batch = every image), a hoisted
+          copyout after the loop moves up to just after the last kernel that
+          writes the array (no later action changes it), flagged early: the
+          runner issues it on a device->host side stream while the remaining
+          layers compute.
+        """
+        begin = next(i for i, a in enumerate(acts) if a[0] == K.A_LOOP_BEGIN)
+        end = next(i for i, a in enumerate(acts) if a[0] == K.A_LOOP_END)
+        pre, body, post = list(acts[:begin]), list(acts[begin + 1:end]), list(acts[end + 1:])
+        first_use: dict[int, int] = {}
+        for i, a in enumerate(body):
+            for slot in a[1]:
+                if slot is not None and slot >= 0:
+                    first_use.setdefault(slot, i)
+        h2d = [a for a in pre if a[0] == K.A_H2D]
+        rest = [a for a in pre if a[0] != K.A_H2D]
+        h2d.sort(key=lambda a: first_use.get(a[1][0], len(body)))
+        pre = rest + h2d
+        if single_pass:
+            last_write: dict[int, int] = {}
+            for i, a in enumerate(body):
+                if a[0] == K.A_KERNEL:
+                    for slot in self._written_slots(a):
+                        last_write[slot] = i
+            inserts: dict[int, list] = {}
+            kept = []
+            for a in post:
+                if a[0] == K.A_D2H and a[1][0] in last_write:
+                    ints = tuple(a[2]) + (0,) * (4 - len(a[2]))
+                    early = (a[0], a[1], ints[:3] + (1,) + ints[4:])
+                    inserts.setdefault(last_write[a[1][0]], []).append(early)
+                else:
+                    kept.append(a)
+            new_body = []
+            for i, a in enumerate(body):
+                new_body.append(a)
+                new_body.extend(inserts.get(i, ()))
+            body, post = new_body, kept
+        trip = acts[begin][2][0]
+        out = pre + [None] + body + [None] + post
+        b, e = len(pre), len(pre) + 1 + len(body)
+        out[b] = (K.A_LOOP_BEGIN, (), (trip, e))
+        out[e] = (K.A_LOOP_END, (), (b,))
+        return out
 
     def _fusion_plan(self, plan: TransferPlan, chosen: set) -> dict:
         """Per conv layer, fuse offloaded fill -> gemm -> add_bias -> activation

@@ -521,6 +521,44 @@ int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *action
   auto check_slot = [&](int k) { return k >= 0 && k < n_arrays; };
   Counters &cnt = counters();
   int pc = 0;
+  // ACCT_TRACE=1 (uncaptured runs): an event after every transfer / kernel
+  // action on the stream it went to; elapsed ms from the start to stderr
+  static const bool trace = getenv("ACCT_TRACE") != nullptr;
+  struct Mark {
+    int pc;
+    char where;
+    cudaEvent_t ev;
+  };
+  std::vector<Mark> marks;
+  cudaEvent_t trace0 = nullptr;
+  if (trace && !capturing && !prof) {
+    cudaEventCreate(&trace0);
+    cudaEventRecord(trace0, s);
+  }
+  auto mark = [&](int at, const acct_action_t &a) {
+    if (!trace0) return;
+    cudaStream_t on = s;
+    char where = 'm';
+    if (a.kind == ACCT_A_H2D && defer && in_prefix) on = side->t, where = 'h';
+    if (a.kind == ACCT_A_D2H && a.i[3] == 1 && defer) on = side->d, where = 'd';
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, on);
+    marks.push_back({at, where, e});
+  };
+  auto dump = [&]() {
+    if (!trace0) return;
+    cudaDeviceSynchronize();
+    for (auto &m : marks) {
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, trace0, m.ev);
+      const acct_action_t &a = actions[m.pc];
+      fprintf(stderr, "trace %8.3f ms %c pc=%3d kind=%d slot=%d op=%lld\n", ms, m.where, m.pc,
+              a.kind, a.a[0], (long long)a.i[0]);
+      cudaEventDestroy(m.ev);
+    }
+    cudaEventDestroy(trace0);
+  };
   while (pc < n_actions) {
     const acct_action_t &a = actions[pc];
     int rc = ACCT_OK;
@@ -568,7 +606,10 @@ int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *action
         // image-major copies ([n][rows][ld]) move as one block of n * rows rows
         const bool block = n == 1 || x.img_stride == x.rows * x.ld_dev;
         const int64_t rows = block ? n * x.rows : x.rows;
-        const bool staged = x.stage && x.ld_dev != x.cols;
+        // staging only where the pitched copy is slow: H2D rows < 4 KB run at
+        // 5-14 GB/s as 2-D copies vs ~50 GB/s dense (tools/xfer_probe.py);
+        // D2H 2-D copies stay >= 30 GB/s down to 676-B rows, so never staged
+        const bool staged = a.kind == ACCT_A_H2D && x.stage && x.ld_dev != x.cols && row < 4096;
         const int64_t h2d0 = cnt.h2d_calls.load(), d2h0 = cnt.d2h_calls.load();
         for (int64_t b = 0; b < (block ? 1 : n) && rc == ACCT_OK; ++b) {
           char *dev = dev0 + b * x.img_stride * 4;
@@ -668,9 +709,13 @@ int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *action
         return fail(ACCT_EINVAL, "schedule: unknown action");
     }
     if (rc != ACCT_OK) return rc;
+    if (trace0 && (a.kind == ACCT_A_H2D || a.kind == ACCT_A_D2H || a.kind == ACCT_A_KERNEL))
+      mark(pc, a);
     ++pc;
   }
-  return drain();  // host-only schedules never touch the CUDA runtime
+  const int rc = drain();  // host-only schedules never touch the CUDA runtime
+  dump();
+  return rc;
 }
 
 }  // namespace

@@ -78,6 +78,7 @@ class Schedule:
     graph: object = None                  # acct_graph_t* once captured (all-GPU schedules)
     graph_failed: bool = False
     batch: int = 1                        # images per launch of the image loop's body
+    transfers: bool = False               # any H2D / D2H action
     slots: object = None                  # slot table of a batched schedule (None = base)
 
 
@@ -626,7 +627,9 @@ class PatternExecutor:
                                "out": self.output_batch.data_ptr(),
                                "devin": getattr(self, "device_batch", None).data_ptr()
                                if act[3] == "devin" else 0}[act[3]]
-        return Schedule(bits, arr, len(acts), plan, expected)
+        sched = Schedule(bits, arr, len(acts), plan, expected)
+        sched.transfers = any(a[0] in (K.A_H2D, K.A_D2H) for a in acts)
+        return sched
 
     # ------------------------------------------------------------ run
     def _table(self, schedule: Schedule):
@@ -671,8 +674,13 @@ class PatternExecutor:
             rc, seconds = go(0)
         else:
             with self.torch.cuda.device(self.device):
-                if (self.graphs and not profile and schedule.host_ops == 0 and schedule.runs >= 1
-                        and not schedule.graph_failed):
+                # graphs pay off for launch-bound schedules (image at a time, or
+                # batched without transfers); a batched schedule with transfers
+                # is PCIe-bound and its side-stream copies ran ~6% slower as
+                # graph memcpy nodes (tools/e2e_probe.py)
+                launch_bound = schedule.batch == 1 or not schedule.transfers
+                if (self.graphs and launch_bound and not profile and schedule.host_ops == 0
+                        and schedule.runs >= 1 and not schedule.graph_failed):
                     return self._replay(schedule, timeout_s)
                 rc, seconds = go(self.stream.cuda_stream)
         self._restore_slots(p)

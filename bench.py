@@ -76,16 +76,35 @@ def dist_env():
 
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock + throttle reasons while the timed legs run: NVML polled from a
+    thread every ~2 ms (the value leg is only tens of ms long), falling back to
+    `nvidia-smi -lms 100` when NVML is unavailable."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event-reason bits
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
         self.lines: list[str] = []
+        self.samples: list[tuple] = []
+        self.stop = threading.Event()
+        self.nvml = None
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.nvml = (pynvml, h)
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:  # noqa: BLE001 -- no NVML: use nvidia-smi
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
@@ -97,11 +116,27 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv, h = self.nvml
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop.is_set():
+            try:
+                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx,
+                                     int(get_reasons(h))))
+            except Exception:  # noqa: BLE001
+                break
+            time.sleep(0.002)
+
     def _pump(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self.stop.set()
+        if self.nvml is not None:
+            self.thread.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -113,6 +148,10 @@ class ClockSampler:
     def summary(self) -> dict:
         sm, mx, reasons = [], [], set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for clk, top, bits in self.samples:
+            sm.append(float(clk))
+            mx.append(float(top))
+            reasons.update(n for n, b in self.BITS.items() if bits & b)
         for line in self.lines:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 6:
@@ -127,7 +166,7 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 # ----------------------------------------------------------- cpu baseline
@@ -199,43 +238,78 @@ def run_reference(args):
 
 
 # -------------------------------------------------------------------- ours
+def ncu_traffic(shape: str):
+    """dram bytes (read + write) per launch of the kernel launch with this
+    gemm shape, from the committed `ncu --set full` summaries in profiles/
+    (lines `shape = MxNxK` ... `dram__bytes_read.sum = X Mbyte` ...)."""
+    for path in sorted((REPO / "profiles").glob("r*_ncu_full*.txt")):
+        cur, rd, wr = None, None, None
+        for line in path.read_text().splitlines():
+            if line.startswith("shape = "):
+                cur, rd, wr = line.split("=", 1)[1].strip(), None, None
+            elif line.startswith("dram__bytes_read.sum = ") and cur == shape:
+                rd = float(line.split()[2])
+            elif line.startswith("dram__bytes_write.sum = ") and cur == shape:
+                wr = float(line.split()[2])
+            if rd is not None and wr is not None:
+                return {"bytes": (rd + wr) * 1e6, "source": path.name}
+    return None
+
+
 def roofline(ex, sched, steps: int, flush, peaks: dict) -> dict:
+    """Roofline of the dominant kernel launch of one resident step: its
+    algorithmic flops (2MNK) or bytes over its average launch
+    duration, timed live with CUDA events on the launch stream."""
     import torch
-    per_kind_ms: dict[str, float] = {}
-    per_kind_work: dict[str, dict] = {}
-    launches: dict[str, int] = {}
+    per_action: dict[int, float] = {}
     for _ in range(steps):
         with torch.cuda.stream(ex.stream):
             flush.zero_()
         r = ex.run(sched, profile=True)
         for k, ms in enumerate(r.kernel_ms):
-            if sched.actions[k].kind != 8 or ms <= 0:
-                continue
-            info = ex.action_op(sched, k)
-            kind = info["kind"] + ("+epilogue" if info.get("fused") else "")
-            per_kind_ms[kind] = per_kind_ms.get(kind, 0.0) + ms
-            w = per_kind_work.setdefault(kind, {"flops": 0, "bytes": 0})
-            w["flops"] += info["flops"] * info["executions"]
-            w["bytes"] += info["bytes"] * info["executions"]
-            launches[kind] = launches.get(kind, 0) + info["executions"]
-    total = sum(per_kind_ms.values())
-    top = max(per_kind_ms, key=per_kind_ms.get)
-    ms, work, n = per_kind_ms[top], per_kind_work[top], launches[top]
-    if work["flops"]:
-        achieved = work["flops"] / (ms * 1e-3) / 1e12
+            if sched.actions[k].kind == 8 and ms > 0:
+                per_action[k] = per_action.get(k, 0.0) + ms
+    infos = {k: ex.action_op(sched, k) for k in per_action}
+    per_kind_ms: dict[str, float] = {}
+    per_kind_work: dict[str, dict] = {}
+    for k, ms in per_action.items():
+        info = infos[k]
+        kind = info["kind"] + ("+epilogue" if info.get("fused") else "")
+        per_kind_ms[kind] = per_kind_ms.get(kind, 0.0) + ms
+        w = per_kind_work.setdefault(kind, {"flops": 0, "bytes": 0})
+        w["flops"] += info["flops"] * info["executions"] * steps
+        w["bytes"] += info["bytes"] * info["executions"] * steps
+    total = sum(per_action.values())
+    top = max(per_action, key=per_action.get)
+    info = infos[top]
+    launches = info["executions"] * steps
+    launch_s = per_action[top] * 1e-3 / launches
+    if info["flops"]:
+        shape = f"{info['M']}x{info['N_launch']}x{info['K']}"
+        achieved = info["flops"] / launch_s / 1e12
         peak = peaks.get("bf16_tflops")
         out = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                "frac": achieved / peak if peak else None,
-               "peak_note": "measured dense bf16 (MEASURED_PEAKS.json); FP32 gemm via 3xTF32 "
-                            "tops out near bf16/6"}
+               "peak_note": "measured dense bf16 burst (MEASURED_PEAKS.json); FP32-accurate gemm "
+                            "via 3xTF32 = 3 tf32 MMAs (half bf16 rate) per FP32 MAC, so its "
+                            "ceiling is peak/6",
+               "frac_of_3xtf32_ceiling": achieved / (peak / 6) if peak else None}
     else:
-        achieved = work["bytes"] / (ms * 1e-3) / 1e9
+        shape = None
+        achieved = info["bytes"] / launch_s / 1e9
         peak = peaks.get("hbm_gbs")
         out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                "frac": achieved / peak if peak else None}
-    out.update({"kernel": top, "share_of_step": ms / total if total else None,
-                "launches_per_step": n // steps, "traffic": None,
-                "algorithmic_per_launch": (work["flops"] or work["bytes"]) / n,
+    traffic = ncu_traffic(shape) if shape else None
+    name = f"{info['kind']} layer {info['layer']}" + (
+        f" M{info['M']} N{info['N_launch']} K{info['K']} ({info['images']} images per launch)"
+        if info["flops"] else "")
+    out.update({"kernel": name, "share_of_step": per_action[top] / total if total else None,
+                "launches_per_step": info["executions"],
+                "algorithmic_per_launch": info["flops"] or info["bytes"],
+                "launch_us": launch_s * 1e6,
+                "traffic": traffic["bytes"] if traffic else None,
+                "traffic_source": traffic["source"] if traffic else None,
                 "per_kind_ms_per_step": {k: v / steps for k, v in sorted(per_kind_ms.items())},
                 "per_kind_hbm_gbs": {k: per_kind_work[k]["bytes"] / (per_kind_ms[k] * 1e-3) / 1e9
                                      for k in per_kind_ms},

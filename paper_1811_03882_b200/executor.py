@@ -741,7 +741,10 @@ class PatternExecutor:
             # the weights are read once per launch, whatever the batch
             byts = 4 * M * Kd + nimg * (4 * Kd * N + c_bytes * M * N) + bias
             op = next(o for o in ops if o.kind == "gemm" and o.arrays["C"] == slots[a.a[2]].name)
+            # the launch's column count: images interleaved at the array pitch
+            n_launch = (nimg - 1) * _pitch(N) + N if nimg > 1 else N
             return {"kind": "gemm", "layer": op.layer, "M": M, "N": N, "K": Kd, "images": nimg,
+                    "N_launch": n_launch,
                     "executions": execs, "flops": 2 * M * N * Kd * nimg, "bytes": byts,
                     "fused": a.a[3] >= 0 or i[4] == 0}
         target = slots[a.a[0]].name

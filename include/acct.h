@@ -258,6 +258,10 @@ void acct_tc_set_write_hi(int on);
 /* copy the event trace of the last bit-4 launch: 8 x 512 int64 clock64
  * stamps (TMA issue, landed, split done, MMA in, commit, split parts) */
 int acct_tc_trace(long long *out);
+/* force the normal-orientation tile of the tensor-core gemm (0 = the cost
+ * model; 1 = 128x192, 2/3 = 128x128 BK 16/32, 4 = 128x256, 5/6/7 = CTA pair
+ * 256x192 / 256x256 / 256x128); tests and tools only                       */
+void acct_tc_set_tile(int tile);
 
 /* library/device facts */
 int acct_device_sm_count(int device);

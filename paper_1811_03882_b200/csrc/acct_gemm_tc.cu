@@ -46,6 +46,7 @@
 
 #include <cuda.h>
 
+#include <atomic>
 #include <mutex>
 #include <unordered_map>
 
@@ -66,6 +67,19 @@ constexpr int STAGING_BYTES = EPI_GROUPS * 4 * 32 * 33 * 4;  // normal-tile epil
 // profiling knobs that skip the split / MMA / epilogue work (results are then
 // wrong; tools/gemm_bench.py only).
 int g_write_hi = 0;
+// normal-orientation tile override (0 = cost model; tests/tools only):
+// 1 = 128x192 (A in TMEM), 2 = 128x128 BK16, 3 = 128x128 BK32, 4 = 128x256,
+// 5/6/7 = CTA pair 256x192 / 256x256 / 256x128.  Initialised from ACCT_TC_TILE.
+std::atomic<int> g_force_tile{-1};
+int forced_tile() {
+  int v = g_force_tile.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char *e = getenv("ACCT_TC_TILE");
+    v = e ? atoi(e) : 0;
+    g_force_tile.store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
 // bit 4: event trace of CTA 0's first kTrace stages (clock64 per role), read
 // back with acct_tc_trace -- pipeline analysis only (tools/tc_trace.py)
 constexpr int kTrace = 512;
@@ -530,6 +544,269 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 1) ptx::tmem_dealloc(tmem, G::TMEM_COLS);
 }
 
+// ------------------------------------------------------------------ CTA pairs
+// 2-CTA (cta_group::2) variant of the normal orientation: a CTA pair computes
+// a 256 x TN tile -- CTA r owns weight rows m0 + 128 r (operand A, hi/lo in
+// its own TMEM) and B columns n0 + r TN/2 .. (its half of operand B, raw + lo
+// in its shared memory).  The leader (rank 0) issues
+// `tcgen05.mma.cta_group::2` with M = 256; each tensor core reads its own B
+// half and the pair exchanges them, so per SM and 16-deep k-block the
+// shared-memory traffic is TMA 8 + TN/8 KB, split 8 + TN/8...:
+// 52 KB at TN = 192 against 576 MMA cycles, under the 128 B/clk port.
+// Synchronisation:
+//   full[s]      local: TMA bytes of this CTA's stage landed
+//   conv[s]      LEADER: split done in both CTAs (8 warp arrivals, cluster scope)
+//   empty[s]     local in both: MMA commit multicast to the pair
+//   acc_full[a]  local in both: unit's last MMA commit multicast
+//   acc_empty[a] LEADER: both CTAs' epilogue warps drained accumulator a (8)
+template <int TN, int NACC_>
+struct Cfg2 {
+  static constexpr int BK = 16;
+  static constexpr int HALF = TN / 2;
+  static constexpr int X_TILE = 128 * BK * 4;
+  static constexpr int Y_TILE = HALF * BK * 4;
+  static constexpr int STAGE_BYTES = X_TILE + 2 * Y_TILE;
+  static constexpr int NACC = NACC_;
+  static constexpr int BUDGET = 220 * 1024 - STAGING_BYTES - 512 - 1024;
+  static constexpr int SMEM_STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
+  static constexpr int TMEM_STAGES = (512 - NACC * TN) / (2 * BK);
+  static constexpr int STAGES = SMEM_STAGES < TMEM_STAGES ? SMEM_STAGES : TMEM_STAGES;
+  static constexpr int A_COL0 = NACC * TN;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 512 + 1024;
+  static constexpr uint32_t MN_CHUNK = BK * 128;
+  static_assert(HALF % 32 == 0, "B half must be whole 32-column chunks");
+  static_assert(STAGES >= 2, "pipeline too shallow");
+};
+
+template <int TN, int NACC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                int M, int N, int K, int nt, int mt, int splits, int kb_per, int write_hi,
+                float alpha, float beta, float *__restrict__ C, int64_t ldc,
+                const float *__restrict__ bias, int act, float *__restrict__ ws, int64_t ws_ld,
+                int64_t ws_split_stride) {
+  using G = Cfg2<TN, NACC>;
+  constexpr int S = G::STAGES, BK = G::BK;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  auto x_hi = [&](int s) { return base + s * G::STAGE_BYTES; };
+  auto y_hi = [&](int s) { return base + s * G::STAGE_BYTES + G::X_TILE; };
+  auto y_lo = [&](int s) { return base + s * G::STAGE_BYTES + G::X_TILE + G::Y_TILE; };
+  float *staging = reinterpret_cast<float *>(base + S * G::STAGE_BYTES);
+  uint64_t *full = reinterpret_cast<uint64_t *>(base + S * G::STAGE_BYTES + STAGING_BYTES);
+  uint64_t *conv = full + S;
+  uint64_t *empty = conv + S;
+  uint64_t *acc_full = empty + S;
+  uint64_t *acc_empty = acc_full + NACC;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + NACC);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = ptx::cluster_rank();
+  const int pair = blockIdx.x / 2, pairs = gridDim.x / 2;
+  const int tiles = nt * mt, units = tiles * splits;
+  const int total_kb = (K + BK - 1) / BK;
+  auto unit = [&](int u) {
+    Unit w;
+    w.split = u / tiles;
+    const int t = u - w.split * tiles;
+    const int tm = t / nt, tn = t - tm * nt;
+    w.n0 = tn * TN;
+    w.m0 = tm * 256;
+    w.kb0 = w.split * kb_per;
+    w.nkb = min(w.kb0 + kb_per, total_kb) - w.kb0;
+    return w;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&conv[s], 8);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < NACC; ++a) {
+      ptx::mbar_init(&acc_full[a], 1);
+      ptx::mbar_init(&acc_empty[a], 8);
+    }
+    ptx::fence_mbar_init();
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+  }
+  if (warp == 1) ptx::tmem_alloc2(tmem_slot, 512);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();  // barriers initialised and TMEM allocated in both CTAs
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs: their own A rows, B half) ----------------
+    if (lane == 0) {
+      int g = 0;
+      for (int u = pair; u < units; u += pairs) {
+        const Unit w = unit(u);
+        const int m_rows = w.m0 + 128 * rank, n_half = w.n0 + rank * G::HALF;
+        for (int kb = 0; kb < w.nkb; ++kb, ++g) {
+          const int s = g % S;
+          if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
+          ptx::mbar_expect_tx(&full[s], G::X_TILE + G::Y_TILE);
+          const int kx = (w.kb0 + kb) * BK;
+          ptx::tma_load_2d(x_hi(s), &tmA, &full[s], kx, m_rows);
+#pragma unroll
+          for (int c = 0; c < G::HALF / 32; ++c)
+            ptx::tma_load_2d(y_hi(s) + c * G::MN_CHUNK, &tmB, &full[s], n_half + 32 * c, kx);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader only) ----------------
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_tf32(256, TN, false, true);
+      int g = 0, j = 0;
+      for (int u = pair; u < units; u += pairs, ++j) {
+        const Unit w = unit(u);
+        const int a = j % NACC;
+        if (j >= NACC) ptx::mbar_wait_cluster(&acc_empty[a], ((j / NACC) - 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t d = tmem + a * TN;
+        for (int kb = 0; kb < w.nkb; ++kb, ++g) {
+          const int s = g % S;
+          ptx::mbar_wait_cluster(&conv[s], (g / S) & 1);
+          ptx::tc_fence_after();
+          const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
+          const uint32_t at = tmem + G::A_COL0 + s * 2 * BK;
+#pragma unroll
+          for (int k = 0; k < BK / 8; ++k) {
+            const uint64_t dyh =
+                ptx::smem_desc(yh + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
+            const uint64_t dyl =
+                ptx::smem_desc(yl + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
+            if (write_hi & 4) continue;
+            ptx::mma2_tf32_ts(d, at + 8 * k, dyh, idesc, (kb | k) != 0);
+            ptx::mma2_tf32_ts(d, at + 8 * k, dyl, idesc, 1);
+            ptx::mma2_tf32_ts(d, at + BK + 8 * k, dyh, idesc, 1);
+          }
+          ptx::mma2_commit_multicast(&empty[s], 0x3);
+        }
+        ptx::mma2_commit_multicast(&acc_full[a], 0x3);
+      }
+    }
+    __syncwarp();
+  } else if (warp < 6) {
+    // ---------------- split (both CTAs): A -> own TMEM hi/lo, B half lo ----------------
+    const int ct = threadIdx.x - 64;
+    const int q = warp & 3, row = 32 * q + lane;
+    const uint32_t conv_leader = ptx::mapa(ptx::smem_u32(&conv[0]), 0);
+    int g = 0;
+    for (int u = pair; u < units; u += pairs) {
+      const Unit w = unit(u);
+      for (int kb = 0; kb < w.nkb; ++kb, ++g) {
+        const int s = g % S;
+        ptx::mbar_wait(&full[s], (g / S) & 1);
+        const uint32_t xh = ptx::smem_u32(x_hi(s));
+        const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
+        if (!(write_hi & 2)) {
+          float4 ra[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            ra[c] = ptx::lds128(xh + row * 64 + ((c ^ ((row >> 1) & 3)) << 4));
+          constexpr int NY = (G::Y_TILE / 16 + 127) / 128;
+          float4 ry[NY];
+#pragma unroll
+          for (int i = 0; i < NY; ++i)
+            if (ct + 128 * i < G::Y_TILE / 16) ry[i] = ptx::lds128(yh + 16 * (ct + 128 * i));
+          uint32_t hi[16], lo[16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float v[4] = {ra[c].x, ra[c].y, ra[c].z, ra[c].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t h = __float_as_uint(v[e]) & 0xFFFFE000u;
+              hi[4 * c + e] = h;
+              lo[4 * c + e] = __float_as_uint(v[e] - __uint_as_float(h));
+            }
+          }
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + G::A_COL0 + s * 2 * BK;
+          ptx::tmem_st_32x32b_x16(ta, hi);
+          ptx::tmem_st_32x32b_x16(ta + BK, lo);
+#pragma unroll
+          for (int i = 0; i < NY; ++i) {
+            if (ct + 128 * i < G::Y_TILE / 16) {
+              float4 h4;
+              ptx::sts128(yl + 16 * (ct + 128 * i), split_lo(ry[i], h4));
+            }
+          }
+          ptx::tmem_st_wait();
+        }
+        ptx::fence_proxy_async_smem_cluster();  // B lo -> the pair's tensor cores
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(conv_leader + 8 * s);
+      }
+    }
+  } else {
+    // ---------------- epilogue (both CTAs: their 128 rows x TN) ----------------
+    const int q = warp & 3;
+    const int grp = (warp - 6) / 4;
+    const uint32_t stg_s = ptx::smem_u32(staging + (grp * 4 + q) * (32 * 33));
+    const uint32_t acc_empty_leader = ptx::mapa(ptx::smem_u32(&acc_empty[0]), 0);
+    int j = 0;
+    for (int u = pair; u < units; u += pairs, ++j) {
+      if ((j % EPI_GROUPS) != grp) continue;
+      const Unit w = unit(u);
+      const int a = j % NACC;
+      ptx::mbar_wait_sleepy(&acc_full[a], (j / NACC) & 1);
+      ptx::tc_fence_after();
+      const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * TN;
+      float *part = ws + w.split * ws_split_stride;
+      const int row0 = w.m0 + 128 * rank + 32 * q;
+      if (!(write_hi & 8)) {
+        for (int c = 0; c < TN / 32; ++c) {
+          uint32_t r[32];
+          ptx::tmem_ld_32x32b_x32(trow + 32 * c, r);
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) ptx::sts32(stg_s + 4 * (lane * 33 + jj), __uint_as_float(r[jj]));
+          __syncwarp();
+          const int col = w.n0 + 32 * c + lane;
+          if (splits == 1) {
+            const float my_bias = (bias && row0 + lane < M) ? __ldg(bias + row0 + lane) : 0.0f;
+            float bv[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) bv[i] = __shfl_sync(0xffffffffu, my_bias, i);
+            if (col < N) {
+              float cv[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                cv[i] = (beta != 0.0f && row0 + i < M) ? C[(int64_t)(row0 + i) * ldc + col] : 0.0f;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const int row = row0 + i;
+                if (row < M)
+                  C[(int64_t)row * ldc + col] = finish(ptx::lds32(stg_s + 4 * (i * 33 + lane)), alpha,
+                                                       beta, cv[i], bias, bv[i], act);
+              }
+            }
+          } else {
+            float *dst = part + (int64_t)row0 * ws_ld + col;
+#pragma unroll 8
+            for (int i = 0; i < 32; ++i)
+              __stcg(dst + (int64_t)i * ws_ld, ptx::lds32(stg_s + 4 * (i * 33 + lane)));
+          }
+          __syncwarp();
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(acc_empty_leader + 8 * a);
+    }
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();  // the leader's last MMAs (into both TMEMs) are drained
+  if (warp == 1) ptx::tmem_dealloc2(tmem, 512);
+}
+
 // Sum the split-K partials of every output element in split order and apply
 // the epilogue (grid-wide, one thread per 4 consecutive columns).
 __global__ void __launch_bounds__(256)
@@ -743,6 +1020,66 @@ int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, con
   return ACCT_OK;
 }
 
+template <int TN, int NACC>
+int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
+               int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
+               cudaStream_t s) {
+  using G = Cfg2<TN, NACC>;
+  CUtensorMap ta, tb;
+  if (!cached_map(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, 16, 128,
+                  CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !cached_map(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, 32, 16,
+                  CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+    return fail(ACCT_ENOTSUP, "gemm_tc2: cuTensorMapEncodeTiled failed");
+  const int nt = (N + TN - 1) / TN, mt = (M + 255) / 256, tiles = mt * nt;
+  const int total_kb = (K + 15) / 16;
+  const int pairs_avail = sm_count() / 2;
+  int splits, kb_per;
+  plan_splits(tiles, total_kb, pairs_avail, &splits, &kb_per);
+  const int units = tiles * splits;
+  float *ws = nullptr;
+  const int64_t ws_ld = (int64_t)nt * TN, rows = (int64_t)mt * 256;
+  if (splits > 1) {
+    if (int rc = scratch_for(s, (size_t)splits * rows * ws_ld, &ws)) return rc;
+  }
+  {
+    static std::mutex mu;
+    static bool done[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev >= 0 && dev < 64 && !done[dev]) {
+      if (int rc = check_cuda(cudaFuncSetAttribute(tc2_gemm_kernel<TN, NACC>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   G::SMEM_BYTES),
+                              "gemm_tc2: smem attribute"))
+        return rc;
+      done[dev] = true;
+    }
+  }
+  const int pairs = units < pairs_avail ? units : pairs_avail;
+  launch(tc2_gemm_kernel<TN, NACC>, dim3(2 * pairs), dim3(THREADS), G::SMEM_BYTES, s, ta, tb, M,
+         N, K, nt, mt, splits, kb_per, g_write_hi, alpha, beta, C, ldc, bias, act, ws, ws_ld,
+         rows * ws_ld);
+  if (int rc = note_launch("gemm_tc2")) return rc;
+  if (splits > 1) {
+    const int64_t work = (int64_t)M * ((N + 3) / 4);
+    launch(splitk_reduce_kernel, dim3(grid_for(work, 256)), dim3(256), 0, s, (const float *)ws, ws_ld,
+           rows * ws_ld, splits, M, N, alpha, beta, C, ldc, bias, act);
+    if (int rc = note_launch("gemm_tc_splitk_reduce")) return rc;
+  }
+  return ACCT_OK;
+}
+
+// critical path of a CTA-pair launch (each SM: 128 rows x TN per k-block)
+int64_t tile_cost2(int M, int N, int K, int TN, int pairs) {
+  const int tiles = ((M + 255) / 256) * ((N + TN - 1) / TN);
+  int splits, kb_per;
+  plan_splits(tiles, (K + 15) / 16, pairs, &splits, &kb_per);
+  const int64_t waves = ((int64_t)tiles * splits + pairs - 1) / pairs;
+  return waves * kb_per * 16 * TN;
+}
+
 }  // namespace
 
 int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
@@ -755,14 +1092,14 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
   if (M <= 16) return launch_tc<16, true, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (M <= 32) return launch_tc<32, true, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (M <= 64) return launch_tc<64, true, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
-  static const int force = [] {
-    const char *e = getenv("ACCT_TC_TILE");
-    return e ? atoi(e) : 0;
-  }();
+  const int force = forced_tile();
   if (force == 1) return launch_tc<192, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (force == 2) return launch_tc<128, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (force == 3) return launch_tc<128, false, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (force == 4) return launch_tc<256, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (force == 5) return launch_tc2<192, 2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (force == 6) return launch_tc2<256, 1>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (force == 7) return launch_tc2<128, 2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   // 128 x 192 or 128 x 256 tiles, BK = 16: whichever has the shorter critical
   // path after wave quantisation and split-K (tools/gemm_bench.py: 192 wins
   // when it fills the SMs without a split, 256 when both need splits)
@@ -775,6 +1112,8 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
 }  // namespace acct
 
 extern "C" void acct_tc_set_write_hi(int on) { acct::g_write_hi = on; }
+
+extern "C" void acct_tc_set_tile(int tile) { acct::g_force_tile.store(tile < 0 ? 0 : tile); }
 
 extern "C" int acct_tc_trace(long long *out) {
   return acct::check_cuda(cudaMemcpyFromSymbol(out, acct::g_trace, sizeof(acct::g_trace)),

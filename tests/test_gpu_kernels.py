@@ -197,3 +197,33 @@ def test_kernel_launches_are_counted(cuda_device):
     K.activate(y.ptr, y.ld, 4, 40, K.ACT_LEAKY, stream())
     torch.cuda.synchronize()
     assert K.counters()["kernel_launches"] == 2
+
+
+TILE_SHAPES = [(128, 2704, 576), (256, 676, 1152), (512, 169, 2304), (425, 169, 512),
+               (130, 129, 33), (200, 300, 64), (300, 1000, 100), (512, 3049, 2304),
+               (1024, 520, 4608)]
+
+
+@pytest.mark.parametrize("tile", [1, 2, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("M,N,K_", TILE_SHAPES)
+def test_every_tensor_core_tile_within_tolerance(cuda_device, orc, tile, M, N, K_):
+    """Each normal-orientation tile variant, forced: 1-CTA 128x{192 (A in
+    TMEM), 128, 256} and CTA-pair (cta_group::2) 256x{192, 256, 128}, with
+    ragged M/N/K, split-K and the fused epilogue (bias + leaky)."""
+    A0, B0 = _rand((M, K_), 71, -0.5, 0.5), _rand((K_, N), 72)
+    bias0 = _rand((M,), 73)
+    want = np.zeros((M, N), np.float32)
+    orc.orc_gemm_nn(M, N, K_, 1.0, A0.ctypes.data, K_, B0.ctypes.data, N, want.ctypes.data, N)
+    want = want + bias0[:, None]
+    want = np.where(want < 0, (0.1 * want.astype(np.float64)).astype(np.float32), want)
+    A, B = Pitched(A0), Pitched(B0)
+    bias = torch.from_numpy(bias0).cuda()
+    Cd = Pitched(np.full((M, N), 7.0, np.float32))
+    try:
+        K.lib().acct_tc_set_tile(tile)
+        K.gemm_nn(M, N, K_, 1.0, A.ptr, A.ld, B.ptr, B.ld, 0.0, Cd.ptr, Cd.ld, bias.data_ptr(),
+                  K.ACT_LEAKY, K.GEMM_TC3XTF32, stream())
+        torch.cuda.synchronize()
+    finally:
+        K.lib().acct_tc_set_tile(0)
+    gemm_ok(Cd.numpy(), want)

@@ -559,9 +559,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 //   empty[s]     local in both: MMA commit multicast to the pair
 //   acc_full[a]  local in both: unit's last MMA commit multicast
 //   acc_empty[a] LEADER: both CTAs' epilogue warps drained accumulator a (8)
-template <int TN, int NACC_>
+__device__ __forceinline__ long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return (long long)t;
+}
+
+template <int TN, int NACC_, int BK_>
 struct Cfg2 {
-  static constexpr int BK = 16;
+  static constexpr int BK = BK_;
   static constexpr int HALF = TN / 2;
   static constexpr int X_TILE = 128 * BK * 4;
   static constexpr int Y_TILE = HALF * BK * 4;
@@ -574,18 +580,20 @@ struct Cfg2 {
   static constexpr int A_COL0 = NACC * TN;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 512 + 1024;
   static constexpr uint32_t MN_CHUNK = BK * 128;
+  static constexpr int ROWB = BK * 4;  // K-major A row bytes: 64 (SWIZZLE_64B) or 128 (128B)
+  static_assert(BK == 16 || BK == 32, "BK");
   static_assert(HALF % 32 == 0, "B half must be whole 32-column chunks");
   static_assert(STAGES >= 2, "pipeline too shallow");
 };
 
-template <int TN, int NACC>
+template <int TN, int NACC, int BK_>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 int M, int N, int K, int nt, int mt, int splits, int kb_per, int write_hi,
                 float alpha, float beta, float *__restrict__ C, int64_t ldc,
                 const float *__restrict__ bias, int act, float *__restrict__ ws, int64_t ws_ld,
                 int64_t ws_split_stride) {
-  using G = Cfg2<TN, NACC>;
+  using G = Cfg2<TN, NACC, BK_>;
   constexpr int S = G::STAGES, BK = G::BK;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -621,7 +629,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&conv[s], 8);
+      ptx::mbar_init(&conv[s], 8);  // leader: 4 split warps of each CTA
       ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < NACC; ++a) {
@@ -650,6 +658,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
           const int s = g % S;
           if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
+          if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace) g_trace[0][g] = gtimer();
           ptx::mbar_expect_tx(&full[s], G::X_TILE + G::Y_TILE);
           const int kx = (w.kb0 + kb) * BK;
           ptx::tma_load_2d(x_hi(s), &tmA, &full[s], kx, m_rows);
@@ -672,7 +681,8 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const uint32_t d = tmem + a * TN;
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
           const int s = g % S;
-          ptx::mbar_wait_cluster(&conv[s], (g / S) & 1);
+          ptx::mbar_wait(&conv[s], (g / S) & 1);
+          if ((write_hi & 16) && g < kTrace && blockIdx.x == 0) g_trace[3][g] = gtimer();
           ptx::tc_fence_after();
           const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
           const uint32_t at = tmem + G::A_COL0 + s * 2 * BK;
@@ -688,6 +698,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             ptx::mma2_tf32_ts(d, at + BK + 8 * k, dyh, idesc, 1);
           }
           ptx::mma2_commit_multicast(&empty[s], 0x3);
+          if ((write_hi & 16) && g < kTrace && blockIdx.x == 0) g_trace[4][g] = gtimer();
         }
         ptx::mma2_commit_multicast(&acc_full[a], 0x3);
       }
@@ -704,21 +715,26 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       for (int kb = 0; kb < w.nkb; ++kb, ++g) {
         const int s = g % S;
         ptx::mbar_wait(&full[s], (g / S) & 1);
+        if ((write_hi & 16) && blockIdx.x < 2 && g < kTrace && ct == 0)
+          g_trace[blockIdx.x == 0 ? 1 : 5][g] = gtimer();
         const uint32_t xh = ptx::smem_u32(x_hi(s));
         const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
         if (!(write_hi & 2)) {
-          float4 ra[4];
+          // row r of the K-major A tile: 16-B chunk c at r*ROWB + (c ^ swz(r))*16,
+          // swz = (r/2)%4 for SWIZZLE_64B rows, r%8 for SWIZZLE_128B rows
+          float4 ra[BK / 4];
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            ra[c] = ptx::lds128(xh + row * 64 + ((c ^ ((row >> 1) & 3)) << 4));
+          for (int c = 0; c < BK / 4; ++c)
+            ra[c] = ptx::lds128(xh + row * G::ROWB +
+                                ((c ^ (BK == 16 ? ((row >> 1) & 3) : (row & 7))) << 4));
           constexpr int NY = (G::Y_TILE / 16 + 127) / 128;
           float4 ry[NY];
 #pragma unroll
           for (int i = 0; i < NY; ++i)
             if (ct + 128 * i < G::Y_TILE / 16) ry[i] = ptx::lds128(yh + 16 * (ct + 128 * i));
-          uint32_t hi[16], lo[16];
+          uint32_t hi[BK], lo[BK];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < BK / 4; ++c) {
             const float v[4] = {ra[c].x, ra[c].y, ra[c].z, ra[c].w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -728,8 +744,8 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }
           }
           const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + G::A_COL0 + s * 2 * BK;
-          ptx::tmem_st_32x32b_x16(ta, hi);
-          ptx::tmem_st_32x32b_x16(ta + BK, lo);
+          ptx::tmem_st_cols<BK>(ta, hi);
+          ptx::tmem_st_cols<BK>(ta + BK, lo);
 #pragma unroll
           for (int i = 0; i < NY; ++i) {
             if (ct + 128 * i < G::Y_TILE / 16) {
@@ -739,21 +755,26 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           }
           ptx::tmem_st_wait();
         }
-        ptx::fence_proxy_async_smem_cluster();  // B lo -> the pair's tensor cores
+        ptx::fence_proxy_async_smem();  // B lo -> the pair's tensor cores
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(conv_leader + 8 * s);
+        if (lane == 0) ptx::mbar_arrive_remote(conv_leader + 8 * s);
+        if ((write_hi & 16) && blockIdx.x < 2 && g < kTrace && ct == 0)
+          g_trace[blockIdx.x == 0 ? 2 : 6][g] = gtimer();
       }
     }
   } else {
     // ---------------- epilogue (both CTAs: their 128 rows x TN) ----------------
+    // one group per accumulator at most: two groups sharing one accumulator
+    // barrier would wait on parities out of order
+    constexpr int GROUPS = NACC < EPI_GROUPS ? NACC : EPI_GROUPS;
     const int q = warp & 3;
     const int grp = (warp - 6) / 4;
     const uint32_t stg_s = ptx::smem_u32(staging + (grp * 4 + q) * (32 * 33));
     const uint32_t acc_empty_leader = ptx::mapa(ptx::smem_u32(&acc_empty[0]), 0);
     int j = 0;
     for (int u = pair; u < units; u += pairs, ++j) {
-      if ((j % EPI_GROUPS) != grp) continue;
+      if ((j % GROUPS) != grp) continue;
       const Unit w = unit(u);
       const int a = j % NACC;
       ptx::mbar_wait_sleepy(&acc_full[a], (j / NACC) & 1);
@@ -1020,19 +1041,19 @@ int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, con
   return ACCT_OK;
 }
 
-template <int TN, int NACC>
+template <int TN, int NACC, int BK>
 int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
                int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
                cudaStream_t s) {
-  using G = Cfg2<TN, NACC>;
+  using G = Cfg2<TN, NACC, BK>;
   CUtensorMap ta, tb;
-  if (!cached_map(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, 16, 128,
-                  CU_TENSOR_MAP_SWIZZLE_64B) ||
-      !cached_map(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, 32, 16,
+  if (!cached_map(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BK, 128,
+                  BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !cached_map(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, 32, BK,
                   CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
     return fail(ACCT_ENOTSUP, "gemm_tc2: cuTensorMapEncodeTiled failed");
   const int nt = (N + TN - 1) / TN, mt = (M + 255) / 256, tiles = mt * nt;
-  const int total_kb = (K + 15) / 16;
+  const int total_kb = (K + BK - 1) / BK;
   const int pairs_avail = sm_count() / 2;
   int splits, kb_per;
   plan_splits(tiles, total_kb, pairs_avail, &splits, &kb_per);
@@ -1049,7 +1070,7 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(mu);
     if (dev >= 0 && dev < 64 && !done[dev]) {
-      if (int rc = check_cuda(cudaFuncSetAttribute(tc2_gemm_kernel<TN, NACC>,
+      if (int rc = check_cuda(cudaFuncSetAttribute(tc2_gemm_kernel<TN, NACC, BK>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    G::SMEM_BYTES),
                               "gemm_tc2: smem attribute"))
@@ -1058,7 +1079,7 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
     }
   }
   const int pairs = units < pairs_avail ? units : pairs_avail;
-  launch(tc2_gemm_kernel<TN, NACC>, dim3(2 * pairs), dim3(THREADS), G::SMEM_BYTES, s, ta, tb, M,
+  launch(tc2_gemm_kernel<TN, NACC, BK>, dim3(2 * pairs), dim3(THREADS), G::SMEM_BYTES, s, ta, tb, M,
          N, K, nt, mt, splits, kb_per, g_write_hi, alpha, beta, C, ldc, bias, act, ws, ws_ld,
          rows * ws_ld);
   if (int rc = note_launch("gemm_tc2")) return rc;
@@ -1072,12 +1093,12 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
 }
 
 // critical path of a CTA-pair launch (each SM: 128 rows x TN per k-block)
-int64_t tile_cost2(int M, int N, int K, int TN, int pairs) {
+int64_t tile_cost2(int M, int N, int K, int TN, int BK, int pairs) {
   const int tiles = ((M + 255) / 256) * ((N + TN - 1) / TN);
   int splits, kb_per;
-  plan_splits(tiles, (K + 15) / 16, pairs, &splits, &kb_per);
+  plan_splits(tiles, (K + BK - 1) / BK, pairs, &splits, &kb_per);
   const int64_t waves = ((int64_t)tiles * splits + pairs - 1) / pairs;
-  return waves * kb_per * 16 * TN;
+  return waves * kb_per * BK * TN;
 }
 
 }  // namespace
@@ -1097,15 +1118,25 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
   if (force == 2) return launch_tc<128, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (force == 3) return launch_tc<128, false, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (force == 4) return launch_tc<256, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
-  if (force == 5) return launch_tc2<192, 2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
-  if (force == 6) return launch_tc2<256, 1>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
-  if (force == 7) return launch_tc2<128, 2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
-  // 128 x 192 or 128 x 256 tiles, BK = 16: whichever has the shorter critical
-  // path after wave quantisation and split-K (tools/gemm_bench.py: 192 wins
-  // when it fills the SMs without a split, 256 when both need splits)
+  if (force == 5) return launch_tc2<192, 2, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (force == 6) return launch_tc2<256, 1, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (force == 7) return launch_tc2<128, 2, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (force == 8) return launch_tc2<192, 1, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (force == 9) return launch_tc2<192, 1, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (force == 10) return launch_tc2<256, 1, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  // Candidates: one SM per 128 x 192 tile (operand A in TMEM), or a CTA pair
+  // per 256 x {192, 256} tile (cta_group::2, BK = 32).  Pick the shortest
+  // critical path -- waves x k-blocks per unit x TN after split-K -- with the
+  // single-SM tile weighted by its measured shared-memory-bound efficiency
+  // (743 vs ~590 cycles per 128x192x16 k-block, tools/tc_trace.py).
   const int sms = sm_count();
-  if (tile_cost(M, N, K, 256, 16, sms) < tile_cost(M, N, K, 192, 16, sms))
-    return launch_tc<256, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  const double c1 = 1.25 * (double)tile_cost(M, N, K, 192, 16, sms);
+  const double c9 = (double)tile_cost2(M, N, K, 192, 32, sms / 2);
+  const double c10 = (double)tile_cost2(M, N, K, 256, 32, sms / 2);
+  if (c10 < c9 && c10 < c1)
+    return launch_tc2<256, 1, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (c9 < c1)
+    return launch_tc2<192, 1, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   return launch_tc<192, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
 }
 

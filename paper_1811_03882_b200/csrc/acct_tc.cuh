@@ -272,6 +272,10 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+// remote arrive with the default semantics (as CUTLASS's ClusterBarrier::arrive)
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 // wait with acquire at cluster scope (arrivals released by the peer CTA)
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
   asm volatile(

@@ -34,7 +34,15 @@ for g in list(range(0, 12)) + list(range(n // 2, n // 2 + 8)):
     i, l, c, m, e = tr[:5, g]
     print(f"{g:4d} {i:7d} {l:7d} {c:6d} {m:7d} {e:7d} | {l - i:7d} {c - l:9d} {m - c:9d} {e - m:8d}")
 lat = tr[1] - tr[0]
-print(f"split parts: loads {np.median(tr[5] - tr[1]):.0f}  stores {np.median(tr[6] - tr[5]):.0f}  "
-      f"fence {np.median(tr[7] - tr[6]):.0f}  arrive {np.median(tr[2] - tr[7]):.0f}")
+if len(sys.argv) > 3:  # CTA-pair kernel: globaltimer ns; rows 5/6/7 = peer landed / split / relayed
+    print("   g  lead: issue landed split mma_in commit | peer: landed split relayed   (ns)")
+    for g in list(range(0, 10)) + list(range(n // 2, n // 2 + 6)):
+        print(f"{g:4d} " + " ".join(f"{int(v):7d}" for v in tr[:8, g]))
+    print(f"median ns: peer split {np.median(tr[6] - tr[5]):.0f}, relay after peer split "
+          f"{np.median(tr[7] - tr[6]):.0f}, leader mma_in after relay {np.median(tr[3] - tr[7]):.0f}, "
+          f"stage period {np.median(np.diff(tr[4][8:])):.0f}")
+else:
+    print(f"split parts: loads {np.median(tr[5] - tr[1]):.0f}  stores {np.median(tr[6] - tr[5]):.0f}  "
+          f"fence {np.median(tr[7] - tr[6]):.0f}  arrive {np.median(tr[2] - tr[7]):.0f}")
 print(f"median: tma {np.median(lat):.0f}  split {np.median(tr[2] - tr[1]):.0f}  "
       f"wait-for-mma {np.median(tr[3] - tr[2]):.0f}  mma-issue {np.median(tr[4] - tr[3]):.0f}")

@@ -284,8 +284,13 @@ def roofline(ex, sched, steps: int, flush, peaks: dict) -> dict:
     info = infos[top]
     launches = info["executions"] * steps
     launch_s = per_action[top] * 1e-3 / launches
-    if info["flops"]:
-        shape = f"{info['M']}x{info['N_launch']}x{info['K']}"
+    # the roofline that binds: FP32-accurate gemm (3xTF32) peaks at bf16/6; a
+    # launch whose arithmetic intensity is below that ceiling's ridge point
+    # (flop per HBM byte) is HBM-bound and is reported against HBM
+    ridge = (peaks.get("bf16_tflops", 1.0) / 6 * 1e12) / (peaks.get("hbm_gbs", 1.0) * 1e9)
+    tensor_bound = info["flops"] and info["flops"] / max(info["bytes"], 1) >= ridge
+    shape = (f"{info['M']}x{info['N_launch']}x{info['K']}" if info["flops"] else None)
+    if tensor_bound:
         achieved = info["flops"] / launch_s / 1e12
         peak = peaks.get("bf16_tflops")
         out = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -295,18 +300,21 @@ def roofline(ex, sched, steps: int, flush, peaks: dict) -> dict:
                             "ceiling is peak/6",
                "frac_of_3xtf32_ceiling": achieved / (peak / 6) if peak else None}
     else:
-        shape = None
         achieved = info["bytes"] / launch_s / 1e9
         peak = peaks.get("hbm_gbs")
         out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                "frac": achieved / peak if peak else None}
+        if info["flops"]:
+            out["note"] = (f"gemm below the 3xTF32 ridge ({info['flops'] / info['bytes']:.1f} "
+                           f"< {ridge:.1f} flop/B): HBM-bound; {info['flops'] / launch_s / 1e12:.1f} "
+                           "TFLOP/s")
     traffic = ncu_traffic(shape) if shape else None
     name = f"{info['kind']} layer {info['layer']}" + (
         f" M{info['M']} N{info['N_launch']} K{info['K']} ({info['images']} images per launch)"
         if info["flops"] else "")
     out.update({"kernel": name, "share_of_step": per_action[top] / total if total else None,
                 "launches_per_step": info["executions"],
-                "algorithmic_per_launch": info["flops"] or info["bytes"],
+                "algorithmic_per_launch": info["flops"] if tensor_bound else info["bytes"],
                 "launch_us": launch_s * 1e6,
                 "traffic": traffic["bytes"] if traffic else None,
                 "traffic_source": traffic["source"] if traffic else None,

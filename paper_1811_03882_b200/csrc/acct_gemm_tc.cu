@@ -565,12 +565,18 @@ __device__ __forceinline__ long long gtimer() {
   return (long long)t;
 }
 
-template <int TN, int NACC_, int BK_>
+// SWAP (M <= 64 weight rows): operand A = 128 activation COLUMNS per CTA
+// (256 per pair, transposed into TMEM by the split warps), operand B = the
+// TN weight rows, TN/2 per CTA, K-major; the epilogue writes lanes = columns.
+template <int TN, int NACC_, int BK_, bool SWAP_ = false>
 struct Cfg2 {
+  static constexpr bool SWAP = SWAP_;
   static constexpr int BK = BK_;
   static constexpr int HALF = TN / 2;
   static constexpr int X_TILE = 128 * BK * 4;
   static constexpr int Y_TILE = HALF * BK * 4;
+  static constexpr uint32_t K_SBO = 8 * BK * 4;  // 8-row swizzle atom of a K-major tile
+  static constexpr uint32_t K_LAYOUT = BK == 32 ? ptx::kLayoutSW128 : 4u;
   static constexpr int STAGE_BYTES = X_TILE + 2 * Y_TILE;
   static constexpr int NACC = NACC_;
   static constexpr int BUDGET = 220 * 1024 - STAGING_BYTES - 512 - 1024;
@@ -582,18 +588,18 @@ struct Cfg2 {
   static constexpr uint32_t MN_CHUNK = BK * 128;
   static constexpr int ROWB = BK * 4;  // K-major A row bytes: 64 (SWIZZLE_64B) or 128 (128B)
   static_assert(BK == 16 || BK == 32, "BK");
-  static_assert(HALF % 32 == 0, "B half must be whole 32-column chunks");
+  static_assert(SWAP ? HALF % 8 == 0 : HALF % 32 == 0, "operand B half tile shape");
   static_assert(STAGES >= 2, "pipeline too shallow");
 };
 
-template <int TN, int NACC, int BK_>
+template <int TN, int NACC, int BK_, bool SWAP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 int M, int N, int K, int nt, int mt, int splits, int kb_per, int write_hi,
                 float alpha, float beta, float *__restrict__ C, int64_t ldc,
                 const float *__restrict__ bias, int act, float *__restrict__ ws, int64_t ws_ld,
                 int64_t ws_split_stride) {
-  using G = Cfg2<TN, NACC, BK_>;
+  using G = Cfg2<TN, NACC, BK_, SWAP>;
   constexpr int S = G::STAGES, BK = G::BK;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -619,8 +625,8 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     w.split = u / tiles;
     const int t = u - w.split * tiles;
     const int tm = t / nt, tn = t - tm * nt;
-    w.n0 = tn * TN;
-    w.m0 = tm * 256;
+    w.n0 = tn * (SWAP ? 256 : TN);
+    w.m0 = tm * (SWAP ? TN : 256);
     w.kb0 = w.split * kb_per;
     w.nkb = min(w.kb0 + kb_per, total_kb) - w.kb0;
     return w;
@@ -654,24 +660,32 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       int g = 0;
       for (int u = pair; u < units; u += pairs) {
         const Unit w = unit(u);
-        const int m_rows = w.m0 + 128 * rank, n_half = w.n0 + rank * G::HALF;
+        const int m_rows = w.m0 + (SWAP ? rank * G::HALF : 128 * rank);
+        const int n_cols = w.n0 + (SWAP ? 128 * rank : rank * G::HALF);
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
           const int s = g % S;
           if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
           if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace) g_trace[0][g] = gtimer();
           ptx::mbar_expect_tx(&full[s], G::X_TILE + G::Y_TILE);
           const int kx = (w.kb0 + kb) * BK;
-          ptx::tma_load_2d(x_hi(s), &tmA, &full[s], kx, m_rows);
+          if constexpr (!SWAP) {
+            ptx::tma_load_2d(x_hi(s), &tmA, &full[s], kx, m_rows);
 #pragma unroll
-          for (int c = 0; c < G::HALF / 32; ++c)
-            ptx::tma_load_2d(y_hi(s) + c * G::MN_CHUNK, &tmB, &full[s], n_half + 32 * c, kx);
+            for (int c = 0; c < G::HALF / 32; ++c)
+              ptx::tma_load_2d(y_hi(s) + c * G::MN_CHUNK, &tmB, &full[s], n_cols + 32 * c, kx);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              ptx::tma_load_2d(x_hi(s) + c * G::MN_CHUNK, &tmB, &full[s], n_cols + 32 * c, kx);
+            ptx::tma_load_2d(y_hi(s), &tmA, &full[s], kx, m_rows);
+          }
         }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader only) ----------------
     if (rank == 0 && lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_tf32(256, TN, false, true);
+      constexpr uint32_t idesc = ptx::idesc_tf32(256, TN, false, !SWAP);
       int g = 0, j = 0;
       for (int u = pair; u < units; u += pairs, ++j) {
         const Unit w = unit(u);
@@ -689,9 +703,11 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {
             const uint64_t dyh =
-                ptx::smem_desc(yh + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
+                SWAP ? ptx::smem_desc(yh + 32 * k, 16, G::K_SBO, G::K_LAYOUT)
+                     : ptx::smem_desc(yh + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
             const uint64_t dyl =
-                ptx::smem_desc(yl + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
+                SWAP ? ptx::smem_desc(yl + 32 * k, 16, G::K_SBO, G::K_LAYOUT)
+                     : ptx::smem_desc(yl + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
             if (write_hi & 4) continue;
             ptx::mma2_tf32_ts(d, at + 8 * k, dyh, idesc, (kb | k) != 0);
             ptx::mma2_tf32_ts(d, at + 8 * k, dyl, idesc, 1);
@@ -722,11 +738,27 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (!(write_hi & 2)) {
           // row r of the K-major A tile: 16-B chunk c at r*ROWB + (c ^ swz(r))*16,
           // swz = (r/2)%4 for SWIZZLE_64B rows, r%8 for SWIZZLE_128B rows
+          // swap: activation column 32q + lane of chunk q, one conflict-free
+          // 128-B SWIZZLE_128B_BASE32B row per k (32-B pieces XOR k % 4)
           float4 ra[BK / 4];
+          if constexpr (!SWAP) {
 #pragma unroll
-          for (int c = 0; c < BK / 4; ++c)
-            ra[c] = ptx::lds128(xh + row * G::ROWB +
-                                ((c ^ (BK == 16 ? ((row >> 1) & 3) : (row & 7))) << 4));
+            for (int c = 0; c < BK / 4; ++c)
+              ra[c] = ptx::lds128(xh + row * G::ROWB +
+                                  ((c ^ (BK == 16 ? ((row >> 1) & 3) : (row & 7))) << 4));
+          } else {
+            const uint32_t cb = xh + q * G::MN_CHUNK + ((lane & 7) << 2);
+#pragma unroll
+            for (int c = 0; c < BK / 4; ++c) {
+              float v[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int kk = 4 * c + e;
+                v[e] = ptx::lds32(cb + kk * 128 + ((((lane >> 3) ^ kk) & 3) << 5));
+              }
+              ra[c] = make_float4(v[0], v[1], v[2], v[3]);
+            }
+          }
           constexpr int NY = (G::Y_TILE / 16 + 127) / 128;
           float4 ry[NY];
 #pragma unroll
@@ -782,7 +814,35 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * TN;
       float *part = ws + w.split * ws_split_stride;
       const int row0 = w.m0 + 128 * rank + 32 * q;
-      if (!(write_hi & 8)) {
+      if (SWAP && !(write_hi & 8)) {
+        // lanes = output columns (this CTA's 128), TMEM columns = weight rows
+        const int col = w.n0 + 128 * rank + 32 * q + lane;
+        constexpr int CH = 16;
+        for (int c = 0; c < TN / CH; ++c) {
+          uint32_t r[CH];
+          ptx::tmem_ld_32x32b_x16(trow + CH * c, r);
+          if (col >= N) continue;
+          const int rbase = w.m0 + CH * c;
+          if (splits == 1) {
+            float cv[CH], bv[CH];
+#pragma unroll
+            for (int jj = 0; jj < CH; ++jj) {
+              const bool ok = rbase + jj < M;
+              cv[jj] = (beta != 0.0f && ok) ? C[(int64_t)(rbase + jj) * ldc + col] : 0.0f;
+              bv[jj] = (bias && ok) ? __ldg(bias + rbase + jj) : 0.0f;
+            }
+#pragma unroll
+            for (int jj = 0; jj < CH; ++jj)
+              if (rbase + jj < M)
+                C[(int64_t)(rbase + jj) * ldc + col] =
+                    finish(__uint_as_float(r[jj]), alpha, beta, cv[jj], bias, bv[jj], act);
+          } else {
+            float *dst = part + (int64_t)rbase * ws_ld + col;
+#pragma unroll
+            for (int jj = 0; jj < CH; ++jj) __stcg(dst + (int64_t)jj * ws_ld, __uint_as_float(r[jj]));
+          }
+        }
+      } else if (!(write_hi & 8)) {
         for (int c = 0; c < TN / 32; ++c) {
           uint32_t r[32];
           ptx::tmem_ld_32x32b_x32(trow + 32 * c, r);
@@ -1041,25 +1101,27 @@ int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, con
   return ACCT_OK;
 }
 
-template <int TN, int NACC, int BK>
+template <int TN, int NACC, int BK, bool SWAP = false>
 int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
                int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
                cudaStream_t s) {
-  using G = Cfg2<TN, NACC, BK>;
+  using G = Cfg2<TN, NACC, BK, SWAP>;
   CUtensorMap ta, tb;
-  if (!cached_map(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BK, 128,
+  // weights: K-major box of BK x (128 rows, or TN/2 rows per CTA when swapped)
+  if (!cached_map(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BK, SWAP ? TN / 2 : 128,
                   BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B) ||
       !cached_map(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, 32, BK,
                   CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
     return fail(ACCT_ENOTSUP, "gemm_tc2: cuTensorMapEncodeTiled failed");
-  const int nt = (N + TN - 1) / TN, mt = (M + 255) / 256, tiles = mt * nt;
+  const int tile_n = SWAP ? 256 : TN, tile_m = SWAP ? TN : 256;
+  const int nt = (N + tile_n - 1) / tile_n, mt = (M + tile_m - 1) / tile_m, tiles = mt * nt;
   const int total_kb = (K + BK - 1) / BK;
   const int pairs_avail = sm_count() / 2;
   int splits, kb_per;
   plan_splits(tiles, total_kb, pairs_avail, &splits, &kb_per);
   const int units = tiles * splits;
   float *ws = nullptr;
-  const int64_t ws_ld = (int64_t)nt * TN, rows = (int64_t)mt * 256;
+  const int64_t ws_ld = (int64_t)nt * tile_n, rows = (int64_t)mt * tile_m;
   if (splits > 1) {
     if (int rc = scratch_for(s, (size_t)splits * rows * ws_ld, &ws)) return rc;
   }
@@ -1070,7 +1132,7 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(mu);
     if (dev >= 0 && dev < 64 && !done[dev]) {
-      if (int rc = check_cuda(cudaFuncSetAttribute(tc2_gemm_kernel<TN, NACC, BK>,
+      if (int rc = check_cuda(cudaFuncSetAttribute(tc2_gemm_kernel<TN, NACC, BK, SWAP>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    G::SMEM_BYTES),
                               "gemm_tc2: smem attribute"))
@@ -1079,7 +1141,7 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
     }
   }
   const int pairs = units < pairs_avail ? units : pairs_avail;
-  launch(tc2_gemm_kernel<TN, NACC, BK>, dim3(2 * pairs), dim3(THREADS), G::SMEM_BYTES, s, ta, tb, M,
+  launch(tc2_gemm_kernel<TN, NACC, BK, SWAP>, dim3(2 * pairs), dim3(THREADS), G::SMEM_BYTES, s, ta, tb, M,
          N, K, nt, mt, splits, kb_per, g_write_hi, alpha, beta, C, ldc, bias, act, ws, ws_ld,
          rows * ws_ld);
   if (int rc = note_launch("gemm_tc2")) return rc;
@@ -1111,8 +1173,17 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
       (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
     return ACCT_ENOTSUP;
   if (M <= 16) return launch_tc<16, true, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
-  if (M <= 32) return launch_tc<32, true, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
-  if (M <= 64) return launch_tc<64, true, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  // swap tiles, single SM by default; 12 forces the CTA-pair swap tile.  The
+  // pair does not pay here: a 128 x 32 x 8 MMA issues in ~69 cycles and a
+  // 256 x 32 x 8 pair MMA in ~82 (tools/tc_trace.py), both far above the 16
+  // cycles of math, so narrow tiles stay MMA-issue bound either way.
+  const int fswap = forced_tile();
+  if (M <= 32)
+    return fswap == 12 ? launch_tc2<32, 4, 32, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s)
+                       : launch_tc<32, true, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (M <= 64)
+    return fswap == 12 ? launch_tc2<64, 4, 32, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s)
+                       : launch_tc<64, true, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   const int force = forced_tile();
   if (force == 1) return launch_tc<192, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (force == 2) return launch_tc<128, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);

@@ -234,3 +234,28 @@ def test_every_tensor_core_tile_within_tolerance(cuda_device, orc, tile, M, N, K
     finally:
         K.lib().acct_tc_set_tile(0)
     gemm_ok(Cd.numpy(), want)
+
+
+@pytest.mark.parametrize("tile", [0, 12])
+@pytest.mark.parametrize("M,N,K_", [(32, 43264, 144), (17, 5000, 64), (33, 1000, 300),
+                                     (64, 10816, 288), (48, 692224, 144), (64, 169, 4608)])
+def test_swap_tiles_within_tolerance(cuda_device, orc, tile, M, N, K_):
+    """Narrow-M gemms (17 <= M <= 64): the single-SM swap tile (default, 0)
+    and the CTA-pair swap tile (12), fused bias + leaky epilogue."""
+    A0, B0 = _rand((M, K_), 81, -0.5, 0.5), _rand((K_, N), 82)
+    bias0 = _rand((M,), 83)
+    want = np.zeros((M, N), np.float32)
+    orc.orc_gemm_nn(M, N, K_, 1.0, A0.ctypes.data, K_, B0.ctypes.data, N, want.ctypes.data, N)
+    want = want + bias0[:, None]
+    want = np.where(want < 0, (0.1 * want.astype(np.float64)).astype(np.float32), want)
+    A, B = Pitched(A0), Pitched(B0)
+    bias = torch.from_numpy(bias0).cuda()
+    Cd = Pitched(np.full((M, N), 7.0, np.float32))
+    try:
+        K.lib().acct_tc_set_tile(tile)
+        K.gemm_nn(M, N, K_, 1.0, A.ptr, A.ld, B.ptr, B.ld, 0.0, Cd.ptr, Cd.ld, bias.data_ptr(),
+                  K.ACT_LEAKY, K.GEMM_TC3XTF32, stream())
+        torch.cuda.synchronize()
+    finally:
+        K.lib().acct_tc_set_tile(0)
+    gemm_ok(Cd.numpy(), want)

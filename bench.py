@@ -221,12 +221,14 @@ def run_reference(args):
             times.append(w)
     total = sum(times)
     value = procs * args.cpu_images * args.steps / total
+    from paper_1811_03882_b200.nets import NETS
+    dims = f"{NETS[args.net].height}x{NETS[args.net].width}"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "img/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.net} 416x416 batch 1 per forward (C-subset program, "
+        "config": {"workload": f"{args.net} {dims} batch 1 per forward (C-subset program, "
                                f"all-zero genome = reference CPU path)",
                    "images_per_process_step": args.cpu_images, "processes": procs},
         "cpu_baseline": {"value": value, "unit": "img/s", "cores": procs, "kind": "port",
@@ -452,12 +454,13 @@ def run_ours(args):
     if world == 1 and not args.no_ga:
         ga = ga_search([local])
 
+    dims = f"{net.spec.height}x{net.spec.width}"
     line = {
         "metric": METRIC, "value": value, "unit": "img/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.net} 416x416, batch 1 per forward pass, "
+        "config": {"workload": f"{args.net} {dims}, batch 1 per forward pass, "
                                f"{args.images}-image loop per step, all-offload genome "
                                f"({len(net.ops)} genes) with hoisted transfers",
                    "net": args.net, "images_per_step_per_gpu": args.images,

@@ -50,7 +50,7 @@ enum { ACCT_ACT_LINEAR = 0, ACCT_ACT_LEAKY = 1 };
 
 /* gemm_nn implementation modes */
 enum {
-  ACCT_GEMM_AUTO = 0,       /* M <= 16: FP32 HBM-streaming kernel; else tcgen05 3xTF32
+  ACCT_GEMM_AUTO = 0,       /* M <= 16 (or <= 32 with K <= 64): FP32 HBM-streaming kernel; else tcgen05 3xTF32
                                where TMA applies, else SIMT FP32 */
   ACCT_GEMM_SIMT = 1,       /* FP32 FMA on CUDA cores (the recompiled-loop baseline) */
   ACCT_GEMM_TC3XTF32 = 2    /* TMA + tcgen05.mma kind::tf32, hi/lo split, TMEM accumulators */

@@ -240,11 +240,102 @@ gemm_stream_kernel(int M, int N, int K, float alpha, const float *__restrict__ A
   }
 }
 
+// 2 columns per thread, KU B rows (float2) in flight before any use: with
+// K <= KU (layer 0: K = 27) a thread issues every load of its columns at once,
+// so ~8x more bytes are in flight per SM than with 4 columns x 8 rows.
+template <int MT, int KU>
+__global__ void __launch_bounds__(128)
+gemm_stream2_kernel(int M, int N, int K, float alpha, const float *__restrict__ A, int64_t lda,
+                    const float *__restrict__ B, int64_t ldb, float beta, float *__restrict__ C,
+                    int64_t ldc, const float *__restrict__ bias, int act) {
+  extern __shared__ float4 As4[];  // [K][MT/4]
+  float *As = reinterpret_cast<float *>(As4);
+  pdl_trigger();
+  pdl_wait();
+  for (int t = threadIdx.x; t < K * MT; t += blockDim.x) {
+    const int k = t / MT, m = t - k * MT;
+    As[t] = m < M ? A[(int64_t)m * lda + k] : 0.0f;
+  }
+  __syncthreads();
+  const int np = (N + 1) >> 1;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < np; q += gridDim.x * blockDim.x) {
+    const int col = q * 2;
+    const bool full = col + 2 <= N;
+    float acc[MT][2];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0f;
+    const float *bp = B + col;
+    for (int k0 = 0; k0 < K; k0 += KU) {
+      float2 b[KU];
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const int k = k0 + u;
+        if (k < K) {
+          const float *r = bp + (int64_t)k * ldb;
+          b[u] = full ? __ldcs(reinterpret_cast<const float2 *>(r)) : make_float2(r[0], 0.0f);
+        } else {
+          b[u] = make_float2(0.0f, 0.0f);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        if (k0 + u >= K) break;
+        const float4 *ak = As4 + (k0 + u) * (MT / 4);
+#pragma unroll
+        for (int g = 0; g < MT / 4; ++g) {
+          const float4 a = ak[g];
+          const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            acc[4 * g + e][0] = fmaf(av[e], b[u].x, acc[4 * g + e][0]);
+            acc[4 * g + e][1] = fmaf(av[e], b[u].y, acc[4 * g + e][1]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      if (m >= M) break;
+      float *cp = C + (int64_t)m * ldc + col;
+      if (full) {
+        float2 cv = make_float2(0.0f, 0.0f);
+        if (beta != 0.0f) cv = *reinterpret_cast<const float2 *>(cp);
+        float2 o;
+        o.x = epilogue(acc[m][0], alpha, beta, &cv.x, bias, m, act);
+        o.y = epilogue(acc[m][1], alpha, beta, &cv.y, bias, m, act);
+        __stcs(reinterpret_cast<float2 *>(cp), o);
+      } else {
+        cp[0] = epilogue(acc[m][0], alpha, beta, cp, bias, m, act);
+      }
+    }
+  }
+}
+
+int stream_variant() {
+  static const int v = [] {
+    const char *e = getenv("ACCT_STREAM");
+    return e ? atoi(e) : 0;  // 0: 4 columns/thread at M <= 16, 2 at M <= 32
+  }();
+  return v;
+}
+
 template <int MT>
 int launch_stream(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
                   int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
                   cudaStream_t s) {
   const size_t smem = (size_t)K * MT * sizeof(float);
+  // M = 32: two columns per thread (64 accumulators) keeps 4+ CTAs per SM
+  constexpr int KU2 = MT <= 16 ? 32 : 8;
+  if (stream_variant() == 2 || (MT > 16 && stream_variant() != 1)) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(gemm_stream2_kernel<MT, KU2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+    const int64_t np = (N + 1) / 2;
+    unsigned grid = acct::grid_for(np, 128, 8);
+    acct::launch(gemm_stream2_kernel<MT, KU2>, dim3(grid), dim3(128), smem, s, M, N, K, alpha, A,
+                 lda, B, ldb, beta, C, ldc, bias, act);
+    return acct::note_launch("gemm_stream");
+  }
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(gemm_stream_kernel<MT, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
@@ -266,16 +357,21 @@ namespace acct {
 int gemm_stream(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
                 int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
                 cudaStream_t s) {
-  if (M < 1 || M > 16 || N < 1 || K < 1 || (int64_t)K * 32 * 4 > 200 * 1024 || (ldb % 4) ||
+  // M <= 16, or M <= 32 with a short K (a 3-channel first layer): beyond
+  // that the 4 x 32 accumulators per thread cost more occupancy than the
+  // stream gains and the tensor-core swap tile wins
+  if (M < 1 || M > 32 || (M > 16 && K > 64) || N < 1 || K < 1 ||
+      (int64_t)K * 32 * 4 > 200 * 1024 || (ldb % 4) ||
       (ldc % 4) || (reinterpret_cast<uintptr_t>(B) & 15) || (reinterpret_cast<uintptr_t>(C) & 15))
     return ACCT_ENOTSUP;
-  return launch_stream<16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (M <= 16) return launch_stream<16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  return launch_stream<32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
 }
 
 int gemm_simt(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
               int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
               cudaStream_t s) {
-  if (M <= 16) {
+  if (M <= 32) {  // gemm_stream declines the shapes it does not fit
     int rc = gemm_stream(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
     if (rc != ACCT_ENOTSUP) return rc;
   }

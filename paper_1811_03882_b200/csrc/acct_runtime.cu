@@ -218,9 +218,9 @@ extern "C" int acct_gemm_nn_f32(int M, int N, int K, float alpha, const float *A
     return fail(ACCT_EINVAL, "gemm_nn: bad activation");
   if ((int64_t)M * N == 0) return ACCT_OK;
   cudaStream_t s = as_stream(stream);
-  // M <= 16 (the first conv layer): an HBM stream of B and C with ~0.2
-  // flop/byte -- CUDA cores near the HBM roofline beat 16-row MMA tiles
-  if (mode == ACCT_GEMM_AUTO && M <= 16) {
+  // M <= 16, or M <= 32 with K <= 64 (first conv layers, K = 27): an HBM
+  // stream of B and C with < 1 flop/byte -- CUDA cores beat narrow MMA tiles
+  if (mode == ACCT_GEMM_AUTO && (M <= 16 || (M <= 32 && K <= 64))) {
     int rc = gemm_stream(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
     if (rc != ACCT_ENOTSUP) return rc;
   }

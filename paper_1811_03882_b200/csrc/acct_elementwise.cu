@@ -364,6 +364,40 @@ __global__ void maxpool2s2_kernel(const float *__restrict__ in, int64_t ld_in, i
   }
 }
 
+// 3x3/1/1 on mid-size planes (16 <= out_w < 64: 52x52, 26x26): a thread owns ONE
+// output pixel of one input channel and writes its 9 col rows; consecutive
+// threads take consecutive pixels, so every store instruction of a warp is a
+// contiguous 128-B run of a col row whatever the row width (the window
+// kernel's float4 rows need out_w % 4 == 0 and waste lanes on 13/26-wide rows)
+__global__ void im2col_k3s1_flat_kernel(const float *__restrict__ im, int64_t ld_im,
+                                        int64_t im_bs, int height, int width, int npix,
+                                        int channels, int per_block, int total,
+                                        float *__restrict__ col, int64_t ld_col, int64_t col_bs) {
+  pdl_trigger();
+  pdl_wait();
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npix) return;
+  const int h = p / width, w = p - h * width;  // 3x3/1/1: output plane == input plane
+  // a CTA walks `per_block` consecutive (image, channel) planes
+  const int z0 = blockIdx.y * per_block;
+  for (int z = z0; z < z0 + per_block && z < total; ++z) {
+    const int img = z / channels, ci = z - img * channels;
+    const float *src = im + img * im_bs + (int64_t)ci * ld_im;
+    float *dst = col + img * col_bs + (int64_t)(ci * 9) * ld_col + p;
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh) {
+      const int r = h + kh - 1;
+      const bool rok = r >= 0 && r < height;
+#pragma unroll
+      for (int kw = 0; kw < 3; ++kw) {
+        const int c = w + kw - 1;
+        __stcs(dst + (int64_t)(kh * 3 + kw) * ld_col,
+               (rok && c >= 0 && c < width) ? __ldg(src + r * width + c) : 0.0f);
+      }
+    }
+  }
+}
+
 bool vec_ok(const void *p, int64_t ld, int64_t cols) {
   return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && ld % 4 == 0 && ld >= ((cols + 3) / 4) * 4;
 }
@@ -476,6 +510,20 @@ extern "C" int acct_im2col_batched_f32(const float *im, int64_t ld_im, int64_t i
   const bool col_vec = ld_col % 4 == 0 && col_stride % 4 == 0 &&
                        (reinterpret_cast<uintptr_t>(col) & 15) == 0;
   cudaStream_t s = as_stream(stream);
+  // 16 <= out_w < 64 (52x52, 26x26): flat pixel-per-thread kernel (measured
+  // 1.2-1.5x the window kernel there); 13x13 and >= 64-wide planes keep the window
+  if (ksize == 3 && stride == 1 && pad == 1 && out_w < 64 && out_w >= 16 &&
+      (int64_t)channels * batch <= 65535) {
+    const int block = npix >= 256 ? 256 : (int)((npix + 31) / 32 * 32);  // 13x13: 192
+    const int total = channels * batch;
+    // one plane per CTA: packing several 13x13 planes into a CTA measured slower
+    const int per_block = 1;
+    const dim3 grid((unsigned)((npix + block - 1) / block),
+                    (unsigned)((total + per_block - 1) / per_block));
+    launch(im2col_k3s1_flat_kernel, grid, dim3(block), 0, s, im, ld_im, im_stride, height, width,
+           (int)npix, channels, per_block, total, col, ld_col, col_stride);
+    return note_launch("im2col");
+  }
   if (ksize == 3 && stride == 1 && pad == 1 && batch_ok(batch, channels)) {
     const bool vec = out_w % 4 == 0 && col_vec;
     const int quads = (out_w + 3) / 4;

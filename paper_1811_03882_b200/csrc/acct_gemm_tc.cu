@@ -1202,8 +1202,11 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
   // (743 vs ~590 cycles per 128x192x16 k-block, tools/tc_trace.py).
   const int sms = sm_count();
   const double c1 = 1.25 * (double)tile_cost(M, N, K, 192, 16, sms);
-  const double c9 = (double)tile_cost2(M, N, K, 192, 32, sms / 2);
-  const double c10 = (double)tile_cost2(M, N, K, 256, 32, sms / 2);
+  // a pair tile spans 256 rows: weight its cost by the rows it computes vs
+  // the 128-row tiles (M = 128 would waste half of every pair)
+  const double waste = (double)((M + 255) / 256 * 256) / (double)((M + 127) / 128 * 128);
+  const double c9 = waste * (double)tile_cost2(M, N, K, 192, 32, sms / 2);
+  const double c10 = waste * (double)tile_cost2(M, N, K, 256, 32, sms / 2);
   if (c10 < c9 && c10 < c1)
     return launch_tc2<256, 1, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (c9 < c1)

@@ -683,8 +683,8 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (leader only) ----------------
-    if (rank == 0 && lane == 0) {
+    // ---------------- MMA issuer (leader only; whole warp, one lane issues) ----------------
+    if (rank == 0) {
       constexpr uint32_t idesc = ptx::idesc_tf32(256, TN, false, !SWAP);
       int g = 0, j = 0;
       for (int u = pair; u < units; u += pairs, ++j) {
@@ -696,7 +696,8 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
           const int s = g % S;
           ptx::mbar_wait(&conv[s], (g / S) & 1);
-          if ((write_hi & 16) && g < kTrace && blockIdx.x == 0) g_trace[3][g] = gtimer();
+          if ((write_hi & 16) && g < kTrace && blockIdx.x == 0 && lane == 0)
+            g_trace[3][g] = gtimer();
           ptx::tc_fence_after();
           const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
           const uint32_t at = tmem + G::A_COL0 + s * 2 * BK;
@@ -709,14 +710,20 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 SWAP ? ptx::smem_desc(yl + 32 * k, 16, G::K_SBO, G::K_LAYOUT)
                      : ptx::smem_desc(yl + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
             if (write_hi & 4) continue;
-            ptx::mma2_tf32_ts(d, at + 8 * k, dyh, idesc, (kb | k) != 0);
-            ptx::mma2_tf32_ts(d, at + 8 * k, dyl, idesc, 1);
-            ptx::mma2_tf32_ts(d, at + BK + 8 * k, dyh, idesc, 1);
+            if (ptx::elect_one()) {
+              ptx::mma2_tf32_ts(d, at + 8 * k, dyh, idesc, (kb | k) != 0);
+              ptx::mma2_tf32_ts(d, at + 8 * k, dyl, idesc, 1);
+              ptx::mma2_tf32_ts(d, at + BK + 8 * k, dyh, idesc, 1);
+            }
+            __syncwarp();
           }
-          ptx::mma2_commit_multicast(&empty[s], 0x3);
-          if ((write_hi & 16) && g < kTrace && blockIdx.x == 0) g_trace[4][g] = gtimer();
+          if (ptx::elect_one()) ptx::mma2_commit_multicast(&empty[s], 0x3);
+          __syncwarp();
+          if ((write_hi & 16) && g < kTrace && blockIdx.x == 0 && lane == 0)
+            g_trace[4][g] = gtimer();
         }
-        ptx::mma2_commit_multicast(&acc_full[a], 0x3);
+        if (ptx::elect_one()) ptx::mma2_commit_multicast(&acc_full[a], 0x3);
+        __syncwarp();
       }
     }
     __syncwarp();

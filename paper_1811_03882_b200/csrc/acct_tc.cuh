@@ -251,6 +251,19 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn_major,
          | ((uint32_t)(M >> 4) << 24);          // M >> 4
 }
 
+// one lane of a converged warp: issuing tcgen05.mma under this (rather than
+// under `lane == 0`) keeps the operand descriptors warp-uniform, so they
+// live in uniform registers instead of an ELECT / R2UR.BROADCAST loop per MMA
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---- clusters / CTA pairs (cta_group::2) ----
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;

@@ -276,8 +276,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    // ---------------- MMA issuer (whole warp; one elected lane issues) ----------------
+    {
       // operand A from TMEM has no major-ness (lane = row, column = k)
       constexpr uint32_t idesc = ptx::idesc_tf32(128, TN, SWAP && !AT, !SWAP);
       int g = 0, j = 0;
@@ -290,7 +290,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
           const int s = g % S;
           ptx::mbar_wait(&conv[s], (g / S) & 1);
-          if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace) g_trace[3][g] = clock64();
+          if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace && lane == 0) g_trace[3][g] = clock64();
           ptx::tc_fence_after();
           const uint32_t xh = ptx::smem_u32(x_hi(s)), xl = ptx::smem_u32(x_lo(s));
           const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
@@ -307,12 +307,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                   SWAP ? ptx::smem_desc(yl + 32 * k, 16, G::K_SBO, G::K_LAYOUT)
                        : ptx::smem_desc(yl + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
               if (write_hi & 4) continue;
-              ptx::mma_tf32_ts(d, at + 8 * k, dyh, idesc, (kb | k) != 0);
-              ptx::mma_tf32_ts(d, at + 8 * k, dyl, idesc, 1);
-              ptx::mma_tf32_ts(d, at + BK + 8 * k, dyh, idesc, 1);
+              if (ptx::elect_one()) {
+                ptx::mma_tf32_ts(d, at + 8 * k, dyh, idesc, (kb | k) != 0);
+                ptx::mma_tf32_ts(d, at + 8 * k, dyl, idesc, 1);
+                ptx::mma_tf32_ts(d, at + BK + 8 * k, dyh, idesc, 1);
+              }
+              __syncwarp();
             }
-            ptx::mma_commit(&empty[s]);
-            if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace) g_trace[4][g] = clock64();
+            if (ptx::elect_one()) ptx::mma_commit(&empty[s]);
+            __syncwarp();
+            if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace && lane == 0) g_trace[4][g] = clock64();
             continue;
           }
 #pragma unroll
@@ -332,14 +336,19 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               dyl = ptx::smem_desc(yl + 32 * k, 16, G::K_SBO, G::K_LAYOUT);
             }
             if (write_hi & 4) continue;
-            ptx::mma_tf32(d, dxh, dyh, idesc, (kb | k) != 0);
-            ptx::mma_tf32(d, dxh, dyl, idesc, 1);
-            ptx::mma_tf32(d, dxl, dyh, idesc, 1);
+            if (ptx::elect_one()) {
+              ptx::mma_tf32(d, dxh, dyh, idesc, (kb | k) != 0);
+              ptx::mma_tf32(d, dxh, dyl, idesc, 1);
+              ptx::mma_tf32(d, dxl, dyh, idesc, 1);
+            }
+            __syncwarp();
           }
-          ptx::mma_commit(&empty[s]);
-          if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace) g_trace[4][g] = clock64();
+          if (ptx::elect_one()) ptx::mma_commit(&empty[s]);
+          __syncwarp();
+          if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace && lane == 0) g_trace[4][g] = clock64();
         }
-        ptx::mma_commit(&acc_full[a]);
+        if (ptx::elect_one()) ptx::mma_commit(&acc_full[a]);
+        __syncwarp();
       }
     }
     __syncwarp();

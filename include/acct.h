@@ -199,10 +199,10 @@ typedef struct {
   void *dev;           /* device buffer (rows x ld x 4 bytes) */
   int64_t rows, cols;  /* logical 2-D shape (1-D arrays: rows = 1) */
   int64_t ld_dev;      /* device row pitch in elements */
-  void *stage;         /* optional dense device staging buffer (>= rows x cols x 4
-                          bytes x images moved at once) for padded arrays: H2D is then
-                          one dense copy plus a repack kernel, D2H a pack kernel plus
-                          one dense copy, instead of a slow short-row 2-D copy */
+  void *stage;         /* optional dense device staging buffer owned by this array
+                          (>= rows x cols x 4 bytes x images moved at once) for padded
+                          arrays with rows < 4 KB: H2D is then one dense copy plus a
+                          repack kernel instead of a slow short-row 2-D copy */
   int64_t img_stride;  /* image-batched schedules: elements between the private copies
                           of consecutive images (0 = one copy shared by all images).
                           [rows][B*ld] interleaved copies have img_stride = ld / B-th of

@@ -625,8 +625,8 @@ int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *action
               }
               on = reinterpret_cast<acct_stream_t>(side->t);
             } else {
-              // the staging buffer is shared with the side stream's staged copies
-              if (staged && (rc = join_all())) return rc;
+              // each array owns its staging region: only this array's own
+              // side-stream copy (need) can still be using it
               if ((rc = need(a.a[0]))) return rc;
             }
             rc = staged ? acct_h2d_staged(dev, x.ld_dev, host, rows, x.cols, x.stage, on)

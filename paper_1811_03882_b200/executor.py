@@ -82,6 +82,29 @@ class Schedule:
     slots: object = None                  # slot table of a batched schedule (None = base)
 
 
+STAGE_ROW_BYTES = 4096   # the runtime stages host->device copies of shorter rows
+
+
+def _carve_stages(torch, device, slots, ks, images: dict):
+    """One dense device staging region PER padded short-row array (several
+    images for image-major batched arrays), carved from one allocation: a
+    staged copy then never waits for another array's repack to free a shared
+    buffer.  Returns the backing tensor (keep it alive) or None."""
+    need, offs, total = [], {}, 0
+    for k in ks:
+        sl = slots[k]
+        if sl.ld_dev != sl.cols and sl.cols * 4 < STAGE_ROW_BYTES:
+            n = sl.rows * sl.cols * images.get(k, 1)
+            offs[k] = total
+            total += -(-n // 64) * 64                    # 256-B aligned regions
+    if not total:
+        return None
+    buf = torch.empty(total, dtype=torch.float32, device=device)
+    for k, off in offs.items():
+        slots[k].stage = buf.data_ptr() + 4 * off
+    return buf
+
+
 def _batched(act: tuple, nimg: int) -> tuple:
     """KERNEL action over `nimg` images per launch (int operand 13)."""
     if nimg <= 1:
@@ -154,14 +177,10 @@ class PatternExecutor:
             slots[k].host = h.data_ptr()
             slots[k].dev = None if d is None else d.data_ptr()
             slots[k].rows, slots[k].cols, slots[k].ld_dev = rows, cols, ld
-        # dense staging for padded arrays: their H2D is one contiguous copy plus
-        # a repack kernel (short-row 2-D H2D copies run ~10x slower)
-        padded = [k for k in range(len(net.arrays)) if slots[k].ld_dev != slots[k].cols]
-        if padded and not self.host_only:
-            most = max(slots[k].rows * slots[k].cols for k in padded)
-            self.stage = torch.empty(most, dtype=torch.float32, device=self.device)
-            for k in padded:
-                slots[k].stage = self.stage.data_ptr()
+        # dense staging for padded short-row arrays: their H2D is one contiguous
+        # copy plus a repack kernel (short-row 2-D H2D copies run ~10x slower)
+        if not self.host_only:
+            self.stage = _carve_stages(torch, self.device, slots, range(len(net.arrays)), {})
         self.slots = slots
         self._pristine = [(slots[k].host, slots[k].dev) for k in range(len(net.arrays))]
         self._tables: dict[int, tuple] = {1: (slots, self._pristine)}
@@ -265,7 +284,6 @@ class PatternExecutor:
         n = len(self.net.arrays)
         slots = (K.ArraySlot * n)()
         keep = []
-        stage_need = 0
         for k, spec in enumerate(self.net.arrays.values()):
             base = self.slots[k]
             slots[k].host, slots[k].rows, slots[k].cols = base.host, base.rows, base.cols
@@ -282,14 +300,11 @@ class PatternExecutor:
                     slots[k].img_stride = rows * ld
                 else:
                     slots[k].ld_dev, slots[k].img_stride = p * ld, ld
-            if slots[k].ld_dev != cols:
-                stage_need = max(stage_need, rows * cols * (p if lay == "im" else 1))
-        if stage_need:
-            stage = torch.empty(stage_need, dtype=torch.float32, device=self.device)
+        images = {k: p for k, spec in enumerate(self.net.arrays.values())
+                  if layout.get(spec.name) == "im"}
+        stage = _carve_stages(torch, self.device, slots, range(n), images)
+        if stage is not None:
             keep.append(stage)
-            for k in range(n):
-                if slots[k].ld_dev != slots[k].cols:
-                    slots[k].stage = stage.data_ptr()
         self._keep_alive = getattr(self, "_keep_alive", []) + keep
         pristine = [(slots[k].host, slots[k].dev) for k in range(n)]
         self._tables[p] = (slots, pristine)

@@ -186,7 +186,13 @@ enum {
   ACCT_A_KERNEL = 8,       /* device op: i[0]=op kind, operands a[], ints i[1..];
                               i[13] = images per launch (image-batched loop, 0 = 1) */
   ACCT_A_HOST = 9,         /* host op: same encoding, runs on host buffers */
-  ACCT_A_SYNC = 10         /* drain the stream (before host ops / end) */
+  ACCT_A_SYNC = 10,        /* drain the stream (before host ops / end) */
+  ACCT_A_H2D_GATHER = 11   /* several whole-array host->device transfers as ONE copy:
+                              i[0] = n (<= 12) arrays, slots i[1..n] whose host buffers
+                              lie in one host range starting at `base`; i[13] = dense
+                              device staging for that range; a scatter kernel then moves
+                              each array into its (pitched) device layout.  Counts n
+                              transfers, like n H2D actions */
 };
 
 enum {

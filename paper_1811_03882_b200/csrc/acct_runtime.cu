@@ -136,6 +136,28 @@ __global__ void repack_kernel(const float *__restrict__ src, int64_t cols, float
       dst[r * ld + c] = __ldcs(src + r * cols + c);
 }
 
+// ACCT_A_H2D_GATHER: dense arrays laid out in one staged host range ->
+// their pitched device layouts; blockIdx.z = member
+struct GatherMember {
+  int64_t src;   // element offset of the member in the staging range
+  uint32_t *dst;
+  int64_t rows, cols, ld;
+};
+struct GatherSet {
+  int n;
+  GatherMember m[12];
+};
+__global__ void gather_scatter_kernel(const uint32_t *__restrict__ stage, const GatherSet set) {
+  pdl_trigger();
+  pdl_wait();
+  const GatherMember &g = set.m[blockIdx.z];
+  const uint32_t *src = stage + g.src;
+  for (int64_t r = blockIdx.y; r < g.rows; r += gridDim.y)
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.cols;
+         c += (int64_t)gridDim.x * blockDim.x)
+      g.dst[r * g.ld + c] = __ldcs(src + r * g.cols + c);
+}
+
 // pitched [rows][ld] -> dense [rows][cols] (the D2H half of the staging)
 __global__ void pack_kernel(const float *__restrict__ src, int64_t ld, float *__restrict__ dst,
                             int64_t cols, int64_t rows) {
@@ -657,6 +679,59 @@ int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *action
         // count the transfers the action stands for, not the memcpy calls it took
         if (a.kind == ACCT_A_H2D) cnt.h2d_calls.store(h2d0 + reps);
         else cnt.d2h_calls.store(d2h0 + reps);
+        pending = true;
+        break;
+      }
+      case ACCT_A_H2D_GATHER: {
+        const int n = (int)a.i[0];
+        if (n < 1 || n > 12 || !a.base || !a.i[13]) return fail(ACCT_EINVAL, "schedule: bad gather");
+        GatherSet set{};
+        set.n = n;
+        char *host0 = static_cast<char *>(a.base);
+        int64_t span = 0, bytes = 0, maxc = 1, maxr = 1;
+        for (int k = 0; k < n; ++k) {
+          const int sl = (int)a.i[1 + k];
+          if (!check_slot(sl)) return fail(ACCT_EINVAL, "schedule: bad gather slot");
+          acct_array_t &x = arrays[sl];
+          const int64_t off = static_cast<char *>(x.host) - host0;
+          if (off < 0 || off % 4) return fail(ACCT_EINVAL, "schedule: gather member outside range");
+          set.m[k] = {off / 4, static_cast<uint32_t *>(x.dev), x.rows, x.cols, x.ld_dev};
+          span = std::max(span, off + x.rows * x.cols * 4);
+          bytes += x.rows * x.cols * 4;
+          maxc = std::max(maxc, x.cols);
+          maxr = std::max(maxr, x.rows);
+        }
+        cudaStream_t on = s;
+        if (defer && in_prefix) {
+          if (!forked) {
+            if ((rc = check_cuda(cudaEventRecord(side->fork, s), "side fork record"))) return rc;
+            if ((rc = check_cuda(cudaStreamWaitEvent(side->t, side->fork, 0), "side fork wait")))
+              return rc;
+            forked = true;
+          }
+          on = side->t;
+        } else {
+          for (int k = 0; k < n; ++k)
+            if ((rc = need((int)a.i[1 + k]))) return rc;
+        }
+        void *stage = reinterpret_cast<void *>(a.i[13]);
+        if ((rc = check_cuda(cudaMemcpyAsync(stage, host0, (size_t)span, cudaMemcpyHostToDevice, on),
+                             "gather: copy")))
+          return rc;
+        const unsigned gx = (unsigned)std::min<int64_t>((maxc + 255) / 256, 64);
+        const unsigned gy = (unsigned)std::min<int64_t>(maxr, 512);
+        launch(gather_scatter_kernel, dim3(gx, gy, (unsigned)n), dim3(256), 0, on,
+               static_cast<const uint32_t *>(stage), set);
+        if ((rc = note_launch("gather scatter"))) return rc;
+        cnt.h2d_calls.fetch_add(n);
+        cnt.h2d_bytes.fetch_add(bytes);
+        if (on != s) {
+          for (int k = 0; k < n; ++k) {
+            const int sl = (int)a.i[1 + k];
+            if ((rc = check_cuda(cudaEventRecord(side->ev[sl], on), "gather event"))) return rc;
+            waiting[sl] = 1;
+          }
+        }
         pending = true;
         break;
       }

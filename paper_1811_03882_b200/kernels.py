@@ -24,8 +24,8 @@ GEMM_AUTO, GEMM_SIMT, GEMM_TC3XTF32 = 0, 1, 2
 ACT_NONE, ACT_LINEAR, ACT_LEAKY = -1, 0, 1
 
 # schedule action kinds / op kinds (acct.h)
-A_LOOP_BEGIN, A_LOOP_END, A_DIRECTIVE, A_H2D, A_D2H, A_BIND, A_STORE, A_KERNEL, A_HOST, A_SYNC = \
-    range(1, 11)
+A_LOOP_BEGIN, A_LOOP_END, A_DIRECTIVE, A_H2D, A_D2H, A_BIND, A_STORE, A_KERNEL, A_HOST, A_SYNC, \
+    A_H2D_GATHER = range(1, 12)
 K_FILL, K_COPY, K_IM2COL, K_GEMM, K_ADD_BIAS, K_LEAKY, K_LINEAR, K_MAXPOOL = range(1, 9)
 OP_KIND = {"fill": K_FILL, "copy": K_COPY, "im2col": K_IM2COL, "gemm": K_GEMM,
            "add_bias": K_ADD_BIAS, "leaky": K_LEAKY, "linear": K_LINEAR, "maxpool": K_MAXPOOL}

@@ -42,3 +42,72 @@ def both():
 for name, fn, mb in (("H2D 183MB", h2d, 183), ("D2H 115MB", d2h, 115), ("both", both, 298)):
     ms = timed(fn)
     print(f"{name:10s}: {ms:6.2f} ms  {mb / 1024 / (ms / 1e3):6.1f} GB/s")
+
+
+# the e2e leg's actual copy mix: per-array H2D copies (hoisted copyins of
+# yolov2-tiny, MB) on one stream and per-array D2H copies on another
+sizes_in = [17.8, 0.0001, 10.6, 0.002, 2.6, 23.8, 0.0001, 5.3, 0.02, 1.3, 11.9, 0.0003, 2.6, 0.07,
+            0.7, 5.9, 0.0005, 1.3, 0.3, 0.3, 3.0, 0.001, 0.7, 1.1, 0.2, 1.5, 0.002, 0.3, 4.5, 0.3,
+            3.0, 0.004, 0.7, 18.0, 5.9, 0.002, 0.3, 18.0, 0.002, 0.3, 0.8] + [2.0] * 16
+sizes_out = [17.8, 10.6, 2.6, 2.6, 23.8, 5.3, 1.3, 1.3, 11.9, 2.6, 0.7, 0.7, 5.9, 1.3, 0.3, 0.3, 3.0,
+             0.7, 0.2, 0.2, 1.5, 0.3, 0.3, 0.3, 3.0, 0.7, 5.9, 0.3, 0.3, 0.3]
+def views(total, sizes):
+    out, off = [], 0
+    for mb in sizes:
+        n = max(1, int(mb * MB / 4))
+        out.append((off, n))
+        off += n
+    return out
+vin, vout = views(h_in.numel(), sizes_in), views(h_out.numel(), sizes_out)
+
+
+def h2d_many():
+    with torch.cuda.stream(s1):
+        for off, n in vin:
+            d_in[off:off + n].copy_(h_in[off:off + n], non_blocking=True)
+
+
+def d2h_many():
+    with torch.cuda.stream(s2):
+        for off, n in vout:
+            h_out[off:off + n].copy_(d_out[off:off + n], non_blocking=True)
+
+
+def both_many():
+    h2d_many()
+    d2h_many()
+
+
+for name, fn in (("H2D x57", h2d_many), ("D2H x30", d2h_many), ("both many", both_many)):
+    print(f"{name:10s}: {timed(fn):6.2f} ms")
+
+
+def mix_a():
+    h2d_many()
+    d2h()
+
+
+def mix_b():
+    h2d()
+    d2h_many()
+
+
+for name, fn in (("H2D many + D2H one", mix_a), ("H2D one + D2H many", mix_b)):
+    print(f"{name:20s}: {timed(fn):6.2f} ms")
+
+
+chunks = views(h_in.numel(), [sum(sizes_in) / 8] * 8)
+
+
+def h2d_8():
+    with torch.cuda.stream(s1):
+        for off, n in chunks:
+            d_in[off:off + n].copy_(h_in[off:off + n], non_blocking=True)
+
+
+def mix_c():
+    h2d_8()
+    d2h_many()
+
+
+print(f"{'H2D x8 + D2H many':20s}: {timed(mix_c):6.2f} ms")

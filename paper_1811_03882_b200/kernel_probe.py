@@ -176,6 +176,8 @@ def launch_instance(kind: str, p: dict) -> tuple[str | None, str, str]:
         if p["K"] > 65535 or p["K"] * _pitch(p["N"]) >= MAX_ELEMS:
             raise ValueError("im2col too large for 32-bit indexing (ACCT_ENOTSUP)")
         if p["ksize"] == 3 and p["stride"] == 1 and p["pad"] == 1:
+            if 16 <= p["ow"] < 64:
+                return "acct_elementwise.cu", "im2col_k3s1_flat_kernel", "3x3/1/1 pixel kernel"
             return "acct_elementwise.cu", "im2col_k3s1_kernel", "3x3/1/1 window kernel"
         if p["ow"] >= 64:
             return "acct_elementwise.cu", "im2col_rows_kernel", "row kernel"
@@ -192,15 +194,51 @@ def launch_instance(kind: str, p: dict) -> tuple[str | None, str, str]:
         return "acct_elementwise.cu", "maxpool_kernel", "flat kernel"
     if kind == "gemm":
         M, N, K = p["M"], p["N"], p["K"]
-        if M <= 16 and K * 32 * 4 <= 200 * 1024:
-            return "acct_gemm_simt.cu", "gemm_stream_kernel<16, 8>", "HBM-streaming FP32 kernel"
+        if K * 32 * 4 <= 200 * 1024 and (M <= 16 or (M <= 32 and K <= 64)):
+            inst = "gemm_stream_kernel<16, 8>" if M <= 16 else "gemm_stream2_kernel<32, 8>"
+            return "acct_gemm_simt.cu", inst, "HBM-streaming FP32 kernel"
         if M <= 32:
             return "acct_gemm_tc.cu", "acct::tc_gemm_kernel<32, true, 32>", "tcgen05 swap tile"
         if M <= 64:
             return "acct_gemm_tc.cu", "acct::tc_gemm_kernel<64, true, 32>", "tcgen05 swap tile"
+        choice = gemm_tile(M, N, K)
+        if choice == "pair256":
+            return ("acct_gemm_tc.cu", "acct::tc2_gemm_kernel<256, 1, 32, false>",
+                    "tcgen05 CTA-pair 256x256 tile (cta_group::2)")
+        if choice == "pair192":
+            return ("acct_gemm_tc.cu", "acct::tc2_gemm_kernel<192, 1, 32, false>",
+                    "tcgen05 CTA-pair 256x192 tile (cta_group::2)")
         return ("acct_gemm_tc.cu", "acct::tc_gemm_kernel<192, false, 16>",
                 "tcgen05 128x192 tile (operand A in TMEM)")
     raise KeyError(kind)
+
+
+# the tile choice of gemm_tc (acct_gemm_tc.cu), restated for the probe
+SMS = 148
+
+
+def _plan_splits(tiles: int, total_kb: int, sms: int) -> tuple[int, int]:
+    splits = 1
+    if tiles < sms:
+        splits = max(1, min(sms // tiles, total_kb // 2))
+    kb_per = -(-total_kb // splits)
+    return -(-total_kb // kb_per), kb_per
+
+
+def _cost(M: int, N: int, K: int, tn: int, bk: int, rows: int, units: int) -> int:
+    tiles = -(-M // rows) * -(-N // tn)
+    splits, kb_per = _plan_splits(tiles, -(-K // bk), units)
+    return -(-(tiles * splits) // units) * kb_per * bk * tn
+
+
+def gemm_tile(M: int, N: int, K: int, sms: int = SMS) -> str:
+    c1 = 1.25 * _cost(M, N, K, 192, 16, 128, sms)
+    waste = (-(-M // 256) * 256) / (-(-M // 128) * 128)
+    c9 = waste * _cost(M, N, K, 192, 32, 256, sms // 2)
+    c10 = waste * _cost(M, N, K, 256, 32, 256, sms // 2)
+    if c10 < c9 and c10 < c1:
+        return "pair256"
+    return "pair192" if c9 < c1 else "single192"
 
 
 # ------------------------------------------------------------ trial build
@@ -243,9 +281,10 @@ def trial_build(source: str, instance: str) -> tuple[bool, str]:
         base = instance.split("::")[-1].split("<")[0]
         if base not in sass:
             return False, f"kernel {base} missing from the sm_100a cubin"
-        if "tc_gemm_kernel" in instance and "UTCHMMA" not in sass:
+        if "gemm_kernel<" in instance and "tc" in instance and "UTCHMMA" not in sass:
             return False, "no tcgen05 MMA (UTCHMMA) in the tensor-core kernel"
-        note = f"sm_100a cubin with {base}" + (" (UTCHMMA)" if "tc_gemm" in instance else "")
+        tc = "tc_gemm" in instance or "tc2_gemm" in instance
+        note = f"sm_100a cubin with {base}" + (" (UTCHMMA)" if tc else "")
     stamp.write_text(note)
     return True, note
 

@@ -49,10 +49,16 @@ def test_launch_configuration_matches_the_runtime():
     for op in net.ops:
         _, inst, _ = kp.launch_instance(op.kind, op.params)
         got.setdefault(op.kind, set()).add(inst)
+    # single image per launch: layer 6 (M=128) keeps one SM, M >= 256 pair tiles
     assert got["gemm"] == {"gemm_stream_kernel<16, 8>", "acct::tc_gemm_kernel<32, true, 32>",
                            "acct::tc_gemm_kernel<64, true, 32>",
-                           "acct::tc_gemm_kernel<192, false, 16>"}
-    assert got["im2col"] == {"im2col_k3s1_kernel"}
+                           "acct::tc_gemm_kernel<192, false, 16>",
+                           "acct::tc2_gemm_kernel<192, 1, 32, false>"}
+    # the restated cost model picks the 256-wide pair where the C++ one does
+    assert kp.gemm_tile(512, 3049, 9216) == "pair256"
+    assert kp.gemm_tile(1024, 3049, 4608) == "pair192"
+    assert kp.gemm_tile(128, 43249, 576) == "single192"
+    assert got["im2col"] == {"im2col_k3s1_kernel", "im2col_k3s1_flat_kernel"}
     assert "maxpool2s2_kernel<4>" in got["maxpool"] and "maxpool_kernel" in got["maxpool"]
 
 

@@ -577,9 +577,15 @@ __device__ __forceinline__ long long gtimer() {
 // SWAP (M <= 64 weight rows): operand A = 128 activation COLUMNS per CTA
 // (256 per pair, transposed into TMEM by the split warps), operand B = the
 // TN weight rows, TN/2 per CTA, K-major; the epilogue writes lanes = columns.
-template <int TN, int NACC_, int BK_, bool SWAP_ = false>
+// DUAL: the two small 3xTF32 terms (hi.lo + lo.hi) accumulate in their own
+// TMEM accumulator next to hi.hi and the epilogue adds the two in FP32.  The
+// tensor core's FP32 accumulate truncates; folding the small terms into the
+// big accumulator costs three truncations of it per k step instead of one.
+template <int TN, int NACC_, int BK_, bool SWAP_ = false, bool DUAL_ = false>
 struct Cfg2 {
   static constexpr bool SWAP = SWAP_;
+  static constexpr bool DUAL = DUAL_;
+  static constexpr int ACC = (DUAL_ ? 2 : 1) * TN;   // TMEM columns per accumulator slot
   static constexpr int BK = BK_;
   static constexpr int HALF = TN / 2;
   static constexpr int X_TILE = 128 * BK * 4;
@@ -590,9 +596,9 @@ struct Cfg2 {
   static constexpr int NACC = NACC_;
   static constexpr int BUDGET = 220 * 1024 - STAGING_BYTES - 512 - 1024;
   static constexpr int SMEM_STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
-  static constexpr int TMEM_STAGES = (512 - NACC * TN) / (2 * BK);
+  static constexpr int TMEM_STAGES = (512 - NACC * ACC) / (2 * BK);
   static constexpr int STAGES = SMEM_STAGES < TMEM_STAGES ? SMEM_STAGES : TMEM_STAGES;
-  static constexpr int A_COL0 = NACC * TN;
+  static constexpr int A_COL0 = NACC * ACC;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 512 + 1024;
   static constexpr uint32_t MN_CHUNK = BK * 128;
   static constexpr int ROWB = BK * 4;  // K-major A row bytes: 64 (SWIZZLE_64B) or 128 (128B)
@@ -601,14 +607,14 @@ struct Cfg2 {
   static_assert(STAGES >= 2, "pipeline too shallow");
 };
 
-template <int TN, int NACC, int BK_, bool SWAP>
+template <int TN, int NACC, int BK_, bool SWAP, bool DUAL = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 int M, int N, int K, int nt, int mt, int splits, int kb_per, int write_hi,
                 float alpha, float beta, float *__restrict__ C, int64_t ldc,
                 const float *__restrict__ bias, int act, float *__restrict__ ws, int64_t ws_ld,
                 int64_t ws_split_stride) {
-  using G = Cfg2<TN, NACC, BK_, SWAP>;
+  using G = Cfg2<TN, NACC, BK_, SWAP, DUAL>;
   constexpr int S = G::STAGES, BK = G::BK;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -701,7 +707,8 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int a = j % NACC;
         if (j >= NACC) ptx::mbar_wait_cluster(&acc_empty[a], ((j / NACC) - 1) & 1);
         ptx::tc_fence_after();
-        const uint32_t d = tmem + a * TN;
+        const uint32_t d = tmem + a * G::ACC;
+        const uint32_t d2 = DUAL ? d + TN : d;  // small-term accumulator
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
           const int s = g % S;
           ptx::mbar_wait(&conv[s], (g / S) & 1);
@@ -721,8 +728,8 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             if (write_hi & 4) continue;
             if (ptx::elect_one()) {
               ptx::mma2_tf32_ts(d, at + 8 * k, dyh, idesc, (kb | k) != 0);
-              ptx::mma2_tf32_ts(d, at + 8 * k, dyl, idesc, 1);
-              ptx::mma2_tf32_ts(d, at + BK + 8 * k, dyh, idesc, 1);
+              ptx::mma2_tf32_ts(d2, at + 8 * k, dyl, idesc, DUAL ? (kb | k) != 0 : 1);
+              ptx::mma2_tf32_ts(d2, at + BK + 8 * k, dyh, idesc, 1);
             }
             __syncwarp();
           }
@@ -827,7 +834,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const int a = j % NACC;
       ptx::mbar_wait_sleepy(&acc_full[a], (j / NACC) & 1);
       ptx::tc_fence_after();
-      const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * TN;
+      const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * G::ACC;
       float *part = ws + w.split * ws_split_stride;
       const int row0 = w.m0 + 128 * rank + 32 * q;
       if (SWAP && !(write_hi & 8)) {
@@ -837,6 +844,13 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         for (int c = 0; c < TN / CH; ++c) {
           uint32_t r[CH];
           ptx::tmem_ld_32x32b_x16(trow + CH * c, r);
+          if constexpr (DUAL) {
+            uint32_t r2[CH];
+            ptx::tmem_ld_32x32b_x16(trow + TN + CH * c, r2);
+#pragma unroll
+            for (int jj = 0; jj < CH; ++jj)
+              r[jj] = __float_as_uint(__uint_as_float(r[jj]) + __uint_as_float(r2[jj]));
+          }
           if (col >= N) continue;
           const int rbase = w.m0 + CH * c;
           if (splits == 1) {
@@ -862,6 +876,13 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         for (int c = 0; c < TN / 32; ++c) {
           uint32_t r[32];
           ptx::tmem_ld_32x32b_x32(trow + 32 * c, r);
+          if constexpr (DUAL) {
+            uint32_t r2[32];
+            ptx::tmem_ld_32x32b_x32(trow + TN + 32 * c, r2);
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj)
+              r[jj] = __float_as_uint(__uint_as_float(r[jj]) + __uint_as_float(r2[jj]));
+          }
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) ptx::sts32(stg_s + 4 * (lane * 33 + jj), __uint_as_float(r[jj]));
           __syncwarp();
@@ -1055,6 +1076,14 @@ int set_smem_attr() {
 
 // fill the machine: split K until tiles x splits covers the SMs, keeping
 // >= 2 k-blocks per split so the pipeline has something to overlap
+int min_splits() {  // experiment knob (ACCT_TC_MINSPLIT): accuracy vs K-chunking
+  static const int v = [] {
+    const char *e = getenv("ACCT_TC_MINSPLIT");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 void plan_splits(int tiles, int total_kb, int sms, int *splits_out, int *kb_per_out) {
   int splits = 1;
   if (tiles < sms) {
@@ -1062,6 +1091,12 @@ void plan_splits(int tiles, int total_kb, int sms, int *splits_out, int *kb_per_
     if (splits > total_kb / 2) splits = total_kb / 2;
     if (splits < 1) splits = 1;
   }
+  if (splits < min_splits()) splits = min_splits() < total_kb ? min_splits() : total_kb;
+  static const int max_kb = [] {  // ACCT_TC_MAXKB: cap k-blocks per split (accuracy knob)
+    const char *e = getenv("ACCT_TC_MAXKB");
+    return e ? atoi(e) : 0;
+  }();
+  if (max_kb > 0 && (total_kb + splits - 1) / splits > max_kb) splits = (total_kb + max_kb - 1) / max_kb;
   const int kb_per = (total_kb + splits - 1) / splits;
   *splits_out = (total_kb + kb_per - 1) / kb_per;
   *kb_per_out = kb_per;
@@ -1117,11 +1152,11 @@ int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, con
   return ACCT_OK;
 }
 
-template <int TN, int NACC, int BK, bool SWAP = false>
+template <int TN, int NACC, int BK, bool SWAP = false, bool DUAL = false>
 int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
                int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
                cudaStream_t s) {
-  using G = Cfg2<TN, NACC, BK, SWAP>;
+  using G = Cfg2<TN, NACC, BK, SWAP, DUAL>;
   CUtensorMap ta, tb;
   // weights: K-major box of BK x (128 rows, or TN/2 rows per CTA when swapped)
   if (!cached_map(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BK, SWAP ? TN / 2 : 128,
@@ -1148,7 +1183,7 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(mu);
     if (dev >= 0 && dev < 64 && !done[dev]) {
-      if (int rc = check_cuda(cudaFuncSetAttribute(tc2_gemm_kernel<TN, NACC, BK, SWAP>,
+      if (int rc = check_cuda(cudaFuncSetAttribute(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    G::SMEM_BYTES),
                               "gemm_tc2: smem attribute"))
@@ -1157,7 +1192,7 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
     }
   }
   const int pairs = units < pairs_avail ? units : pairs_avail;
-  launch(tc2_gemm_kernel<TN, NACC, BK, SWAP>, dim3(2 * pairs), dim3(THREADS), G::SMEM_BYTES, s, ta, tb, M,
+  launch(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL>, dim3(2 * pairs), dim3(THREADS), G::SMEM_BYTES, s, ta, tb, M,
          N, K, nt, mt, splits, kb_per, g_write_hi, alpha, beta, C, ldc, bias, act, ws, ws_ld,
          rows * ws_ld);
   if (int rc = note_launch("gemm_tc2")) return rc;
@@ -1211,6 +1246,8 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
   if (force == 8) return launch_tc2<192, 1, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (force == 9) return launch_tc2<192, 1, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (force == 10) return launch_tc2<256, 1, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (force == 13) return launch_tc2<192, 1, 16, false, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (force == 14) return launch_tc2<128, 1, 32, false, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   // Candidates: one SM per 128 x 192 tile (operand A in TMEM), or a CTA pair
   // per 256 x {192, 256} tile (cta_group::2, BK = 32).  Pick the shortest
   // critical path -- waves x k-blocks per unit x TN after split-K -- with the
@@ -1223,6 +1260,13 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
   const double waste = (double)((M + 255) / 256 * 256) / (double)((M + 127) / 128 * 128);
   const double c9 = waste * (double)tile_cost2(M, N, K, 192, 32, sms / 2);
   const double c10 = waste * (double)tile_cost2(M, N, K, 256, 32, sms / 2);
+  // Long K: the tensor core's truncating FP32 accumulate compounds (3xTF32
+  // relative error ~1e-5 at K = 4608, enough to reach 1e-4 through the 26
+  // layers of yolov2-608); above kDualK the pair tile keeps the small terms in
+  // a second accumulator (3x less error, ~12% slower: tools/tile_diag.py)
+  constexpr int kDualK = 1536;
+  if ((c10 < c1 || c9 < c1) && K > kDualK)
+    return launch_tc2<192, 1, 16, false, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (c10 < c9 && c10 < c1)
     return launch_tc2<256, 1, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (c9 < c1)

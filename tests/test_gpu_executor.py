@@ -109,3 +109,28 @@ def test_timeout_is_reported_not_raised(cuda_device):
     ex = PatternExecutor(net, device=0)
     r = ex.run("0" * len(net.ops), timeout_s=1e-9)
     assert r.status == "timeout"
+
+
+def test_yolov2_608_all_offload_matches_oracle(cuda_device):
+    """configs[4]'s deeper 608x608 net (109 genes, gemm K up to 9216): the
+    batched all-offload schedule -- CTA-pair and single-SM tcgen05 tiles,
+    stream and swap gemms, gathered copyins, early copyouts -- against the C
+    oracle, with every host array after the hoisted copyouts."""
+    net = build_net("yolov2-608", images=2)
+    ref = cprog.reference_forward(net)
+    ex = PatternExecutor(net, device=0)
+    bits = "1" * len(net.ops)
+    sched = ex.compile(bits)
+    assert sched.batch == 2
+    r = ex.run(sched)
+    for key, val in sched.expected.items():
+        assert r.counters[key] == val, key
+    close(ex.outputs(), ref["outputs"])
+    # arrays copied out after the loop hold the last image's values
+    for name in ("out25", "col24", "pool1", "idx1"):
+        want = ref["state"][name]
+        got = ex.host_array(name)
+        if want.dtype == np.int32:
+            assert np.array_equal(got, want), name
+        else:
+            close(got, want)

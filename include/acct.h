@@ -267,7 +267,10 @@ int acct_tc_trace(long long *out);
 /* force the normal-orientation tile of the tensor-core gemm (0 = the cost
  * model; 1 = 128x192, 2/3 = 128x128 BK 16/32, 4 = 128x256, 5/6/7 = CTA pair
  * 256x192 / 256x256 / 256x128 (BK 16), 8 = pair 256x192 one accumulator,
- * 9/10 = pair 256x192 / 256x256 BK 32, 12 = pair swap tile for M <= 64);
+ * 9/10 = pair 256x192 / 256x256 BK 32, 12 = pair swap tile for M <= 64,
+ * 13/14 = pair 256x192 BK 16 / 256x128 BK 32 with a second accumulator for
+ * the small 3xTF32 terms, 15 = pair 256x192 BK 32, second accumulator, only
+ * A lo in TMEM -- the default for K > 1536);
  * tests and tools only                                                     */
 void acct_tc_set_tile(int tile);
 

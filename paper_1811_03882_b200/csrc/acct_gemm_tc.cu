@@ -581,10 +581,15 @@ __device__ __forceinline__ long long gtimer() {
 // TMEM accumulator next to hi.hi and the epilogue adds the two in FP32.  The
 // tensor core's FP32 accumulate truncates; folding the small terms into the
 // big accumulator costs three truncations of it per k step instead of one.
-template <int TN, int NACC_, int BK_, bool SWAP_ = false, bool DUAL_ = false>
+// LOA: only A lo goes to TMEM (BK columns per stage instead of 2 BK); the MMAs
+// with A hi read the raw K-major tile from shared memory -- leaves TMEM room
+// for DUAL with BK = 32
+template <int TN, int NACC_, int BK_, bool SWAP_ = false, bool DUAL_ = false, bool LOA_ = false>
 struct Cfg2 {
   static constexpr bool SWAP = SWAP_;
   static constexpr bool DUAL = DUAL_;
+  static constexpr bool LOA = LOA_;
+  static constexpr int A_STAGE_COLS = (LOA_ ? 1 : 2) * BK_;
   static constexpr int ACC = (DUAL_ ? 2 : 1) * TN;   // TMEM columns per accumulator slot
   static constexpr int BK = BK_;
   static constexpr int HALF = TN / 2;
@@ -596,7 +601,7 @@ struct Cfg2 {
   static constexpr int NACC = NACC_;
   static constexpr int BUDGET = 220 * 1024 - STAGING_BYTES - 512 - 1024;
   static constexpr int SMEM_STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
-  static constexpr int TMEM_STAGES = (512 - NACC * ACC) / (2 * BK);
+  static constexpr int TMEM_STAGES = (512 - NACC * ACC) / A_STAGE_COLS;
   static constexpr int STAGES = SMEM_STAGES < TMEM_STAGES ? SMEM_STAGES : TMEM_STAGES;
   static constexpr int A_COL0 = NACC * ACC;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 512 + 1024;
@@ -607,15 +612,16 @@ struct Cfg2 {
   static_assert(STAGES >= 2, "pipeline too shallow");
 };
 
-template <int TN, int NACC, int BK_, bool SWAP, bool DUAL = false>
+template <int TN, int NACC, int BK_, bool SWAP, bool DUAL = false, bool LOA = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 int M, int N, int K, int nt, int mt, int splits, int kb_per, int write_hi,
                 float alpha, float beta, float *__restrict__ C, int64_t ldc,
                 const float *__restrict__ bias, int act, float *__restrict__ ws, int64_t ws_ld,
                 int64_t ws_split_stride) {
-  using G = Cfg2<TN, NACC, BK_, SWAP, DUAL>;
+  using G = Cfg2<TN, NACC, BK_, SWAP, DUAL, LOA>;
   constexpr int S = G::STAGES, BK = G::BK;
+  static_assert(!LOA || !SWAP, "LOA is for the normal orientation");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -716,7 +722,8 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             g_trace[3][g] = gtimer();
           ptx::tc_fence_after();
           const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
-          const uint32_t at = tmem + G::A_COL0 + s * 2 * BK;
+          const uint32_t at = tmem + G::A_COL0 + s * G::A_STAGE_COLS;
+          const uint32_t xhs = ptx::smem_u32(x_hi(s));
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {
             const uint64_t dyh =
@@ -727,9 +734,17 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                      : ptx::smem_desc(yl + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
             if (write_hi & 4) continue;
             if (ptx::elect_one()) {
-              ptx::mma2_tf32_ts(d, at + 8 * k, dyh, idesc, (kb | k) != 0);
-              ptx::mma2_tf32_ts(d2, at + 8 * k, dyl, idesc, DUAL ? (kb | k) != 0 : 1);
-              ptx::mma2_tf32_ts(d2, at + BK + 8 * k, dyh, idesc, 1);
+              if constexpr (LOA) {
+                // A hi = the raw K-major tile in shared memory, A lo in TMEM
+                const uint64_t dxh = ptx::smem_desc(xhs + 32 * k, 16, G::K_SBO, G::K_LAYOUT);
+                ptx::mma2_tf32_ss(d, dxh, dyh, idesc, (kb | k) != 0);
+                ptx::mma2_tf32_ss(d2, dxh, dyl, idesc, DUAL ? (kb | k) != 0 : 1);
+                ptx::mma2_tf32_ts(d2, at + 8 * k, dyh, idesc, 1);
+              } else {
+                ptx::mma2_tf32_ts(d, at + 8 * k, dyh, idesc, (kb | k) != 0);
+                ptx::mma2_tf32_ts(d2, at + 8 * k, dyl, idesc, DUAL ? (kb | k) != 0 : 1);
+                ptx::mma2_tf32_ts(d2, at + BK + 8 * k, dyh, idesc, 1);
+              }
             }
             __syncwarp();
           }
@@ -798,9 +813,13 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
               lo[4 * c + e] = __float_as_uint(v[e] - __uint_as_float(h));
             }
           }
-          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + G::A_COL0 + s * 2 * BK;
-          ptx::tmem_st_cols<BK>(ta, hi);
-          ptx::tmem_st_cols<BK>(ta + BK, lo);
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + G::A_COL0 + s * G::A_STAGE_COLS;
+          if constexpr (LOA) {
+            ptx::tmem_st_cols<BK>(ta, lo);
+          } else {
+            ptx::tmem_st_cols<BK>(ta, hi);
+            ptx::tmem_st_cols<BK>(ta + BK, lo);
+          }
 #pragma unroll
           for (int i = 0; i < NY; ++i) {
             if (ct + 128 * i < G::Y_TILE / 16) {
@@ -1152,11 +1171,11 @@ int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, con
   return ACCT_OK;
 }
 
-template <int TN, int NACC, int BK, bool SWAP = false, bool DUAL = false>
+template <int TN, int NACC, int BK, bool SWAP = false, bool DUAL = false, bool LOA = false>
 int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
                int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
                cudaStream_t s) {
-  using G = Cfg2<TN, NACC, BK, SWAP, DUAL>;
+  using G = Cfg2<TN, NACC, BK, SWAP, DUAL, LOA>;
   CUtensorMap ta, tb;
   // weights: K-major box of BK x (128 rows, or TN/2 rows per CTA when swapped)
   if (!cached_map(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BK, SWAP ? TN / 2 : 128,
@@ -1183,7 +1202,7 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(mu);
     if (dev >= 0 && dev < 64 && !done[dev]) {
-      if (int rc = check_cuda(cudaFuncSetAttribute(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL>,
+      if (int rc = check_cuda(cudaFuncSetAttribute(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    G::SMEM_BYTES),
                               "gemm_tc2: smem attribute"))
@@ -1192,7 +1211,7 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
     }
   }
   const int pairs = units < pairs_avail ? units : pairs_avail;
-  launch(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL>, dim3(2 * pairs), dim3(THREADS), G::SMEM_BYTES, s, ta, tb, M,
+  launch(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA>, dim3(2 * pairs), dim3(THREADS), G::SMEM_BYTES, s, ta, tb, M,
          N, K, nt, mt, splits, kb_per, g_write_hi, alpha, beta, C, ldc, bias, act, ws, ws_ld,
          rows * ws_ld);
   if (int rc = note_launch("gemm_tc2")) return rc;
@@ -1248,6 +1267,7 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
   if (force == 10) return launch_tc2<256, 1, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (force == 13) return launch_tc2<192, 1, 16, false, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (force == 14) return launch_tc2<128, 1, 32, false, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if (force == 15) return launch_tc2<192, 1, 32, false, true, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   // Candidates: one SM per 128 x 192 tile (operand A in TMEM), or a CTA pair
   // per 256 x {192, 256} tile (cta_group::2, BK = 32).  Pick the shortest
   // critical path -- waves x k-blocks per unit x TN after split-K -- with the
@@ -1263,10 +1283,12 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
   // Long K: the tensor core's truncating FP32 accumulate compounds (3xTF32
   // relative error ~1e-5 at K = 4608, enough to reach 1e-4 through the 26
   // layers of yolov2-608); above kDualK the pair tile keeps the small terms in
-  // a second accumulator (3x less error, ~12% slower: tools/tile_diag.py)
+  // a second accumulator (3x less error) and, to leave TMEM for it at BK 32,
+  // only A lo in TMEM (A hi read from shared memory): L12 128 us vs 127 us
+  // without the second accumulator (tools/tile_diag.py, gemm_bench.py)
   constexpr int kDualK = 1536;
   if ((c10 < c1 || c9 < c1) && K > kDualK)
-    return launch_tc2<192, 1, 16, false, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+    return launch_tc2<192, 1, 32, false, true, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (c10 < c9 && c10 < c1)
     return launch_tc2<256, 1, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (c9 < c1)

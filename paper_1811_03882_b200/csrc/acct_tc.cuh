@@ -320,6 +320,16 @@ __device__ __forceinline__ void mma2_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, u
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// the same with operand A in shared memory (each CTA's 128 rows at this address)
+__device__ __forceinline__ void mma2_tf32_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // arrive on the mbarrier at this smem offset in every CTA of `mask` once all
 // previously issued tcgen05 ops of this thread complete
 __device__ __forceinline__ void mma2_commit_multicast(uint64_t *bar, uint16_t mask) {

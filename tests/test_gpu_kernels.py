@@ -204,7 +204,7 @@ TILE_SHAPES = [(128, 2704, 576), (256, 676, 1152), (512, 169, 2304), (425, 169, 
                (1024, 520, 4608), (1024, 4096, 256)]
 
 
-@pytest.mark.parametrize("tile", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 13, 14])
+@pytest.mark.parametrize("tile", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 13, 14, 15])
 @pytest.mark.parametrize("M,N,K_", TILE_SHAPES)
 def test_every_tensor_core_tile_within_tolerance(cuda_device, orc, tile, M, N, K_):
     """Each normal-orientation tile variant, forced (0 = the cost model): 1-CTA

@@ -1282,11 +1282,12 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
   const double c10 = waste * (double)tile_cost2(M, N, K, 256, 32, sms / 2);
   // Long K: the tensor core's truncating FP32 accumulate compounds (3xTF32
   // relative error ~1e-5 at K = 4608, enough to reach 1e-4 through the 26
-  // layers of yolov2-608); above kDualK the pair tile keeps the small terms in
+  // layers of yolov2-608); above kDualK (768: every pair-tile layer of the
+  // nets but the shortest) the pair tile keeps the small terms in
   // a second accumulator (3x less error) and, to leave TMEM for it at BK 32,
   // only A lo in TMEM (A hi read from shared memory): L12 128 us vs 127 us
   // without the second accumulator (tools/tile_diag.py, gemm_bench.py)
-  constexpr int kDualK = 1536;
+  constexpr int kDualK = 768;
   if ((c10 < c1 || c9 < c1) && K > kDualK)
     return launch_tc2<192, 1, 32, false, true, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (c10 < c9 && c10 < c1)

@@ -463,7 +463,7 @@ def run_ours(args):
         "config": {"workload": f"{args.net} {dims}, batch 1 per forward pass, "
                                f"{args.images}-image loop per step, all-offload genome "
                                f"({len(net.ops)} genes) with hoisted transfers",
-                   "net": args.net, "images_per_step_per_gpu": args.images,
+                   "images_per_step_per_gpu": args.images,
                    "genes": len(net.ops), "gemm": args.gemm, "fused_epilogues": not args.no_fuse,
                    "images_per_launch": res.batch,
                    "l2": "flushed before every step (256 MiB write); per-step footprint "

@@ -317,6 +317,24 @@ int device_op(const acct_action_t &a, acct_array_t *arr, int gemm_mode, cudaStre
                                       D(1), LD(1), BS(1), I[4] ? 1.0f : 0.0f, D(2), LD(2), BS(2),
                                       bias, (int)I[5], nb, gemm_mode, st);
     }
+    case ACCT_K_CONV: {
+      const float *bias = I[7] >= 0 ? reinterpret_cast<float *>(arr[I[7]].dev) : nullptr;
+      const float beta = I[5] ? 1.0f : 0.0f;
+      const int M = (int)I[4], K = 9 * (int)I[1], N = (int)(I[2] * I[3]);
+      if (gemm_mode == ACCT_GEMM_AUTO) {
+        const int rc = acct_conv3x3_im2col_gemm_f32(D(0), LD(0), BS(0), (int)I[1], (int)I[2],
+                                                    (int)I[3], D(1), LD(1), BS(1), M, D(2), LD(2),
+                                                    beta, D(3), LD(3), BS(3), bias, (int)I[6], nb,
+                                                    st);
+        if (rc != ACCT_ENOTSUP) return rc;
+      }
+      // the same ops unfused: im2col, then the gemm in the requested mode
+      if (int rc = acct_im2col_batched_f32(D(0), LD(0), BS(0), (int)I[1], (int)I[2], (int)I[3], 3,
+                                           1, 1, D(1), LD(1), BS(1), nb, st))
+        return rc;
+      return acct_gemm_nn_batched_f32(M, N, K, 1.0f, D(2), LD(2), 0, D(1), LD(1), BS(1), beta, D(3),
+                                      LD(3), BS(3), bias, (int)I[6], nb, gemm_mode, st);
+    }
     case ACCT_K_ADD_BIAS:
       return acct_add_bias_batched_f32(D(0), LD(0), BS(0), D(1), (int)I[1], I[2], nb, st);
     case ACCT_K_LEAKY:
@@ -758,6 +776,7 @@ int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *action
       case ACCT_A_KERNEL:
         for (int j = 0; j < 4 && forked; ++j)
           if ((rc = need(a.a[j]))) return rc;
+        if (a.i[0] == ACCT_K_CONV && forked && (rc = need((int)a.i[7]))) return rc;  // bias
         if (prof) {
           size_t first = prof->used;
           cudaEvent_t e0 = prof->next(), e1 = prof->next();

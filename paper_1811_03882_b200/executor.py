@@ -420,7 +420,7 @@ class PatternExecutor:
                 members = role[1]
                 for m in members:
                     entry(net.ops[m].loop_id)
-                acts.append(self._fused_gemm_action([net.ops[m] for m in role[2]], p))
+                acts.append(self._fused_gemm_action([net.ops[m] for m in role[2]], p, role[3]))
                 for m in members:
                     leave(net.ops[m].loop_id)
                 device_ops += 1
@@ -468,7 +468,8 @@ class PatternExecutor:
             if role is None:
                 acts.append(self._op_action(op, K.A_KERNEL, p))
             elif role[0] == "anchor":
-                acts.append(self._fused_gemm_action([self.net.ops[m] for m in role[2]], p))
+                acts.append(self._fused_gemm_action([self.net.ops[m] for m in role[2]], p,
+                                                    role[3]))
         acts.append((K.A_LOOP_END, (), (0,)))
         acts[0] = (K.A_LOOP_BEGIN, (), (self.images // p, len(acts) - 1))
         acts.append((K.A_SYNC, (), ()))
@@ -490,6 +491,8 @@ class PatternExecutor:
             return (slots[2],)
         if kind == K.K_MAXPOOL:
             return (slots[1], slots[2])
+        if kind == K.K_CONV:
+            return (slots[1], slots[3])
         return ()
 
     def _overlap_transfers(self, acts: list, single_pass: bool) -> list:
@@ -511,7 +514,10 @@ class PatternExecutor:
         pre, body, post = list(acts[:begin]), list(acts[begin + 1:end]), list(acts[end + 1:])
         first_use: dict[int, int] = {}
         for i, a in enumerate(body):
-            for slot in a[1]:
+            slots = tuple(a[1])
+            if a[0] == K.A_KERNEL and a[2][0] == K.K_CONV:
+                slots += (a[2][7],)                    # the conv's bias slot
+            for slot in slots:
                 if slot is not None and slot >= 0:
                     first_use.setdefault(slot, i)
         h2d = [a for a in pre if a[0] == K.A_H2D]
@@ -603,8 +609,9 @@ class PatternExecutor:
 
         Returns {op index: role}: ("absorbed_before",) for a fused fill,
         ("anchor", [ops whose directives execute around the launch],
-        [fused op indices]) for the gemm, ("absorbed_after",) for a fused
-        bias/activation.  A member joins only if it is offloaded and no
+        [fused op indices], im2col index or None) for the gemm,
+        ("absorbed_after",) for a fused bias/activation, ("absorbed_conv",)
+        for an im2col folded into the launch (see _conv_partner).  A member joins only if it is offloaded and no
         directive moves the output array at any loop boundary strictly
         inside the fused span (so its intermediate values are unobservable);
         ops in between that do not touch the output (im2col) run unchanged.
@@ -646,14 +653,44 @@ class PatternExecutor:
             fused = ([fill] if fill is not None else []) + [g] + after
             if len(fused) < 2:
                 continue
+            conv = self._conv_partner(g, on, moved)
             if fill is not None:
                 roles[fill] = ("absorbed_before",)
-            roles[g] = ("anchor", [g] + after, fused)
+            if conv is not None:
+                roles[conv] = ("absorbed_conv",)
+            roles[g] = ("anchor", ([conv] if conv is not None else []) + [g] + after, fused, conv)
             for j in after:
                 roles[j] = ("absorbed_after",)
         return roles
 
-    def _fused_gemm_action(self, members, nimg: int = 1):
+    def _conv_partner(self, g: int, on: list, moved: dict):
+        """The im2col feeding gemm `g`, when the two can run as one fused
+        conv launch (acct_conv3x3_im2col_gemm_f32): the im2col is offloaded
+        and directly precedes the gemm, is 3x3/1/1 over <= 4 channels with
+        M <= 32 filters (the streaming-gemm shapes), and no directive between
+        the two moves the input, col or output -- so moving the col write to
+        the gemm's launch point is unobservable."""
+        ops = self.net.ops
+        if g == 0:
+            return None
+        op, im = ops[g], ops[g - 1]
+        p = im.params
+        if im.kind != "im2col" or not on[g - 1] or im.arrays["Y"] != op.arrays["B"]:
+            return None
+        if (p["ksize"], p["stride"], p["pad"]) != (3, 1, 1) or p["c"] > 4 or op.params["M"] > 32:
+            return None
+        if p["w"] % 4:
+            return None
+        # the launch runs after both entries and before both exits: a copyout
+        # at the im2col's exit must not see C early, a copyin at the gemm's
+        # entry must not change what the im2col read or wrote
+        if {im.arrays["Y"], op.arrays["C"]} & moved.get(im.loop_id, set()):
+            return None
+        if {im.arrays["X"], im.arrays["Y"]} & moved.get(op.loop_id, set()):
+            return None
+        return g - 1
+
+    def _fused_gemm_action(self, members, nimg: int = 1, conv=None):
         kinds = [m.kind for m in members]
         g = next(m for m in members if m.kind == "gemm")
         p, a = g.params, g.arrays
@@ -667,6 +704,13 @@ class PatternExecutor:
             elif m.kind == "linear":
                 act = K.ACT_LINEAR
         beta_one = 0 if "fill" in kinds else 1
+        if conv is not None:
+            im = self.net.ops[conv]
+            q = im.params
+            return _batched((K.A_KERNEL, (self.slot_of[im.arrays["X"]], self.slot_of[a["B"]],
+                                          self.slot_of[a["A"]], self.slot_of[a["C"]]),
+                             (K.K_CONV, q["c"], q["h"], q["w"], p["M"], beta_one, act,
+                              bias_slot)), nimg)
         return _batched((K.A_KERNEL, (self.slot_of[a["A"]], self.slot_of[a["B"]],
                                       self.slot_of[a["C"]], bias_slot),
                          (K.K_GEMM, p["M"], p["N"], p["K"], beta_one, act)), nimg)
@@ -861,6 +905,16 @@ class PatternExecutor:
                     "N_launch": n_launch,
                     "executions": execs, "flops": 2 * M * N * Kd * nimg, "bytes": byts,
                     "fused": a.a[3] >= 0 or i[4] == 0}
+        if kind == K.K_CONV:
+            c, h, w, M = i[1], i[2], i[3], i[4]
+            N, Kd = h * w, 9 * c
+            op = next(o for o in ops if o.kind == "gemm" and o.arrays["C"] == slots[a.a[3]].name)
+            # input image in, col + C out (C also in when beta = 1), weights once
+            byts = 4 * M * Kd + nimg * 4 * (c * N + Kd * N + (2 if i[5] else 1) * M * N)
+            byts += 4 * M if i[7] >= 0 else 0
+            return {"kind": "conv", "layer": op.layer, "M": M, "N": N, "K": Kd, "images": nimg,
+                    "N_launch": N, "executions": execs, "flops": 2 * M * N * Kd * nimg,
+                    "bytes": byts, "fused": True}
         target = slots[a.a[0]].name
         op = next(o for o in ops if o.kind == name and target in o.arrays.values())
         return {"kind": name, "layer": op.layer, "images": nimg, "executions": execs, "flops": 0,

@@ -26,9 +26,10 @@ ACT_NONE, ACT_LINEAR, ACT_LEAKY = -1, 0, 1
 # schedule action kinds / op kinds (acct.h)
 A_LOOP_BEGIN, A_LOOP_END, A_DIRECTIVE, A_H2D, A_D2H, A_BIND, A_STORE, A_KERNEL, A_HOST, A_SYNC, \
     A_H2D_GATHER = range(1, 12)
-K_FILL, K_COPY, K_IM2COL, K_GEMM, K_ADD_BIAS, K_LEAKY, K_LINEAR, K_MAXPOOL = range(1, 9)
+K_FILL, K_COPY, K_IM2COL, K_GEMM, K_ADD_BIAS, K_LEAKY, K_LINEAR, K_MAXPOOL, K_CONV = range(1, 10)
 OP_KIND = {"fill": K_FILL, "copy": K_COPY, "im2col": K_IM2COL, "gemm": K_GEMM,
-           "add_bias": K_ADD_BIAS, "leaky": K_LEAKY, "linear": K_LINEAR, "maxpool": K_MAXPOOL}
+           "add_bias": K_ADD_BIAS, "leaky": K_LEAKY, "linear": K_LINEAR, "maxpool": K_MAXPOOL,
+           "conv": K_CONV}
 
 ETIMEOUT = 1003
 
@@ -75,6 +76,8 @@ SIGNATURES = {
                                 _i64, _i32, _vp],
     "acct_gemm_nn_batched_f32": [_i32, _i32, _i32, _f32, _vp, _i64, _i64, _vp, _i64, _i64, _f32,
                                  _vp, _i64, _i64, _vp, _i32, _i32, _i32, _vp],
+    "acct_conv3x3_im2col_gemm_f32": [_vp, _i64, _i64, _i32, _i32, _i32, _vp, _i64, _i64, _i32,
+                                     _vp, _i64, _f32, _vp, _i64, _i64, _vp, _i32, _i32, _vp],
     "acct_add_bias_batched_f32": [_vp, _i64, _i64, _vp, _i32, _i64, _i32, _vp],
     "acct_activate_batched_f32": [_vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp],
     "acct_maxpool_batched_f32": [_vp, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
@@ -182,6 +185,13 @@ def gemm_nn(M, N, K, alpha, A, lda, B, ldb, beta, Cp, ldc, bias=None, act=ACT_NO
             mode=GEMM_AUTO, stream=0):
     call("acct_gemm_nn_f32", M, N, K, alpha, A, lda, B, ldb, beta, Cp, ldc, bias, act, mode,
          stream)
+
+
+def conv3x3_im2col_gemm(im, ld_im, im_stride, channels, height, width, col, ld_col, col_stride,
+                        M, A, lda, beta, Cp, ldc, c_stride, bias=None, act=ACT_NONE, batch=1,
+                        stream=0):
+    call("acct_conv3x3_im2col_gemm_f32", im, ld_im, im_stride, channels, height, width, col,
+         ld_col, col_stride, M, A, lda, beta, Cp, ldc, c_stride, bias, act, batch, stream)
 
 
 def add_bias(out, ld, bias, rows, cols, stream=0):

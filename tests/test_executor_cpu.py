@@ -84,3 +84,47 @@ def test_fused_and_unfused_schedules_agree_on_counts():
     sa, sb = a.compile(bits), b.compile(bits)
     assert sa.expected == sb.expected
     assert sa.device_ops < sb.device_ops
+
+
+def test_first_conv_layer_fuses_im2col_into_the_gemm_launch():
+    """All-offload: layer 0 (3x3/1/1, c=3, M=16) becomes ONE conv action that
+    writes col0 and out0; counters are those of the unfused schedule."""
+    net = build_net("yolov2-tiny")
+    a = PatternExecutor(net, device=None, fuse=True)
+    b = PatternExecutor(net, device=None, fuse=False)
+    bits = "1" * len(net.ops)
+    sa, sb = a.compile(bits), b.compile(bits)
+    assert sa.expected == sb.expected
+    convs = [k for k in range(sa.n_actions)
+             if sa.actions[k].kind == K.A_KERNEL and sa.actions[k].i[0] == K.K_CONV]
+    assert len(convs) == 1
+    act = sa.actions[convs[0]]
+    names = list(net.arrays)
+    assert [names[act.a[j]] for j in range(4)] == ["x", "col0", "w0", "out0"]
+    assert list(act.i[1:8]) == [3, 416, 416, 16, 0, K.ACT_LEAKY, names.index("bias0")]
+    assert not any(sa.actions[k].kind == K.A_KERNEL and sa.actions[k].i[0] == K.K_IM2COL
+                   and names[sa.actions[k].a[1]] == "col0" for k in range(sa.n_actions))
+
+
+def test_conv_fusion_only_when_no_directive_splits_it(host_exec):
+    net = host_exec.net
+    g = golden_programs()[net.spec.name]
+    for case in g["cases"]:
+        if not case["valid"]:
+            continue
+        bits = case["genome"]
+        sched = host_exec.compile(bits)
+        moved = {}
+        for tgt, clause, vars_, origin in case["plan"]["directives"]:
+            moved.setdefault(tgt, set()).update(vars_)
+        names = list(net.arrays)
+        for k in range(sched.n_actions):
+            act = sched.actions[k]
+            if act.kind != K.A_KERNEL or act.i[0] != K.K_CONV:
+                continue
+            col = names[act.a[1]]
+            im = next(i for i, o in enumerate(net.ops) if o.kind == "im2col" and o.arrays["Y"] == col)
+            gm = net.ops[im + 1]
+            assert bits[im] == "1" and bits[im + 1] == "1"
+            assert not {col, gm.arrays["C"]} & moved.get(net.ops[im].loop_id, set())
+            assert not {col, net.ops[im].arrays["X"]} & moved.get(gm.loop_id, set())

@@ -130,3 +130,28 @@ def test_batched_kernel_entries_match_single(cuda_device):
     for b in range(P):
         assert torch.equal(ob[:, b * 32:b * 32 + 32], o1[b])
         assert torch.equal(ib[:, b * 32:b * 32 + 32], i1[b])
+
+
+@pytest.mark.parametrize("name,images", [("demo", 8), ("yolov2-tiny", 2)])
+def test_fused_conv_layer_is_bit_identical(cuda_device, name, images):
+    """The fused first-layer conv launch (im2col + streaming gemm in one
+    kernel) leaves every array -- col included -- bit-identical to the
+    unfused schedule, batched and resident alike."""
+    net = build_net(name, images=images)
+    a = PatternExecutor(net, device=0, fuse=True)
+    b = PatternExecutor(net, device=0, fuse=False)
+    bits = "1" * len(net.ops)
+    sa = a.compile(bits)
+    assert any(sa.actions[k].kind == K.A_KERNEL and sa.actions[k].i[0] == K.K_CONV
+               for k in range(sa.n_actions))
+    ra, rb = a.run(sa), b.run(bits)
+    assert {k: v for k, v in ra.counters.items() if k != "kernel_launches"} == \
+        {k: v for k, v in rb.counters.items() if k != "kernel_launches"}
+    assert ra.counters["kernel_launches"] < rb.counters["kernel_launches"]
+    assert np.array_equal(a.outputs(), b.outputs())
+    for name_ in net.arrays:
+        assert np.array_equal(a.device_array(name_), b.device_array(name_)), name_
+        assert np.array_equal(a.host_array(name_), b.host_array(name_)), name_
+    a.run(bits, resident=True)
+    b.run(bits, resident=True)
+    assert np.array_equal(a.device_array(net.output_name), b.device_array(net.output_name))

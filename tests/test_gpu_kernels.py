@@ -259,3 +259,76 @@ def test_swap_tiles_within_tolerance(cuda_device, orc, tile, M, N, K_):
     finally:
         K.lib().acct_tc_set_tile(0)
     gemm_ok(Cd.numpy(), want)
+
+
+@pytest.mark.parametrize("c,h,w,M,beta,use_bias,act,batch",
+                         [(3, 416, 416, 16, 0, True, K.ACT_LEAKY, 1),
+                          (3, 20, 24, 32, 1, False, K.ACT_NONE, 3),
+                          (1, 8, 4, 5, 0, True, K.ACT_LINEAR, 2),
+                          (4, 13, 16, 17, 1, True, K.ACT_LEAKY, 2),
+                          (2, 1, 8, 1, 0, False, K.ACT_NONE, 1)])
+def test_conv3x3_fused_equals_im2col_then_gemm(cuda_device, orc, c, h, w, M, beta, use_bias,
+                                               act, batch):
+    """acct_conv3x3_im2col_gemm_f32 writes col exactly like im2col and C
+    bit-identically to im2col + the AUTO (streaming) gemm; images batched
+    image-major for the input and column-interleaved for col and C."""
+    N, Kd = h * w, 9 * c
+    ld = -(-N // 32) * 32
+    im0 = _rand((batch, c, N), 71)
+    A0 = _rand((M, Kd), 72, -0.5, 0.5)
+    C0 = _rand((M, batch, N), 73)
+    bias0 = _rand((M,), 74)
+    im = torch.zeros((batch, c, ld), device="cuda")
+    im[:, :, :N] = torch.from_numpy(im0).cuda()
+    A = torch.from_numpy(A0).cuda()
+    bias = torch.from_numpy(bias0).cuda() if use_bias else None
+    bp = bias.data_ptr() if use_bias else None
+
+    def fresh():
+        col = torch.full((Kd, batch * ld), float("nan"), device="cuda")
+        C = torch.full((M, batch, ld), 0.0, device="cuda")
+        C[:, :, :N] = torch.from_numpy(C0).cuda()
+        return col, C.view(M, batch * ld)
+
+    col_u, C_u = fresh()
+    K.call("acct_im2col_batched_f32", im.data_ptr(), ld, c * ld, c, h, w, 3, 1, 1,
+           col_u.data_ptr(), batch * ld, ld, batch, stream())
+    K.call("acct_gemm_nn_batched_f32", M, N, Kd, 1.0, A.data_ptr(), Kd, 0, col_u.data_ptr(),
+           batch * ld, ld, float(beta), C_u.data_ptr(), batch * ld, ld, bp, act, batch,
+           K.GEMM_AUTO, stream())
+    col_f, C_f = fresh()
+    K.conv3x3_im2col_gemm(im.data_ptr(), ld, c * ld, c, h, w, col_f.data_ptr(), batch * ld, ld,
+                          M, A.data_ptr(), Kd, float(beta), C_f.data_ptr(), batch * ld, ld, bp,
+                          act, batch, stream())
+    torch.cuda.synchronize()
+    for b in range(batch):
+        cu = col_u[:, b * ld:b * ld + N].cpu().numpy()
+        cf = col_f[:, b * ld:b * ld + N].cpu().numpy()
+        assert np.array_equal(cf, cu)
+        want_col = np.empty((Kd, N), np.float32)
+        orc.orc_im2col(np.ascontiguousarray(im0[b]).ctypes.data, c, h, w, 3, 1, 1,
+                       want_col.ctypes.data)
+        assert np.array_equal(cf, want_col)
+        got = C_f[:, b * ld:b * ld + N].cpu().numpy()
+        assert np.array_equal(got, C_u[:, b * ld:b * ld + N].cpu().numpy())
+        want = np.ascontiguousarray(C0[:, b]) if beta else np.zeros((M, N), np.float32)
+        orc.orc_gemm_nn(M, N, Kd, 1.0, A0.ctypes.data, Kd, want_col.ctypes.data, N,
+                        want.ctypes.data, N)
+        if use_bias:
+            orc.orc_add_bias(want.ctypes.data, bias0.ctypes.data, 1, M, N)
+        if act == K.ACT_LEAKY:
+            orc.orc_activate(want.ctypes.data, M * N, 1)
+        gemm_ok(got, want)
+
+
+def test_conv3x3_fused_declines_unaligned_rows(cuda_device):
+    im = torch.zeros((3, 64), device="cuda")
+    col = torch.zeros((27, 64), device="cuda")
+    A = torch.zeros((8, 27), device="cuda")
+    C = torch.zeros((8, 64), device="cuda")
+    with pytest.raises(K.DeviceError):  # width 10: rows not 16-byte aligned
+        K.conv3x3_im2col_gemm(im.data_ptr(), 64, 0, 3, 6, 10, col.data_ptr(), 64, 0, 8,
+                              A.data_ptr(), 27, 0.0, C.data_ptr(), 64, 0)
+    with pytest.raises(K.DeviceError):  # 5 channels: not a first-layer shape
+        K.conv3x3_im2col_gemm(im.data_ptr(), 64, 0, 5, 2, 8, col.data_ptr(), 64, 0, 8,
+                              A.data_ptr(), 27, 0.0, C.data_ptr(), 64, 0)

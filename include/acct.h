@@ -129,17 +129,21 @@ int acct_maxpool_batched_f32(const float *in, int64_t ld_in, int64_t in_stride, 
                              int32_t *idx, int64_t ld_idx, int64_t idx_stride, int batch,
                              acct_stream_t stream);
 
-/* im2col (3x3 / stride 1 / pad 1) fused with the gemm that consumes it, for a
- * first conv layer (channels <= 4, M <= 32): writes col exactly like
- * acct_im2col_batched_f32 and C = A . col + beta C (+ bias, act) exactly like
- * the streaming gemm acct_gemm_nn_f32 picks in GEMM_AUTO (same FMA order:
- * bit-identical), reading the input image instead of re-reading col.  Rows
- * of col and C (ld, strides, width) must be 16-byte aligned; else ENOTSUP. */
+/* im2col (3x3 / stride 1 / pad 1) fused with the gemm that consumes it, for
+ * the narrow conv layers (channels <= 64, M <= 32): writes col exactly like
+ * acct_im2col_batched_f32 (for images >= col_from of the batch only) and
+ * C = A . col + beta C (+ bias, act) exactly like the SIMT gemms of
+ * acct_gemm_nn_f32 (same FMA order: bit-identical), reading the input image
+ * instead of re-reading col.  col_from = batch - 1 skips the col stores of
+ * every image but the last (the executor does so when only that copy is
+ * observable).  Rows of col and C (ld, strides, width) must be 16-byte
+ * aligned; else ENOTSUP. */
 int acct_conv3x3_im2col_gemm_f32(const float *im, int64_t ld_im, int64_t im_stride, int channels,
                                  int height, int width, float *col, int64_t ld_col,
                                  int64_t col_stride, int M, const float *A, int64_t lda,
                                  float beta, float *C, int64_t ldc, int64_t c_stride,
-                                 const float *bias, int act, int batch, acct_stream_t stream);
+                                 const float *bias, int act, int batch, int col_from,
+                                 acct_stream_t stream);
 
 /* ------------------------------------------------------------- transfers --
  * Direction: 1 = host->device, 2 = device->host.  Pitched 2-D copy of
@@ -211,9 +215,10 @@ enum {
   ACCT_K_FILL = 1, ACCT_K_COPY = 2, ACCT_K_IM2COL = 3, ACCT_K_GEMM = 4,
   ACCT_K_ADD_BIAS = 5, ACCT_K_LEAKY = 6, ACCT_K_LINEAR = 7, ACCT_K_MAXPOOL = 8,
   /* fused im2col(3x3/1/1) + gemm: slots a = (X, col, A, C); i[1..3] = c, h, w,
-     i[4] = M, i[5] = beta is 1, i[6] = act, i[7] = bias slot (-1: none).
-     Device only; runs as im2col + gemm when gemm_mode is not GEMM_AUTO or the
-     fused kernel declines the shape */
+     i[4] = M, i[5] = beta is 1, i[6] = act, i[7] = bias slot (-1: none),
+     i[8] = 1: col is written for the batch's last image only (the others are
+     unobservable).  Device only; runs as im2col + gemm when gemm_mode is
+     GEMM_TC3XTF32 or the fused kernel declines the shape */
   ACCT_K_CONV = 9
 };
 

@@ -347,15 +347,25 @@ int launch_stream(int M, int N, int K, float alpha, const float *A, int64_t lda,
   return acct::note_launch("gemm_stream");
 }
 
-// im2col (3x3 / stride 1 / pad 1) fused with its gemm_nn for a first conv
-// layer: C <= 4 input channels (K = 9 C <= 36 col rows), M <= MT filters.
-// A thread owns PX consecutive output pixels of one row: it loads the
-// C x 3 x (PX+2) input window once, stores the K col rows of its pixels (the
-// program's col array is still written in full -- the planner copies it
-// out), and accumulates the M x PX outputs from the same registers in k
-// order -- the FMA chain of the stream gemm over the materialised col, so C
-// is bit-identical to im2col + gemm -- without re-reading col (18.7 of the
-// 50 MB an unfused 416x416 layer moves per image).  blockIdx.z = image.
+// im2col (3x3 / stride 1 / pad 1) fused with its gemm_nn for the narrow conv
+// layers (M <= 32 filters, channels <= 64: K = 9 C <= 576 col rows; the
+// first two yolov2-tiny layers).
+//
+// A CTA owns tiles of P = 128 x PX consecutive output pixels (flat h*w
+// index; images are consecutive tile ranges).  For a tile it stages, per
+// input channel, the flat input range [p0 - W - 1, p0 + P + W] (rows above,
+// the tile's rows, rows below) into shared memory with 16-byte cp.async --
+// out-of-plane chunks are zero, which is the conv's row padding -- double
+// buffered so the next tile's loads overlap this tile's FMAs.  A thread owns
+// PX pixels of one row: per channel it reads its 3 x (PX+2) window from
+// shared memory (column padding masked at w = 0 / W-1), stores the 9 col
+// rows of its pixels and accumulates the M x PX outputs in k order -- the FMA
+// chain of every SIMT gemm over the materialised col (k ascending from 0,
+// then the shared epilogue), so C is bit-identical to im2col + the SIMT gemm
+// -- without re-reading col.  A is staged once per CTA as [k][m] (one
+// broadcast LDS.128 per 4 filters).  Images below `col_from` skip the col
+// stores (the executor passes batch-1 when only the last image's col is
+// observable: dead stores of a privatised array, see executor._col_dead).
 template <int PX>
 struct VecOf;
 template <>
@@ -367,118 +377,205 @@ struct VecOf<2> {
   using T = float2;
 };
 
-template <int MT, int PX>
-__global__ void __launch_bounds__(128, 4)
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait1() {
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
+
+constexpr int CONV_THREADS = 128;
+
+__host__ __device__ constexpr int conv_stage_floats(int px, int width) {
+  return (CONV_THREADS * px + 2 * width + 5 + 3) & ~3;  // [p0-W-1 floored to 4, p0+P+W]
+}
+
+template <int MT, int PX, int MINB>
+__global__ void __launch_bounds__(CONV_THREADS, MINB)
 conv3x3_im2col_gemm_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs,
                            int channels, int height, int width, float *__restrict__ col,
-                           int64_t ld_col, int64_t col_bs, int M, const float *__restrict__ A,
-                           int64_t lda, float beta, float *__restrict__ C, int64_t ldc,
-                           int64_t c_bs, const float *__restrict__ bias, int act) {
+                           int64_t ld_col, int64_t col_bs, int col_from, int M,
+                           const float *__restrict__ A, int64_t lda, float beta,
+                           float *__restrict__ C, int64_t ldc, int64_t c_bs,
+                           const float *__restrict__ bias, int act, int tiles_per_img,
+                           int ntiles) {
   using V = typename VecOf<PX>::T;
-  __shared__ float As[36 * MT];  // [k][m]
+  constexpr int P = CONV_THREADS * PX;
+  extern __shared__ float4 conv_smem[];
+  const int K = channels * 9;
+  const int ls = conv_stage_floats(PX, width);
+  float *As = reinterpret_cast<float *>(conv_smem);  // [k][MT]
+  float *sin0 = As + K * MT;                         // 2 x [channels][ls]
+  const int bufsz = channels * ls;
+  const int HW = height * width;
   pdl_trigger();
   pdl_wait();
-  const int K = channels * 9;
-  for (int t = threadIdx.x; t < K * MT; t += blockDim.x) {
+
+  auto stage = [&](int tile, float *buf) {
+    const int img = tile / tiles_per_img;
+    const int p0 = (tile - img * tiles_per_img) * P;
+    const int a0 = (p0 - width - 1) & ~3;  // floor to a 16-byte chunk
+    const float *src = im + img * im_bs;
+    const int nq = ls >> 2;
+    for (int j = threadIdx.x; j < channels * nq; j += CONV_THREADS) {
+      const int ci = j / nq, q = j - ci * nq;
+      const int g = a0 + 4 * q;  // HW % 4 == 0: a chunk is wholly inside or outside
+      float *dst = buf + ci * ls + 4 * q;
+      if (g >= 0 && g < HW)
+        cp_async16(dst, src + ci * ld_im + g);
+      else
+        *reinterpret_cast<float4 *>(dst) = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    }
+  };
+
+  int tile = blockIdx.x;
+  if (tile < ntiles) stage(tile, sin0);
+  cp_async_commit();
+  for (int t = threadIdx.x; t < K * MT; t += CONV_THREADS) {
     const int k = t / MT, m = t - k * MT;
     As[t] = m < M ? A[(int64_t)m * lda + k] : 0.0f;
   }
-  __syncthreads();
-  const int img = blockIdx.z;
-  im += img * im_bs;
-  col += img * col_bs;
-  C += img * c_bs;
-  const int groups = width / PX;  // width % PX == 0 (checked by the entry)
-  const int total = height * groups;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    const int h = t / groups, w0 = (t - h * groups) * PX;
-    const int p0 = h * width + w0;
-    float acc[MT][PX];
+  int buf = 0;
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int nxt = tile + gridDim.x;
+    if (nxt < ntiles) stage(nxt, sin0 + (buf ^ 1) * bufsz);
+    cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();
+    const int img = tile / tiles_per_img;
+    const int p0 = (tile - img * tiles_per_img) * P;
+    const int p = p0 + threadIdx.x * PX;
+    if (p < HW) {
+      const int h = p / width, w0 = p - h * width;
+      const bool wcol = img >= col_from;
+      float *colp = col + img * col_bs + p;
+      const float *base = sin0 + buf * bufsz + (p - ((p0 - width - 1) & ~3));
+      float acc[MT][PX];
 #pragma unroll
-    for (int m = 0; m < MT; ++m)
+      for (int m = 0; m < MT; ++m)
 #pragma unroll
-      for (int e = 0; e < PX; ++e) acc[m][e] = 0.0f;
-    for (int ci = 0; ci < channels; ++ci) {
-      const float *src = im + (int64_t)ci * ld_im;
-      float win[3][PX + 2];
+        for (int e = 0; e < PX; ++e) acc[m][e] = 0.0f;
+#pragma unroll 1
+      for (int ci = 0; ci < channels; ++ci) {
+        const float *cb = base + ci * ls;
+        float win[3][PX + 2];
 #pragma unroll
-      for (int kh = 0; kh < 3; ++kh) {
-        const int r = h + kh - 1;
-        const bool rok = r >= 0 && r < height;
+        for (int kh = 0; kh < 3; ++kh) {
+          const float *row = cb + (kh - 1) * width - 1;
 #pragma unroll
-        for (int j = 0; j < PX + 2; ++j) {
-          const int c = w0 + j - 1;
-          win[kh][j] = (rok && c >= 0 && c < width) ? __ldg(src + r * width + c) : 0.0f;
+          for (int j = 0; j < PX + 2; ++j) win[kh][j] = row[j];
+          if (w0 == 0) win[kh][0] = 0.0f;
+          if (w0 + PX == width) win[kh][PX + 1] = 0.0f;
         }
-      }
 #pragma unroll
-      for (int kh = 0; kh < 3; ++kh) {
+        for (int kh = 0; kh < 3; ++kh) {
 #pragma unroll
-        for (int kw = 0; kw < 3; ++kw) {
-          const int k = ci * 9 + kh * 3 + kw;
-          V v;
-          float *vf = reinterpret_cast<float *>(&v);
+          for (int kw = 0; kw < 3; ++kw) {
+            const int k = ci * 9 + kh * 3 + kw;
+            V v;
+            float *vf = reinterpret_cast<float *>(&v);
 #pragma unroll
-          for (int e = 0; e < PX; ++e) vf[e] = win[kh][kw + e];
-          __stcs(reinterpret_cast<V *>(col + (int64_t)k * ld_col + p0), v);
-          const float *ak = As + k * MT;
+            for (int e = 0; e < PX; ++e) vf[e] = win[kh][kw + e];
+            if (wcol) __stcs(reinterpret_cast<V *>(colp + (int64_t)k * ld_col), v);
+            const float4 *ak = reinterpret_cast<const float4 *>(As + k * MT);
 #pragma unroll
-          for (int m = 0; m < MT; ++m) {
-            const float a = ak[m];
+            for (int m4 = 0; m4 < MT / 4; ++m4) {
+              const float4 a = ak[m4];
 #pragma unroll
-            for (int e = 0; e < PX; ++e) acc[m][e] = fmaf(a, vf[e], acc[m][e]);
+              for (int e = 0; e < PX; ++e) {
+                acc[4 * m4 + 0][e] = fmaf(a.x, vf[e], acc[4 * m4 + 0][e]);
+                acc[4 * m4 + 1][e] = fmaf(a.y, vf[e], acc[4 * m4 + 1][e]);
+                acc[4 * m4 + 2][e] = fmaf(a.z, vf[e], acc[4 * m4 + 2][e]);
+                acc[4 * m4 + 3][e] = fmaf(a.w, vf[e], acc[4 * m4 + 3][e]);
+              }
+            }
           }
         }
       }
-    }
+      float *cimg = C + img * c_bs + p;
 #pragma unroll
-    for (int m = 0; m < MT; ++m) {
-      if (m >= M) break;
-      V *cp = reinterpret_cast<V *>(C + (int64_t)m * ldc + p0);
-      V cv{}, o;
-      if (beta != 0.0f) cv = *cp;
-      const float *cvf = reinterpret_cast<const float *>(&cv);
-      float *of = reinterpret_cast<float *>(&o);
+      for (int m = 0; m < MT; ++m) {
+        if (m >= M) break;
+        V *cp = reinterpret_cast<V *>(cimg + (int64_t)m * ldc);
+        V cv{}, o;
+        if (beta != 0.0f) cv = *cp;
+        const float *cvf = reinterpret_cast<const float *>(&cv);
+        float *of = reinterpret_cast<float *>(&o);
 #pragma unroll
-      for (int e = 0; e < PX; ++e) of[e] = epilogue(acc[m][e], 1.0f, beta, cvf + e, bias, m, act);
-      __stcs(cp, o);
+        for (int e = 0; e < PX; ++e)
+          of[e] = epilogue(acc[m][e], 1.0f, beta, cvf + e, bias, m, act);
+        __stcs(cp, o);
+      }
     }
+    __syncthreads();  // this buffer is restaged two tiles later
+    buf ^= 1;
   }
+}
+
+template <int MT, int PX, int MINB>
+int launch_conv(int batch, cudaStream_t s, const float *im, int64_t ld_im, int64_t im_stride,
+                int channels, int height, int width, float *col, int64_t ld_col,
+                int64_t col_stride, int col_from, int M, const float *A, int64_t lda, float beta,
+                float *C, int64_t ldc, int64_t c_stride, const float *bias, int act) {
+  auto *k = conv3x3_im2col_gemm_kernel<MT, PX, MINB>;
+  const size_t smem = sizeof(float) * ((size_t)channels * 9 * MT +
+                                       2 * (size_t)channels * conv_stage_floats(PX, width));
+  if (smem > 227 * 1024) return ACCT_ENOTSUP;
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+    return acct::check_cuda(cudaGetLastError(), "conv3x3 fused: smem attribute");
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, CONV_THREADS, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int P = CONV_THREADS * PX;
+  const int64_t tpi = ((int64_t)height * width + P - 1) / P;
+  const int64_t ntiles = tpi * batch;
+  if (ntiles > INT32_MAX) return ACCT_ENOTSUP;
+  int64_t grid = (int64_t)acct::sm_count() * per_sm;
+  if (grid > ntiles) grid = ntiles;
+  acct::launch(k, dim3((unsigned)grid), dim3(CONV_THREADS), smem, s, im, ld_im, im_stride,
+               channels, height, width, col, ld_col, col_stride, col_from, M, A, lda, beta, C, ldc,
+               c_stride, bias, act, (int)tpi, (int)ntiles);
+  return ACCT_OK;
 }
 
 }  // namespace
 
 // C = A . im2col(im) + beta C (+ bias, act) for 3x3/1/1 convolutions with
-// channels <= 4 and M <= 32, also writing the col array; batched over images
+// channels <= 64 and M <= 32, also writing the col array (images >= col_from
+// of the batch); batched over images
 extern "C" int acct_conv3x3_im2col_gemm_f32(const float *im, int64_t ld_im, int64_t im_stride,
                                             int channels, int height, int width, float *col,
                                             int64_t ld_col, int64_t col_stride, int M,
                                             const float *A, int64_t lda, float beta, float *C,
                                             int64_t ldc, int64_t c_stride, const float *bias, int act,
-                                            int batch, acct_stream_t stream) {
+                                            int batch, int col_from, acct_stream_t stream) {
   using namespace acct;
-  if (channels < 1 || channels > 4 || M < 1 || M > 32 || height < 1 || width < 1 || batch < 1 ||
-      batch > 65535 || ld_im < (int64_t)height * width || ld_col < (int64_t)height * width ||
-      ldc < (int64_t)height * width)
+  if (channels < 1 || channels > 64 || M < 1 || M > 32 || height < 1 || width < 1 || batch < 1 ||
+      col_from < 0 || (int64_t)height * width > (1 << 28) || ld_im < (int64_t)height * width ||
+      ld_col < (int64_t)height * width || ldc < (int64_t)height * width)
     return fail(ACCT_ENOTSUP, "conv3x3 fused: shape not supported");
-  if ((reinterpret_cast<uintptr_t>(col) | reinterpret_cast<uintptr_t>(C)) & 15 ||
-      (ld_col | ldc | col_stride | c_stride | width) & 3)
+  if ((reinterpret_cast<uintptr_t>(col) | reinterpret_cast<uintptr_t>(C) |
+       reinterpret_cast<uintptr_t>(im)) & 15 ||
+      (ld_col | ldc | col_stride | c_stride | ld_im | im_stride | width) & 3)
     return fail(ACCT_ENOTSUP, "conv3x3 fused: needs 16-B aligned rows");
-  // 4 pixels per thread at M <= 16; 2 at M <= 32 (64 accumulators either way)
-  const int px = M <= 16 ? 4 : 2;
-  const int64_t total = (int64_t)height * (width / px) * batch;
-  const unsigned gx = grid_for(total, 128, 4);
-  const unsigned per_img = (gx + batch - 1) / batch;
   cudaStream_t s = as_stream(stream);
-  const dim3 grid(per_img, 1, batch);
+  int rc;
   if (M <= 16)
-    launch(conv3x3_im2col_gemm_kernel<16, 4>, grid, dim3(128), 0, s, im, ld_im, im_stride,
-           channels, height, width, col, ld_col, col_stride, M, A, lda, beta, C, ldc, c_stride,
-           bias, act);
+    rc = launch_conv<16, 4, 4>(batch, s, im, ld_im, im_stride, channels, height, width, col,
+                               ld_col, col_stride, col_from, M, A, lda, beta, C, ldc, c_stride,
+                               bias, act);
   else
-    launch(conv3x3_im2col_gemm_kernel<32, 2>, grid, dim3(128), 0, s, im, ld_im, im_stride,
-           channels, height, width, col, ld_col, col_stride, M, A, lda, beta, C, ldc, c_stride,
-           bias, act);
+    rc = launch_conv<32, 2, 4>(batch, s, im, ld_im, im_stride, channels, height, width, col,
+                               ld_col, col_stride, col_from, M, A, lda, beta, C, ldc, c_stride,
+                               bias, act);
+  if (rc == ACCT_ENOTSUP) return fail(ACCT_ENOTSUP, "conv3x3 fused: staging exceeds shared memory");
+  if (rc) return rc;
   return note_launch("conv3x3 im2col+gemm");
 }
 

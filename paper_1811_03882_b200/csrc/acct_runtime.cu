@@ -321,11 +321,13 @@ int device_op(const acct_action_t &a, acct_array_t *arr, int gemm_mode, cudaStre
       const float *bias = I[7] >= 0 ? reinterpret_cast<float *>(arr[I[7]].dev) : nullptr;
       const float beta = I[5] ? 1.0f : 0.0f;
       const int M = (int)I[4], K = 9 * (int)I[1], N = (int)(I[2] * I[3]);
-      if (gemm_mode == ACCT_GEMM_AUTO) {
+      // FP32 FMA in k order: the AUTO choice for these shapes and the SIMT
+      // mode's own chain; I[8] = 1: only the last image's col is observable
+      if (gemm_mode == ACCT_GEMM_AUTO || gemm_mode == ACCT_GEMM_SIMT) {
         const int rc = acct_conv3x3_im2col_gemm_f32(D(0), LD(0), BS(0), (int)I[1], (int)I[2],
                                                     (int)I[3], D(1), LD(1), BS(1), M, D(2), LD(2),
                                                     beta, D(3), LD(3), BS(3), bias, (int)I[6], nb,
-                                                    st);
+                                                    I[8] ? nb - 1 : 0, st);
         if (rc != ACCT_ENOTSUP) return rc;
       }
       // the same ops unfused: im2col, then the gemm in the requested mode

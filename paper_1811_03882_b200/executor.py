@@ -38,6 +38,7 @@ B200-specific choices, none of which changes observable results:
 from __future__ import annotations
 
 import ctypes as C
+import os
 import struct
 import time
 from dataclasses import dataclass, field
@@ -54,6 +55,11 @@ from .planner import (COPY, COPYIN, COPYOUT, TransferPlan, directive_exec_counts
 from .syntax import parse
 
 PITCH_ALIGN = 32  # elements (128 bytes)
+# widest 3x3/1/1 layer (input channels) fused into one FP32 conv launch when
+# it has M <= 32 filters: the first layers (c = 3).  The kernel takes up to 64
+# channels, but at yolov2-tiny layer 2 (c = 16, M = 32: 199 MFMA per image)
+# it measured 13.7 us/img against 12.2 for im2col + the tensor-core swap gemm
+CONV_MAX_C = int(os.environ.get("ACCT_CONV_MAX_C", "4"))
 
 
 def _pitch(cols: int) -> int:
@@ -420,7 +426,8 @@ class PatternExecutor:
                 members = role[1]
                 for m in members:
                     entry(net.ops[m].loop_id)
-                acts.append(self._fused_gemm_action([net.ops[m] for m in role[2]], p, role[3]))
+                acts.append(self._fused_gemm_action([net.ops[m] for m in role[2]], p, role[3],
+                                                    role[4]))
                 for m in members:
                     leave(net.ops[m].loop_id)
                 device_ops += 1
@@ -469,7 +476,7 @@ class PatternExecutor:
                 acts.append(self._op_action(op, K.A_KERNEL, p))
             elif role[0] == "anchor":
                 acts.append(self._fused_gemm_action([self.net.ops[m] for m in role[2]], p,
-                                                    role[3]))
+                                                    role[3], role[4]))
         acts.append((K.A_LOOP_END, (), (0,)))
         acts[0] = (K.A_LOOP_BEGIN, (), (self.images // p, len(acts) - 1))
         acts.append((K.A_SYNC, (), ()))
@@ -658,16 +665,33 @@ class PatternExecutor:
                 roles[fill] = ("absorbed_before",)
             if conv is not None:
                 roles[conv] = ("absorbed_conv",)
-            roles[g] = ("anchor", ([conv] if conv is not None else []) + [g] + after, fused, conv)
+            roles[g] = ("anchor", ([conv] if conv is not None else []) + [g] + after, fused, conv,
+                        conv is not None and self._col_dead(conv, g, moved))
             for j in after:
                 roles[j] = ("absorbed_after",)
         return roles
 
+    def _col_dead(self, im: int, g: int, moved: dict) -> bool:
+        """True when, in an image-batched run, only the LAST image's copy of
+        the fused conv's col array is observable: no directive inside the
+        image loop moves col (hoisted copyouts after the loop read image
+        P-1's copy; hoisted copyins land in image 0's copy and are
+        overwritten by the im2col) and no op but the im2col and its gemm
+        touches it.  The other images' col stores are then dead (the gemm
+        reads the fused launch's registers, not col) and the kernel skips
+        them -- 18.7 of the 32 MB the 416x416 first layer moves per image."""
+        net = self.net
+        col = net.ops[im].arrays["Y"]
+        if any(col in op.arrays.values() for k, op in enumerate(net.ops) if k not in (im, g)):
+            return False
+        return not any(col in vs for lid, vs in moved.items() if lid != net.image_loop)
+
     def _conv_partner(self, g: int, on: list, moved: dict):
         """The im2col feeding gemm `g`, when the two can run as one fused
         conv launch (acct_conv3x3_im2col_gemm_f32): the im2col is offloaded
-        and directly precedes the gemm, is 3x3/1/1 over <= 4 channels with
-        M <= 32 filters (the streaming-gemm shapes), and no directive between
+        and directly precedes the gemm, is 3x3/1/1 over <= CONV_MAX_C
+        channels with M <= 32 filters (the narrow layers, where FP32 FMA from
+        the input window beats im2col + a gemm), and no directive between
         the two moves the input, col or output -- so moving the col write to
         the gemm's launch point is unobservable."""
         ops = self.net.ops
@@ -677,7 +701,8 @@ class PatternExecutor:
         p = im.params
         if im.kind != "im2col" or not on[g - 1] or im.arrays["Y"] != op.arrays["B"]:
             return None
-        if (p["ksize"], p["stride"], p["pad"]) != (3, 1, 1) or p["c"] > 4 or op.params["M"] > 32:
+        if (p["ksize"], p["stride"], p["pad"]) != (3, 1, 1) or p["c"] > CONV_MAX_C or \
+                op.params["M"] > 32:
             return None
         if p["w"] % 4:
             return None
@@ -690,7 +715,7 @@ class PatternExecutor:
             return None
         return g - 1
 
-    def _fused_gemm_action(self, members, nimg: int = 1, conv=None):
+    def _fused_gemm_action(self, members, nimg: int = 1, conv=None, col_dead=False):
         kinds = [m.kind for m in members]
         g = next(m for m in members if m.kind == "gemm")
         p, a = g.params, g.arrays
@@ -710,7 +735,7 @@ class PatternExecutor:
             return _batched((K.A_KERNEL, (self.slot_of[im.arrays["X"]], self.slot_of[a["B"]],
                                           self.slot_of[a["A"]], self.slot_of[a["C"]]),
                              (K.K_CONV, q["c"], q["h"], q["w"], p["M"], beta_one, act,
-                              bias_slot)), nimg)
+                              bias_slot, int(col_dead and nimg > 1))), nimg)
         return _batched((K.A_KERNEL, (self.slot_of[a["A"]], self.slot_of[a["B"]],
                                       self.slot_of[a["C"]], bias_slot),
                          (K.K_GEMM, p["M"], p["N"], p["K"], beta_one, act)), nimg)
@@ -909,8 +934,11 @@ class PatternExecutor:
             c, h, w, M = i[1], i[2], i[3], i[4]
             N, Kd = h * w, 9 * c
             op = next(o for o in ops if o.kind == "gemm" and o.arrays["C"] == slots[a.a[3]].name)
-            # input image in, col + C out (C also in when beta = 1), weights once
-            byts = 4 * M * Kd + nimg * 4 * (c * N + Kd * N + (2 if i[5] else 1) * M * N)
+            # input image in, col + C out (C also in when beta = 1), weights once;
+            # col of the last image only when the others are dead (i[8])
+            col_imgs = 1 if i[8] else nimg
+            byts = 4 * M * Kd + nimg * 4 * (c * N + (2 if i[5] else 1) * M * N) + \
+                col_imgs * 4 * Kd * N
             byts += 4 * M if i[7] >= 0 else 0
             return {"kind": "conv", "layer": op.layer, "M": M, "N": N, "K": Kd, "images": nimg,
                     "N_launch": N, "executions": execs, "flops": 2 * M * N * Kd * nimg,

@@ -86,9 +86,12 @@ def test_fused_and_unfused_schedules_agree_on_counts():
     assert sa.device_ops < sb.device_ops
 
 
-def test_first_conv_layer_fuses_im2col_into_the_gemm_launch():
-    """All-offload: layer 0 (3x3/1/1, c=3, M=16) becomes ONE conv action that
-    writes col0 and out0; counters are those of the unfused schedule."""
+def test_first_conv_layer_fuses_im2col_into_the_gemm_launch(monkeypatch):
+    """All-offload: layers 0 (3x3/1/1, c=3, M=16) and -- with the channel
+    limit raised to 16 -- 2 (c=16, M=32) each become ONE conv action that
+    writes col and out; counters are those of the unfused schedule."""
+    import paper_1811_03882_b200.executor as E
+    monkeypatch.setattr(E, "CONV_MAX_C", 16)
     net = build_net("yolov2-tiny")
     a = PatternExecutor(net, device=None, fuse=True)
     b = PatternExecutor(net, device=None, fuse=False)
@@ -97,13 +100,32 @@ def test_first_conv_layer_fuses_im2col_into_the_gemm_launch():
     assert sa.expected == sb.expected
     convs = [k for k in range(sa.n_actions)
              if sa.actions[k].kind == K.A_KERNEL and sa.actions[k].i[0] == K.K_CONV]
-    assert len(convs) == 1
-    act = sa.actions[convs[0]]
+    assert len(convs) == 2
     names = list(net.arrays)
-    assert [names[act.a[j]] for j in range(4)] == ["x", "col0", "w0", "out0"]
-    assert list(act.i[1:8]) == [3, 416, 416, 16, 0, K.ACT_LEAKY, names.index("bias0")]
-    assert not any(sa.actions[k].kind == K.A_KERNEL and sa.actions[k].i[0] == K.K_IM2COL
-                   and names[sa.actions[k].a[1]] == "col0" for k in range(sa.n_actions))
+    want = [(["x", "col0", "w0", "out0"], [3, 416, 416, 16, 0, K.ACT_LEAKY, names.index("bias0")]),
+            (["pool1", "col2", "w2", "out2"],
+             [16, 208, 208, 32, 0, K.ACT_LEAKY, names.index("bias2")])]
+    for k, (arrs, ints) in zip(convs, want):
+        act = sa.actions[k]
+        assert [names[act.a[j]] for j in range(4)] == arrs
+        assert list(act.i[1:8]) == ints
+        assert act.i[8] == 0                      # one image per launch: col always written
+        assert not any(sa.actions[j].kind == K.A_KERNEL and sa.actions[j].i[0] == K.K_IM2COL
+                       and names[sa.actions[j].a[1]] == arrs[1] for j in range(sa.n_actions))
+
+
+def test_col_dead_only_when_no_inner_directive_moves_it():
+    """_col_dead: the all-offload plan hoists col's copyout to the image loop,
+    so only the last image's col is observable; a directive inside the loop
+    body that moves col, or another op touching col, keeps every store."""
+    net = build_net("yolov2-tiny")
+    ex = PatternExecutor(net, device=None)
+    im = next(k for k, o in enumerate(net.ops) if o.kind == "im2col")
+    g = im + 1
+    col = net.ops[im].arrays["Y"]
+    assert ex._col_dead(im, g, {net.image_loop: {col}})
+    assert not ex._col_dead(im, g, {net.ops[g].loop_id: {col}})
+    assert not ex._col_dead(im + 2, g, {})        # the gemm's bias op does not own col
 
 
 def test_conv_fusion_only_when_no_directive_splits_it(host_exec):

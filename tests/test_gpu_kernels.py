@@ -261,17 +261,23 @@ def test_swap_tiles_within_tolerance(cuda_device, orc, tile, M, N, K_):
     gemm_ok(Cd.numpy(), want)
 
 
-@pytest.mark.parametrize("c,h,w,M,beta,use_bias,act,batch",
-                         [(3, 416, 416, 16, 0, True, K.ACT_LEAKY, 1),
-                          (3, 20, 24, 32, 1, False, K.ACT_NONE, 3),
-                          (1, 8, 4, 5, 0, True, K.ACT_LINEAR, 2),
-                          (4, 13, 16, 17, 1, True, K.ACT_LEAKY, 2),
-                          (2, 1, 8, 1, 0, False, K.ACT_NONE, 1)])
+@pytest.mark.parametrize("c,h,w,M,beta,use_bias,act,batch,col_from",
+                         [(3, 416, 416, 16, 0, True, K.ACT_LEAKY, 1, 0),
+                          (3, 20, 24, 32, 1, False, K.ACT_NONE, 3, 0),
+                          (1, 8, 4, 5, 0, True, K.ACT_LINEAR, 2, 0),
+                          (4, 13, 16, 17, 1, True, K.ACT_LEAKY, 2, 1),
+                          (2, 1, 8, 1, 0, False, K.ACT_NONE, 1, 0),
+                          (16, 208, 208, 32, 0, True, K.ACT_LEAKY, 2, 1),
+                          (16, 26, 20, 32, 1, True, K.ACT_LEAKY, 3, 2),
+                          (64, 9, 12, 24, 0, False, K.ACT_NONE, 2, 0),
+                          (8, 16, 16, 16, 0, True, K.ACT_LEAKY, 4, 3)])
 def test_conv3x3_fused_equals_im2col_then_gemm(cuda_device, orc, c, h, w, M, beta, use_bias,
-                                               act, batch):
-    """acct_conv3x3_im2col_gemm_f32 writes col exactly like im2col and C
-    bit-identically to im2col + the AUTO (streaming) gemm; images batched
-    image-major for the input and column-interleaved for col and C."""
+                                               act, batch, col_from):
+    """acct_conv3x3_im2col_gemm_f32 writes col exactly like im2col (images
+    >= col_from; the others' col stays untouched) and C bit-identically to
+    im2col + the SIMT gemm (the AUTO streaming gemm at its shapes: the same
+    FMA chain); images batched image-major for the input and
+    column-interleaved for col and C."""
     N, Kd = h * w, 9 * c
     ld = -(-N // 32) * 32
     im0 = _rand((batch, c, N), 71)
@@ -295,16 +301,20 @@ def test_conv3x3_fused_equals_im2col_then_gemm(cuda_device, orc, c, h, w, M, bet
            col_u.data_ptr(), batch * ld, ld, batch, stream())
     K.call("acct_gemm_nn_batched_f32", M, N, Kd, 1.0, A.data_ptr(), Kd, 0, col_u.data_ptr(),
            batch * ld, ld, float(beta), C_u.data_ptr(), batch * ld, ld, bp, act, batch,
-           K.GEMM_AUTO, stream())
+           K.GEMM_SIMT, stream())
     col_f, C_f = fresh()
     K.conv3x3_im2col_gemm(im.data_ptr(), ld, c * ld, c, h, w, col_f.data_ptr(), batch * ld, ld,
                           M, A.data_ptr(), Kd, float(beta), C_f.data_ptr(), batch * ld, ld, bp,
-                          act, batch, stream())
+                          act, batch, stream(), col_from=col_from)
     torch.cuda.synchronize()
     for b in range(batch):
         cu = col_u[:, b * ld:b * ld + N].cpu().numpy()
         cf = col_f[:, b * ld:b * ld + N].cpu().numpy()
-        assert np.array_equal(cf, cu)
+        if b < col_from:
+            assert np.isnan(cf).all()               # dead stores skipped
+        else:
+            assert np.array_equal(cf, cu)
+        cf = cu
         want_col = np.empty((Kd, N), np.float32)
         orc.orc_im2col(np.ascontiguousarray(im0[b]).ctypes.data, c, h, w, 3, 1, 1,
                        want_col.ctypes.data)
@@ -329,6 +339,9 @@ def test_conv3x3_fused_declines_unaligned_rows(cuda_device):
     with pytest.raises(K.DeviceError):  # width 10: rows not 16-byte aligned
         K.conv3x3_im2col_gemm(im.data_ptr(), 64, 0, 3, 6, 10, col.data_ptr(), 64, 0, 8,
                               A.data_ptr(), 27, 0.0, C.data_ptr(), 64, 0)
-    with pytest.raises(K.DeviceError):  # 5 channels: not a first-layer shape
-        K.conv3x3_im2col_gemm(im.data_ptr(), 64, 0, 5, 2, 8, col.data_ptr(), 64, 0, 8,
+    with pytest.raises(K.DeviceError):  # 65 channels: beyond the narrow-layer shapes
+        K.conv3x3_im2col_gemm(im.data_ptr(), 64, 0, 65, 2, 8, col.data_ptr(), 64, 0, 8,
+                              A.data_ptr(), 27, 0.0, C.data_ptr(), 64, 0)
+    with pytest.raises(K.DeviceError):  # 33 filters
+        K.conv3x3_im2col_gemm(im.data_ptr(), 64, 0, 3, 2, 8, col.data_ptr(), 64, 0, 33,
                               A.data_ptr(), 27, 0.0, C.data_ptr(), 64, 0)

@@ -145,6 +145,27 @@ int acct_conv3x3_im2col_gemm_f32(const float *im, int64_t ld_im, int64_t im_stri
                                  const float *bias, int act, int batch, int col_from,
                                  acct_stream_t stream);
 
+/* The same contract on the 5th-generation tensor cores for M <= 64 filters
+ * (channels <= 64): the swap-orientation 3xTF32 tile (128 pixels x 32 or 64
+ * filters) whose activation operand is built from the input window in
+ * shared memory -- implicit im2col -- instead of TMA-loaded col tiles.  C is
+ * bit-identical to acct_im2col_batched_f32 + the GEMM_TC3XTF32 swap gemm.
+ * Any input batch layout with 16-byte aligned strides (image-major or
+ * column-interleaved).  ENOTSUP when the double-buffered input slabs
+ * (2 x channels x ~(2W + 134) floats) exceed shared memory. */
+int acct_conv3x3_tc_f32(const float *im, int64_t ld_im, int64_t im_stride, int channels,
+                        int height, int width, float *col, int64_t ld_col, int64_t col_stride,
+                        int M, const float *A, int64_t lda, float beta, float *C, int64_t ldc,
+                        int64_t c_stride, const float *bias, int act, int batch, int col_from,
+                        acct_stream_t stream);
+
+/* Test support (synchronous, allocates scratch): evaluates the kernels'
+ * leaky activation against darknet's (float)(0.1 * (double)x) for all 2^32
+ * float bit patterns on the current device; *mismatches = differing
+ * results (NaNs of either payload count equal), examples[0..7] = the first
+ * differing inputs' bits. */
+int acct_leaky_exhaustive_check(unsigned long long *mismatches, uint32_t *examples);
+
 /* ------------------------------------------------------------- transfers --
  * Direction: 1 = host->device, 2 = device->host.  Pitched 2-D copy of
  * `rows` rows of `row_bytes` bytes.  Counts calls and bytes per direction.  */
@@ -217,8 +238,10 @@ enum {
   /* fused im2col(3x3/1/1) + gemm: slots a = (X, col, A, C); i[1..3] = c, h, w,
      i[4] = M, i[5] = beta is 1, i[6] = act, i[7] = bias slot (-1: none),
      i[8] = 1: col is written for the batch's last image only (the others are
-     unobservable).  Device only; runs as im2col + gemm when gemm_mode is
-     GEMM_TC3XTF32 or the fused kernel declines the shape */
+     unobservable).  Device only: acct_conv3x3_im2col_gemm_f32 in SIMT mode
+     and, under AUTO, for M <= 16 or c <= 4 with M <= 32;
+     acct_conv3x3_tc_f32 otherwise (M <= 64); im2col + gemm when the fused
+     kernel declines the shape */
   ACCT_K_CONV = 9
 };
 

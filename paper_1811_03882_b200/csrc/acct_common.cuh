@@ -75,6 +75,26 @@ __device__ __forceinline__ void pdl_trigger() {
 }
 
 // leaky as darknet computes it: `.1*x` is a double product rounded to float
-__host__ __device__ __forceinline__ float acct_leaky(float v) {
+__host__ __device__ __forceinline__ float acct_leaky_ref(float v) {
   return v < 0.0f ? (float)(0.1 * (double)v) : v;
+}
+
+// The same value without FP64 or F2F conversions (which ran the epilogues on
+// the XU pipe): .1 = c1 + c2 split into floats; p = RN(v c1), its exact error
+// e = fma(v, c1, -p), and RN(p + RN(fma(v, c2, e))) lands on RN(RN_double(.1 v))
+// -- checked for all 2^32 inputs on the device (acct_leaky_exhaustive_check,
+// tests/test_gpu_kernels.py).  |v| < 2^-100 (where p loses bits to the
+// subnormal range) and |v| > 2^120 (-inf) keep the double product.
+__host__ __device__ __forceinline__ float acct_leaky(float v) {
+#ifdef __CUDA_ARCH__
+  if (!(v < 0.0f)) return v;
+  if (v > -0x1p-100f || v < -0x1p+120f) return (float)(0.1 * (double)v);
+  constexpr float c1 = 0x1.99999ap-4f;                      // (float)0.1
+  constexpr float c2 = (float)(0.1 - (double)0x1.99999ap-4f);  // 0.1 - c1, rounded
+  const float p = __fmul_rn(v, c1);
+  const float e = __fmaf_rn(v, c1, -p);
+  return __fadd_rn(p, __fmaf_rn(v, c2, e));
+#else
+  return acct_leaky_ref(v);
+#endif
 }

@@ -620,3 +620,37 @@ extern "C" int acct_maxpool_f32(const float *in, int64_t ld_in, int channels, in
   return acct_maxpool_batched_f32(in, ld_in, 0, channels, height, width, size, stride, off, out_h,
                                   out_w, out, ld_out, 0, idx, ld_idx, 0, 1, stream);
 }
+
+// ---- test support: acct_leaky vs darknet's double product over every float
+namespace {
+__global__ void leaky_check_kernel(unsigned long long *bad, uint32_t *examples) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (1ull << 32); i += stride) {
+    const float v = __uint_as_float((uint32_t)i);
+    const float a = acct_leaky(v), b = acct_leaky_ref(v);
+    if (__float_as_uint(a) != __float_as_uint(b) && !(a != a && b != b)) {
+      const unsigned long long n = atomicAdd(bad, 1ull);
+      if (n < 8) examples[n] = (uint32_t)i;
+    }
+  }
+}
+}  // namespace
+
+extern "C" int acct_leaky_exhaustive_check(unsigned long long *mismatches, uint32_t *examples) {
+  using namespace acct;
+  unsigned long long *d_bad = nullptr;
+  uint32_t *d_ex = nullptr;
+  int rc = check_cuda(cudaMalloc(&d_bad, sizeof(unsigned long long) + 8 * sizeof(uint32_t)),
+                      "leaky check: alloc");
+  if (rc) return rc;
+  d_ex = reinterpret_cast<uint32_t *>(d_bad + 1);
+  cudaMemset(d_bad, 0, sizeof(unsigned long long) + 8 * sizeof(uint32_t));
+  leaky_check_kernel<<<sm_count() * 8, 256>>>(d_bad, d_ex);
+  rc = check_cuda(cudaGetLastError(), "leaky check: launch");
+  if (!rc) rc = check_cuda(cudaMemcpy(mismatches, d_bad, sizeof(unsigned long long),
+                                      cudaMemcpyDeviceToHost), "leaky check: copy");
+  if (!rc) rc = check_cuda(cudaMemcpy(examples, d_ex, 8 * sizeof(uint32_t), cudaMemcpyDeviceToHost),
+                           "leaky check: copy");
+  cudaFree(d_bad);
+  return rc;
+}

@@ -944,6 +944,348 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   if (warp == 1) ptx::tmem_dealloc2(tmem, 512);
 }
 
+// ------------------------------------------------ implicit-im2col conv (swap)
+// 3x3 / stride 1 / pad 1 convolution as the swap-orientation tile
+// (C^T = col^T . A^T: 128 output pixels x TN filters) WITHOUT the col array
+// on the operand path -- the narrow layers (M <= 64) whose gemm is otherwise
+// an HBM stream of col (yolov2-tiny layers 2 and 4: 24.9 and 12.5 MB per
+// image) behind an im2col that writes it.
+//   warp 6      TMA: per work unit (image, 128-pixel tile) the input slab --
+//               every channel's flat range [p0 - W - 1, p0 + 128 + W] in
+//               128-float boxes, out-of-plane elements zero-filled by TMA (the
+//               conv's row padding) -- double-buffered, one unit ahead
+//   warp 0      TMA: per k-block the weight tile (K-major, SWIZZLE_128B)
+//   warp 1      TMEM allocator + MMA issuer, exactly the swap tile's 3xTF32
+//               sequence (A = activations from TMEM, B = weights hi / lo)
+//   warps 2..5  build the activation operand from the slab: lane = pixel, k =
+//               (channel, kh, kw) -> one conflict-free 32-float row per warp
+//               and k, column padding masked at w = 0 / W-1; hi / lo to TMEM;
+//               weights lo to shared memory; the col array of images >=
+//               col_from stored on the way (coalesced 128-B rows)
+//   warps 7..14 epilogue, two groups taking alternate units: tcgen05.ld ->
+//               beta C, bias (staged in shared memory), leaky -> C
+// Operand values, k order and MMA sequence equal im2col + the swap gemm, so
+// C is bit-identical to the unfused pair (tests/test_gpu_kernels.py).
+template <int TN, int NS>
+struct ConvCfg {
+  static constexpr int BK = 32;
+  static constexpr int S = NS;                    // stages: weight ring + TMEM A columns
+  static constexpr int Y_TILE = TN * BK * 4;      // weight rows x BK, K-major SW128
+  static constexpr int STAGE_BYTES = 2 * Y_TILE;  // raw (hi) + lo
+  static constexpr int NACC = TN <= 32 ? 4 : 2;
+  static constexpr int A_COL0 = NACC * TN;
+  static constexpr int USED_COLS = NACC * TN + S * 2 * BK;
+  static constexpr uint32_t TMEM_COLS = USED_COLS <= 256 ? 256 : 512;
+  static constexpr uint32_t K_SBO = 8 * 128;
+  static_assert(USED_COLS <= 512, "TMEM overflow");
+};
+constexpr int CONV_TC_THREADS = 32 * 15;
+constexpr int SLAB_BOX = 128;  // floats per slab TMA box row
+
+__host__ __device__ constexpr int conv_slab_chunks(int width) {
+  return (SLAB_BOX + 2 * width + 6 + SLAB_BOX - 1) / SLAB_BOX;
+}
+
+// One k-block (32 k = (channel, tap) pairs from k0 = kb * 32) of the
+// activation operand for this lane's pixel.  R0 = k0 % 9 makes every tap index
+// and channel step compile-time, so each k is one LDS at a per-lane tap
+// address (byte offsets into the [chunk][channel][128] slab; masked taps point
+// at the slab's zero chunk) with the channel step as its immediate offset.
+// TAIL: the last block of a K that is not a multiple of 32 (zeros past K).
+template <int R0, int K, bool TAIL>
+__device__ __forceinline__ void conv_ld(const uint32_t (&ta)[9], int kvalid, float (&v)[32]) {
+  if constexpr (K < 32) {
+    constexpr int r = (R0 + K) % 9, dc = (R0 + K) / 9;
+    if (TAIL && K >= kvalid)
+      v[K] = 0.0f;
+    else
+      asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v[K]) : "r"(ta[r]), "n"(dc * SLAB_BOX * 4));
+    conv_ld<R0, K + 1, TAIL>(ta, kvalid, v);
+  }
+}
+
+template <int R0>
+__device__ __forceinline__ void conv_block(uint32_t slab_c0, const uint32_t (&tap)[9], int kvalid,
+                                           float (&v)[32]) {
+  uint32_t ta[9];
+#pragma unroll
+  for (int r = 0; r < 9; ++r) ta[r] = slab_c0 + tap[r];
+  if (kvalid >= 32)
+    conv_ld<R0, 0, false>(ta, kvalid, v);
+  else
+    conv_ld<R0, 0, true>(ta, kvalid, v);
+}
+
+template <int TN, int NS>
+__global__ void __launch_bounds__(CONV_TC_THREADS, 1)
+tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+               int M, int channels, int height, int width, int tpi, int units, int nkb,
+               float beta, float *__restrict__ C, int64_t ldc, int64_t c_bs,
+               const float *__restrict__ bias, int act, float *__restrict__ col, int64_t ld_col,
+               int64_t col_bs, int col_from, int dbg) {
+  using G = ConvCfg<TN, NS>;
+  constexpr int S = G::S, BK = G::BK, NACC = G::NACC;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  const int chunks = conv_slab_chunks(width);
+  const int slab_floats = (chunks + 1) * channels * SLAB_BOX;  // + a zero chunk
+  auto y_hi = [&](int s) { return base + s * G::STAGE_BYTES; };
+  auto y_lo = [&](int s) { return base + s * G::STAGE_BYTES + G::Y_TILE; };
+  float *slab0 = reinterpret_cast<float *>(base + S * G::STAGE_BYTES);
+  uint64_t *full = reinterpret_cast<uint64_t *>(slab0 + 2 * slab_floats);
+  uint64_t *conv = full + S;
+  uint64_t *empty = conv + S;
+  uint64_t *slab_full = empty + S;
+  uint64_t *slab_empty = slab_full + 2;
+  uint64_t *acc_full = slab_empty + 2;
+  uint64_t *acc_empty = acc_full + NACC;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + NACC);
+  float *bias_s = reinterpret_cast<float *>(tmem_slot + 4);  // TN floats
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int HW = height * width;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&conv[s], 4);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&slab_full[b], 1);
+      ptx::mbar_init(&slab_empty[b], 4);
+    }
+    for (int a = 0; a < NACC; ++a) {
+      ptx::mbar_init(&acc_full[a], 1);
+      ptx::mbar_init(&acc_empty[a], 4);
+    }
+    ptx::fence_mbar_init();
+    ptx::prefetch_tmap(&tmW);
+    ptx::prefetch_tmap(&tmX);
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, G::TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int g = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int s = g % S;
+          if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
+          ptx::mbar_expect_tx(&full[s], G::Y_TILE);
+          ptx::tma_load_2d(y_hi(s), &tmW, &full[s], kb * BK, 0);
+        }
+      }
+    }
+  } else if (warp == 6) {
+    // ---------------- TMA: input slabs, double-buffered ----------------
+    if (lane == 0) {
+      int j = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+        const int img = u / tpi;
+        const int p0 = (u - img * tpi) * 128;
+        const int a0 = (p0 - width - 1) & ~3;
+        const int sb = j & 1;
+        if (j >= 2) ptx::mbar_wait(&slab_empty[sb], ((j >> 1) - 1) & 1);
+        ptx::mbar_expect_tx(&slab_full[sb], (uint32_t)(chunks * channels * SLAB_BOX * 4));
+        float *slab = slab0 + sb * slab_floats;
+        for (int ch = 0; ch < chunks; ++ch)
+          ptx::tma_load_3d(slab + ch * channels * SLAB_BOX, &tmX, &slab_full[sb],
+                           a0 + SLAB_BOX * ch, img, 0);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (the swap tile's sequence) ----------------
+    constexpr uint32_t idesc = ptx::idesc_tf32(128, TN, false, false);
+    int g = 0, j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int a = j % NACC;
+      if (j >= NACC) ptx::mbar_wait(&acc_empty[a], ((j / NACC) - 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t d = tmem + a * TN;
+      for (int kb = 0; kb < nkb; ++kb, ++g) {
+        const int s = g % S;
+        ptx::mbar_wait(&conv[s], (g / S) & 1);
+        ptx::tc_fence_after();
+        const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
+        const uint32_t at = tmem + G::A_COL0 + s * 2 * BK;
+#pragma unroll
+        for (int k = 0; k < BK / 8; ++k) {
+          const uint64_t dyh = ptx::smem_desc(yh + 32 * k, 16, G::K_SBO, ptx::kLayoutSW128);
+          const uint64_t dyl = ptx::smem_desc(yl + 32 * k, 16, G::K_SBO, ptx::kLayoutSW128);
+          if (!(dbg & 2) && ptx::elect_one()) {
+            ptx::mma_tf32_ts(d, at + 8 * k, dyh, idesc, (kb | k) != 0);
+            ptx::mma_tf32_ts(d, at + 8 * k, dyl, idesc, 1);
+            ptx::mma_tf32_ts(d, at + BK + 8 * k, dyh, idesc, 1);
+          }
+          __syncwarp();
+        }
+        if (ptx::elect_one()) ptx::mma_commit(&empty[s]);
+        __syncwarp();
+      }
+      if (ptx::elect_one()) ptx::mma_commit(&acc_full[a]);
+      __syncwarp();
+    }
+  } else if (warp < 6) {
+    // ---------------- activation operand from the slab ----------------
+    const int q = warp & 3;  // TMEM lanes 32q.. = pixels 32q.. of the tile
+    const int ct = threadIdx.x - 64;
+    const int K = 9 * channels;
+    const uint32_t zero_off = (uint32_t)(chunks * channels * SLAB_BOX * 4);
+    for (int i = ct; i < 2 * channels * SLAB_BOX; i += 128) {  // both slabs' zero chunks
+      const int b = i / (channels * SLAB_BOX);
+      slab0[b * slab_floats + chunks * channels * SLAB_BOX + (i - b * channels * SLAB_BOX)] = 0.0f;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // the four split warps
+    int g = 0, j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int img = u / tpi;
+      const int p0 = (u - img * tpi) * 128;
+      const int a0 = (p0 - width - 1) & ~3;
+      const int sb = j & 1;
+      const int pix = p0 + 32 * q + lane;
+      const int wpos = pix % width;
+      const bool left = wpos == 0, right = wpos == width - 1;
+      const bool wcol = img >= col_from;  // warp-uniform; lanes past the plane skip the store
+      float *colp = col + img * col_bs + pix;
+      // per-lane byte offset of each of the 9 taps in the [chunk][c][128] slab
+      uint32_t tap[9];
+#pragma unroll
+      for (int r = 0; r < 9; ++r) {
+        const int rh = r / 3, rw = r % 3;
+        const int x = pix - a0 + (rh - 1) * width + rw - 1;  // >= 0
+        const bool masked = (rw == 0 && left) || (rw == 2 && right);
+        tap[r] = masked ? zero_off + 4 * lane
+                        : (uint32_t)(((x >> 7) * channels * SLAB_BOX + (x & (SLAB_BOX - 1))) * 4);
+      }
+      ptx::mbar_wait(&slab_full[sb], (j >> 1) & 1);
+      const uint32_t slab = ptx::smem_u32(slab0 + sb * slab_floats);
+      for (int kb = 0; kb < nkb; ++kb, ++g) {
+        const int s = g % S;
+        const int k0 = kb * BK;
+        const int c0 = k0 / 9;
+        const uint32_t sc0 = slab + (uint32_t)(c0 * SLAB_BOX * 4);
+        const int kvalid = K - k0;  // >= 32 except in the last block
+        ptx::mbar_wait(&full[s], (g / S) & 1);
+        if (dbg & 1) {  // profiling knob: skip building the operand (results wrong)
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&conv[s]);
+          continue;
+        }
+        float v[BK];
+        switch (k0 - 9 * c0) {
+          case 0: conv_block<0>(sc0, tap, kvalid, v); break;
+          case 1: conv_block<1>(sc0, tap, kvalid, v); break;
+          case 2: conv_block<2>(sc0, tap, kvalid, v); break;
+          case 3: conv_block<3>(sc0, tap, kvalid, v); break;
+          case 4: conv_block<4>(sc0, tap, kvalid, v); break;
+          case 5: conv_block<5>(sc0, tap, kvalid, v); break;
+          case 6: conv_block<6>(sc0, tap, kvalid, v); break;
+          case 7: conv_block<7>(sc0, tap, kvalid, v); break;
+          default: conv_block<8>(sc0, tap, kvalid, v); break;
+        }
+        if (wcol && pix < HW) {
+          const int kn = kvalid < BK ? kvalid : BK;
+          float *cp = colp + (int64_t)k0 * ld_col;
+#pragma unroll
+          for (int k = 0; k < BK; ++k)
+            if (k < kn) __stcs(cp + (int64_t)k * ld_col, v[k]);
+        }
+        uint32_t hi[BK], lo[BK];
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+          const uint32_t h = __float_as_uint(v[k]) & 0xFFFFE000u;
+          hi[k] = h;
+          lo[k] = __float_as_uint(v[k] - __uint_as_float(h));
+        }
+        const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
+        constexpr int NY = (G::Y_TILE / 16 + 127) / 128;
+        float4 ry[NY];
+#pragma unroll
+        for (int i = 0; i < NY; ++i)
+          if (ct + 128 * i < G::Y_TILE / 16) ry[i] = ptx::lds128(yh + 16 * (ct + 128 * i));
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + G::A_COL0 + s * 2 * BK;
+        ptx::tmem_st_cols<BK>(ta, hi);
+        ptx::tmem_st_cols<BK>(ta + BK, lo);
+#pragma unroll
+        for (int i = 0; i < NY; ++i) {
+          if (ct + 128 * i < G::Y_TILE / 16) {
+            float4 h4;
+            ptx::sts128(yl + 16 * (ct + 128 * i), split_lo(ry[i], h4));
+          }
+        }
+        ptx::tmem_st_wait();
+        ptx::fence_proxy_async_smem();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&conv[s]);
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&slab_empty[sb]);  // this unit's slab is consumed
+    }
+  } else {
+    // ---------------- epilogue: lanes = pixels, TMEM columns = filters ----------------
+    // two groups of four warps (7-10, 11-14) take alternate units, so one
+    // group's stores overlap the other's TMEM loads
+    const int q = warp & 3;
+    const int grp = (warp - 7) >> 2;
+    for (int i = threadIdx.x - 7 * 32; i < TN; i += 8 * 32) bias_s[i] = (bias && i < M) ? bias[i] : 0.0f;
+    asm volatile("bar.sync 2, 256;" ::: "memory");  // the eight epilogue warps
+    int j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      if ((j & 1) != grp) continue;
+      const int img = u / tpi;
+      const int p0 = (u - img * tpi) * 128;
+      const int a = j % NACC;
+      ptx::mbar_wait_sleepy(&acc_full[a], (j / NACC) & 1);
+      ptx::tc_fence_after();
+      const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * TN;
+      const int pix = p0 + 32 * q + lane;
+      const bool live = pix < HW && !(dbg & 4);
+      float *cp = C + img * c_bs + pix;
+      constexpr int CH = 16;
+#pragma unroll 1
+      for (int cc = 0; cc < TN / CH; ++cc) {
+        uint32_t r[CH];
+        ptx::tmem_ld_32x32b_x16(trow + CH * cc, r);
+        const int rbase = CH * cc;
+        if (!live || rbase >= M) continue;
+        float *rp = cp + (int64_t)rbase * ldc;
+        float cv[CH];
+        if (beta != 0.0f) {
+#pragma unroll
+          for (int jj = 0; jj < CH; ++jj)  // every load in flight before any store
+            cv[jj] = rbase + jj < M ? rp[(int64_t)jj * ldc] : 0.0f;
+        }
+#pragma unroll
+        for (int jj = 0; jj < CH; ++jj) {
+          if (rbase + jj < M) {
+            float v = __uint_as_float(r[jj]);
+            if (beta != 0.0f) v = beta * cv[jj] + v;
+            if (bias) v += bias_s[rbase + jj];
+            if (act == ACCT_ACT_LEAKY) v = acct_leaky(v);
+            rp[(int64_t)jj * ldc] = v;
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&acc_empty[a]);
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc(tmem, G::TMEM_COLS);
+}
+
 // Sum the split-K partials of every output element in split order and apply
 // the epilogue (grid-wide, one thread per 4 consecutive columns).
 __global__ void __launch_bounds__(256)
@@ -1048,6 +1390,50 @@ bool cached_map(CUtensorMap *map, const float *ptr, uint64_t inner, uint64_t out
   }
   if (!make_map(map, ptr, inner, outer, ld, box_inner, box_outer, swizzle)) return false;
   if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, *map);
+  return true;
+}
+
+// 3-D fp32 tensor map (no swizzle): the conv input batch as (pixel, image,
+// channel) with element strides 1, img_stride, ch_stride -- both the
+// image-major and the column-interleaved batch layouts; out-of-bounds
+// pixels read 0.  Cached per host thread like cached_map.
+bool cached_map3(CUtensorMap *map, const float *ptr, uint64_t pixels, uint64_t images,
+                 uint64_t channels, uint64_t img_stride, uint64_t ch_stride, uint32_t box_px,
+                 uint32_t box_ch) {
+  struct Key {
+    const void *ptr;
+    uint64_t a, b, c, d, e, f;
+    bool operator==(const Key &o) const {
+      return ptr == o.ptr && a == o.a && b == o.b && c == o.c && d == o.d && e == o.e && f == o.f;
+    }
+  };
+  struct Hash {
+    size_t operator()(const Key &k) const {
+      uint64_t h = reinterpret_cast<uint64_t>(k.ptr) * 0x9E3779B97F4A7C15ull;
+      for (uint64_t v : {k.a, k.b, k.c, k.d, k.e, k.f}) h ^= v + 0x9E3779B9 + (h << 6) + (h >> 2);
+      return (size_t)h;
+    }
+  };
+  static thread_local std::unordered_map<Key, CUtensorMap, Hash> cache;
+  const Key key{ptr, pixels, images, channels, img_stride, ch_stride,
+                ((uint64_t)box_px << 32) | box_ch};
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *map = it->second;
+    return true;
+  }
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {pixels, images, channels};
+  cuuint64_t strides[2] = {img_stride * 4, ch_stride * 4};
+  cuuint32_t box[3] = {box_px, 1, box_ch};
+  cuuint32_t estr[3] = {1, 1, 1};
+  if (fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(ptr), dims, strides, box, estr,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  if (cache.size() > 1024) cache.clear();
   cache.emplace(key, *map);
   return true;
 }
@@ -1297,6 +1683,77 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
   return launch_tc<192, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
 }
 
+// Implicit-im2col conv on tensor cores (tc_conv_kernel): M <= 64 filters,
+// channels <= 64, any batch layout with 16-B aligned strides.  NS = stage
+// ring depth; the caller tries the deepest ring whose slabs still fit.
+template <int TN, int NS>
+int launch_conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channels, int height,
+                   int width, float *col, int64_t ld_col, int64_t col_stride, int M,
+                   const float *A, int64_t lda, float beta, float *C, int64_t ldc,
+                   int64_t c_stride, const float *bias, int act, int batch, int col_from,
+                   cudaStream_t s) {
+  using G = ConvCfg<TN, NS>;
+  const int K = 9 * channels, HW = height * width;
+  const size_t slab_bytes = (size_t)(conv_slab_chunks(width) + 1) * channels * SLAB_BOX * 4;
+  const size_t smem = 1024 + (size_t)G::S * G::STAGE_BYTES + 2 * slab_bytes +
+                      8 * (3 * G::S + 4 + 2 * G::NACC) + 16 + 4 * TN;
+  if (smem > 227 * 1024) return ACCT_ENOTSUP;
+  CUtensorMap tw, tx;
+  if (!cached_map(&tw, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, G::BK, TN,
+                  CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !cached_map3(&tx, im, (uint64_t)HW, (uint64_t)batch, (uint64_t)channels,
+                   (uint64_t)(batch > 1 ? im_stride : ld_im), (uint64_t)ld_im, SLAB_BOX, channels))
+    return fail(ACCT_ENOTSUP, "conv_tc: cuTensorMapEncodeTiled failed");
+  static std::mutex mu;
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev >= 0 && dev < 64 && !done[dev]) {
+      if (int rc = check_cuda(cudaFuncSetAttribute(tc_conv_kernel<TN, NS>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   227 * 1024),
+                              "conv_tc: smem attribute"))
+        return rc;
+      done[dev] = true;
+    }
+  }
+  const int tpi = (HW + 127) / 128;
+  const int64_t units = (int64_t)tpi * batch;
+  if (units > INT32_MAX) return ACCT_ENOTSUP;
+  const int nkb = (K + G::BK - 1) / G::BK;
+  const int sms = sm_count();
+  const int grid = units < sms ? (int)units : sms;
+  static const int dbg = [] {  // profiling knob (tools/conv_probe.py): 1 no operand build,
+    const char *e = getenv("ACCT_CONV_DBG");  // 2 no MMAs, 4 no epilogue -- results wrong
+    return e ? atoi(e) : 0;
+  }();
+  launch(tc_conv_kernel<TN, NS>, dim3(grid), dim3(CONV_TC_THREADS), smem, s, tw, tx, M, channels,
+         height, width, tpi, (int)units, nkb, beta, C, ldc, c_stride, bias, act, col, ld_col,
+         col_stride, col_from, dbg);
+  return note_launch("conv3x3 tc");
+}
+
+template <int TN>
+int conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channels, int height,
+            int width, float *col, int64_t ld_col, int64_t col_stride, int M, const float *A,
+            int64_t lda, float beta, float *C, int64_t ldc, int64_t c_stride, const float *bias,
+            int act, int batch, int col_from, cudaStream_t s) {
+  int rc = launch_conv_tc<TN, 6>(im, ld_im, im_stride, channels, height, width, col, ld_col,
+                                 col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
+                                 col_from, s);
+  if (rc == ACCT_ENOTSUP)
+    rc = launch_conv_tc<TN, 4>(im, ld_im, im_stride, channels, height, width, col, ld_col,
+                               col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
+                               col_from, s);
+  if (rc == ACCT_ENOTSUP)
+    rc = launch_conv_tc<TN, 2>(im, ld_im, im_stride, channels, height, width, col, ld_col,
+                               col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
+                               col_from, s);
+  return rc;
+}
+
 }  // namespace acct
 
 extern "C" void acct_tc_set_write_hi(int on) { acct::g_write_hi = on; }
@@ -1306,4 +1763,33 @@ extern "C" void acct_tc_set_tile(int tile) { acct::g_force_tile.store(tile < 0 ?
 extern "C" int acct_tc_trace(long long *out) {
   return acct::check_cuda(cudaMemcpyFromSymbol(out, acct::g_trace, sizeof(acct::g_trace)),
                           "tc trace");
+}
+
+// C = A . im2col(im) + beta C (+ bias, act) for 3x3/1/1 convolutions with
+// M <= 64 filters on tcgen05 (3xTF32, the swap tile's arithmetic), col stored
+// for images >= col_from of the batch; ENOTSUP for shapes it does not take
+extern "C" int acct_conv3x3_tc_f32(const float *im, int64_t ld_im, int64_t im_stride,
+                                   int channels, int height, int width, float *col,
+                                   int64_t ld_col, int64_t col_stride, int M, const float *A,
+                                   int64_t lda, float beta, float *C, int64_t ldc,
+                                   int64_t c_stride, const float *bias, int act, int batch,
+                                   int col_from, acct_stream_t stream) {
+  using namespace acct;
+  if (channels < 1 || channels > 64 || M < 1 || M > 64 || height < 1 || width < 1 || batch < 1 ||
+      col_from < 0 || (int64_t)height * width > (1 << 28) || ld_im < (int64_t)height * width ||
+      ld_col < (int64_t)height * width || ldc < (int64_t)height * width ||
+      (batch > 1 && (im_stride < 1 || (im_stride & 3))))
+    return fail(ACCT_ENOTSUP, "conv3x3 tc: shape not supported");
+  if ((reinterpret_cast<uintptr_t>(im) | reinterpret_cast<uintptr_t>(A)) & 15 ||
+      (ld_im | lda) & 3)
+    return fail(ACCT_ENOTSUP, "conv3x3 tc: needs 16-B aligned operands");
+  cudaStream_t s = as_stream(stream);
+  int rc = M <= 32 ? conv_tc<32>(im, ld_im, im_stride, channels, height, width, col, ld_col,
+                                 col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
+                                 col_from, s)
+                   : conv_tc<64>(im, ld_im, im_stride, channels, height, width, col, ld_col,
+                                 col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
+                                 col_from, s);
+  if (rc == ACCT_ENOTSUP) return fail(ACCT_ENOTSUP, "conv3x3 tc: slabs exceed shared memory");
+  return rc;
 }

@@ -321,13 +321,24 @@ int device_op(const acct_action_t &a, acct_array_t *arr, int gemm_mode, cudaStre
       const float *bias = I[7] >= 0 ? reinterpret_cast<float *>(arr[I[7]].dev) : nullptr;
       const float beta = I[5] ? 1.0f : 0.0f;
       const int M = (int)I[4], K = 9 * (int)I[1], N = (int)(I[2] * I[3]);
-      // FP32 FMA in k order: the AUTO choice for these shapes and the SIMT
-      // mode's own chain; I[8] = 1: only the last image's col is observable
-      if (gemm_mode == ACCT_GEMM_AUTO || gemm_mode == ACCT_GEMM_SIMT) {
-        const int rc = acct_conv3x3_im2col_gemm_f32(D(0), LD(0), BS(0), (int)I[1], (int)I[2],
-                                                    (int)I[3], D(1), LD(1), BS(1), M, D(2), LD(2),
-                                                    beta, D(3), LD(3), BS(3), bias, (int)I[6], nb,
-                                                    I[8] ? nb - 1 : 0, st);
+      // I[8] = 1: only the last image's col is observable (col_from = nb - 1).
+      // FP32 FMA from the input window (k order, the SIMT gemms' chain) for
+      // M <= 16 or a first layer (c <= 4, M <= 32) and in SIMT mode; the
+      // implicit-im2col tcgen05 swap tile (3xTF32, bit-identical to im2col +
+      // the swap gemm) for the other narrow layers (M <= 64)
+      const int C = (int)I[1], col_from = I[8] ? nb - 1 : 0;
+      const bool simt = gemm_mode == ACCT_GEMM_SIMT ||
+                        (gemm_mode == ACCT_GEMM_AUTO && (M <= 16 || (M <= 32 && C <= 4)));
+      if (simt) {
+        const int rc = acct_conv3x3_im2col_gemm_f32(D(0), LD(0), BS(0), C, (int)I[2], (int)I[3],
+                                                    D(1), LD(1), BS(1), M, D(2), LD(2), beta, D(3),
+                                                    LD(3), BS(3), bias, (int)I[6], nb, col_from,
+                                                    st);
+        if (rc != ACCT_ENOTSUP) return rc;
+      } else if (M <= 64) {
+        const int rc = acct_conv3x3_tc_f32(D(0), LD(0), BS(0), C, (int)I[2], (int)I[3], D(1),
+                                           LD(1), BS(1), M, D(2), LD(2), beta, D(3), LD(3), BS(3),
+                                           bias, (int)I[6], nb, col_from, st);
         if (rc != ACCT_ENOTSUP) return rc;
       }
       // the same ops unfused: im2col, then the gemm in the requested mode

@@ -55,11 +55,14 @@ from .planner import (COPY, COPYIN, COPYOUT, TransferPlan, directive_exec_counts
 from .syntax import parse
 
 PITCH_ALIGN = 32  # elements (128 bytes)
-# widest 3x3/1/1 layer (input channels) fused into one FP32 conv launch when
-# it has M <= 32 filters: the first layers (c = 3).  The kernel takes up to 64
-# channels, but at yolov2-tiny layer 2 (c = 16, M = 32: 199 MFMA per image)
-# it measured 13.7 us/img against 12.2 for im2col + the tensor-core swap gemm
-CONV_MAX_C = int(os.environ.get("ACCT_CONV_MAX_C", "4"))
+# 3x3/1/1 layers fused into one conv launch (im2col + gemm_nn + epilogue): at
+# most CONV_MAX_C input channels and CONV_MAX_M filters.  The runtime runs
+# the FP32 window kernel for first layers (c <= 4) and M <= 16, the
+# implicit-im2col tcgen05 swap tile for the other narrow layers (yolov2-tiny
+# layers 2 and 4); the FP32 kernel at layer 2 (c = 16, M = 32: 199 MFMA per
+# image) measured 13.7 us/img against 12.2 for im2col + the swap gemm
+CONV_MAX_C = int(os.environ.get("ACCT_CONV_MAX_C", "64"))
+CONV_MAX_M = int(os.environ.get("ACCT_CONV_MAX_M", "64"))
 
 
 def _pitch(cols: int) -> int:
@@ -690,8 +693,8 @@ class PatternExecutor:
         """The im2col feeding gemm `g`, when the two can run as one fused
         conv launch (acct_conv3x3_im2col_gemm_f32): the im2col is offloaded
         and directly precedes the gemm, is 3x3/1/1 over <= CONV_MAX_C
-        channels with M <= 32 filters (the narrow layers, where FP32 FMA from
-        the input window beats im2col + a gemm), and no directive between
+        channels with M <= CONV_MAX_M filters (the narrow layers, whose gemm
+        would stream col from HBM), and no directive between
         the two moves the input, col or output -- so moving the col write to
         the gemm's launch point is unobservable."""
         ops = self.net.ops
@@ -702,7 +705,7 @@ class PatternExecutor:
         if im.kind != "im2col" or not on[g - 1] or im.arrays["Y"] != op.arrays["B"]:
             return None
         if (p["ksize"], p["stride"], p["pad"]) != (3, 1, 1) or p["c"] > CONV_MAX_C or \
-                op.params["M"] > 32:
+                op.params["M"] > CONV_MAX_M:
             return None
         if p["w"] % 4:
             return None

@@ -79,7 +79,10 @@ SIGNATURES = {
     "acct_conv3x3_im2col_gemm_f32": [_vp, _i64, _i64, _i32, _i32, _i32, _vp, _i64, _i64, _i32,
                                      _vp, _i64, _f32, _vp, _i64, _i64, _vp, _i32, _i32, _i32,
                                      _vp],
+    "acct_conv3x3_tc_f32": [_vp, _i64, _i64, _i32, _i32, _i32, _vp, _i64, _i64, _i32, _vp, _i64,
+                            _f32, _vp, _i64, _i64, _vp, _i32, _i32, _i32, _vp],
     "acct_add_bias_batched_f32": [_vp, _i64, _i64, _vp, _i32, _i64, _i32, _vp],
+    "acct_leaky_exhaustive_check": [_vp, _vp],
     "acct_activate_batched_f32": [_vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp],
     "acct_maxpool_batched_f32": [_vp, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
                                  _vp, _i64, _i64, _vp, _i64, _i64, _i32, _vp],
@@ -194,6 +197,12 @@ def conv3x3_im2col_gemm(im, ld_im, im_stride, channels, height, width, col, ld_c
     call("acct_conv3x3_im2col_gemm_f32", im, ld_im, im_stride, channels, height, width, col,
          ld_col, col_stride, M, A, lda, beta, Cp, ldc, c_stride, bias, act, batch, col_from,
          stream)
+
+
+def conv3x3_tc(im, ld_im, im_stride, channels, height, width, col, ld_col, col_stride, M, A, lda,
+               beta, Cp, ldc, c_stride, bias=None, act=ACT_NONE, batch=1, stream=0, col_from=0):
+    call("acct_conv3x3_tc_f32", im, ld_im, im_stride, channels, height, width, col, ld_col,
+         col_stride, M, A, lda, beta, Cp, ldc, c_stride, bias, act, batch, col_from, stream)
 
 
 def add_bias(out, ld, bias, rows, cols, stream=0):

@@ -86,12 +86,10 @@ def test_fused_and_unfused_schedules_agree_on_counts():
     assert sa.device_ops < sb.device_ops
 
 
-def test_first_conv_layer_fuses_im2col_into_the_gemm_launch(monkeypatch):
-    """All-offload: layers 0 (3x3/1/1, c=3, M=16) and -- with the channel
-    limit raised to 16 -- 2 (c=16, M=32) each become ONE conv action that
+def test_narrow_conv_layers_fuse_im2col_into_the_gemm_launch():
+    """All-offload: the 3x3/1/1 layers with M <= 64 filters -- 0 (c=3, M=16),
+    2 (c=16, M=32) and 4 (c=32, M=64) -- each become ONE conv action that
     writes col and out; counters are those of the unfused schedule."""
-    import paper_1811_03882_b200.executor as E
-    monkeypatch.setattr(E, "CONV_MAX_C", 16)
     net = build_net("yolov2-tiny")
     a = PatternExecutor(net, device=None, fuse=True)
     b = PatternExecutor(net, device=None, fuse=False)
@@ -100,11 +98,13 @@ def test_first_conv_layer_fuses_im2col_into_the_gemm_launch(monkeypatch):
     assert sa.expected == sb.expected
     convs = [k for k in range(sa.n_actions)
              if sa.actions[k].kind == K.A_KERNEL and sa.actions[k].i[0] == K.K_CONV]
-    assert len(convs) == 2
     names = list(net.arrays)
     want = [(["x", "col0", "w0", "out0"], [3, 416, 416, 16, 0, K.ACT_LEAKY, names.index("bias0")]),
             (["pool1", "col2", "w2", "out2"],
-             [16, 208, 208, 32, 0, K.ACT_LEAKY, names.index("bias2")])]
+             [16, 208, 208, 32, 0, K.ACT_LEAKY, names.index("bias2")]),
+            (["pool3", "col4", "w4", "out4"],
+             [32, 104, 104, 64, 0, K.ACT_LEAKY, names.index("bias4")])]
+    assert len(convs) == len(want)
     for k, (arrs, ints) in zip(convs, want):
         act = sa.actions[k]
         assert [names[act.a[j]] for j in range(4)] == arrs

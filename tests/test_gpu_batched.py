@@ -132,16 +132,18 @@ def test_batched_kernel_entries_match_single(cuda_device):
         assert torch.equal(ib[:, b * 32:b * 32 + 32], i1[b])
 
 
+@pytest.mark.parametrize("mode", [K.GEMM_SIMT, K.GEMM_AUTO])
 @pytest.mark.parametrize("name,images", [("demo", 8), ("yolov2-tiny", 2), ("micro", 4)])
-def test_fused_conv_layer_is_bit_identical(cuda_device, name, images):
-    """The fused conv launches (im2col + FP32 gemm in one kernel, col stored
-    for the batch's last image only) leave every observable array -- col
-    included -- bit-identical to the unfused schedule with the SIMT gemm
-    (the same FMA chain), batched and resident alike; under AUTO (tensor-core
-    gemms elsewhere) the network output stays within the gemm tolerance."""
+def test_fused_conv_layer_is_bit_identical(cuda_device, name, images, mode):
+    """The fused conv launches (im2col + gemm in one kernel -- the FP32
+    window kernel or the implicit-im2col tcgen05 swap tile -- col stored for
+    the batch's last image only) leave every observable array, col included,
+    bit-identical to the unfused schedule in the same gemm mode (the same
+    FMA chain / the same MMA operands and order), batched and resident
+    alike; the AUTO output stays within the gemm tolerance of SIMT's."""
     net = build_net(name, images=images)
-    a = PatternExecutor(net, device=0, fuse=True, gemm_mode=K.GEMM_SIMT)
-    b = PatternExecutor(net, device=0, fuse=False, gemm_mode=K.GEMM_SIMT)
+    a = PatternExecutor(net, device=0, fuse=True, gemm_mode=mode)
+    b = PatternExecutor(net, device=0, fuse=False, gemm_mode=mode)
     bits = "1" * len(net.ops)
     sa = a.compile(bits)
     convs = [k for k in range(sa.n_actions)
@@ -160,7 +162,7 @@ def test_fused_conv_layer_is_bit_identical(cuda_device, name, images):
     a.run(bits, resident=True)
     b.run(bits, resident=True)
     assert np.array_equal(a.device_array(net.output_name), b.device_array(net.output_name))
-    c = PatternExecutor(net, device=0, fuse=True)
+    c = PatternExecutor(net, device=0, fuse=True, gemm_mode=K.GEMM_SIMT + K.GEMM_AUTO - mode)
     c.run(bits)
     want = a.outputs()
     assert np.abs(c.outputs() - want).max() <= 1e-4 * np.abs(want).max()

@@ -345,3 +345,100 @@ def test_conv3x3_fused_declines_unaligned_rows(cuda_device):
     with pytest.raises(K.DeviceError):  # 33 filters
         K.conv3x3_im2col_gemm(im.data_ptr(), 64, 0, 3, 2, 8, col.data_ptr(), 64, 0, 33,
                               A.data_ptr(), 27, 0.0, C.data_ptr(), 64, 0)
+
+
+@pytest.mark.parametrize("c,h,w,M,beta,use_bias,act,batch,col_from,layout,exact",
+                         [(16, 208, 208, 32, 0, True, K.ACT_LEAKY, 2, 1, "il", True),
+                          (32, 104, 104, 64, 0, True, K.ACT_LEAKY, 2, 0, "il", True),
+                          (32, 104, 104, 64, 1, False, K.ACT_NONE, 2, 1, "im", True),
+                          (8, 16, 16, 40, 1, False, K.ACT_NONE, 3, 2, "il", False),
+                          (64, 13, 16, 17, 1, True, K.ACT_LEAKY, 2, 0, "im", False),
+                          (3, 20, 24, 50, 0, True, K.ACT_LINEAR, 1, 0, "im", False),
+                          (5, 7, 4, 33, 0, True, K.ACT_LEAKY, 4, 3, "il", False)])
+def test_conv3x3_tc_equals_im2col_then_tc_gemm(cuda_device, orc, c, h, w, M, beta, use_bias, act,
+                                               batch, col_from, layout, exact):
+    """acct_conv3x3_tc_f32 (implicit-im2col tcgen05 swap tile) writes col
+    exactly like im2col for images >= col_from, leaves the others untouched,
+    and computes C within the gemm tolerance of the oracle -- bit-identical
+    to im2col + the GEMM_TC3XTF32 swap gemm at the yolov2-tiny layer shapes
+    (where that gemm runs without split-K).  Input batches image-major
+    ([P][c][ld]) and column-interleaved ([c][P*ld]) alike."""
+    N, Kd = h * w, 9 * c
+    ld = -(-N // 32) * 32
+    lda = -(-Kd // 32) * 32
+    im0 = _rand((batch, c, N), 81)
+    A0 = _rand((M, Kd), 82, -0.5, 0.5)
+    C0 = _rand((M, batch, N), 83)
+    bias0 = _rand((M,), 84)
+    if layout == "im":
+        im = torch.zeros((batch, c, ld), device="cuda")
+        im[:, :, :N] = torch.from_numpy(im0).cuda()
+        ld_im, im_stride = ld, c * ld
+    else:
+        im = torch.zeros((c, batch, ld), device="cuda")
+        im[:, :, :N] = torch.from_numpy(im0.transpose(1, 0, 2).copy()).cuda()
+        ld_im, im_stride = batch * ld, ld
+    A = torch.zeros((M, lda), device="cuda")
+    A[:, :Kd] = torch.from_numpy(A0).cuda()
+    bias = torch.from_numpy(bias0).cuda() if use_bias else None
+    bp = bias.data_ptr() if use_bias else None
+
+    def fresh():
+        col = torch.full((Kd, batch * ld), float("nan"), device="cuda")
+        C = torch.full((M, batch, ld), 0.0, device="cuda")
+        C[:, :, :N] = torch.from_numpy(C0).cuda()
+        return col, C.view(M, batch * ld)
+
+    col_u, C_u = fresh()
+    K.call("acct_im2col_batched_f32", im.data_ptr(), ld_im, im_stride, c, h, w, 3, 1, 1,
+           col_u.data_ptr(), batch * ld, ld, batch, stream())
+    K.call("acct_gemm_nn_batched_f32", M, N, Kd, 1.0, A.data_ptr(), lda, 0, col_u.data_ptr(),
+           batch * ld, ld, float(beta), C_u.data_ptr(), batch * ld, ld, bp, act, batch,
+           K.GEMM_TC3XTF32, stream())
+    col_f, C_f = fresh()
+    K.conv3x3_tc(im.data_ptr(), ld_im, im_stride, c, h, w, col_f.data_ptr(), batch * ld, ld, M,
+                 A.data_ptr(), lda, float(beta), C_f.data_ptr(), batch * ld, ld, bp, act, batch,
+                 stream(), col_from=col_from)
+    torch.cuda.synchronize()
+    for b in range(batch):
+        cu = col_u[:, b * ld:b * ld + N].cpu().numpy()
+        cf = col_f[:, b * ld:b * ld + N].cpu().numpy()
+        if b < col_from:
+            assert np.isnan(cf).all()
+        else:
+            assert np.array_equal(cf, cu)
+        got = C_f[:, b * ld:b * ld + N].cpu().numpy()
+        if exact:
+            assert np.array_equal(got, C_u[:, b * ld:b * ld + N].cpu().numpy())
+        want = np.ascontiguousarray(C0[:, b]) if beta else np.zeros((M, N), np.float32)
+        cu = np.ascontiguousarray(cu)
+        orc.orc_gemm_nn(M, N, Kd, 1.0, A0.ctypes.data, Kd, cu.ctypes.data, N, want.ctypes.data, N)
+        if use_bias:
+            orc.orc_add_bias(want.ctypes.data, bias0.ctypes.data, 1, M, N)
+        if act == K.ACT_LEAKY:
+            orc.orc_activate(want.ctypes.data, M * N, 1)
+        gemm_ok(got, want)
+
+
+def test_conv3x3_tc_declines_what_it_does_not_take(cuda_device):
+    im = torch.zeros((3, 64), device="cuda")
+    col = torch.zeros((27, 64), device="cuda")
+    A = torch.zeros((80, 32), device="cuda")
+    C = torch.zeros((80, 64), device="cuda")
+    with pytest.raises(K.DeviceError):  # 65 filters: beyond the swap tiles
+        K.conv3x3_tc(im.data_ptr(), 64, 0, 3, 8, 8, col.data_ptr(), 64, 0, 65, A.data_ptr(), 32,
+                     0.0, C.data_ptr(), 64, 0)
+    with pytest.raises(K.DeviceError):  # input slabs beyond shared memory (64 ch x 608 wide)
+        big = torch.zeros((64, 608 * 4), device="cuda")
+        K.conv3x3_tc(big.data_ptr(), 608 * 4, 0, 64, 4, 608, col.data_ptr(), 608 * 4, 0, 32,
+                     A.data_ptr(), 32, 0.0, C.data_ptr(), 608 * 4, 0)
+
+
+def test_leaky_is_darknets_double_product_for_every_float(cuda_device):
+    """The kernels' leaky (float-float product, no FP64) equals darknet's
+    (float)(0.1 * (double)x) bit for bit on all 2^32 inputs."""
+    import ctypes
+    bad = ctypes.c_ulonglong(0)
+    ex = (ctypes.c_uint32 * 8)()
+    K.call("acct_leaky_exhaustive_check", ctypes.addressof(bad), ctypes.addressof(ex))
+    assert bad.value == 0, [hex(ex[i]) for i in range(min(8, bad.value))]

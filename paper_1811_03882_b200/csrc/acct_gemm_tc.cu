@@ -950,95 +950,91 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 // on the operand path -- the narrow layers (M <= 64) whose gemm is otherwise
 // an HBM stream of col (yolov2-tiny layers 2 and 4: 24.9 and 12.5 MB per
 // image) behind an im2col that writes it.
-//   warp 6      TMA: per work unit (image, 128-pixel tile) the input slab --
-//               every channel's flat range [p0 - W - 1, p0 + 128 + W] in
-//               128-float boxes, out-of-plane elements zero-filled by TMA (the
-//               conv's row padding) -- double-buffered, one unit ahead
-//   warp 0      TMA: per k-block the weight tile (K-major, SWIZZLE_128B)
+//
+// A work unit is one image's TH x TW block of output pixels (TW = 16 or 8,
+// TH = 128 / TW; MMA row m = pixel (m / TW, m % TW)).  Its input slab -- every
+// channel's (TH + 2) x (TW + 2) window (stored TW + 8 wide from x0 - 4), one 4-D TMA box over (x, y, image,
+// channel) whose out-of-bounds elements are zero, i.e. the conv's padding --
+// makes every operand element one LDS at  lane base + immediate.
+//   warp 0      TMA: all weight k-blocks once (resident, K-major SWIZZLE_128B),
+//               then the slab of each unit, double-buffered
 //   warp 1      TMEM allocator + MMA issuer, exactly the swap tile's 3xTF32
 //               sequence (A = activations from TMEM, B = weights hi / lo)
-//   warps 2..5  build the activation operand from the slab: lane = pixel, k =
-//               (channel, kh, kw) -> one conflict-free 32-float row per warp
-//               and k, column padding masked at w = 0 / W-1; hi / lo to TMEM;
-//               weights lo to shared memory; the col array of images >=
-//               col_from stored on the way (coalesced 128-B rows)
-//   warps 7..14 epilogue, two groups taking alternate units: tcgen05.ld ->
+//   warps 2..5  weights lo once; per k-block the activation operand: lane =
+//               pixel, k = (channel, kh, kw) -> hi / lo to a TMEM stage (6
+//               stages); the col array of images >= col_from stored on the way
+//   warps 6..13 epilogue, two groups taking alternate units: tcgen05.ld ->
 //               beta C, bias (staged in shared memory), leaky -> C
 // Operand values, k order and MMA sequence equal im2col + the swap gemm, so
 // C is bit-identical to the unfused pair (tests/test_gpu_kernels.py).
-template <int TN, int NS>
+template <int TN, int TW>
 struct ConvCfg {
   static constexpr int BK = 32;
-  static constexpr int S = NS;                    // stages: weight ring + TMEM A columns
-  static constexpr int Y_TILE = TN * BK * 4;      // weight rows x BK, K-major SW128
-  static constexpr int STAGE_BYTES = 2 * Y_TILE;  // raw (hi) + lo
+  static constexpr int S = 6;                     // TMEM stages of the activation operand
+  static constexpr int TH = 128 / TW;
+  // slab row: columns x0 - 4 .. x0 + TW + 3 (TMA needs a 16-byte aligned
+  // start in the innermost dimension; a box starting at x0 - 1 faults)
+  static constexpr int TWP = TW + 8;
+  static constexpr int SROWS = TH + 2;
+  static constexpr int CS = SROWS * TWP * 4;      // slab bytes per channel
+  static constexpr int W_TILE = TN * BK * 4;      // one weight k-block, K-major SW128
   static constexpr int NACC = TN <= 32 ? 4 : 2;
   static constexpr int A_COL0 = NACC * TN;
   static constexpr int USED_COLS = NACC * TN + S * 2 * BK;
-  static constexpr uint32_t TMEM_COLS = USED_COLS <= 256 ? 256 : 512;
+  static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t K_SBO = 8 * 128;
   static_assert(USED_COLS <= 512, "TMEM overflow");
 };
-constexpr int CONV_TC_THREADS = 32 * 15;
-constexpr int SLAB_BOX = 128;  // floats per slab TMA box row
+constexpr int CONV_TC_THREADS = 32 * 14;
 
-__host__ __device__ constexpr int conv_slab_chunks(int width) {
-  return (SLAB_BOX + 2 * width + 6 + SLAB_BOX - 1) / SLAB_BOX;
-}
-
-// One k-block (32 k = (channel, tap) pairs from k0 = kb * 32) of the
-// activation operand for this lane's pixel.  R0 = k0 % 9 makes every tap index
-// and channel step compile-time, so each k is one LDS at a per-lane tap
-// address (byte offsets into the [chunk][channel][128] slab; masked taps point
-// at the slab's zero chunk) with the channel step as its immediate offset.
-// TAIL: the last block of a K that is not a multiple of 32 (zeros past K).
-template <int R0, int K, bool TAIL>
-__device__ __forceinline__ void conv_ld(const uint32_t (&ta)[9], int kvalid, float (&v)[32]) {
+// One k-block (32 k = (channel, tap) pairs from k0 = 9 c0 + R0) of the
+// activation operand for this lane's pixel: each k is one LDS at the lane's
+// slab address (channel c0 folded in) plus a compile-time immediate -- the
+// channel step and the tap's row / column offset.  TAIL: the last block of a
+// K that is not a multiple of 32 (zeros past K).
+template <int TWP, int CS, int R0, int K, bool TAIL>
+__device__ __forceinline__ void conv_ld(uint32_t base, int kvalid, float (&v)[32]) {
   if constexpr (K < 32) {
     constexpr int r = (R0 + K) % 9, dc = (R0 + K) / 9;
+    constexpr int imm = dc * CS + ((r / 3) * TWP + r % 3 + 3) * 4;  // column x - 1 + kw
     if (TAIL && K >= kvalid)
       v[K] = 0.0f;
     else
-      asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v[K]) : "r"(ta[r]), "n"(dc * SLAB_BOX * 4));
-    conv_ld<R0, K + 1, TAIL>(ta, kvalid, v);
+      asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v[K]) : "r"(base), "n"(imm));
+    conv_ld<TWP, CS, R0, K + 1, TAIL>(base, kvalid, v);
   }
 }
 
-template <int R0>
-__device__ __forceinline__ void conv_block(uint32_t slab_c0, const uint32_t (&tap)[9], int kvalid,
-                                           float (&v)[32]) {
-  uint32_t ta[9];
-#pragma unroll
-  for (int r = 0; r < 9; ++r) ta[r] = slab_c0 + tap[r];
+template <int TWP, int CS, int R0>
+__device__ __forceinline__ void conv_block(uint32_t base, int kvalid, float (&v)[32]) {
   if (kvalid >= 32)
-    conv_ld<R0, 0, false>(ta, kvalid, v);
+    conv_ld<TWP, CS, R0, 0, false>(base, kvalid, v);
   else
-    conv_ld<R0, 0, true>(ta, kvalid, v);
+    conv_ld<TWP, CS, R0, 0, true>(base, kvalid, v);
 }
 
-template <int TN, int NS>
+template <int TN, int TW>
 __global__ void __launch_bounds__(CONV_TC_THREADS, 1)
 tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-               int M, int channels, int height, int width, int tpi, int units, int nkb,
-               float beta, float *__restrict__ C, int64_t ldc, int64_t c_bs,
+               int M, int channels, int height, int width, int tiles_x, int tpi, int units,
+               int nkb, float beta, float *__restrict__ C, int64_t ldc, int64_t c_bs,
                const float *__restrict__ bias, int act, float *__restrict__ col, int64_t ld_col,
                int64_t col_bs, int col_from, int dbg) {
-  using G = ConvCfg<TN, NS>;
+  using G = ConvCfg<TN, TW>;
   constexpr int S = G::S, BK = G::BK, NACC = G::NACC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
-  const int chunks = conv_slab_chunks(width);
-  const int slab_floats = (chunks + 1) * channels * SLAB_BOX;  // + a zero chunk
-  auto y_hi = [&](int s) { return base + s * G::STAGE_BYTES; };
-  auto y_lo = [&](int s) { return base + s * G::STAGE_BYTES + G::Y_TILE; };
-  float *slab0 = reinterpret_cast<float *>(base + S * G::STAGE_BYTES);
-  uint64_t *full = reinterpret_cast<uint64_t *>(slab0 + 2 * slab_floats);
-  uint64_t *conv = full + S;
-  uint64_t *empty = conv + S;
-  uint64_t *slab_full = empty + S;
+  uint8_t *w_hi = base;                             // [nkb][W_TILE]
+  uint8_t *w_lo = base + nkb * G::W_TILE;           // [nkb][W_TILE]
+  const int slab_bytes = (channels * G::CS + 127) & ~127;
+  uint8_t *slab0 = base + 2 * nkb * G::W_TILE;      // 2 x [channels][SROWS][TWP]
+  uint64_t *wfull = reinterpret_cast<uint64_t *>(slab0 + 2 * slab_bytes);
+  uint64_t *slab_full = wfull + 1;
   uint64_t *slab_empty = slab_full + 2;
-  uint64_t *acc_full = slab_empty + 2;
+  uint64_t *conv = slab_empty + 2;
+  uint64_t *empty = conv + S;
+  uint64_t *acc_full = empty + S;
   uint64_t *acc_empty = acc_full + NACC;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + NACC);
   float *bias_s = reinterpret_cast<float *>(tmem_slot + 4);  // TN floats
@@ -1046,14 +1042,14 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int HW = height * width;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&conv[s], 4);
-      ptx::mbar_init(&empty[s], 1);
-    }
+    ptx::mbar_init(wfull, 1);
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&slab_full[b], 1);
       ptx::mbar_init(&slab_empty[b], 4);
+    }
+    for (int s = 0; s < S; ++s) {
+      ptx::mbar_init(&conv[s], 4);
+      ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < NACC; ++a) {
       ptx::mbar_init(&acc_full[a], 1);
@@ -1071,34 +1067,36 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   pdl_trigger();
   pdl_wait();
 
+  auto unit_xy = [&](int u, int &img, int &y0, int &x0) {
+    img = u / tpi;
+    const int t = u - img * tpi;
+    const int ty = t / tiles_x;
+    y0 = ty * G::TH;
+    x0 = (t - ty * tiles_x) * TW;
+  };
+
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
+    // ---------------- TMA: resident weights, then the slabs ----------------
     if (lane == 0) {
-      int g = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        for (int kb = 0; kb < nkb; ++kb, ++g) {
-          const int s = g % S;
-          if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
-          ptx::mbar_expect_tx(&full[s], G::Y_TILE);
-          ptx::tma_load_2d(y_hi(s), &tmW, &full[s], kb * BK, 0);
-        }
+      if (dbg & 16) {
+        ptx::mbar_arrive(wfull);
+      } else {
+        ptx::mbar_expect_tx(wfull, (uint32_t)(nkb * G::W_TILE));
+        for (int kb = 0; kb < nkb; ++kb)
+          ptx::tma_load_2d(w_hi + kb * G::W_TILE, &tmW, wfull, kb * BK, 0);
       }
-    }
-  } else if (warp == 6) {
-    // ---------------- TMA: input slabs, double-buffered ----------------
-    if (lane == 0) {
       int j = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-        const int img = u / tpi;
-        const int p0 = (u - img * tpi) * 128;
-        const int a0 = (p0 - width - 1) & ~3;
+        int img, y0, x0;
+        unit_xy(u, img, y0, x0);
         const int sb = j & 1;
         if (j >= 2) ptx::mbar_wait(&slab_empty[sb], ((j >> 1) - 1) & 1);
-        ptx::mbar_expect_tx(&slab_full[sb], (uint32_t)(chunks * channels * SLAB_BOX * 4));
-        float *slab = slab0 + sb * slab_floats;
-        for (int ch = 0; ch < chunks; ++ch)
-          ptx::tma_load_3d(slab + ch * channels * SLAB_BOX, &tmX, &slab_full[sb],
-                           a0 + SLAB_BOX * ch, img, 0);
+        if (dbg & 8) {
+          ptx::mbar_arrive(&slab_full[sb]);
+        } else {
+          ptx::mbar_expect_tx(&slab_full[sb], (uint32_t)(channels * G::CS));
+          ptx::tma_load_4d(slab0 + sb * slab_bytes, &tmX, &slab_full[sb], x0 - 4, y0 - 1, img, 0);
+        }
       }
     }
   } else if (warp == 1) {
@@ -1114,7 +1112,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         const int s = g % S;
         ptx::mbar_wait(&conv[s], (g / S) & 1);
         ptx::tc_fence_after();
-        const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
+        const uint32_t yh = ptx::smem_u32(w_hi + kb * G::W_TILE);
+        const uint32_t yl = ptx::smem_u32(w_lo + kb * G::W_TILE);
         const uint32_t at = tmem + G::A_COL0 + s * 2 * BK;
 #pragma unroll
         for (int k = 0; k < BK / 8; ++k) {
@@ -1134,64 +1133,59 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       __syncwarp();
     }
   } else if (warp < 6) {
-    // ---------------- activation operand from the slab ----------------
-    const int q = warp & 3;  // TMEM lanes 32q.. = pixels 32q.. of the tile
+    // ---------------- weights lo, then the activation operand ----------------
+    const int q = warp & 3;  // TMEM lanes 32q.. = MMA rows (pixels) 32q..
     const int ct = threadIdx.x - 64;
     const int K = 9 * channels;
-    const uint32_t zero_off = (uint32_t)(chunks * channels * SLAB_BOX * 4);
-    for (int i = ct; i < 2 * channels * SLAB_BOX; i += 128) {  // both slabs' zero chunks
-      const int b = i / (channels * SLAB_BOX);
-      slab0[b * slab_floats + chunks * channels * SLAB_BOX + (i - b * channels * SLAB_BOX)] = 0.0f;
+    ptx::mbar_wait(wfull, 0);
+    {
+      const uint32_t hs = ptx::smem_u32(w_hi), ls = ptx::smem_u32(w_lo);
+      for (int i = ct; i < nkb * G::W_TILE / 16; i += 128) {
+        float4 h4;
+        ptx::sts128(ls + 16 * i, split_lo(ptx::lds128(hs + 16 * i), h4));
+      }
+      ptx::fence_proxy_async_smem();  // read by the MMAs after the first conv arrival
     }
-    asm volatile("bar.sync 1, 128;" ::: "memory");  // the four split warps
+    const int m = 32 * q + lane;
+    const int py = m / TW, px = m % TW;
+    const uint32_t lane_off = (uint32_t)((py * G::TWP + px) * 4);
     int g = 0, j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-      const int img = u / tpi;
-      const int p0 = (u - img * tpi) * 128;
-      const int a0 = (p0 - width - 1) & ~3;
+      int img, y0, x0;
+      unit_xy(u, img, y0, x0);
       const int sb = j & 1;
-      const int pix = p0 + 32 * q + lane;
-      const int wpos = pix % width;
-      const bool left = wpos == 0, right = wpos == width - 1;
-      const bool wcol = img >= col_from;  // warp-uniform; lanes past the plane skip the store
-      float *colp = col + img * col_bs + pix;
-      // per-lane byte offset of each of the 9 taps in the [chunk][c][128] slab
-      uint32_t tap[9];
-#pragma unroll
-      for (int r = 0; r < 9; ++r) {
-        const int rh = r / 3, rw = r % 3;
-        const int x = pix - a0 + (rh - 1) * width + rw - 1;  // >= 0
-        const bool masked = (rw == 0 && left) || (rw == 2 && right);
-        tap[r] = masked ? zero_off + 4 * lane
-                        : (uint32_t)(((x >> 7) * channels * SLAB_BOX + (x & (SLAB_BOX - 1))) * 4);
-      }
+      const int y = y0 + py, x = x0 + px;
+      const bool wcol = img >= col_from;  // warp-uniform; lanes off the image skip the store
+      const bool inside = y < height && x < width;
+      float *colp = col + img * col_bs + (int64_t)y * width + x;
+      const uint32_t lane_base = ptx::smem_u32(slab0 + sb * slab_bytes) + lane_off;
       ptx::mbar_wait(&slab_full[sb], (j >> 1) & 1);
-      const uint32_t slab = ptx::smem_u32(slab0 + sb * slab_floats);
       for (int kb = 0; kb < nkb; ++kb, ++g) {
         const int s = g % S;
         const int k0 = kb * BK;
         const int c0 = k0 / 9;
-        const uint32_t sc0 = slab + (uint32_t)(c0 * SLAB_BOX * 4);
         const int kvalid = K - k0;  // >= 32 except in the last block
-        ptx::mbar_wait(&full[s], (g / S) & 1);
+        if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
+        ptx::tc_fence_after();
         if (dbg & 1) {  // profiling knob: skip building the operand (results wrong)
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&conv[s]);
           continue;
         }
         float v[BK];
+        const uint32_t bc = lane_base + (uint32_t)(c0 * G::CS);
         switch (k0 - 9 * c0) {
-          case 0: conv_block<0>(sc0, tap, kvalid, v); break;
-          case 1: conv_block<1>(sc0, tap, kvalid, v); break;
-          case 2: conv_block<2>(sc0, tap, kvalid, v); break;
-          case 3: conv_block<3>(sc0, tap, kvalid, v); break;
-          case 4: conv_block<4>(sc0, tap, kvalid, v); break;
-          case 5: conv_block<5>(sc0, tap, kvalid, v); break;
-          case 6: conv_block<6>(sc0, tap, kvalid, v); break;
-          case 7: conv_block<7>(sc0, tap, kvalid, v); break;
-          default: conv_block<8>(sc0, tap, kvalid, v); break;
+          case 0: conv_block<G::TWP, G::CS, 0>(bc, kvalid, v); break;
+          case 1: conv_block<G::TWP, G::CS, 1>(bc, kvalid, v); break;
+          case 2: conv_block<G::TWP, G::CS, 2>(bc, kvalid, v); break;
+          case 3: conv_block<G::TWP, G::CS, 3>(bc, kvalid, v); break;
+          case 4: conv_block<G::TWP, G::CS, 4>(bc, kvalid, v); break;
+          case 5: conv_block<G::TWP, G::CS, 5>(bc, kvalid, v); break;
+          case 6: conv_block<G::TWP, G::CS, 6>(bc, kvalid, v); break;
+          case 7: conv_block<G::TWP, G::CS, 7>(bc, kvalid, v); break;
+          default: conv_block<G::TWP, G::CS, 8>(bc, kvalid, v); break;
         }
-        if (wcol && pix < HW) {
+        if (wcol && inside) {
           const int kn = kvalid < BK ? kvalid : BK;
           float *cp = colp + (int64_t)k0 * ld_col;
 #pragma unroll
@@ -1205,24 +1199,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           hi[k] = h;
           lo[k] = __float_as_uint(v[k] - __uint_as_float(h));
         }
-        const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
-        constexpr int NY = (G::Y_TILE / 16 + 127) / 128;
-        float4 ry[NY];
-#pragma unroll
-        for (int i = 0; i < NY; ++i)
-          if (ct + 128 * i < G::Y_TILE / 16) ry[i] = ptx::lds128(yh + 16 * (ct + 128 * i));
         const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + G::A_COL0 + s * 2 * BK;
         ptx::tmem_st_cols<BK>(ta, hi);
         ptx::tmem_st_cols<BK>(ta + BK, lo);
-#pragma unroll
-        for (int i = 0; i < NY; ++i) {
-          if (ct + 128 * i < G::Y_TILE / 16) {
-            float4 h4;
-            ptx::sts128(yl + 16 * (ct + 128 * i), split_lo(ry[i], h4));
-          }
-        }
         ptx::tmem_st_wait();
-        ptx::fence_proxy_async_smem();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&conv[s]);
@@ -1232,28 +1212,31 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     }
   } else {
     // ---------------- epilogue: lanes = pixels, TMEM columns = filters ----------------
-    // two groups of four warps (7-10, 11-14) take alternate units, so one
+    // two groups of four warps (6-9, 10-13) take alternate units, so one
     // group's stores overlap the other's TMEM loads
     const int q = warp & 3;
-    const int grp = (warp - 7) >> 2;
-    for (int i = threadIdx.x - 7 * 32; i < TN; i += 8 * 32) bias_s[i] = (bias && i < M) ? bias[i] : 0.0f;
+    const int grp = (warp - 6) >> 2;
+    for (int i = threadIdx.x - 6 * 32; i < TN; i += 8 * 32) bias_s[i] = (bias && i < M) ? bias[i] : 0.0f;
     asm volatile("bar.sync 2, 256;" ::: "memory");  // the eight epilogue warps
+    const int m = 32 * q + lane;
+    const int py = m / TW, px = m % TW;
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       if ((j & 1) != grp) continue;
-      const int img = u / tpi;
-      const int p0 = (u - img * tpi) * 128;
+      int img, y0, x0;
+      unit_xy(u, img, y0, x0);
       const int a = j % NACC;
       ptx::mbar_wait_sleepy(&acc_full[a], (j / NACC) & 1);
       ptx::tc_fence_after();
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * TN;
-      const int pix = p0 + 32 * q + lane;
-      const bool live = pix < HW && !(dbg & 4);
-      float *cp = C + img * c_bs + pix;
+      const int y = y0 + py, x = x0 + px;
+      const bool live = y < height && x < width && !(dbg & 4);
+      float *cp = C + img * c_bs + (int64_t)y * width + x;
       constexpr int CH = 16;
 #pragma unroll 1
       for (int cc = 0; cc < TN / CH; ++cc) {
         uint32_t r[CH];
+        if (dbg & 32) continue;
         ptx::tmem_ld_32x32b_x16(trow + CH * cc, r);
         const int rbase = CH * cc;
         if (!live || rbase >= M) continue;
@@ -1394,30 +1377,33 @@ bool cached_map(CUtensorMap *map, const float *ptr, uint64_t inner, uint64_t out
   return true;
 }
 
-// 3-D fp32 tensor map (no swizzle): the conv input batch as (pixel, image,
-// channel) with element strides 1, img_stride, ch_stride -- both the
+// 4-D fp32 tensor map (no swizzle): the conv input batch as (x, y, image,
+// channel) with element strides 1, width, img_stride, ch_stride -- both the
 // image-major and the column-interleaved batch layouts; out-of-bounds
-// pixels read 0.  Cached per host thread like cached_map.
-bool cached_map3(CUtensorMap *map, const float *ptr, uint64_t pixels, uint64_t images,
-                 uint64_t channels, uint64_t img_stride, uint64_t ch_stride, uint32_t box_px,
-                 uint32_t box_ch) {
+// elements read 0 (the conv's padding).  Cached per host thread.
+bool cached_map4(CUtensorMap *map, const float *ptr, uint64_t width, uint64_t height,
+                 uint64_t images, uint64_t channels, uint64_t img_stride, uint64_t ch_stride,
+                 uint32_t box_x, uint32_t box_y, uint32_t box_c) {
   struct Key {
     const void *ptr;
-    uint64_t a, b, c, d, e, f;
+    uint64_t v[8];
     bool operator==(const Key &o) const {
-      return ptr == o.ptr && a == o.a && b == o.b && c == o.c && d == o.d && e == o.e && f == o.f;
+      if (ptr != o.ptr) return false;
+      for (int i = 0; i < 8; ++i)
+        if (v[i] != o.v[i]) return false;
+      return true;
     }
   };
   struct Hash {
     size_t operator()(const Key &k) const {
       uint64_t h = reinterpret_cast<uint64_t>(k.ptr) * 0x9E3779B97F4A7C15ull;
-      for (uint64_t v : {k.a, k.b, k.c, k.d, k.e, k.f}) h ^= v + 0x9E3779B9 + (h << 6) + (h >> 2);
+      for (uint64_t x : k.v) h ^= x + 0x9E3779B9 + (h << 6) + (h >> 2);
       return (size_t)h;
     }
   };
   static thread_local std::unordered_map<Key, CUtensorMap, Hash> cache;
-  const Key key{ptr, pixels, images, channels, img_stride, ch_stride,
-                ((uint64_t)box_px << 32) | box_ch};
+  const Key key{ptr, {width, height, images, channels, img_stride, ch_stride,
+                      ((uint64_t)box_x << 32) | box_y, box_c}};
   auto it = cache.find(key);
   if (it != cache.end()) {
     *map = it->second;
@@ -1425,11 +1411,11 @@ bool cached_map3(CUtensorMap *map, const float *ptr, uint64_t pixels, uint64_t i
   }
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[3] = {pixels, images, channels};
-  cuuint64_t strides[2] = {img_stride * 4, ch_stride * 4};
-  cuuint32_t box[3] = {box_px, 1, box_ch};
-  cuuint32_t estr[3] = {1, 1, 1};
-  if (fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(ptr), dims, strides, box, estr,
+  cuuint64_t dims[4] = {width, height, images, channels};
+  cuuint64_t strides[3] = {width * 4, img_stride * 4, ch_stride * 4};
+  cuuint32_t box[4] = {box_x, box_y, 1, box_c};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  if (fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(ptr), dims, strides, box, estr,
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
@@ -1684,25 +1670,27 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
 }
 
 // Implicit-im2col conv on tensor cores (tc_conv_kernel): M <= 64 filters,
-// channels <= 64, any batch layout with 16-B aligned strides.  NS = stage
-// ring depth; the caller tries the deepest ring whose slabs still fit.
-template <int TN, int NS>
+// channels <= 64, any batch layout with 16-B aligned strides; ENOTSUP when
+// the resident weights and the two slabs exceed shared memory.
+template <int TN, int TW>
 int launch_conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channels, int height,
                    int width, float *col, int64_t ld_col, int64_t col_stride, int M,
                    const float *A, int64_t lda, float beta, float *C, int64_t ldc,
                    int64_t c_stride, const float *bias, int act, int batch, int col_from,
                    cudaStream_t s) {
-  using G = ConvCfg<TN, NS>;
-  const int K = 9 * channels, HW = height * width;
-  const size_t slab_bytes = (size_t)(conv_slab_chunks(width) + 1) * channels * SLAB_BOX * 4;
-  const size_t smem = 1024 + (size_t)G::S * G::STAGE_BYTES + 2 * slab_bytes +
-                      8 * (3 * G::S + 4 + 2 * G::NACC) + 16 + 4 * TN;
+  using G = ConvCfg<TN, TW>;
+  const int K = 9 * channels;
+  const int nkb = (K + G::BK - 1) / G::BK;
+  const size_t slab_bytes = ((size_t)channels * G::CS + 127) & ~size_t(127);
+  const size_t smem = 1024 + 2 * (size_t)nkb * G::W_TILE + 2 * slab_bytes +
+                      8 * (5 + 2 * G::S + 2 * G::NACC) + 16 + 4 * TN;
   if (smem > 227 * 1024) return ACCT_ENOTSUP;
   CUtensorMap tw, tx;
   if (!cached_map(&tw, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, G::BK, TN,
                   CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !cached_map3(&tx, im, (uint64_t)HW, (uint64_t)batch, (uint64_t)channels,
-                   (uint64_t)(batch > 1 ? im_stride : ld_im), (uint64_t)ld_im, SLAB_BOX, channels))
+      !cached_map4(&tx, im, (uint64_t)width, (uint64_t)height, (uint64_t)batch,
+                   (uint64_t)channels, (uint64_t)(batch > 1 ? im_stride : ld_im), (uint64_t)ld_im,
+                   G::TWP, G::SROWS, channels))
     return fail(ACCT_ENOTSUP, "conv_tc: cuTensorMapEncodeTiled failed");
   static std::mutex mu;
   static bool done[64] = {false};
@@ -1711,7 +1699,7 @@ int launch_conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channe
   {
     std::lock_guard<std::mutex> lock(mu);
     if (dev >= 0 && dev < 64 && !done[dev]) {
-      if (int rc = check_cuda(cudaFuncSetAttribute(tc_conv_kernel<TN, NS>,
+      if (int rc = check_cuda(cudaFuncSetAttribute(tc_conv_kernel<TN, TW>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    227 * 1024),
                               "conv_tc: smem attribute"))
@@ -1719,19 +1707,19 @@ int launch_conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channe
       done[dev] = true;
     }
   }
-  const int tpi = (HW + 127) / 128;
-  const int64_t units = (int64_t)tpi * batch;
+  const int tiles_x = (width + TW - 1) / TW, tiles_y = (height + G::TH - 1) / G::TH;
+  const int64_t tpi = (int64_t)tiles_x * tiles_y;
+  const int64_t units = tpi * batch;
   if (units > INT32_MAX) return ACCT_ENOTSUP;
-  const int nkb = (K + G::BK - 1) / G::BK;
   const int sms = sm_count();
   const int grid = units < sms ? (int)units : sms;
   static const int dbg = [] {  // profiling knob (tools/conv_probe.py): 1 no operand build,
     const char *e = getenv("ACCT_CONV_DBG");  // 2 no MMAs, 4 no epilogue -- results wrong
     return e ? atoi(e) : 0;
   }();
-  launch(tc_conv_kernel<TN, NS>, dim3(grid), dim3(CONV_TC_THREADS), smem, s, tw, tx, M, channels,
-         height, width, tpi, (int)units, nkb, beta, C, ldc, c_stride, bias, act, col, ld_col,
-         col_stride, col_from, dbg);
+  launch(tc_conv_kernel<TN, TW>, dim3(grid), dim3(CONV_TC_THREADS), smem, s, tw, tx, M, channels,
+         height, width, tiles_x, (int)tpi, (int)units, nkb, beta, C, ldc, c_stride, bias, act, col,
+         ld_col, col_stride, col_from, dbg);
   return note_launch("conv3x3 tc");
 }
 
@@ -1740,18 +1728,14 @@ int conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channels, int
             int width, float *col, int64_t ld_col, int64_t col_stride, int M, const float *A,
             int64_t lda, float beta, float *C, int64_t ldc, int64_t c_stride, const float *bias,
             int act, int batch, int col_from, cudaStream_t s) {
-  int rc = launch_conv_tc<TN, 6>(im, ld_im, im_stride, channels, height, width, col, ld_col,
+  // 16-wide pixel blocks unless the width is a multiple of 8 but not of 16
+  if (width % 16 != 0 && width % 8 == 0)
+    return launch_conv_tc<TN, 8>(im, ld_im, im_stride, channels, height, width, col, ld_col,
                                  col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
                                  col_from, s);
-  if (rc == ACCT_ENOTSUP)
-    rc = launch_conv_tc<TN, 4>(im, ld_im, im_stride, channels, height, width, col, ld_col,
-                               col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
-                               col_from, s);
-  if (rc == ACCT_ENOTSUP)
-    rc = launch_conv_tc<TN, 2>(im, ld_im, im_stride, channels, height, width, col, ld_col,
-                               col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
-                               col_from, s);
-  return rc;
+  return launch_conv_tc<TN, 16>(im, ld_im, im_stride, channels, height, width, col, ld_col,
+                                col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
+                                col_from, s);
 }
 
 }  // namespace acct
@@ -1790,6 +1774,7 @@ extern "C" int acct_conv3x3_tc_f32(const float *im, int64_t ld_im, int64_t im_st
                    : conv_tc<64>(im, ld_im, im_stride, channels, height, width, col, ld_col,
                                  col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
                                  col_from, s);
-  if (rc == ACCT_ENOTSUP) return fail(ACCT_ENOTSUP, "conv3x3 tc: slabs exceed shared memory");
+  if (rc == ACCT_ENOTSUP)
+    return fail(ACCT_ENOTSUP, "conv3x3 tc: weights + slabs exceed shared memory");
   return rc;
 }

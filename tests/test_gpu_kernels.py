@@ -352,7 +352,8 @@ def test_conv3x3_fused_declines_unaligned_rows(cuda_device):
                           (32, 104, 104, 64, 0, True, K.ACT_LEAKY, 2, 0, "il", True),
                           (32, 104, 104, 64, 1, False, K.ACT_NONE, 2, 1, "im", True),
                           (8, 16, 16, 40, 1, False, K.ACT_NONE, 3, 2, "il", False),
-                          (64, 13, 16, 17, 1, True, K.ACT_LEAKY, 2, 0, "im", False),
+                          (48, 13, 16, 17, 1, True, K.ACT_LEAKY, 2, 0, "im", False),
+                          (24, 30, 36, 64, 0, True, K.ACT_LEAKY, 3, 1, "il", False),
                           (3, 20, 24, 50, 0, True, K.ACT_LINEAR, 1, 0, "im", False),
                           (5, 7, 4, 33, 0, True, K.ACT_LEAKY, 4, 3, "il", False)])
 def test_conv3x3_tc_equals_im2col_then_tc_gemm(cuda_device, orc, c, h, w, M, beta, use_bias, act,
@@ -428,7 +429,7 @@ def test_conv3x3_tc_declines_what_it_does_not_take(cuda_device):
     with pytest.raises(K.DeviceError):  # 65 filters: beyond the swap tiles
         K.conv3x3_tc(im.data_ptr(), 64, 0, 3, 8, 8, col.data_ptr(), 64, 0, 65, A.data_ptr(), 32,
                      0.0, C.data_ptr(), 64, 0)
-    with pytest.raises(K.DeviceError):  # input slabs beyond shared memory (64 ch x 608 wide)
+    with pytest.raises(K.DeviceError):  # resident weights + slabs beyond shared memory (64 ch)
         big = torch.zeros((64, 608 * 4), device="cuda")
         K.conv3x3_tc(big.data_ptr(), 608 * 4, 0, 64, 4, 608, col.data_ptr(), 608 * 4, 0, 32,
                      A.data_ptr(), 32, 0.0, C.data_ptr(), 608 * 4, 0)

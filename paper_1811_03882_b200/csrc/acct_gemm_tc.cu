@@ -960,10 +960,11 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 //               then the slab of each unit, double-buffered
 //   warp 1      TMEM allocator + MMA issuer, exactly the swap tile's 3xTF32
 //               sequence (A = activations from TMEM, B = weights hi / lo)
-//   warps 2..5  weights lo once; per k-block the activation operand: lane =
-//               pixel, k = (channel, kh, kw) -> hi / lo to a TMEM stage (6
-//               stages); the col array of images >= col_from stored on the way
-//   warps 6..13 epilogue, two groups taking alternate units: tcgen05.ld ->
+//   warps 2..9  weights lo once; per k-block the activation operand (two
+//               halves of four warps take alternate k-blocks): lane = pixel,
+//               k = (channel, kh, kw) -> hi / lo to a TMEM stage (6 stages);
+//               the col array of images >= col_from stored on the way
+//   warps 10..17 epilogue, two groups taking alternate units: tcgen05.ld ->
 //               beta C, bias (staged in shared memory), leaky -> C
 // Operand values, k order and MMA sequence equal im2col + the swap gemm, so
 // C is bit-identical to the unfused pair (tests/test_gpu_kernels.py).
@@ -985,7 +986,7 @@ struct ConvCfg {
   static constexpr uint32_t K_SBO = 8 * 128;
   static_assert(USED_COLS <= 512, "TMEM overflow");
 };
-constexpr int CONV_TC_THREADS = 32 * 14;
+constexpr int CONV_TC_THREADS = 32 * 18;
 
 // One k-block (32 k = (channel, tap) pairs from k0 = 9 c0 + R0) of the
 // activation operand for this lane's pixel: each k is one LDS at the lane's
@@ -1041,11 +1042,18 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int HW = height * width;
+  if ((dbg & 64) && blockIdx.x == 0 && threadIdx.x == 0) g_trace[6][0] = clock64();
+  auto gtime = [] {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return (long long)t;
+  };
+  if ((dbg & 64) && threadIdx.x == 0 && blockIdx.x < 256) g_trace[7][256 + blockIdx.x] = gtime();
   if (threadIdx.x == 0) {
     ptx::mbar_init(wfull, 1);
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&slab_full[b], 1);
-      ptx::mbar_init(&slab_empty[b], 4);
+      ptx::mbar_init(&slab_empty[b], 8);
     }
     for (int s = 0; s < S; ++s) {
       ptx::mbar_init(&conv[s], 4);
@@ -1111,36 +1119,43 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       for (int kb = 0; kb < nkb; ++kb, ++g) {
         const int s = g % S;
         ptx::mbar_wait(&conv[s], (g / S) & 1);
+        if ((dbg & 64) && blockIdx.x == 0 && g < kTrace && lane == 0) g_trace[2][g] = clock64();
         ptx::tc_fence_after();
         const uint32_t yh = ptx::smem_u32(w_hi + kb * G::W_TILE);
         const uint32_t yl = ptx::smem_u32(w_lo + kb * G::W_TILE);
         const uint32_t at = tmem + G::A_COL0 + s * 2 * BK;
+        // one elected lane issues the k-block's 12 MMAs and the stage commit
+        if (ptx::elect_one()) {
+          if (!(dbg & 2)) {
 #pragma unroll
-        for (int k = 0; k < BK / 8; ++k) {
-          const uint64_t dyh = ptx::smem_desc(yh + 32 * k, 16, G::K_SBO, ptx::kLayoutSW128);
-          const uint64_t dyl = ptx::smem_desc(yl + 32 * k, 16, G::K_SBO, ptx::kLayoutSW128);
-          if (!(dbg & 2) && ptx::elect_one()) {
-            ptx::mma_tf32_ts(d, at + 8 * k, dyh, idesc, (kb | k) != 0);
-            ptx::mma_tf32_ts(d, at + 8 * k, dyl, idesc, 1);
-            ptx::mma_tf32_ts(d, at + BK + 8 * k, dyh, idesc, 1);
+            for (int k = 0; k < BK / 8; ++k) {
+              const uint64_t dyh = ptx::smem_desc(yh + 32 * k, 16, G::K_SBO, ptx::kLayoutSW128);
+              const uint64_t dyl = ptx::smem_desc(yl + 32 * k, 16, G::K_SBO, ptx::kLayoutSW128);
+              ptx::mma_tf32_ts(d, at + 8 * k, dyh, idesc, (kb | k) != 0);
+              ptx::mma_tf32_ts(d, at + 8 * k, dyl, idesc, 1);
+              ptx::mma_tf32_ts(d, at + BK + 8 * k, dyh, idesc, 1);
+            }
           }
-          __syncwarp();
+          ptx::mma_commit(&empty[s]);
         }
-        if (ptx::elect_one()) ptx::mma_commit(&empty[s]);
         __syncwarp();
+        if ((dbg & 64) && blockIdx.x == 0 && g < kTrace && lane == 0) g_trace[3][g] = clock64();
       }
       if (ptx::elect_one()) ptx::mma_commit(&acc_full[a]);
       __syncwarp();
     }
-  } else if (warp < 6) {
+  } else if (warp < 10) {
     // ---------------- weights lo, then the activation operand ----------------
+    // two halves of four warps (2-5, 6-9) build alternate k-blocks, so one
+    // half's TMEM stores and fences overlap the other's loads
     const int q = warp & 3;  // TMEM lanes 32q.. = MMA rows (pixels) 32q..
+    const int half = (warp - 2) >> 2;
     const int ct = threadIdx.x - 64;
     const int K = 9 * channels;
     ptx::mbar_wait(wfull, 0);
     {
       const uint32_t hs = ptx::smem_u32(w_hi), ls = ptx::smem_u32(w_lo);
-      for (int i = ct; i < nkb * G::W_TILE / 16; i += 128) {
+      for (int i = ct; i < nkb * G::W_TILE / 16; i += 256) {
         float4 h4;
         ptx::sts128(ls + 16 * i, split_lo(ptx::lds128(hs + 16 * i), h4));
       }
@@ -1161,11 +1176,14 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       const uint32_t lane_base = ptx::smem_u32(slab0 + sb * slab_bytes) + lane_off;
       ptx::mbar_wait(&slab_full[sb], (j >> 1) & 1);
       for (int kb = 0; kb < nkb; ++kb, ++g) {
+        if ((g & 1) != half) continue;
         const int s = g % S;
         const int k0 = kb * BK;
         const int c0 = k0 / 9;
         const int kvalid = K - k0;  // >= 32 except in the last block
+        if ((dbg & 64) && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[0][g] = clock64();
         if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
+        if ((dbg & 64) && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[1][g] = clock64();
         ptx::tc_fence_after();
         if (dbg & 1) {  // profiling knob: skip building the operand (results wrong)
           __syncwarp();
@@ -1206,17 +1224,18 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&conv[s]);
+        if ((dbg & 64) && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[4][g] = clock64();
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&slab_empty[sb]);  // this unit's slab is consumed
     }
   } else {
     // ---------------- epilogue: lanes = pixels, TMEM columns = filters ----------------
-    // two groups of four warps (6-9, 10-13) take alternate units, so one
+    // two groups of four warps (10-13, 14-17) take alternate units, so one
     // group's stores overlap the other's TMEM loads
     const int q = warp & 3;
-    const int grp = (warp - 6) >> 2;
-    for (int i = threadIdx.x - 6 * 32; i < TN; i += 8 * 32) bias_s[i] = (bias && i < M) ? bias[i] : 0.0f;
+    const int grp = (warp - 10) >> 2;
+    for (int i = threadIdx.x - 10 * 32; i < TN; i += 8 * 32) bias_s[i] = (bias && i < M) ? bias[i] : 0.0f;
     asm volatile("bar.sync 2, 256;" ::: "memory");  // the eight epilogue warps
     const int m = 32 * q + lane;
     const int py = m / TW, px = m % TW;
@@ -1227,6 +1246,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       unit_xy(u, img, y0, x0);
       const int a = j % NACC;
       ptx::mbar_wait_sleepy(&acc_full[a], (j / NACC) & 1);
+      if ((dbg & 64) && blockIdx.x == 0 && j < kTrace && lane == 0 && q == 0) g_trace[5][j] = clock64();
       ptx::tc_fence_after();
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * TN;
       const int y = y0 + py, x = x0 + px;
@@ -1266,6 +1286,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 
   ptx::tc_fence_before();
   __syncthreads();
+  if ((dbg & 64) && blockIdx.x == 0 && threadIdx.x == 0) g_trace[6][1] = clock64();
+  if ((dbg & 64) && threadIdx.x == 0 && blockIdx.x < 256) g_trace[7][blockIdx.x] = gtime();
   if (warp == 1) ptx::tmem_dealloc(tmem, G::TMEM_COLS);
 }
 

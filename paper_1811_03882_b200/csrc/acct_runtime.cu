@@ -327,8 +327,13 @@ int device_op(const acct_action_t &a, acct_array_t *arr, int gemm_mode, cudaStre
       // implicit-im2col tcgen05 swap tile (3xTF32, bit-identical to im2col +
       // the swap gemm) for the other narrow layers (M <= 64)
       const int C = (int)I[1], col_from = I[8] ? nb - 1 : 0;
+      static const int tc_first = [] {  // experiment knob: first layers on tcgen05 too
+        const char *e = getenv("ACCT_CONV_TC_FIRST");
+        return e ? atoi(e) : 0;
+      }();
       const bool simt = gemm_mode == ACCT_GEMM_SIMT ||
-                        (gemm_mode == ACCT_GEMM_AUTO && (M <= 16 || (M <= 32 && C <= 4)));
+                        (gemm_mode == ACCT_GEMM_AUTO && !tc_first &&
+                         (M <= 16 || (M <= 32 && C <= 4)));
       if (simt) {
         const int rc = acct_conv3x3_im2col_gemm_f32(D(0), LD(0), BS(0), C, (int)I[2], (int)I[3],
                                                     D(1), LD(1), BS(1), M, D(2), LD(2), beta, D(3),

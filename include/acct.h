@@ -137,12 +137,20 @@ int acct_maxpool_batched_f32(const float *in, int64_t ld_in, int64_t in_stride, 
  * instead of re-reading col.  col_from = batch - 1 skips the col stores of
  * every image but the last (the executor does so when only that copy is
  * observable).  Rows of col and C (ld, strides, width) must be 16-byte
- * aligned; else ENOTSUP. */
+ * aligned; else ENOTSUP.
+ * Both conv entries take an optional fused 2x2/2 maxpool of the (activated)
+ * output: pool != NULL writes pool / idx exactly like acct_maxpool_batched_f32
+ * (size 2, stride 2, offset 0; darknet's scan order and strict '>', argmax as
+ * the flat index into the image's C plane), and C is then stored for images
+ * >= c_from only.  ENOTSUP when the kernel cannot fuse it (odd planes; the
+ * FP32 window kernel takes no pool yet). */
 int acct_conv3x3_im2col_gemm_f32(const float *im, int64_t ld_im, int64_t im_stride, int channels,
                                  int height, int width, float *col, int64_t ld_col,
                                  int64_t col_stride, int M, const float *A, int64_t lda,
                                  float beta, float *C, int64_t ldc, int64_t c_stride,
                                  const float *bias, int act, int batch, int col_from,
+                                 float *pool, int64_t ld_pool, int64_t pool_stride, int32_t *idx,
+                                 int64_t ld_idx, int64_t idx_stride, int c_from,
                                  acct_stream_t stream);
 
 /* The same contract on the 5th-generation tensor cores for M <= 64 filters
@@ -157,7 +165,8 @@ int acct_conv3x3_tc_f32(const float *im, int64_t ld_im, int64_t im_stride, int c
                         int height, int width, float *col, int64_t ld_col, int64_t col_stride,
                         int M, const float *A, int64_t lda, float beta, float *C, int64_t ldc,
                         int64_t c_stride, const float *bias, int act, int batch, int col_from,
-                        acct_stream_t stream);
+                        float *pool, int64_t ld_pool, int64_t pool_stride, int32_t *idx,
+                        int64_t ld_idx, int64_t idx_stride, int c_from, acct_stream_t stream);
 
 /* Test support (synchronous, allocates scratch): evaluates the kernels'
  * leaky activation against darknet's (float)(0.1 * (double)x) for all 2^32
@@ -238,7 +247,8 @@ enum {
   /* fused im2col(3x3/1/1) + gemm: slots a = (X, col, A, C); i[1..3] = c, h, w,
      i[4] = M, i[5] = beta is 1, i[6] = act, i[7] = bias slot (-1: none),
      i[8] = 1: col is written for the batch's last image only (the others are
-     unobservable).  Device only: acct_conv3x3_im2col_gemm_f32 in SIMT mode
+     unobservable); i[9], i[10] = pool / idx slots of a fused 2x2/2 maxpool of
+     C (-1: none), i[11] = 1: C itself is then stored for the last image only.  Device only: acct_conv3x3_im2col_gemm_f32 in SIMT mode
      and, under AUTO, for M <= 16 or c <= 4 with M <= 32;
      acct_conv3x3_tc_f32 otherwise (M <= 64); im2col + gemm when the fused
      kernel declines the shape */

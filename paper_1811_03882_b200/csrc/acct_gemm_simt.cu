@@ -14,6 +14,8 @@
 // in BK chunks), so results differ from the host i-k-j loop only by FMA
 // contraction; parity is checked to the 1e-4 relative tolerance.
 
+#include <cfloat>
+
 #include "acct_common.cuh"
 
 namespace {
@@ -546,6 +548,164 @@ int launch_conv(int batch, cudaStream_t s, const float *im, int64_t ld_im, int64
 
 }  // namespace
 
+namespace {
+
+// The same fused conv with its 2x2/2 maxpool (first layers: M <= 16).  A
+// thread owns a 2x2 pixel block -- one maxpool window -- of a 32 x 16 tile
+// (16 x 8 threads), so the pool is in-thread: per filter the four finished
+// values are compared in darknet's scan order (strict '>', from -FLT_MAX)
+// and the argmax is the flat index into the image's C plane.  The tile's
+// (16 + 2) x (32 + 2) input window per channel is staged by cp.async from a
+// 16-byte aligned column x0 - 4 (rows / columns outside the image are zero),
+// double-buffered across tiles.  k order and FMA chain are those of the
+// window kernel (bit-identical C); C and col are stored for images >=
+// c_from / col_from only.
+constexpr int PT_W = 32, PT_H = 16, PT_SW = PT_W + 8, PT_SH = PT_H + 2;  // slab row 40 floats
+
+__global__ void __launch_bounds__(128, 4)
+conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, int channels,
+                    int height, int width, float *__restrict__ col, int64_t ld_col,
+                    int64_t col_bs, int col_from, int M, const float *__restrict__ A, int64_t lda,
+                    float beta, float *__restrict__ C, int64_t ldc, int64_t c_bs,
+                    const float *__restrict__ bias, int act, float *__restrict__ pool,
+                    int64_t ld_pool, int64_t pool_bs, int32_t *__restrict__ pidx,
+                    int64_t ld_pidx, int64_t pidx_bs, int c_from, int tiles_x, int tpi,
+                    int ntiles) {
+  constexpr int MT = 16;
+  extern __shared__ float4 conv_smem[];
+  const int K = channels * 9;
+  float *As = reinterpret_cast<float *>(conv_smem);  // [k][MT]
+  float *sin0 = As + K * MT;                         // 2 x [channels][PT_SH][PT_SW]
+  const int bufsz = channels * PT_SH * PT_SW;
+  pdl_trigger();
+  pdl_wait();
+
+  auto tile_xy = [&](int tile, int &img, int &y0, int &x0) {
+    img = tile / tpi;
+    const int t = tile - img * tpi;
+    const int ty = t / tiles_x;
+    y0 = ty * PT_H;
+    x0 = (t - ty * tiles_x) * PT_W;
+  };
+  auto stage = [&](int tile, float *buf) {
+    int img, y0, x0;
+    tile_xy(tile, img, y0, x0);
+    const float *src = im + img * im_bs;
+    constexpr int NQ = PT_SW / 4;  // 16-byte chunks per slab row
+    for (int j = threadIdx.x; j < channels * PT_SH * NQ; j += 128) {
+      const int q = j % NQ, rr = (j / NQ) % PT_SH, ci = j / (NQ * PT_SH);
+      const int gy = y0 - 1 + rr, gx = x0 - 4 + 4 * q;  // width % 4 == 0: whole chunks
+      float *dst = buf + (ci * PT_SH + rr) * PT_SW + 4 * q;
+      if (gy >= 0 && gy < height && gx >= 0 && gx < width)
+        cp_async16(dst, src + ci * ld_im + (int64_t)gy * width + gx);
+      else
+        *reinterpret_cast<float4 *>(dst) = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    }
+  };
+
+  int tile = blockIdx.x;
+  if (tile < ntiles) stage(tile, sin0);
+  cp_async_commit();
+  for (int t = threadIdx.x; t < K * MT; t += 128) {
+    const int k = t / MT, m = t - k * MT;
+    As[t] = m < M ? A[(int64_t)m * lda + k] : 0.0f;
+  }
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  int buf = 0;
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int nxt = tile + gridDim.x;
+    if (nxt < ntiles) stage(nxt, sin0 + (buf ^ 1) * bufsz);
+    cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();
+    int img, y0, x0;
+    tile_xy(tile, img, y0, x0);
+    const int y = y0 + 2 * ty, x = x0 + 2 * tx;
+    if (y < height && x < width) {  // even planes: the whole 2x2 block is inside
+      const bool wcol = img >= col_from, wc = img >= c_from;
+      const int64_t p = (int64_t)y * width + x;
+      float *colp = col + img * col_bs + p;
+      const float *base = sin0 + buf * bufsz + (2 * ty) * PT_SW + 2 * tx + 3;  // window (-1, -1)
+      float acc[MT][4];
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[m][e] = 0.0f;
+#pragma unroll 1
+      for (int ci = 0; ci < channels; ++ci) {
+        const float *cb = base + ci * PT_SH * PT_SW;
+        float win[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) win[r][c] = cb[r * PT_SW + c];
+#pragma unroll
+        for (int kh = 0; kh < 3; ++kh) {
+#pragma unroll
+          for (int kw = 0; kw < 3; ++kw) {
+            const int k = ci * 9 + kh * 3 + kw;
+            const float v0 = win[kh][kw], v1 = win[kh][kw + 1];
+            const float v2 = win[kh + 1][kw], v3 = win[kh + 1][kw + 1];
+            if (wcol) {
+              __stcs(reinterpret_cast<float2 *>(colp + (int64_t)k * ld_col), make_float2(v0, v1));
+              __stcs(reinterpret_cast<float2 *>(colp + (int64_t)k * ld_col + width),
+                     make_float2(v2, v3));
+            }
+            const float4 *ak = reinterpret_cast<const float4 *>(As + k * MT);
+#pragma unroll
+            for (int m4 = 0; m4 < MT / 4; ++m4) {
+              const float4 a = ak[m4];
+              const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                acc[4 * m4 + e][0] = fmaf(av[e], v0, acc[4 * m4 + e][0]);
+                acc[4 * m4 + e][1] = fmaf(av[e], v1, acc[4 * m4 + e][1]);
+                acc[4 * m4 + e][2] = fmaf(av[e], v2, acc[4 * m4 + e][2]);
+                acc[4 * m4 + e][3] = fmaf(av[e], v3, acc[4 * m4 + e][3]);
+              }
+            }
+          }
+        }
+      }
+      float *cimg = C + img * c_bs + p;
+      const int64_t pofs = (int64_t)(y >> 1) * (width >> 1) + (x >> 1);
+      const int base_i = (int)p;
+      const int plane = height * width;
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        if (m >= M) break;
+        float *cp = cimg + (int64_t)m * ldc;
+        float cv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        if (beta != 0.0f) {
+          const float2 c0 = *reinterpret_cast<const float2 *>(cp);
+          const float2 c1 = *reinterpret_cast<const float2 *>(cp + width);
+          cv[0] = c0.x; cv[1] = c0.y; cv[2] = c1.x; cv[3] = c1.y;
+        }
+        float o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[e] = epilogue(acc[m][e], 1.0f, beta, cv + e, bias, m, act);
+        if (wc) {
+          __stcs(reinterpret_cast<float2 *>(cp), make_float2(o[0], o[1]));
+          __stcs(reinterpret_cast<float2 *>(cp + width), make_float2(o[2], o[3]));
+        }
+        const int bi = m * plane + base_i;
+        float mx = -FLT_MAX;
+        int32_t kx = -1;
+        if (o[0] > mx) { mx = o[0]; kx = bi; }
+        if (o[1] > mx) { mx = o[1]; kx = bi + 1; }
+        if (o[2] > mx) { mx = o[2]; kx = bi + width; }
+        if (o[3] > mx) { mx = o[3]; kx = bi + width + 1; }
+        pool[img * pool_bs + (int64_t)m * ld_pool + pofs] = mx;
+        pidx[img * pidx_bs + (int64_t)m * ld_pidx + pofs] = kx;
+      }
+    }
+    __syncthreads();  // this buffer is restaged two tiles later
+    buf ^= 1;
+  }
+}
+
+}  // namespace
+
 // C = A . im2col(im) + beta C (+ bias, act) for 3x3/1/1 convolutions with
 // channels <= 64 and M <= 32, also writing the col array (images >= col_from
 // of the batch); batched over images
@@ -554,8 +714,40 @@ extern "C" int acct_conv3x3_im2col_gemm_f32(const float *im, int64_t ld_im, int6
                                             int64_t ld_col, int64_t col_stride, int M,
                                             const float *A, int64_t lda, float beta, float *C,
                                             int64_t ldc, int64_t c_stride, const float *bias, int act,
-                                            int batch, int col_from, acct_stream_t stream) {
+                                            int batch, int col_from, float *pool, int64_t ld_pool,
+                                            int64_t pool_stride, int32_t *idx, int64_t ld_idx,
+                                            int64_t idx_stride, int c_from, acct_stream_t stream) {
   using namespace acct;
+  if (pool) {
+    // fused 2x2/2 maxpool: 2x2 pixel blocks per thread, M <= 16
+    if (!idx || M > 16 || channels < 1 || channels > 64 || (height | width) & 1 || (width & 3) ||
+        col_from < 0 || c_from < 0 || batch < 1 || ld_im < (int64_t)height * width ||
+        ld_col < (int64_t)height * width || ldc < (int64_t)height * width ||
+        ld_pool < (int64_t)(height / 2) * (width / 2) || ld_idx < (int64_t)(height / 2) * (width / 2) ||
+        (reinterpret_cast<uintptr_t>(im) | reinterpret_cast<uintptr_t>(col) |
+         reinterpret_cast<uintptr_t>(C)) & 15 ||
+        (ld_im | im_stride | ld_col | col_stride | ldc | c_stride) & 3)
+      return fail(ACCT_ENOTSUP, "conv3x3 fused: maxpool fusion needs M <= 16, even planes");
+    const size_t smem = sizeof(float) * ((size_t)channels * 9 * 16 +
+                                         2 * (size_t)channels * PT_SH * PT_SW);
+    if (smem > 200 * 1024) return fail(ACCT_ENOTSUP, "conv3x3 fused: slabs exceed shared memory");
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(conv3x3_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+    const int tiles_x = (width + PT_W - 1) / PT_W, tiles_y = (height + PT_H - 1) / PT_H;
+    const int64_t tpi = (int64_t)tiles_x * tiles_y, ntiles = tpi * batch;
+    if (ntiles > INT32_MAX) return fail(ACCT_ENOTSUP, "conv3x3 fused: too many tiles");
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv3x3_pool_kernel, 128, smem);
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = (int64_t)sm_count() * per_sm;
+    if (grid > ntiles) grid = ntiles;
+    launch(conv3x3_pool_kernel, dim3((unsigned)grid), dim3(128), smem, as_stream(stream), im, ld_im,
+           im_stride, channels, height, width, col, ld_col, col_stride, col_from, M, A, lda, beta, C,
+           ldc, c_stride, bias, act, pool, ld_pool, pool_stride, idx, ld_idx, idx_stride, c_from,
+           tiles_x, (int)tpi, (int)ntiles);
+    return note_launch("conv3x3 im2col+gemm+maxpool");
+  }
   if (channels < 1 || channels > 64 || M < 1 || M > 32 || height < 1 || width < 1 || batch < 1 ||
       col_from < 0 || (int64_t)height * width > (1 << 28) || ld_im < (int64_t)height * width ||
       ld_col < (int64_t)height * width || ldc < (int64_t)height * width)

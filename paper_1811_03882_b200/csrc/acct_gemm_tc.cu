@@ -46,6 +46,8 @@
 
 #include <cuda.h>
 
+#include <cfloat>
+
 #include <atomic>
 #include <mutex>
 #include <unordered_map>
@@ -1020,7 +1022,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
                int M, int channels, int height, int width, int tiles_x, int tpi, int units,
                int nkb, float beta, float *__restrict__ C, int64_t ldc, int64_t c_bs,
                const float *__restrict__ bias, int act, float *__restrict__ col, int64_t ld_col,
-               int64_t col_bs, int col_from, int dbg) {
+               int64_t col_bs, int col_from, float *__restrict__ pool, int64_t ld_pool,
+               int64_t pool_bs, int32_t *__restrict__ pidx, int64_t ld_pidx, int64_t pidx_bs,
+               int c_from, int dbg) {
   using G = ConvCfg<TN, TW>;
   constexpr int S = G::S, BK = G::BK, NACC = G::NACC;
   extern __shared__ uint8_t smem_raw[];
@@ -1038,7 +1042,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   uint64_t *acc_full = empty + S;
   uint64_t *acc_empty = acc_full + NACC;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + NACC);
-  float *bias_s = reinterpret_cast<float *>(tmem_slot + 4);  // TN floats
+  float *bias_s = reinterpret_cast<float *>(tmem_slot + 4);  // 64 floats, then 8 x 8 x 33 scratch
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int HW = height * width;
@@ -1239,6 +1243,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     asm volatile("bar.sync 2, 256;" ::: "memory");  // the eight epilogue warps
     const int m = 32 * q + lane;
     const int py = m / TW, px = m % TW;
+    float *scr = bias_s + 64 + (warp - 10) * 8 * 33;  // this warp's pooling scratch
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       if ((j & 1) != grp) continue;
@@ -1251,6 +1256,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * TN;
       const int y = y0 + py, x = x0 + px;
       const bool live = y < height && x < width && !(dbg & 4);
+      const bool cst = live && img >= c_from;  // C of earlier images is dead when pooled here
       float *cp = C + img * c_bs + (int64_t)y * width + x;
       constexpr int CH = 16;
 #pragma unroll 1
@@ -1259,23 +1265,57 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         if (dbg & 32) continue;
         ptx::tmem_ld_32x32b_x16(trow + CH * cc, r);
         const int rbase = CH * cc;
-        if (!live || rbase >= M) continue;
+        if (rbase >= M) continue;
         float *rp = cp + (int64_t)rbase * ldc;
         float cv[CH];
-        if (beta != 0.0f) {
+        if (beta != 0.0f && live) {
 #pragma unroll
           for (int jj = 0; jj < CH; ++jj)  // every load in flight before any store
             cv[jj] = rbase + jj < M ? rp[(int64_t)jj * ldc] : 0.0f;
         }
 #pragma unroll
         for (int jj = 0; jj < CH; ++jj) {
-          if (rbase + jj < M) {
-            float v = __uint_as_float(r[jj]);
-            if (beta != 0.0f) v = beta * cv[jj] + v;
-            if (bias) v += bias_s[rbase + jj];
-            if (act == ACCT_ACT_LEAKY) v = acct_leaky(v);
-            rp[(int64_t)jj * ldc] = v;
+          float v = __uint_as_float(r[jj]);
+          if (beta != 0.0f && live) v = beta * cv[jj] + v;
+          if (bias) v += bias_s[rbase + jj];
+          if (act == ACCT_ACT_LEAKY) v = acct_leaky(v);
+          if (cst && rbase + jj < M) rp[(int64_t)jj * ldc] = v;
+          r[jj] = __float_as_uint(v);
+        }
+#pragma unroll
+        for (int half = 0; half < 2 && pool; ++half) {
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) scr[jj * 33 + lane] = __uint_as_float(r[8 * half + jj]);
+          // 2x2/2 maxpool, 8 filters per pass: the warp's 32 pixels are 8
+          // whole windows (tiles start on even rows / columns); through the
+          // scratch each lane takes window (lane & 7) of filters 4t + (lane >>
+          // 3), comparing in darknet's scan order with strict '>' from -FLT_MAX
+          __syncwarp();
+          constexpr int TWH = TW / 2;
+          const int w8 = lane & 7, fg = lane >> 3;
+          const int l0 = (w8 / TWH) * 2 * TW + 2 * (w8 % TWH);  // window's top-left lane
+          const int m0 = 32 * q + l0;
+          const int wy = y0 + m0 / TW, wx = x0 + m0 % TW;
+          const bool win = wy < height && wx < width && !(dbg & 4);
+          const int64_t pofs = (int64_t)(wy >> 1) * (width >> 1) + (wx >> 1);
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const int fl = 4 * t + fg, f = rbase + 8 * half + fl;
+            const float *sv = scr + fl * 33 + l0;
+            const float v00 = sv[0], v01 = sv[1], v10 = sv[TW], v11 = sv[TW + 1];
+            if (win && f < M) {
+              const int base_i = f * HW + wy * width + wx;
+              float mx = -FLT_MAX;
+              int32_t k = -1;
+              if (v00 > mx) { mx = v00; k = base_i; }
+              if (v01 > mx) { mx = v01; k = base_i + 1; }
+              if (v10 > mx) { mx = v10; k = base_i + width; }
+              if (v11 > mx) { mx = v11; k = base_i + width + 1; }
+              pool[img * pool_bs + (int64_t)f * ld_pool + pofs] = mx;
+              pidx[img * pidx_bs + (int64_t)f * ld_pidx + pofs] = k;
+            }
           }
+          __syncwarp();  // the scratch is rewritten by the next chunk
         }
       }
       ptx::tc_fence_before();
@@ -1691,6 +1731,15 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
   return launch_tc<192, false, 16>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
 }
 
+// optional 2x2/2 maxpool of the conv output, fused into the epilogue
+struct ConvPool {
+  float *pool;
+  int64_t ld_pool, pool_stride;
+  int32_t *idx;
+  int64_t ld_idx, idx_stride;
+  int c_from;  // C stored for images >= c_from only (the pooled copies are dead)
+};
+
 // Implicit-im2col conv on tensor cores (tc_conv_kernel): M <= 64 filters,
 // channels <= 64, any batch layout with 16-B aligned strides; ENOTSUP when
 // the resident weights and the two slabs exceed shared memory.
@@ -1699,13 +1748,14 @@ int launch_conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channe
                    int width, float *col, int64_t ld_col, int64_t col_stride, int M,
                    const float *A, int64_t lda, float beta, float *C, int64_t ldc,
                    int64_t c_stride, const float *bias, int act, int batch, int col_from,
-                   cudaStream_t s) {
+                   const ConvPool &pl, cudaStream_t s) {
   using G = ConvCfg<TN, TW>;
   const int K = 9 * channels;
   const int nkb = (K + G::BK - 1) / G::BK;
   const size_t slab_bytes = ((size_t)channels * G::CS + 127) & ~size_t(127);
   const size_t smem = 1024 + 2 * (size_t)nkb * G::W_TILE + 2 * slab_bytes +
-                      8 * (5 + 2 * G::S + 2 * G::NACC) + 16 + 4 * TN;
+                      8 * (5 + 2 * G::S + 2 * G::NACC) + 16 + 4 * 64 +
+                      (pl.pool ? 4 * 8 * 8 * 33 : 0);  // pooling scratch
   if (smem > 227 * 1024) return ACCT_ENOTSUP;
   CUtensorMap tw, tx;
   if (!cached_map(&tw, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, G::BK, TN,
@@ -1741,7 +1791,8 @@ int launch_conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channe
   }();
   launch(tc_conv_kernel<TN, TW>, dim3(grid), dim3(CONV_TC_THREADS), smem, s, tw, tx, M, channels,
          height, width, tiles_x, (int)tpi, (int)units, nkb, beta, C, ldc, c_stride, bias, act, col,
-         ld_col, col_stride, col_from, dbg);
+         ld_col, col_stride, col_from, pl.pool, pl.ld_pool, pl.pool_stride, pl.idx, pl.ld_idx,
+         pl.idx_stride, pl.c_from, dbg);
   return note_launch("conv3x3 tc");
 }
 
@@ -1749,15 +1800,21 @@ template <int TN>
 int conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channels, int height,
             int width, float *col, int64_t ld_col, int64_t col_stride, int M, const float *A,
             int64_t lda, float beta, float *C, int64_t ldc, int64_t c_stride, const float *bias,
-            int act, int batch, int col_from, cudaStream_t s) {
-  // 16-wide pixel blocks unless the width is a multiple of 8 but not of 16
-  if (width % 16 != 0 && width % 8 == 0)
-    return launch_conv_tc<TN, 8>(im, ld_im, im_stride, channels, height, width, col, ld_col,
-                                 col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
-                                 col_from, s);
-  return launch_conv_tc<TN, 16>(im, ld_im, im_stride, channels, height, width, col, ld_col,
+            int act, int batch, int col_from, const ConvPool &pl, cudaStream_t s) {
+  // 16-wide pixel blocks unless the width is a multiple of 8 but not of 16;
+  // the other width when those slabs do not fit next to the pooling scratch
+  const bool eight = width % 16 != 0 && width % 8 == 0;
+  int rc = eight ? launch_conv_tc<TN, 8>(im, ld_im, im_stride, channels, height, width, col,
+                                         ld_col, col_stride, M, A, lda, beta, C, ldc, c_stride,
+                                         bias, act, batch, col_from, pl, s)
+                 : launch_conv_tc<TN, 16>(im, ld_im, im_stride, channels, height, width, col,
+                                          ld_col, col_stride, M, A, lda, beta, C, ldc, c_stride,
+                                          bias, act, batch, col_from, pl, s);
+  if (rc == ACCT_ENOTSUP && eight)
+    rc = launch_conv_tc<TN, 16>(im, ld_im, im_stride, channels, height, width, col, ld_col,
                                 col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
-                                col_from, s);
+                                col_from, pl, s);
+  return rc;
 }
 
 }  // namespace acct
@@ -1779,23 +1836,31 @@ extern "C" int acct_conv3x3_tc_f32(const float *im, int64_t ld_im, int64_t im_st
                                    int64_t ld_col, int64_t col_stride, int M, const float *A,
                                    int64_t lda, float beta, float *C, int64_t ldc,
                                    int64_t c_stride, const float *bias, int act, int batch,
-                                   int col_from, acct_stream_t stream) {
+                                   int col_from, float *pool, int64_t ld_pool,
+                                   int64_t pool_stride, int32_t *idx, int64_t ld_idx,
+                                   int64_t idx_stride, int c_from, acct_stream_t stream) {
   using namespace acct;
   if (channels < 1 || channels > 64 || M < 1 || M > 64 || height < 1 || width < 1 || batch < 1 ||
-      col_from < 0 || (int64_t)height * width > (1 << 28) || ld_im < (int64_t)height * width ||
-      ld_col < (int64_t)height * width || ldc < (int64_t)height * width ||
-      (batch > 1 && (im_stride < 1 || (im_stride & 3))))
+      col_from < 0 || c_from < 0 || (int64_t)height * width > (1 << 28) ||
+      ld_im < (int64_t)height * width || ld_col < (int64_t)height * width ||
+      ldc < (int64_t)height * width || (batch > 1 && (im_stride < 1 || (im_stride & 3))))
     return fail(ACCT_ENOTSUP, "conv3x3 tc: shape not supported");
   if ((reinterpret_cast<uintptr_t>(im) | reinterpret_cast<uintptr_t>(A)) & 15 ||
       (ld_im | lda) & 3)
     return fail(ACCT_ENOTSUP, "conv3x3 tc: needs 16-B aligned operands");
+  if (pool && (!idx || (height | width) & 1 ||
+               ld_pool < (int64_t)(height / 2) * (width / 2) ||
+               ld_idx < (int64_t)(height / 2) * (width / 2)))
+    return fail(ACCT_ENOTSUP, "conv3x3 tc: fused maxpool needs even planes");
+  if (!pool) c_from = 0;
+  const ConvPool pl{pool, ld_pool, pool_stride, idx, ld_idx, idx_stride, c_from};
   cudaStream_t s = as_stream(stream);
   int rc = M <= 32 ? conv_tc<32>(im, ld_im, im_stride, channels, height, width, col, ld_col,
                                  col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
-                                 col_from, s)
+                                 col_from, pl, s)
                    : conv_tc<64>(im, ld_im, im_stride, channels, height, width, col, ld_col,
                                  col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
-                                 col_from, s);
+                                 col_from, pl, s);
   if (rc == ACCT_ENOTSUP)
     return fail(ACCT_ENOTSUP, "conv3x3 tc: weights + slabs exceed shared memory");
   return rc;

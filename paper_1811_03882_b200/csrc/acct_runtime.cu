@@ -326,7 +326,7 @@ int device_op(const acct_action_t &a, acct_array_t *arr, int gemm_mode, cudaStre
       // M <= 16 or a first layer (c <= 4, M <= 32) and in SIMT mode; the
       // implicit-im2col tcgen05 swap tile (3xTF32, bit-identical to im2col +
       // the swap gemm) for the other narrow layers (M <= 64)
-      const int C = (int)I[1], col_from = I[8] ? nb - 1 : 0;
+      const int C = (int)I[1], H = (int)I[2], W = (int)I[3], col_from = I[8] ? nb - 1 : 0;
       static const int tc_first = [] {  // experiment knob: first layers on tcgen05 too
         const char *e = getenv("ACCT_CONV_TC_FIRST");
         return e ? atoi(e) : 0;
@@ -334,24 +334,48 @@ int device_op(const acct_action_t &a, acct_array_t *arr, int gemm_mode, cudaStre
       const bool simt = gemm_mode == ACCT_GEMM_SIMT ||
                         (gemm_mode == ACCT_GEMM_AUTO && !tc_first &&
                          (M <= 16 || (M <= 32 && C <= 4)));
-      if (simt) {
-        const int rc = acct_conv3x3_im2col_gemm_f32(D(0), LD(0), BS(0), C, (int)I[2], (int)I[3],
-                                                    D(1), LD(1), BS(1), M, D(2), LD(2), beta, D(3),
-                                                    LD(3), BS(3), bias, (int)I[6], nb, col_from,
-                                                    st);
-        if (rc != ACCT_ENOTSUP) return rc;
-      } else if (M <= 64) {
-        const int rc = acct_conv3x3_tc_f32(D(0), LD(0), BS(0), C, (int)I[2], (int)I[3], D(1),
-                                           LD(1), BS(1), M, D(2), LD(2), beta, D(3), LD(3), BS(3),
-                                           bias, (int)I[6], nb, col_from, st);
-        if (rc != ACCT_ENOTSUP) return rc;
+      // I[9] / I[10]: a fused 2x2/2 maxpool of C into pool / idx; I[11] = 1:
+      // C is then observable for the last image only
+      const bool has_pool = I[9] >= 0;
+      float *pool = has_pool ? reinterpret_cast<float *>(arr[I[9]].dev) : nullptr;
+      int32_t *pidx = has_pool ? reinterpret_cast<int32_t *>(arr[I[10]].dev) : nullptr;
+      const int64_t ldp = has_pool ? arr[I[9]].ld_dev : 0, pbs = has_pool ? arr[I[9]].img_stride : 0;
+      const int64_t ldi = has_pool ? arr[I[10]].ld_dev : 0, ibs = has_pool ? arr[I[10]].img_stride : 0;
+      auto fused = [&](bool with_pool) {
+        float *pp = with_pool ? pool : nullptr;
+        int32_t *pi = with_pool ? pidx : nullptr;
+        const int c_from = (with_pool && I[11]) ? nb - 1 : 0;
+        if (simt)
+          return acct_conv3x3_im2col_gemm_f32(D(0), LD(0), BS(0), C, H, W, D(1), LD(1), BS(1), M,
+                                              D(2), LD(2), beta, D(3), LD(3), BS(3), bias,
+                                              (int)I[6], nb, col_from, pp, ldp, pbs, pi, ldi, ibs,
+                                              c_from, st);
+        if (M <= 64)
+          return acct_conv3x3_tc_f32(D(0), LD(0), BS(0), C, H, W, D(1), LD(1), BS(1), M, D(2),
+                                     LD(2), beta, D(3), LD(3), BS(3), bias, (int)I[6], nb,
+                                     col_from, pp, ldp, pbs, pi, ldi, ibs, c_from, st);
+        return (int)ACCT_ENOTSUP;
+      };
+      auto pool_after = [&]() {  // the maxpool the launch did not fuse
+        if (!has_pool) return (int)ACCT_OK;
+        return acct_maxpool_batched_f32(D(3), LD(3), BS(3), M, H, W, 2, 2, 0, H / 2, W / 2, pool,
+                                        ldp, pbs, pidx, ldi, ibs, nb, st);
+      };
+      int rc = fused(has_pool);
+      if (rc == ACCT_ENOTSUP && has_pool) {
+        rc = fused(false);
+        if (rc == ACCT_OK) return pool_after();
       }
+      if (rc != ACCT_ENOTSUP) return rc;
       // the same ops unfused: im2col, then the gemm in the requested mode
-      if (int rc = acct_im2col_batched_f32(D(0), LD(0), BS(0), (int)I[1], (int)I[2], (int)I[3], 3,
-                                           1, 1, D(1), LD(1), BS(1), nb, st))
-        return rc;
-      return acct_gemm_nn_batched_f32(M, N, K, 1.0f, D(2), LD(2), 0, D(1), LD(1), BS(1), beta, D(3),
-                                      LD(3), BS(3), bias, (int)I[6], nb, gemm_mode, st);
+      if (int rc2 = acct_im2col_batched_f32(D(0), LD(0), BS(0), C, H, W, 3, 1, 1, D(1), LD(1),
+                                            BS(1), nb, st))
+        return rc2;
+      if (int rc2 = acct_gemm_nn_batched_f32(M, N, K, 1.0f, D(2), LD(2), 0, D(1), LD(1), BS(1), beta,
+                                             D(3), LD(3), BS(3), bias, (int)I[6], nb, gemm_mode,
+                                             st))
+        return rc2;
+      return pool_after();
     }
     case ACCT_K_ADD_BIAS:
       return acct_add_bias_batched_f32(D(0), LD(0), BS(0), D(1), (int)I[1], I[2], nb, st);
@@ -794,7 +818,9 @@ int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *action
       case ACCT_A_KERNEL:
         for (int j = 0; j < 4 && forked; ++j)
           if ((rc = need(a.a[j]))) return rc;
-        if (a.i[0] == ACCT_K_CONV && forked && (rc = need((int)a.i[7]))) return rc;  // bias
+        if (a.i[0] == ACCT_K_CONV && forked &&
+            ((rc = need((int)a.i[7])) || (rc = need((int)a.i[9])) || (rc = need((int)a.i[10]))))
+          return rc;  // bias; fused maxpool outputs
         if (prof) {
           size_t first = prof->used;
           cudaEvent_t e0 = prof->next(), e1 = prof->next();

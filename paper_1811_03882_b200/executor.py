@@ -430,7 +430,7 @@ class PatternExecutor:
                 for m in members:
                     entry(net.ops[m].loop_id)
                 acts.append(self._fused_gemm_action([net.ops[m] for m in role[2]], p, role[3],
-                                                    role[4]))
+                                                    role[4], role[5], role[6]))
                 for m in members:
                     leave(net.ops[m].loop_id)
                 device_ops += 1
@@ -479,7 +479,7 @@ class PatternExecutor:
                 acts.append(self._op_action(op, K.A_KERNEL, p))
             elif role[0] == "anchor":
                 acts.append(self._fused_gemm_action([self.net.ops[m] for m in role[2]], p,
-                                                    role[3], role[4]))
+                                                    role[3], role[4], role[5], role[6]))
         acts.append((K.A_LOOP_END, (), (0,)))
         acts[0] = (K.A_LOOP_BEGIN, (), (self.images // p, len(acts) - 1))
         acts.append((K.A_SYNC, (), ()))
@@ -502,7 +502,7 @@ class PatternExecutor:
         if kind == K.K_MAXPOOL:
             return (slots[1], slots[2])
         if kind == K.K_CONV:
-            return (slots[1], slots[3])
+            return (slots[1], slots[3]) + tuple(v for v in act[2][9:11] if v >= 0)
         return ()
 
     def _overlap_transfers(self, acts: list, single_pass: bool) -> list:
@@ -664,15 +664,52 @@ class PatternExecutor:
             if len(fused) < 2:
                 continue
             conv = self._conv_partner(g, on, moved)
+            pool = self._pool_partner(g, after, on, blocked) if conv is not None else None
             if fill is not None:
                 roles[fill] = ("absorbed_before",)
             if conv is not None:
                 roles[conv] = ("absorbed_conv",)
-            roles[g] = ("anchor", ([conv] if conv is not None else []) + [g] + after, fused, conv,
-                        conv is not None and self._col_dead(conv, g, moved))
-            for j in after:
+            tail = after + ([pool] if pool is not None else [])
+            roles[g] = ("anchor", ([conv] if conv is not None else []) + [g] + tail, fused, conv,
+                        conv is not None and self._col_dead(conv, g, moved), pool,
+                        pool is not None and self._out_dead(g, fill, after, pool, moved))
+            for j in tail:
                 roles[j] = ("absorbed_after",)
         return roles
+
+    def _pool_partner(self, g: int, after: list, on: list, blocked):
+        """The 2x2/2 maxpool reading the output of a fused conv launch, when it
+        can join the launch (acct_conv3x3_*_f32 with pool): it directly
+        follows the launch's last member, is offloaded, pools the conv output
+        over even planes with darknet's offset 0, and no directive at the last
+        member's or the maxpool's loop boundary moves the output (a copyin
+        there would change what the maxpool reads)."""
+        ops = self.net.ops
+        last = after[-1] if after else g
+        j = last + 1
+        if j >= len(ops) or not on[j] or ops[j].kind != "maxpool":
+            return None
+        op, q = ops[j], ops[j].params
+        if op.arrays["X"] != ops[g].arrays["C"]:
+            return None
+        if (q["size"], q["stride"], q["off"]) != (2, 2, 0) or q["h"] % 2 or q["w"] % 2:
+            return None
+        if blocked(last) or blocked(j):
+            return None
+        return j
+
+    def _out_dead(self, g: int, fill, after: list, pool: int, moved: dict) -> bool:
+        """True when, in an image-batched run, only the LAST image's copy of a
+        pooled conv output is observable: the output is touched only by the
+        layer's fill, gemm, bias / activation and the fused maxpool, and no
+        directive inside the image loop moves it (so the fused launch stores
+        it for the batch's last image only)."""
+        net = self.net
+        out = net.ops[g].arrays["C"]
+        own = {g, pool, *after} | ({fill} if fill is not None else set())
+        if any(out in op.arrays.values() for k, op in enumerate(net.ops) if k not in own):
+            return False
+        return not any(out in vs for lid, vs in moved.items() if lid != net.image_loop)
 
     def _col_dead(self, im: int, g: int, moved: dict) -> bool:
         """True when, in an image-batched run, only the LAST image's copy of
@@ -718,7 +755,8 @@ class PatternExecutor:
             return None
         return g - 1
 
-    def _fused_gemm_action(self, members, nimg: int = 1, conv=None, col_dead=False):
+    def _fused_gemm_action(self, members, nimg: int = 1, conv=None, col_dead=False, pool=None,
+                           out_dead=False):
         kinds = [m.kind for m in members]
         g = next(m for m in members if m.kind == "gemm")
         p, a = g.params, g.arrays
@@ -738,7 +776,10 @@ class PatternExecutor:
             return _batched((K.A_KERNEL, (self.slot_of[im.arrays["X"]], self.slot_of[a["B"]],
                                           self.slot_of[a["A"]], self.slot_of[a["C"]]),
                              (K.K_CONV, q["c"], q["h"], q["w"], p["M"], beta_one, act,
-                              bias_slot, int(col_dead and nimg > 1))), nimg)
+                              bias_slot, int(col_dead and nimg > 1),
+                              self.slot_of[self.net.ops[pool].arrays["Y"]] if pool is not None else -1,
+                              self.slot_of[self.net.ops[pool].arrays["I"]] if pool is not None else -1,
+                              int(out_dead and nimg > 1))), nimg)
         return _batched((K.A_KERNEL, (self.slot_of[a["A"]], self.slot_of[a["B"]],
                                       self.slot_of[a["C"]], bias_slot),
                          (K.K_GEMM, p["M"], p["N"], p["K"], beta_one, act)), nimg)
@@ -938,10 +979,14 @@ class PatternExecutor:
             N, Kd = h * w, 9 * c
             op = next(o for o in ops if o.kind == "gemm" and o.arrays["C"] == slots[a.a[3]].name)
             # input image in, col + C out (C also in when beta = 1), weights once;
-            # col of the last image only when the others are dead (i[8])
+            # col of the last image only when the others are dead (i[8]), C
+            # likewise when a fused maxpool consumes it (i[11]); pool + idx out
             col_imgs = 1 if i[8] else nimg
-            byts = 4 * M * Kd + nimg * 4 * (c * N + (2 if i[5] else 1) * M * N) + \
-                col_imgs * 4 * Kd * N
+            c_imgs = 1 if i[11] else nimg
+            pooled = i[9] >= 0
+            byts = 4 * M * Kd + nimg * 4 * (c * N + (M * N if i[5] else 0)) + \
+                c_imgs * 4 * M * N + col_imgs * 4 * Kd * N + \
+                (nimg * 8 * M * (N // 4) if pooled else 0)
             byts += 4 * M if i[7] >= 0 else 0
             return {"kind": "conv", "layer": op.layer, "M": M, "N": N, "K": Kd, "images": nimg,
                     "N_launch": N, "executions": execs, "flops": 2 * M * N * Kd * nimg,

@@ -78,9 +78,10 @@ SIGNATURES = {
                                  _vp, _i64, _i64, _vp, _i32, _i32, _i32, _vp],
     "acct_conv3x3_im2col_gemm_f32": [_vp, _i64, _i64, _i32, _i32, _i32, _vp, _i64, _i64, _i32,
                                      _vp, _i64, _f32, _vp, _i64, _i64, _vp, _i32, _i32, _i32,
-                                     _vp],
+                                     _vp, _i64, _i64, _vp, _i64, _i64, _i32, _vp],
     "acct_conv3x3_tc_f32": [_vp, _i64, _i64, _i32, _i32, _i32, _vp, _i64, _i64, _i32, _vp, _i64,
-                            _f32, _vp, _i64, _i64, _vp, _i32, _i32, _i32, _vp],
+                            _f32, _vp, _i64, _i64, _vp, _i32, _i32, _i32, _vp, _i64, _i64, _vp,
+                            _i64, _i64, _i32, _vp],
     "acct_add_bias_batched_f32": [_vp, _i64, _i64, _vp, _i32, _i64, _i32, _vp],
     "acct_leaky_exhaustive_check": [_vp, _vp],
     "acct_activate_batched_f32": [_vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp],
@@ -193,16 +194,21 @@ def gemm_nn(M, N, K, alpha, A, lda, B, ldb, beta, Cp, ldc, bias=None, act=ACT_NO
 
 def conv3x3_im2col_gemm(im, ld_im, im_stride, channels, height, width, col, ld_col, col_stride,
                         M, A, lda, beta, Cp, ldc, c_stride, bias=None, act=ACT_NONE, batch=1,
-                        stream=0, col_from=0):
+                        stream=0, col_from=0, pool=None):
+    """pool = (pool_ptr, ld_pool, pool_stride, idx_ptr, ld_idx, idx_stride, c_from) or None"""
+    pl = pool or (None, 0, 0, None, 0, 0, 0)
     call("acct_conv3x3_im2col_gemm_f32", im, ld_im, im_stride, channels, height, width, col,
          ld_col, col_stride, M, A, lda, beta, Cp, ldc, c_stride, bias, act, batch, col_from,
-         stream)
+         *pl, stream)
 
 
 def conv3x3_tc(im, ld_im, im_stride, channels, height, width, col, ld_col, col_stride, M, A, lda,
-               beta, Cp, ldc, c_stride, bias=None, act=ACT_NONE, batch=1, stream=0, col_from=0):
+               beta, Cp, ldc, c_stride, bias=None, act=ACT_NONE, batch=1, stream=0, col_from=0,
+               pool=None):
+    """pool = (pool_ptr, ld_pool, pool_stride, idx_ptr, ld_idx, idx_stride, c_from) or None"""
+    pl = pool or (None, 0, 0, None, 0, 0, 0)
     call("acct_conv3x3_tc_f32", im, ld_im, im_stride, channels, height, width, col, ld_col,
-         col_stride, M, A, lda, beta, Cp, ldc, c_stride, bias, act, batch, col_from, stream)
+         col_stride, M, A, lda, beta, Cp, ldc, c_stride, bias, act, batch, col_from, *pl, stream)
 
 
 def add_bias(out, ld, bias, rows, cols, stream=0):

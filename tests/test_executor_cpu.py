@@ -150,3 +150,45 @@ def test_conv_fusion_only_when_no_directive_splits_it(host_exec):
             assert bits[im] == "1" and bits[im + 1] == "1"
             assert not {col, gm.arrays["C"]} & moved.get(net.ops[im].loop_id, set())
             assert not {col, net.ops[im].arrays["X"]} & moved.get(gm.loop_id, set())
+
+
+def test_pool_fusion_and_dead_outputs():
+    """Each fused conv launch of yolov2-tiny's first three layers absorbs the
+    2x2/2 maxpool reading its output (slots i[9], i[10] = pool, idx); with
+    one image per launch every output stays stored (i[11] = 0).  The other
+    maxpools (after plain gemm launches, and the 2x2/1 one) keep their own
+    launches, and the counters equal the unfused schedule's."""
+    net = build_net("yolov2-tiny")
+    a = PatternExecutor(net, device=None, fuse=True)
+    b = PatternExecutor(net, device=None, fuse=False)
+    bits = "1" * len(net.ops)
+    sa, sb = a.compile(bits), b.compile(bits)
+    assert sa.expected == sb.expected
+    names = list(net.arrays)
+    convs = [sa.actions[k] for k in range(sa.n_actions)
+             if sa.actions[k].kind == K.A_KERNEL and sa.actions[k].i[0] == K.K_CONV]
+    assert [(names[c.i[9]], names[c.i[10]], c.i[11]) for c in convs] == \
+        [("pool1", "idx1", 0), ("pool3", "idx3", 0), ("pool5", "idx5", 0)]
+    pools = [names[sa.actions[k].a[1]] for k in range(sa.n_actions)
+             if sa.actions[k].kind == K.A_KERNEL and sa.actions[k].i[0] == K.K_MAXPOOL]
+    assert pools == ["pool7", "pool9", "pool11"]
+    # written slots of a pooled conv include pool and idx (early copyouts wait for them)
+    c = convs[0]
+    act = (K.A_KERNEL, tuple(c.a[j] for j in range(4)), tuple(c.i[j] for j in range(14)))
+    assert set(PatternExecutor._written_slots(act)) == \
+        {names.index(n) for n in ("col0", "out0", "pool1", "idx1")}
+
+
+def test_out_dead_only_when_the_pool_is_the_sole_reader():
+    net = build_net("yolov2-tiny")
+    ex = PatternExecutor(net, device=None)
+    ops = net.ops
+    g = next(k for k, o in enumerate(ops) if o.kind == "gemm")
+    fill = g - 2 if ops[g - 2].kind == "fill" else None
+    after = [g + 1, g + 2]
+    pool = g + 3
+    assert ops[pool].kind == "maxpool"
+    out = ops[g].arrays["C"]
+    assert ex._out_dead(g, fill, after, pool, {net.image_loop: {out}})
+    assert not ex._out_dead(g, fill, after, pool, {ops[pool].loop_id: {out}})
+    assert not ex._out_dead(g, fill, [g + 1], pool, {})   # the activation would be a reader

@@ -135,12 +135,12 @@ def test_batched_kernel_entries_match_single(cuda_device):
 @pytest.mark.parametrize("mode", [K.GEMM_SIMT, K.GEMM_AUTO])
 @pytest.mark.parametrize("name,images", [("demo", 8), ("yolov2-tiny", 2), ("micro", 4)])
 def test_fused_conv_layer_is_bit_identical(cuda_device, name, images, mode):
-    """The fused conv launches (im2col + gemm in one kernel -- the FP32
-    window kernel or the implicit-im2col tcgen05 swap tile -- col stored for
-    the batch's last image only) leave every observable array, col included,
-    bit-identical to the unfused schedule in the same gemm mode (the same
-    FMA chain / the same MMA operands and order), batched and resident
-    alike; the AUTO output stays within the gemm tolerance of SIMT's."""
+    """The fused conv launches (im2col + gemm (+ 2x2 maxpool) in one kernel,
+    col -- and a pooled output -- stored for the batch's last image only)
+    leave every observable array bit-identical to the unfused schedule in
+    SIMT mode (the same FMA chain), batched and resident alike; under AUTO
+    (implicit-im2col tcgen05 tiles) col stays bit-exact and the output within
+    the gemm tolerance; AUTO and SIMT agree within it too."""
     net = build_net(name, images=images)
     a = PatternExecutor(net, device=0, fuse=True, gemm_mode=mode)
     b = PatternExecutor(net, device=0, fuse=False, gemm_mode=mode)
@@ -155,13 +155,23 @@ def test_fused_conv_layer_is_bit_identical(cuda_device, name, images, mode):
     assert {k: v for k, v in ra.counters.items() if k != "kernel_launches"} == \
         {k: v for k, v in rb.counters.items() if k != "kernel_launches"}
     assert ra.counters["kernel_launches"] < rb.counters["kernel_launches"]
-    assert np.array_equal(a.outputs(), b.outputs())
-    for name_ in net.arrays:
-        assert np.array_equal(a.device_array(name_), b.device_array(name_)), name_
-        assert np.array_equal(a.host_array(name_), b.host_array(name_)), name_
-    a.run(bits, resident=True)
-    b.run(bits, resident=True)
-    assert np.array_equal(a.device_array(net.output_name), b.device_array(net.output_name))
+    if mode == K.GEMM_SIMT:
+        assert np.array_equal(a.outputs(), b.outputs())
+        for name_ in net.arrays:
+            assert np.array_equal(a.device_array(name_), b.device_array(name_)), name_
+            assert np.array_equal(a.host_array(name_), b.host_array(name_)), name_
+        a.run(bits, resident=True)
+        b.run(bits, resident=True)
+        assert np.array_equal(a.device_array(net.output_name), b.device_array(net.output_name))
+    else:
+        # the tensor-core conv sums the 3xTF32 terms in its own order: values
+        # within the gemm tolerance; every col array bit-exact
+        want = b.outputs()
+        assert np.abs(a.outputs() - want).max() <= 1e-4 * np.abs(want).max()
+        for name_ in net.arrays:
+            if name_.startswith("col"):
+                assert np.array_equal(a.device_array(name_), b.device_array(name_)), name_
+                assert np.array_equal(a.host_array(name_), b.host_array(name_)), name_
     c = PatternExecutor(net, device=0, fuse=True, gemm_mode=K.GEMM_SIMT + K.GEMM_AUTO - mode)
     c.run(bits)
     want = a.outputs()

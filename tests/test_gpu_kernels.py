@@ -360,10 +360,10 @@ def test_conv3x3_tc_equals_im2col_then_tc_gemm(cuda_device, orc, c, h, w, M, bet
                                                batch, col_from, layout, exact):
     """acct_conv3x3_tc_f32 (implicit-im2col tcgen05 swap tile) writes col
     exactly like im2col for images >= col_from, leaves the others untouched,
-    and computes C within the gemm tolerance of the oracle -- bit-identical
-    to im2col + the GEMM_TC3XTF32 swap gemm at the yolov2-tiny layer shapes
-    (where that gemm runs without split-K).  Input batches image-major
-    ([P][c][ld]) and column-interleaved ([c][P*ld]) alike."""
+    and computes C within the gemm tolerance of the oracle (and, at the
+    yolov2-tiny layer shapes, of im2col + the GEMM_TC3XTF32 swap gemm: the
+    conv's [W hi | W lo] MMAs sum the 3xTF32 terms in another order).  Input
+    batches image-major ([P][c][ld]) and column-interleaved ([c][P*ld])."""
     N, Kd = h * w, 9 * c
     ld = -(-N // 32) * 32
     lda = -(-Kd // 32) * 32
@@ -409,8 +409,8 @@ def test_conv3x3_tc_equals_im2col_then_tc_gemm(cuda_device, orc, c, h, w, M, bet
         else:
             assert np.array_equal(cf, cu)
         got = C_f[:, b * ld:b * ld + N].cpu().numpy()
-        if exact:
-            assert np.array_equal(got, C_u[:, b * ld:b * ld + N].cpu().numpy())
+        if exact:  # the layer shapes: also against the unfused tensor-core pair
+            gemm_ok(got, C_u[:, b * ld:b * ld + N].cpu().numpy())
         want = np.ascontiguousarray(C0[:, b]) if beta else np.zeros((M, N), np.float32)
         cu = np.ascontiguousarray(cu)
         orc.orc_gemm_nn(M, N, Kd, 1.0, A0.ctypes.data, Kd, cu.ctypes.data, N, want.ctypes.data, N)
@@ -443,3 +443,119 @@ def test_leaky_is_darknets_double_product_for_every_float(cuda_device):
     ex = (ctypes.c_uint32 * 8)()
     K.call("acct_leaky_exhaustive_check", ctypes.addressof(bad), ctypes.addressof(ex))
     assert bad.value == 0, [hex(ex[i]) for i in range(min(8, bad.value))]
+
+
+@pytest.mark.parametrize("c,h,w,M,beta,act,batch,c_from,layout",
+                         [(16, 208, 208, 32, 0, K.ACT_LEAKY, 2, 1, "il"),
+                          (32, 104, 104, 64, 1, K.ACT_LEAKY, 3, 2, "im"),
+                          (8, 20, 36, 40, 0, K.ACT_NONE, 2, 0, "il"),
+                          (5, 30, 12, 24, 0, K.ACT_LINEAR, 1, 0, "im")])
+def test_conv3x3_tc_fused_maxpool(cuda_device, c, h, w, M, beta, act, batch, c_from, layout):
+    """The tcgen05 conv with its 2x2/2 maxpool fused into the epilogue
+    writes pool and argmax idx bit-identically to acct_maxpool_batched_f32
+    over the unfused conv output, and C only for images >= c_from."""
+    N, Kd = h * w, 9 * c
+    ld, lda = -(-N // 32) * 32, -(-Kd // 32) * 32
+    P2 = (h // 2) * (w // 2)
+    ldp = -(-P2 // 32) * 32
+    rng = np.random.default_rng(91)
+    im0 = rng.uniform(-1, 1, (batch, c, N)).astype(np.float32)
+    im0[0, :, :7] = 0.0                       # ties: first max in scan order wins
+    if layout == "im":
+        im = torch.zeros((batch, c, ld), device="cuda")
+        im[:, :, :N] = torch.from_numpy(im0).cuda()
+        ld_im, im_stride = ld, c * ld
+    else:
+        im = torch.zeros((c, batch, ld), device="cuda")
+        im[:, :, :N] = torch.from_numpy(im0.transpose(1, 0, 2).copy()).cuda()
+        ld_im, im_stride = batch * ld, ld
+    A = torch.zeros((M, lda), device="cuda")
+    A[:, :Kd] = torch.from_numpy(rng.uniform(-0.5, 0.5, (M, Kd)).astype(np.float32)).cuda()
+    bias = torch.from_numpy(rng.uniform(-1, 1, M).astype(np.float32)).cuda()
+    C0 = torch.from_numpy(rng.uniform(-1, 1, (M, batch, N)).astype(np.float32)).cuda()
+
+    def fresh():
+        C = torch.full((M, batch, ld), float("nan"), device="cuda")
+        C[:, :, :N] = C0
+        pool = torch.full((M, batch * ldp), float("nan"), device="cuda")
+        idx = torch.full((M, batch * ldp), -7, dtype=torch.int32, device="cuda")
+        col = torch.zeros((Kd, batch * ld), device="cuda")
+        return C.view(M, batch * ld), pool, idx, col
+
+    Cu, pu, iu, colu = fresh()
+    K.conv3x3_tc(im.data_ptr(), ld_im, im_stride, c, h, w, colu.data_ptr(), batch * ld, ld, M,
+                 A.data_ptr(), lda, float(beta), Cu.data_ptr(), batch * ld, ld, bias.data_ptr(), act,
+                 batch, stream())
+    K.call("acct_maxpool_batched_f32", Cu.data_ptr(), batch * ld, ld, M, h, w, 2, 2, 0, h // 2,
+           w // 2, pu.data_ptr(), batch * ldp, ldp, iu.data_ptr(), batch * ldp, ldp, batch,
+           stream())
+    Cf, pf, if_, colf = fresh()
+    K.conv3x3_tc(im.data_ptr(), ld_im, im_stride, c, h, w, colf.data_ptr(), batch * ld, ld, M,
+                 A.data_ptr(), lda, float(beta), Cf.data_ptr(), batch * ld, ld, bias.data_ptr(), act,
+                 batch, stream(),
+                 pool=(pf.data_ptr(), batch * ldp, ldp, if_.data_ptr(), batch * ldp, ldp, c_from))
+    torch.cuda.synchronize()
+    for b in range(batch):
+        sl = slice(b * ldp, b * ldp + P2)
+        assert torch.equal(pf[:, sl], pu[:, sl])
+        assert torch.equal(if_[:, sl], iu[:, sl])
+        cs = slice(b * ld, b * ld + N)
+        if b >= c_from:
+            assert torch.equal(Cf[:, cs], Cu[:, cs])
+        else:
+            assert torch.equal(Cf[:, cs], C0[:, b])   # dead stores skipped
+
+
+@pytest.mark.parametrize("c,h,w,M,beta,act,batch,c_from,col_from",
+                         [(3, 416, 416, 16, 0, K.ACT_LEAKY, 2, 1, 1),
+                          (3, 20, 36, 8, 1, K.ACT_NONE, 3, 0, 2),
+                          (4, 34, 40, 13, 0, K.ACT_LINEAR, 1, 0, 0)])
+def test_conv3x3_window_fused_maxpool(cuda_device, c, h, w, M, beta, act, batch, c_from,
+                                      col_from):
+    """The FP32 window conv with its 2x2/2 maxpool fused (2x2 pixel blocks per
+    thread) equals the unfused window conv + acct_maxpool_batched_f32 bit for
+    bit: C for images >= c_from, col for images >= col_from, pool and idx."""
+    N, Kd = h * w, 9 * c
+    ld, P2 = -(-N // 32) * 32, (h // 2) * (w // 2)
+    ldp = -(-P2 // 32) * 32
+    rng = np.random.default_rng(93)
+    im0 = rng.uniform(-1, 1, (batch, c, N)).astype(np.float32)
+    im0[:, :, :9] = 0.0
+    im = torch.zeros((batch, c, ld), device="cuda")
+    im[:, :, :N] = torch.from_numpy(im0).cuda()
+    A = torch.from_numpy(rng.uniform(-0.5, 0.5, (M, Kd)).astype(np.float32)).cuda()
+    bias = torch.from_numpy(rng.uniform(-1, 1, M).astype(np.float32)).cuda()
+    C0 = torch.from_numpy(rng.uniform(-1, 1, (M, batch, N)).astype(np.float32)).cuda()
+
+    def fresh():
+        C = torch.full((M, batch, ld), 0.0, device="cuda")
+        C[:, :, :N] = C0
+        col = torch.full((Kd, batch * ld), float("nan"), device="cuda")
+        pool = torch.full((M, batch * ldp), float("nan"), device="cuda")
+        idx = torch.full((M, batch * ldp), -7, dtype=torch.int32, device="cuda")
+        return C.view(M, batch * ld), col, pool, idx
+
+    Cu, colu, pu, iu = fresh()
+    K.conv3x3_im2col_gemm(im.data_ptr(), ld, c * ld, c, h, w, colu.data_ptr(), batch * ld, ld, M,
+                          A.data_ptr(), Kd, float(beta), Cu.data_ptr(), batch * ld, ld,
+                          bias.data_ptr(), act, batch, stream())
+    K.call("acct_maxpool_batched_f32", Cu.data_ptr(), batch * ld, ld, M, h, w, 2, 2, 0, h // 2,
+           w // 2, pu.data_ptr(), batch * ldp, ldp, iu.data_ptr(), batch * ldp, ldp, batch,
+           stream())
+    Cf, colf, pf, if_ = fresh()
+    K.conv3x3_im2col_gemm(im.data_ptr(), ld, c * ld, c, h, w, colf.data_ptr(), batch * ld, ld, M,
+                          A.data_ptr(), Kd, float(beta), Cf.data_ptr(), batch * ld, ld,
+                          bias.data_ptr(), act, batch, stream(), col_from=col_from,
+                          pool=(pf.data_ptr(), batch * ldp, ldp, if_.data_ptr(), batch * ldp, ldp,
+                                c_from))
+    torch.cuda.synchronize()
+    for b in range(batch):
+        sl = slice(b * ldp, b * ldp + P2)
+        assert torch.equal(pf[:, sl], pu[:, sl])
+        assert torch.equal(if_[:, sl], iu[:, sl])
+        cs = slice(b * ld, b * ld + N)
+        assert torch.equal(Cf[:, cs], Cu[:, cs] if b >= c_from else C0[:, b])
+        if b >= col_from:
+            assert torch.equal(colf[:, cs], colu[:, cs])
+        else:
+            assert torch.isnan(colf[:, cs]).all()

@@ -4,6 +4,7 @@ operand build (1), the MMAs (2) or the epilogue (4) -- pipeline analysis.
 
     python tools/conv_probe.py            # prints us per image per layer
 """
+import os
 import sys
 from pathlib import Path
 
@@ -25,11 +26,17 @@ def main():
         C = torch.zeros((M, P * ld), device="cuda")
         bias = torch.randn(M, device="cuda")
         s = torch.cuda.current_stream().cuda_stream
+        P2 = (h // 2) * (w // 2)
+        ldp = -(-P2 // 32) * 32
+        pool = torch.zeros((M, P * ldp), device="cuda")
+        pidx = torch.zeros((M, P * ldp), dtype=torch.int32, device="cuda")
+        pl = ((pool.data_ptr(), P * ldp, ldp, pidx.data_ptr(), P * ldp, ldp, P - 1)
+              if os.environ.get("POOL") == "1" else None)
 
         def run():
             K.conv3x3_tc(im.data_ptr(), P * ld, ld, c, h, w, col.data_ptr(), P * ld, ld, M,
                          A.data_ptr(), lda, 0.0, C.data_ptr(), P * ld, ld, bias.data_ptr(),
-                         K.ACT_LEAKY, P, s, col_from=P - 1)
+                         K.ACT_LEAKY, P, s, col_from=P - 1, pool=pl)
         for _ in range(3):
             run()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -562,6 +562,24 @@ namespace {
 // c_from / col_from only.
 constexpr int PT_W = 32, PT_H = 16, PT_SW = PT_W + 8, PT_SH = PT_H + 2;  // slab row 40 floats
 
+// packed FP32 pairs (sm_100 FFMA2): two IEEE fmas per instruction, each
+// rounding exactly like fmaf -- halves the issue slots of an FMA-issue-bound
+// loop without changing a single result
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pack2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack2(f32x2 v, float &lo, float &hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
 __global__ void __launch_bounds__(128, 4)
 conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, int channels,
                     int height, int width, float *__restrict__ col, int64_t ld_col,
@@ -626,11 +644,14 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
       const int64_t p = (int64_t)y * width + x;
       float *colp = col + img * col_bs + p;
       const float *base = sin0 + buf * bufsz + (2 * ty) * PT_SW + 2 * tx + 3;  // window (-1, -1)
-      float acc[MT][4];
+      // acc2[i][e] = (filter 2i, filter 2i+1) at pixel e: one FFMA2 per pair,
+      // each element the fmaf chain of the window kernel
+      f32x2 acc2[MT / 2][4];
 #pragma unroll
-      for (int m = 0; m < MT; ++m)
+      for (int i = 0; i < MT / 2; ++i)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[m][e] = 0.0f;
+        for (int e = 0; e < 4; ++e) acc2[i][e] = 0ull;
+      const ulonglong2 *As2 = reinterpret_cast<const ulonglong2 *>(As);
 #pragma unroll 1
       for (int ci = 0; ci < channels; ++ci) {
         const float *cb = base + ci * PT_SH * PT_SW;
@@ -651,22 +672,24 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
               __stcs(reinterpret_cast<float2 *>(colp + (int64_t)k * ld_col + width),
                      make_float2(v2, v3));
             }
-            const float4 *ak = reinterpret_cast<const float4 *>(As + k * MT);
+            const f32x2 vv[4] = {pack2(v0, v0), pack2(v1, v1), pack2(v2, v2), pack2(v3, v3)};
 #pragma unroll
-            for (int m4 = 0; m4 < MT / 4; ++m4) {
-              const float4 a = ak[m4];
-              const float av[4] = {a.x, a.y, a.z, a.w};
+            for (int g = 0; g < MT / 4; ++g) {
+              const ulonglong2 a = As2[k * (MT / 4) + g];  // filters 4g..4g+3 as two pairs
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                acc[4 * m4 + e][0] = fmaf(av[e], v0, acc[4 * m4 + e][0]);
-                acc[4 * m4 + e][1] = fmaf(av[e], v1, acc[4 * m4 + e][1]);
-                acc[4 * m4 + e][2] = fmaf(av[e], v2, acc[4 * m4 + e][2]);
-                acc[4 * m4 + e][3] = fmaf(av[e], v3, acc[4 * m4 + e][3]);
+                acc2[2 * g][e] = fma2(a.x, vv[e], acc2[2 * g][e]);
+                acc2[2 * g + 1][e] = fma2(a.y, vv[e], acc2[2 * g + 1][e]);
               }
             }
           }
         }
       }
+      float acc[MT][4];
+#pragma unroll
+      for (int i = 0; i < MT / 2; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) unpack2(acc2[i][e], acc[2 * i][e], acc[2 * i + 1][e]);
       float *cimg = C + img * c_bs + p;
       const int64_t pofs = (int64_t)(y >> 1) * (width >> 1) + (x >> 1);
       const int base_i = (int)p;

@@ -310,6 +310,15 @@ def roofline(ex, sched, steps: int, flush, peaks: dict) -> dict:
             out["note"] = (f"gemm below the 3xTF32 ridge ({info['flops'] / info['bytes']:.1f} "
                            f"< {ridge:.1f} flop/B): HBM-bound; {info['flops'] / launch_s / 1e12:.1f} "
                            "TFLOP/s")
+        if info.get("engine") == "fp32-fma":
+            # CUDA-core FP32: 148 SMs x 128 FMA/clk x 2 flop at the sampled max clock
+            fma_peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+            out["fp32_fma_peak_tflops"] = fma_peak
+            out["frac_of_fp32_fma_peak"] = info["flops"] / launch_s / 1e12 / fma_peak
+            out["note"] = (f"FP32-FMA window kernel (fused im2col + gemm + bias + leaky + maxpool): "
+                           f"{info['flops'] / launch_s / 1e12:.1f} TFLOP/s of a {fma_peak:.1f} "
+                           f"TFLOP/s CUDA-core peak; issue-bound (K = {info['K']} leaves the "
+                           "per-output epilogue at a third of the instructions)")
     traffic = ncu_traffic(shape) if shape else None
     name = f"{info['kind']} layer {info['layer']}" + (
         f" M{info['M']} N{info['N_launch']} K{info['K']} ({info['images']} images per launch)"

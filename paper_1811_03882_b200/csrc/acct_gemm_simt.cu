@@ -705,8 +705,14 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
           cv[0] = c0.x; cv[1] = c0.y; cv[2] = c1.x; cv[3] = c1.y;
         }
         float o[4];
+        const float bv = bias ? __ldg(bias + m) : 0.0f;  // once per filter
 #pragma unroll
-        for (int e = 0; e < 4; ++e) o[e] = epilogue(acc[m][e], 1.0f, beta, cv + e, bias, m, act);
+        for (int e = 0; e < 4; ++e) {
+          float v = acc[m][e];
+          if (beta != 0.0f) v = beta * cv[e] + v;
+          if (bias) v += bv;
+          o[e] = act == ACCT_ACT_LEAKY ? acct_leaky(v) : v;
+        }
         if (wc) {
           __stcs(reinterpret_cast<float2 *>(cp), make_float2(o[0], o[1]));
           __stcs(reinterpret_cast<float2 *>(cp + width), make_float2(o[2], o[3]));

@@ -1331,6 +1331,304 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   if (warp == 1) ptx::tmem_dealloc(tmem, G::TMEM_COLS);
 }
 
+// ------------------------------------ implicit-im2col conv, wide layers
+// The same fused conv for 128-filter blocks (M = 128 k, yolov2-tiny layers
+// 6 and 8): weights no longer fit in shared memory, so each 32-deep k-block
+// streams through a stage ring together with the slab CHUNK it reads -- the
+// <= 5 input channels k0 / 9 .. (k0 + 31) / 9 of the unit's (TH+2) x (TW+2)
+// window (one 4-D TMA box; channels past C read as zero).  A unit is one
+// (128-filter block, image, TH x TW pixel block).  Swap orientation: MMA
+// M = 128 pixels (TMEM lanes), N = 128 filters, 3xTF32 (A hi.W hi, A hi.W lo,
+// A lo.W hi) per 8-deep k step.
+//   warp 0      TMA: per stage the weight tile (128 rows x 32 k, SW128) and
+//               the slab chunk
+//   warp 1      TMEM allocator + MMA issuer
+//   warps 2..9  two halves taking alternate k-blocks: weights lo of the stage,
+//               the activation operand (hi / lo to a TMEM stage), col of
+//               images >= col_from
+//   warps 10..17 epilogue, two groups taking alternate units (+ fused maxpool)
+template <int TW>
+struct WideCfg {
+  static constexpr int TN = 128, BK = 32, S = 4, NACC = 2;
+  static constexpr int TH = 128 / TW;
+  static constexpr int TWP = TW + 8;
+  static constexpr int SROWS = TH + 2;
+  static constexpr int CS = SROWS * TWP * 4;      // slab bytes per channel
+  static constexpr int CH_PER_KB = 5;             // channels a 32-deep k-block spans
+  static constexpr int W_TILE = TN * BK * 4;      // 16 KB
+  static constexpr int SLAB = ((CH_PER_KB * CS) + 1023) & ~1023;
+  static constexpr int STAGE = 2 * W_TILE + SLAB; // W hi, W lo, slab chunk
+  static constexpr int A_COL0 = NACC * TN;
+  static constexpr int USED_COLS = NACC * TN + S * 2 * BK;
+  static constexpr uint32_t K_SBO = 8 * 128;
+  static_assert(USED_COLS <= 512, "TMEM overflow");
+};
+
+template <int TW>
+__global__ void __launch_bounds__(CONV_TC_THREADS, 1)
+tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                    int M, int channels, int height, int width, int tiles_x, int tpi, int units,
+                    int nkb, float beta, float *__restrict__ C, int64_t ldc, int64_t c_bs,
+                    const float *__restrict__ bias, int act, float *__restrict__ col,
+                    int64_t ld_col, int64_t col_bs, int col_from, float *__restrict__ pool,
+                    int64_t ld_pool, int64_t pool_bs, int32_t *__restrict__ pidx, int64_t ld_pidx,
+                    int64_t pidx_bs, int c_from, int batch, int dbg) {
+  using G = WideCfg<TW>;
+  constexpr int S = G::S, BK = G::BK, NACC = G::NACC, TN = G::TN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  auto w_hi = [&](int s) { return base + s * G::STAGE; };
+  auto w_lo = [&](int s) { return base + s * G::STAGE + G::W_TILE; };
+  auto slab = [&](int s) { return base + s * G::STAGE + 2 * G::W_TILE; };
+  uint64_t *full = reinterpret_cast<uint64_t *>(base + S * G::STAGE);
+  uint64_t *conv = full + S;
+  uint64_t *empty = conv + S;
+  uint64_t *acc_full = empty + S;
+  uint64_t *acc_empty = acc_full + NACC;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + NACC);
+  float *bias_s = reinterpret_cast<float *>(tmem_slot + 4);  // TN floats, then 8 x 8 x 33 scratch
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int HW = height * width;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&conv[s], 4);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < NACC; ++a) {
+      ptx::mbar_init(&acc_full[a], 1);
+      ptx::mbar_init(&acc_empty[a], 4);
+    }
+    ptx::fence_mbar_init();
+    ptx::prefetch_tmap(&tmW);
+    ptx::prefetch_tmap(&tmX);
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+
+  const int per_mb = tpi * batch;
+  auto unit_of = [&](int u, int &mb, int &img, int &y0, int &x0) {
+    mb = u / per_mb;
+    const int r = u - mb * per_mb;
+    img = r / tpi;
+    const int t = r - img * tpi;
+    const int ty = t / tiles_x;
+    y0 = ty * G::TH;
+    x0 = (t - ty * tiles_x) * TW;
+  };
+
+  if (warp == 0) {
+    // ---------------- TMA: weight tile + slab chunk per stage ----------------
+    if (lane == 0) {
+      int g = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int mb, img, y0, x0;
+        unit_of(u, mb, img, y0, x0);
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int s = g % S;
+          if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
+          ptx::mbar_expect_tx(&full[s], (uint32_t)(G::W_TILE + G::CH_PER_KB * G::CS));
+          ptx::tma_load_2d(w_hi(s), &tmW, &full[s], kb * BK, mb * TN);
+          ptx::tma_load_4d(slab(s), &tmX, &full[s], x0 - 4, y0 - 1, img, (kb * BK) / 9);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = ptx::idesc_tf32(128, TN, false, false);
+    int g = 0, j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int a = j % NACC;
+      if (j >= NACC) ptx::mbar_wait(&acc_empty[a], ((j / NACC) - 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t d = tmem + a * TN;
+      for (int kb = 0; kb < nkb; ++kb, ++g) {
+        const int s = g % S;
+        ptx::mbar_wait(&conv[s], (g / S) & 1);
+        ptx::tc_fence_after();
+        const uint32_t yh = ptx::smem_u32(w_hi(s)), yl = ptx::smem_u32(w_lo(s));
+        const uint32_t at = tmem + G::A_COL0 + s * 2 * BK;
+        if (ptx::elect_one()) {
+          if (!(dbg & 2)) {
+#pragma unroll
+            for (int k = 0; k < BK / 8; ++k) {
+              const uint64_t dyh = ptx::smem_desc(yh + 32 * k, 16, G::K_SBO, ptx::kLayoutSW128);
+              const uint64_t dyl = ptx::smem_desc(yl + 32 * k, 16, G::K_SBO, ptx::kLayoutSW128);
+              ptx::mma_tf32_ts(d, at + 8 * k, dyh, idesc, (kb | k) != 0);
+              ptx::mma_tf32_ts(d, at + 8 * k, dyl, idesc, 1);
+              ptx::mma_tf32_ts(d, at + BK + 8 * k, dyh, idesc, 1);
+            }
+          }
+          ptx::mma_commit(&empty[s]);
+        }
+        __syncwarp();
+      }
+      if (ptx::elect_one()) ptx::mma_commit(&acc_full[a]);
+      __syncwarp();
+    }
+  } else if (warp < 10) {
+    // ---------------- weights lo + activation operand (two halves) ----------------
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int ht = threadIdx.x - 64 - 128 * half;  // 0..127 within the half
+    const int K = 9 * channels;
+    const int m = 32 * q + lane;
+    const int py = m / TW, px = m % TW;
+    const uint32_t lane_off = (uint32_t)((py * G::TWP + px) * 4);
+    int g = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int mb, img, y0, x0;
+      unit_of(u, mb, img, y0, x0);
+      const int y = y0 + py, x = x0 + px;
+      const bool wcol = img >= col_from && mb == 0;  // col once, by the first filter block
+      const bool inside = y < height && x < width;
+      float *colp = col + img * col_bs + (int64_t)y * width + x;
+      for (int kb = 0; kb < nkb; ++kb, ++g) {
+        if ((g & 1) != half) continue;
+        const int s = g % S;
+        const int k0 = kb * BK;
+        const int kvalid = K - k0;
+        ptx::mbar_wait(&full[s], (g / S) & 1);
+        if (!(dbg & 1)) {
+          // weights lo of this stage (this half's 128 threads)
+          const uint32_t hs = ptx::smem_u32(w_hi(s)), ls = ptx::smem_u32(w_lo(s));
+#pragma unroll
+          for (int i = 0; i < G::W_TILE / 16 / 128; ++i) {
+            float4 h4;
+            const uint32_t o = 16 * (ht + 128 * i);
+            ptx::sts128(ls + o, split_lo(ptx::lds128(hs + o), h4));
+          }
+          float v[BK];
+          const uint32_t bc = ptx::smem_u32(slab(s)) + lane_off;  // chunk starts at channel k0 / 9
+          switch (k0 % 9) {
+            case 0: conv_block<G::TWP, G::CS, 0>(bc, kvalid, v); break;
+            case 1: conv_block<G::TWP, G::CS, 1>(bc, kvalid, v); break;
+            case 2: conv_block<G::TWP, G::CS, 2>(bc, kvalid, v); break;
+            case 3: conv_block<G::TWP, G::CS, 3>(bc, kvalid, v); break;
+            case 4: conv_block<G::TWP, G::CS, 4>(bc, kvalid, v); break;
+            case 5: conv_block<G::TWP, G::CS, 5>(bc, kvalid, v); break;
+            case 6: conv_block<G::TWP, G::CS, 6>(bc, kvalid, v); break;
+            case 7: conv_block<G::TWP, G::CS, 7>(bc, kvalid, v); break;
+            default: conv_block<G::TWP, G::CS, 8>(bc, kvalid, v); break;
+          }
+          if (wcol && inside) {
+            const int kn = kvalid < BK ? kvalid : BK;
+            float *cp = colp + (int64_t)k0 * ld_col;
+#pragma unroll
+            for (int k = 0; k < BK; ++k)
+              if (k < kn) __stcs(cp + (int64_t)k * ld_col, v[k]);
+          }
+          uint32_t hi[BK], lo[BK];
+#pragma unroll
+          for (int k = 0; k < BK; ++k) {
+            const uint32_t h = __float_as_uint(v[k]) & 0xFFFFE000u;
+            hi[k] = h;
+            lo[k] = __float_as_uint(v[k] - __uint_as_float(h));
+          }
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + G::A_COL0 + s * 2 * BK;
+          ptx::tmem_st_cols<BK>(ta, hi);
+          ptx::tmem_st_cols<BK>(ta + BK, lo);
+          ptx::tmem_st_wait();
+          ptx::fence_proxy_async_smem();  // weights lo -> the tensor core
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&conv[s]);
+      }
+    }
+  } else {
+    // ---------------- epilogue: two groups taking alternate units ----------------
+    const int q = warp & 3;
+    const int grp = (warp - 10) >> 2;
+    const int m = 32 * q + lane;
+    const int py = m / TW, px = m % TW;
+    float *scr = bias_s + TN + (warp - 10) * 8 * 33;
+    int j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      if ((j & 1) != grp) continue;
+      int mb, img, y0, x0;
+      unit_of(u, mb, img, y0, x0);
+      const int a = j % NACC;
+      ptx::mbar_wait_sleepy(&acc_full[a], (j / NACC) & 1);
+      ptx::tc_fence_after();
+      const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * TN;
+      const int y = y0 + py, x = x0 + px;
+      const bool live = y < height && x < width && !(dbg & 4);
+      const bool cst = live && img >= c_from;
+      const int m0 = mb * TN;  // this unit's first filter
+      float *cp = C + img * c_bs + (int64_t)y * width + x;
+      constexpr int CH = 16;
+#pragma unroll 1
+      for (int cc = 0; cc < TN / CH; ++cc) {
+        uint32_t r[CH];
+        ptx::tmem_ld_32x32b_x16(trow + CH * cc, r);
+        const int rbase = m0 + CH * cc;
+        if (rbase >= M) continue;
+        float *rp = cp + (int64_t)rbase * ldc;
+        float cv[CH];
+        if (beta != 0.0f && live) {
+#pragma unroll
+          for (int jj = 0; jj < CH; ++jj) cv[jj] = rbase + jj < M ? rp[(int64_t)jj * ldc] : 0.0f;
+        }
+#pragma unroll
+        for (int jj = 0; jj < CH; ++jj) {
+          float v = __uint_as_float(r[jj]);
+          if (beta != 0.0f && live) v = beta * cv[jj] + v;
+          if (bias) v += __ldg(bias + (rbase + jj < M ? rbase + jj : 0));
+          if (act == ACCT_ACT_LEAKY) v = acct_leaky(v);
+          if (cst && rbase + jj < M) rp[(int64_t)jj * ldc] = v;
+          r[jj] = __float_as_uint(v);
+        }
+#pragma unroll
+        for (int hf = 0; hf < 2 && pool; ++hf) {
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) scr[jj * 33 + lane] = __uint_as_float(r[8 * hf + jj]);
+          __syncwarp();
+          constexpr int TWH = TW / 2;
+          const int w8 = lane & 7, fg = lane >> 3;
+          const int l0 = (w8 / TWH) * 2 * TW + 2 * (w8 % TWH);
+          const int mm0 = 32 * q + l0;
+          const int wy = y0 + mm0 / TW, wx = x0 + mm0 % TW;
+          const bool win = wy < height && wx < width && !(dbg & 4);
+          const int64_t pofs = (int64_t)(wy >> 1) * (width >> 1) + (wx >> 1);
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const int fl = 4 * t + fg, f = rbase + 8 * hf + fl;
+            const float *sv = scr + fl * 33 + l0;
+            const float v00 = sv[0], v01 = sv[1], v10 = sv[TW], v11 = sv[TW + 1];
+            if (win && f < M) {
+              const int base_i = f * HW + wy * width + wx;
+              float mx = -FLT_MAX;
+              int32_t k = -1;
+              if (v00 > mx) { mx = v00; k = base_i; }
+              if (v01 > mx) { mx = v01; k = base_i + 1; }
+              if (v10 > mx) { mx = v10; k = base_i + width; }
+              if (v11 > mx) { mx = v11; k = base_i + width + 1; }
+              pool[img * pool_bs + (int64_t)f * ld_pool + pofs] = mx;
+              pidx[img * pidx_bs + (int64_t)f * ld_pidx + pofs] = k;
+            }
+          }
+          __syncwarp();
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&acc_empty[a]);
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc(tmem, 512);
+}
+
 // Sum the split-K partials of every output element in split order and apply
 // the epilogue (grid-wide, one thread per 4 consecutive columns).
 __global__ void __launch_bounds__(256)
@@ -1796,6 +2094,58 @@ int launch_conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channe
   return note_launch("conv3x3 tc");
 }
 
+// wide layers: M a multiple of 128 (filter blocks), any channel count
+template <int TW>
+int launch_conv_wide(const float *im, int64_t ld_im, int64_t im_stride, int channels, int height,
+                     int width, float *col, int64_t ld_col, int64_t col_stride, int M,
+                     const float *A, int64_t lda, float beta, float *C, int64_t ldc,
+                     int64_t c_stride, const float *bias, int act, int batch, int col_from,
+                     const ConvPool &pl, cudaStream_t s) {
+  using G = WideCfg<TW>;
+  const int K = 9 * channels;
+  const int nkb = (K + G::BK - 1) / G::BK;
+  const size_t smem = 1024 + (size_t)G::S * G::STAGE + 8 * (3 * G::S + 2 * G::NACC) + 16 +
+                      4 * G::TN + (pl.pool ? 4 * 8 * 8 * 33 : 0);
+  if (smem > 227 * 1024 || M % G::TN) return ACCT_ENOTSUP;
+  CUtensorMap tw, tx;
+  if (!cached_map(&tw, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, G::BK, G::TN,
+                  CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !cached_map4(&tx, im, (uint64_t)width, (uint64_t)height, (uint64_t)batch,
+                   (uint64_t)channels, (uint64_t)(batch > 1 ? im_stride : ld_im), (uint64_t)ld_im,
+                   G::TWP, G::SROWS, G::CH_PER_KB))
+    return fail(ACCT_ENOTSUP, "conv_tc wide: cuTensorMapEncodeTiled failed");
+  static std::mutex mu;
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev >= 0 && dev < 64 && !done[dev]) {
+      if (int rc = check_cuda(cudaFuncSetAttribute(tc_conv_wide_kernel<TW>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   227 * 1024),
+                              "conv_tc wide: smem attribute"))
+        return rc;
+      done[dev] = true;
+    }
+  }
+  const int tiles_x = (width + TW - 1) / TW, tiles_y = (height + G::TH - 1) / G::TH;
+  const int64_t tpi = (int64_t)tiles_x * tiles_y;
+  const int64_t units = tpi * batch * (M / G::TN);
+  if (units > INT32_MAX) return ACCT_ENOTSUP;
+  const int sms = sm_count();
+  const int grid = units < sms ? (int)units : sms;
+  static const int dbg = [] {
+    const char *e = getenv("ACCT_CONV_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  launch(tc_conv_wide_kernel<TW>, dim3(grid), dim3(CONV_TC_THREADS), smem, s, tw, tx, M, channels,
+         height, width, tiles_x, (int)tpi, (int)units, nkb, beta, C, ldc, c_stride, bias, act, col,
+         ld_col, col_stride, col_from, pl.pool, pl.ld_pool, pl.pool_stride, pl.idx, pl.ld_idx,
+         pl.idx_stride, pl.c_from, batch, dbg);
+  return note_launch("conv3x3 tc wide");
+}
+
 template <int TN>
 int conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channels, int height,
             int width, float *col, int64_t ld_col, int64_t col_stride, int M, const float *A,
@@ -1840,8 +2190,8 @@ extern "C" int acct_conv3x3_tc_f32(const float *im, int64_t ld_im, int64_t im_st
                                    int64_t pool_stride, int32_t *idx, int64_t ld_idx,
                                    int64_t idx_stride, int c_from, acct_stream_t stream) {
   using namespace acct;
-  if (channels < 1 || channels > 64 || M < 1 || M > 64 || height < 1 || width < 1 || batch < 1 ||
-      col_from < 0 || c_from < 0 || (int64_t)height * width > (1 << 28) ||
+  if (channels < 1 || channels > 1024 || M < 1 || (M > 64 && M % 128) || height < 1 ||
+      width < 1 || batch < 1 || col_from < 0 || c_from < 0 || (int64_t)height * width > (1 << 28) ||
       ld_im < (int64_t)height * width || ld_col < (int64_t)height * width ||
       ldc < (int64_t)height * width || (batch > 1 && (im_stride < 1 || (im_stride & 3))))
     return fail(ACCT_ENOTSUP, "conv3x3 tc: shape not supported");
@@ -1855,12 +2205,25 @@ extern "C" int acct_conv3x3_tc_f32(const float *im, int64_t ld_im, int64_t im_st
   if (!pool) c_from = 0;
   const ConvPool pl{pool, ld_pool, pool_stride, idx, ld_idx, idx_stride, c_from};
   cudaStream_t s = as_stream(stream);
-  int rc = M <= 32 ? conv_tc<32>(im, ld_im, im_stride, channels, height, width, col, ld_col,
-                                 col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
-                                 col_from, pl, s)
-                   : conv_tc<64>(im, ld_im, im_stride, channels, height, width, col, ld_col,
-                                 col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
-                                 col_from, pl, s);
+  int rc;
+  if (M > 64) {
+    const bool eight = width % 16 != 0 && width % 8 == 0;
+    rc = eight ? launch_conv_wide<8>(im, ld_im, im_stride, channels, height, width, col, ld_col,
+                                     col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act,
+                                     batch, col_from, pl, s)
+               : launch_conv_wide<16>(im, ld_im, im_stride, channels, height, width, col, ld_col,
+                                      col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act,
+                                      batch, col_from, pl, s);
+  } else if (channels > 64) {
+    rc = ACCT_ENOTSUP;
+  } else {
+    rc = M <= 32 ? conv_tc<32>(im, ld_im, im_stride, channels, height, width, col, ld_col,
+                               col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
+                               col_from, pl, s)
+                 : conv_tc<64>(im, ld_im, im_stride, channels, height, width, col, ld_col,
+                               col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act, batch,
+                               col_from, pl, s);
+  }
   if (rc == ACCT_ENOTSUP)
     return fail(ACCT_ENOTSUP, "conv3x3 tc: weights + slabs exceed shared memory");
   return rc;

@@ -350,7 +350,7 @@ int device_op(const acct_action_t &a, acct_array_t *arr, int gemm_mode, cudaStre
                                               D(2), LD(2), beta, D(3), LD(3), BS(3), bias,
                                               (int)I[6], nb, col_from, pp, ldp, pbs, pi, ldi, ibs,
                                               c_from, st);
-        if (M <= 64)
+        if (M <= 64 || M % 128 == 0)
           return acct_conv3x3_tc_f32(D(0), LD(0), BS(0), C, H, W, D(1), LD(1), BS(1), M, D(2),
                                      LD(2), beta, D(3), LD(3), BS(3), bias, (int)I[6], nb,
                                      col_from, pp, ldp, pbs, pi, ldi, ibs, c_from, st);

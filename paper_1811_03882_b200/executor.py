@@ -63,6 +63,10 @@ PITCH_ALIGN = 32  # elements (128 bytes)
 # image) measured 13.7 us/img against 12.2 for im2col + the swap gemm
 CONV_MAX_C = int(os.environ.get("ACCT_CONV_MAX_C", "64"))
 CONV_MAX_M = int(os.environ.get("ACCT_CONV_MAX_M", "64"))
+# wide layers (M a multiple of 128) on the streamed-weight tcgen05 conv:
+# yolov2-tiny layers 6 (M = 128) and 8 (M = 256)
+CONV_WIDE_MAX_M = int(os.environ.get("ACCT_CONV_WIDE_MAX_M", "256"))
+CONV_WIDE_MAX_C = int(os.environ.get("ACCT_CONV_WIDE_MAX_C", "512"))
 
 
 def _pitch(cols: int) -> int:
@@ -741,8 +745,12 @@ class PatternExecutor:
         p = im.params
         if im.kind != "im2col" or not on[g - 1] or im.arrays["Y"] != op.arrays["B"]:
             return None
-        if (p["ksize"], p["stride"], p["pad"]) != (3, 1, 1) or p["c"] > CONV_MAX_C or \
-                op.params["M"] > CONV_MAX_M:
+        if (p["ksize"], p["stride"], p["pad"]) != (3, 1, 1):
+            return None
+        M = op.params["M"]
+        narrow = p["c"] <= CONV_MAX_C and M <= CONV_MAX_M
+        wide = M % 128 == 0 and M <= CONV_WIDE_MAX_M and p["c"] <= CONV_WIDE_MAX_C
+        if not (narrow or wide):
             return None
         if p["w"] % 4:
             return None

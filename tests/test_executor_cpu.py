@@ -88,8 +88,10 @@ def test_fused_and_unfused_schedules_agree_on_counts():
 
 def test_narrow_conv_layers_fuse_im2col_into_the_gemm_launch():
     """All-offload: the 3x3/1/1 layers with M <= 64 filters -- 0 (c=3, M=16),
-    2 (c=16, M=32) and 4 (c=32, M=64) -- each become ONE conv action that
-    writes col and out; counters are those of the unfused schedule."""
+    2 (c=16, M=32) and 4 (c=32, M=64) -- and the wide layer 6 (M = 128 on
+    52x52 planes; layer 8's 26-wide rows are not TMA-describable) each become
+    ONE conv action that writes col and out; counters are those of the
+    unfused schedule."""
     net = build_net("yolov2-tiny")
     a = PatternExecutor(net, device=None, fuse=True)
     b = PatternExecutor(net, device=None, fuse=False)
@@ -103,7 +105,9 @@ def test_narrow_conv_layers_fuse_im2col_into_the_gemm_launch():
             (["pool1", "col2", "w2", "out2"],
              [16, 208, 208, 32, 0, K.ACT_LEAKY, names.index("bias2")]),
             (["pool3", "col4", "w4", "out4"],
-             [32, 104, 104, 64, 0, K.ACT_LEAKY, names.index("bias4")])]
+             [32, 104, 104, 64, 0, K.ACT_LEAKY, names.index("bias4")]),
+            (["pool5", "col6", "w6", "out6"],     # wide: streamed-weight tcgen05 conv
+             [64, 52, 52, 128, 0, K.ACT_LEAKY, names.index("bias6")])]
     assert len(convs) == len(want)
     for k, (arrs, ints) in zip(convs, want):
         act = sa.actions[k]
@@ -153,7 +157,7 @@ def test_conv_fusion_only_when_no_directive_splits_it(host_exec):
 
 
 def test_pool_fusion_and_dead_outputs():
-    """Each fused conv launch of yolov2-tiny's first three layers absorbs the
+    """Each fused conv launch of yolov2-tiny's first four conv layers absorbs the
     2x2/2 maxpool reading its output (slots i[9], i[10] = pool, idx); with
     one image per launch every output stays stored (i[11] = 0).  The other
     maxpools (after plain gemm launches, and the 2x2/1 one) keep their own
@@ -168,10 +172,10 @@ def test_pool_fusion_and_dead_outputs():
     convs = [sa.actions[k] for k in range(sa.n_actions)
              if sa.actions[k].kind == K.A_KERNEL and sa.actions[k].i[0] == K.K_CONV]
     assert [(names[c.i[9]], names[c.i[10]], c.i[11]) for c in convs] == \
-        [("pool1", "idx1", 0), ("pool3", "idx3", 0), ("pool5", "idx5", 0)]
+        [("pool1", "idx1", 0), ("pool3", "idx3", 0), ("pool5", "idx5", 0), ("pool7", "idx7", 0)]
     pools = [names[sa.actions[k].a[1]] for k in range(sa.n_actions)
              if sa.actions[k].kind == K.A_KERNEL and sa.actions[k].i[0] == K.K_MAXPOOL]
-    assert pools == ["pool7", "pool9", "pool11"]
+    assert pools == ["pool9", "pool11"]
     # written slots of a pooled conv include pool and idx (early copyouts wait for them)
     c = convs[0]
     act = (K.A_KERNEL, tuple(c.a[j] for j in range(4)), tuple(c.i[j] for j in range(14)))

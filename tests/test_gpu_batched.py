@@ -164,14 +164,19 @@ def test_fused_conv_layer_is_bit_identical(cuda_device, name, images, mode):
         b.run(bits, resident=True)
         assert np.array_equal(a.device_array(net.output_name), b.device_array(net.output_name))
     else:
-        # the tensor-core conv sums the 3xTF32 terms in its own order: values
-        # within the gemm tolerance; every col array bit-exact
+        # the tensor-core convs sum the 3xTF32 terms in their own order:
+        # values within the gemm tolerance; col0 (an im2col of the input)
+        # bit-exact, the later col arrays as exact as their inputs
         want = b.outputs()
         assert np.abs(a.outputs() - want).max() <= 1e-4 * np.abs(want).max()
         for name_ in net.arrays:
             if name_.startswith("col"):
-                assert np.array_equal(a.device_array(name_), b.device_array(name_)), name_
-                assert np.array_equal(a.host_array(name_), b.host_array(name_)), name_
+                for arr_a, arr_b in ((a.device_array(name_), b.device_array(name_)),
+                                     (a.host_array(name_), b.host_array(name_))):
+                    if name_ == "col0":
+                        assert np.array_equal(arr_a, arr_b), name_
+                    else:
+                        assert np.abs(arr_a - arr_b).max() <= 1e-4 * max(np.abs(arr_b).max(), 1e-30)
     c = PatternExecutor(net, device=0, fuse=True, gemm_mode=K.GEMM_SIMT + K.GEMM_AUTO - mode)
     c.run(bits)
     want = a.outputs()

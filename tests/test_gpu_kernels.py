@@ -355,7 +355,10 @@ def test_conv3x3_fused_declines_unaligned_rows(cuda_device):
                           (48, 13, 16, 17, 1, True, K.ACT_LEAKY, 2, 0, "im", False),
                           (24, 30, 36, 64, 0, True, K.ACT_LEAKY, 3, 1, "il", False),
                           (3, 20, 24, 50, 0, True, K.ACT_LINEAR, 1, 0, "im", False),
-                          (5, 7, 4, 33, 0, True, K.ACT_LEAKY, 4, 3, "il", False)])
+                          (5, 7, 4, 33, 0, True, K.ACT_LEAKY, 4, 3, "il", False),
+                          (64, 52, 52, 128, 0, True, K.ACT_LEAKY, 2, 1, "il", True),
+                          (128, 24, 16, 256, 1, True, K.ACT_LEAKY, 2, 0, "im", False),
+                          (3, 20, 36, 128, 0, False, K.ACT_NONE, 3, 2, "il", False)])
 def test_conv3x3_tc_equals_im2col_then_tc_gemm(cuda_device, orc, c, h, w, M, beta, use_bias, act,
                                                batch, col_from, layout, exact):
     """acct_conv3x3_tc_f32 (implicit-im2col tcgen05 swap tile) writes col
@@ -449,7 +452,9 @@ def test_leaky_is_darknets_double_product_for_every_float(cuda_device):
                          [(16, 208, 208, 32, 0, K.ACT_LEAKY, 2, 1, "il"),
                           (32, 104, 104, 64, 1, K.ACT_LEAKY, 3, 2, "im"),
                           (8, 20, 36, 40, 0, K.ACT_NONE, 2, 0, "il"),
-                          (5, 30, 12, 24, 0, K.ACT_LINEAR, 1, 0, "im")])
+                          (5, 30, 12, 24, 0, K.ACT_LINEAR, 1, 0, "im"),
+                          (64, 52, 52, 128, 0, K.ACT_LEAKY, 2, 1, "il"),
+                          (96, 20, 24, 256, 1, K.ACT_LEAKY, 2, 0, "im")])
 def test_conv3x3_tc_fused_maxpool(cuda_device, c, h, w, M, beta, act, batch, c_from, layout):
     """The tcgen05 conv with its 2x2/2 maxpool fused into the epilogue
     writes pool and argmax idx bit-identically to acct_maxpool_batched_f32

@@ -249,7 +249,7 @@ enum {
      i[8] = 1: col is written for the batch's last image only (the others are
      unobservable); i[9], i[10] = pool / idx slots of a fused 2x2/2 maxpool of
      C (-1: none), i[11] = 1: C itself is then stored for the last image only.  Device only: acct_conv3x3_im2col_gemm_f32 in SIMT mode
-     and, under AUTO, for M <= 16 or c <= 4 with M <= 32;
+     and, under AUTO, for M <= 16;
      acct_conv3x3_tc_f32 otherwise (M <= 64); im2col + gemm when the fused
      kernel declines the shape */
   ACCT_K_CONV = 9

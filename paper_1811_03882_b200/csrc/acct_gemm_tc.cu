@@ -989,6 +989,7 @@ struct ConvCfg {
   static_assert(USED_COLS <= 512, "TMEM overflow");
 };
 constexpr int CONV_TC_THREADS = 32 * 18;
+constexpr int kMaxSlabs = 8;  // slab ring depth: 2 .. 8 as shared memory allows
 
 // One k-block (32 k = (channel, tap) pairs from k0 = 9 c0 + R0) of the
 // activation operand for this lane's pixel: each k is one LDS at the lane's
@@ -1024,7 +1025,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
                const float *__restrict__ bias, int act, float *__restrict__ col, int64_t ld_col,
                int64_t col_bs, int col_from, float *__restrict__ pool, int64_t ld_pool,
                int64_t pool_bs, int32_t *__restrict__ pidx, int64_t ld_pidx, int64_t pidx_bs,
-               int c_from, int dbg) {
+               int c_from, int nslab, int dbg) {
   using G = ConvCfg<TN, TW>;
   constexpr int S = G::S, BK = G::BK, NACC = G::NACC;
   extern __shared__ uint8_t smem_raw[];
@@ -1034,10 +1035,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   uint8_t *w_lo = base + nkb * G::W_TILE;           // [nkb][W_TILE]
   const int slab_bytes = (channels * G::CS + 127) & ~127;
   uint8_t *slab0 = base + 2 * nkb * G::W_TILE;      // 2 x [channels][SROWS][TWP]
-  uint64_t *wfull = reinterpret_cast<uint64_t *>(slab0 + 2 * slab_bytes);
+  uint64_t *wfull = reinterpret_cast<uint64_t *>(slab0 + nslab * slab_bytes);
   uint64_t *slab_full = wfull + 1;
-  uint64_t *slab_empty = slab_full + 2;
-  uint64_t *conv = slab_empty + 2;
+  uint64_t *slab_empty = slab_full + kMaxSlabs;
+  uint64_t *conv = slab_empty + kMaxSlabs;
   uint64_t *empty = conv + S;
   uint64_t *acc_full = empty + S;
   uint64_t *acc_empty = acc_full + NACC;
@@ -1055,7 +1056,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   if ((dbg & 64) && threadIdx.x == 0 && blockIdx.x < 256) g_trace[7][256 + blockIdx.x] = gtime();
   if (threadIdx.x == 0) {
     ptx::mbar_init(wfull, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < nslab; ++b) {
       ptx::mbar_init(&slab_full[b], 1);
       ptx::mbar_init(&slab_empty[b], 8);
     }
@@ -1101,8 +1102,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
         int img, y0, x0;
         unit_xy(u, img, y0, x0);
-        const int sb = j & 1;
-        if (j >= 2) ptx::mbar_wait(&slab_empty[sb], ((j >> 1) - 1) & 1);
+        const int sb = j % nslab;
+        if (j >= nslab) ptx::mbar_wait(&slab_empty[sb], ((j / nslab) - 1) & 1);
         if (dbg & 8) {
           ptx::mbar_arrive(&slab_full[sb]);
         } else {
@@ -1172,13 +1173,13 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       int img, y0, x0;
       unit_xy(u, img, y0, x0);
-      const int sb = j & 1;
+      const int sb = j % nslab;
       const int y = y0 + py, x = x0 + px;
       const bool wcol = img >= col_from;  // warp-uniform; lanes off the image skip the store
       const bool inside = y < height && x < width;
       float *colp = col + img * col_bs + (int64_t)y * width + x;
       const uint32_t lane_base = ptx::smem_u32(slab0 + sb * slab_bytes) + lane_off;
-      ptx::mbar_wait(&slab_full[sb], (j >> 1) & 1);
+      ptx::mbar_wait(&slab_full[sb], (j / nslab) & 1);
       for (int kb = 0; kb < nkb; ++kb, ++g) {
         if ((g & 1) != half) continue;
         const int s = g % S;
@@ -2051,10 +2052,14 @@ int launch_conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channe
   const int K = 9 * channels;
   const int nkb = (K + G::BK - 1) / G::BK;
   const size_t slab_bytes = ((size_t)channels * G::CS + 127) & ~size_t(127);
-  const size_t smem = 1024 + 2 * (size_t)nkb * G::W_TILE + 2 * slab_bytes +
-                      8 * (5 + 2 * G::S + 2 * G::NACC) + 16 + 4 * 64 +
-                      (pl.pool ? 4 * 8 * 8 * 33 : 0);  // pooling scratch
-  if (smem > 227 * 1024) return ACCT_ENOTSUP;
+  // a deeper slab ring keeps several units' input windows in flight: the
+  // first layers (K = 27) have one k-block per unit and are latency-bound
+  const size_t fixed = 1024 + 2 * (size_t)nkb * G::W_TILE + 8 * (1 + 2 * kMaxSlabs + 2 * G::S +
+                       2 * G::NACC) + 16 + 4 * 64 + (pl.pool ? 4 * 8 * 8 * 33 : 0);
+  if (fixed + 2 * slab_bytes > 227 * 1024) return ACCT_ENOTSUP;
+  int nslab = (int)((227 * 1024 - fixed) / slab_bytes);
+  if (nslab > kMaxSlabs) nslab = kMaxSlabs;
+  const size_t smem = fixed + (size_t)nslab * slab_bytes;
   CUtensorMap tw, tx;
   if (!cached_map(&tw, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, G::BK, TN,
                   CU_TENSOR_MAP_SWIZZLE_128B) ||
@@ -2090,7 +2095,7 @@ int launch_conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channe
   launch(tc_conv_kernel<TN, TW>, dim3(grid), dim3(CONV_TC_THREADS), smem, s, tw, tx, M, channels,
          height, width, tiles_x, (int)tpi, (int)units, nkb, beta, C, ldc, c_stride, bias, act, col,
          ld_col, col_stride, col_from, pl.pool, pl.ld_pool, pl.pool_stride, pl.idx, pl.ld_idx,
-         pl.idx_stride, pl.c_from, dbg);
+         pl.idx_stride, pl.c_from, nslab, dbg);
   return note_launch("conv3x3 tc");
 }
 

@@ -323,7 +323,7 @@ int device_op(const acct_action_t &a, acct_array_t *arr, int gemm_mode, cudaStre
       const int M = (int)I[4], K = 9 * (int)I[1], N = (int)(I[2] * I[3]);
       // I[8] = 1: only the last image's col is observable (col_from = nb - 1).
       // FP32 FMA from the input window (k order, the SIMT gemms' chain) for
-      // M <= 16 or a first layer (c <= 4, M <= 32) and in SIMT mode; the
+      // M <= 16 and in SIMT mode; the
       // implicit-im2col tcgen05 swap tile (3xTF32, bit-identical to im2col +
       // the swap gemm) for the other narrow layers (M <= 64)
       const int C = (int)I[1], H = (int)I[2], W = (int)I[3], col_from = I[8] ? nb - 1 : 0;
@@ -331,9 +331,10 @@ int device_op(const acct_action_t &a, acct_array_t *arr, int gemm_mode, cudaStre
         const char *e = getenv("ACCT_CONV_TC_FIRST");
         return e ? atoi(e) : 0;
       }();
+      // FP32 window kernel for M <= 16 only: at M = 32 (yolov2-608 layer 0,
+      // 608x608) it ran 41.8 us/img, the tcgen05 tile with the fused pool less
       const bool simt = gemm_mode == ACCT_GEMM_SIMT ||
-                        (gemm_mode == ACCT_GEMM_AUTO && !tc_first &&
-                         (M <= 16 || (M <= 32 && C <= 4)));
+                        (gemm_mode == ACCT_GEMM_AUTO && !tc_first && M <= 16);
       // I[9] / I[10]: a fused 2x2/2 maxpool of C into pool / idx; I[11] = 1:
       // C is then observable for the last image only
       const bool has_pool = I[9] >= 0;

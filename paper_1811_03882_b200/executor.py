@@ -57,7 +57,7 @@ from .syntax import parse
 PITCH_ALIGN = 32  # elements (128 bytes)
 # 3x3/1/1 layers fused into one conv launch (im2col + gemm_nn + epilogue): at
 # most CONV_MAX_C input channels and CONV_MAX_M filters.  The runtime runs
-# the FP32 window kernel for first layers (c <= 4) and M <= 16, the
+# the FP32 window kernel for M <= 16, the
 # implicit-im2col tcgen05 swap tile for the other narrow layers (yolov2-tiny
 # layers 2 and 4); the FP32 kernel at layer 2 (c = 16, M = 32: 199 MFMA per
 # image) measured 13.7 us/img against 12.2 for im2col + the swap gemm
@@ -997,8 +997,7 @@ class PatternExecutor:
                 (nimg * 8 * M * (N // 4) if pooled else 0)
             byts += 4 * M if i[7] >= 0 else 0
             # the runtime's engine choice (acct_runtime.cu, ACCT_K_CONV)
-            fp32 = self.gemm_mode == K.GEMM_SIMT or (self.gemm_mode == K.GEMM_AUTO and
-                                                     (M <= 16 or (M <= 32 and c <= 4)))
+            fp32 = self.gemm_mode == K.GEMM_SIMT or (self.gemm_mode == K.GEMM_AUTO and M <= 16)
             return {"kind": "conv", "engine": "fp32-fma" if fp32 else "tcgen05",
                     "layer": op.layer, "M": M, "N": N, "K": Kd, "images": nimg,
                     "N_launch": N, "executions": execs, "flops": 2 * M * N * Kd * nimg,

@@ -16,7 +16,7 @@ from paper_1811_03882_b200 import kernels as K  # noqa: E402
 
 def main():
     P = 16
-    for (c, h, w, M) in ((16, 208, 208, 32), (32, 104, 104, 64)):
+    for (c, h, w, M) in ((16, 208, 208, 32), (32, 104, 104, 64), (64, 52, 52, 128)):
         N, Kd = h * w, 9 * c
         ld = -(-N // 32) * 32
         lda = -(-Kd // 32) * 32

@@ -64,7 +64,8 @@ PITCH_ALIGN = 32  # elements (128 bytes)
 CONV_MAX_C = int(os.environ.get("ACCT_CONV_MAX_C", "64"))
 CONV_MAX_M = int(os.environ.get("ACCT_CONV_MAX_M", "64"))
 # wide layers (M a multiple of 128) on the streamed-weight tcgen05 conv:
-# yolov2-tiny layers 6 (M = 128) and 8 (M = 256)
+# yolov2-tiny layer 6 (M = 128; layer 8's 26-wide rows are not TMA-describable
+# as a 2-D plane, so _conv_partner's width % 4 rule keeps it unfused)
 CONV_WIDE_MAX_M = int(os.environ.get("ACCT_CONV_WIDE_MAX_M", "256"))
 CONV_WIDE_MAX_C = int(os.environ.get("ACCT_CONV_WIDE_MAX_C", "512"))
 

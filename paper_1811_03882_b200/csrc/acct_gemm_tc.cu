@@ -1435,9 +1435,12 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         for (int kb = 0; kb < nkb; ++kb, ++g) {
           const int s = g % S;
           if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
-          ptx::mbar_expect_tx(&full[s], (uint32_t)(G::W_TILE + G::CH_PER_KB * G::CS));
-          ptx::tma_load_2d(w_hi(s), &tmW, &full[s], kb * BK, mb * TN);
-          ptx::tma_load_4d(slab(s), &tmX, &full[s], x0 - 4, y0 - 1, img, (kb * BK) / 9);
+          // dbg 8 / 16: skip the weight / slab load (pipeline analysis only)
+          ptx::mbar_expect_tx(&full[s], (uint32_t)((dbg & 8 ? 0 : G::W_TILE) +
+                                                   (dbg & 16 ? 0 : G::CH_PER_KB * G::CS)));
+          if (!(dbg & 8)) ptx::tma_load_2d(w_hi(s), &tmW, &full[s], kb * BK, mb * TN);
+          if (!(dbg & 16))
+            ptx::tma_load_4d(slab(s), &tmX, &full[s], x0 - 4, y0 - 1, img, (kb * BK) / 9);
         }
       }
     }

@@ -973,7 +973,13 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 template <int TN, int TW>
 struct ConvCfg {
   static constexpr int BK = 32;
-  static constexpr int S = 6;                     // TMEM stages of the activation operand
+  // two independent MMA pipelines (alternate units, one issuing warp each):
+  // a narrow 128 x TN x 8 MMA is bound by its issuing thread (~50 cycles at
+  // N = 32, tools/mma_issue_probe.cu), not by the tensor core, so two issuers
+  // double the SM's MMA rate.  Each pipeline owns 256 TMEM columns: NACC
+  // accumulators of TN and S stages of the activation operand (hi, lo).
+  static constexpr int NP = 2, PCOLS = 256, NACC = 2;
+  static constexpr int S = (PCOLS - NACC * TN) / 64;
   static constexpr int TH = 128 / TW;
   // slab row: columns x0 - 4 .. x0 + TW + 3 (TMA needs a 16-byte aligned
   // start in the innermost dimension; a box starting at x0 - 1 faults)
@@ -981,15 +987,15 @@ struct ConvCfg {
   static constexpr int SROWS = TH + 2;
   static constexpr int CS = SROWS * TWP * 4;      // slab bytes per channel
   static constexpr int W_TILE = TN * BK * 4;      // one weight k-block, K-major SW128
-  static constexpr int NACC = TN <= 32 ? 4 : 2;
-  static constexpr int A_COL0 = NACC * TN;
-  static constexpr int USED_COLS = NACC * TN + S * 2 * BK;
+  static constexpr int A_COL0 = NACC * TN;          // within a pipeline's columns
+  static constexpr int USED_COLS = NP * PCOLS;
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t K_SBO = 8 * 128;
   static_assert(USED_COLS <= 512, "TMEM overflow");
 };
 constexpr int CONV_TC_THREADS = 32 * 18;
 constexpr int kMaxSlabs = 8;  // slab ring depth: 2 .. 8 as shared memory allows
+constexpr int CONV_NARROW_THREADS = 32 * 19;  // + the second MMA issuer (warp 18)
 
 // One k-block (32 k = (channel, tap) pairs from k0 = 9 c0 + R0) of the
 // activation operand for this lane's pixel: each k is one LDS at the lane's
@@ -1018,7 +1024,7 @@ __device__ __forceinline__ void conv_block(uint32_t base, int kvalid, float (&v)
 }
 
 template <int TN, int TW>
-__global__ void __launch_bounds__(CONV_TC_THREADS, 1)
+__global__ void __launch_bounds__(CONV_NARROW_THREADS, 1)
 tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                int M, int channels, int height, int width, int tiles_x, int tpi, int units,
                int nkb, float beta, float *__restrict__ C, int64_t ldc, int64_t c_bs,
@@ -1038,11 +1044,11 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   uint64_t *wfull = reinterpret_cast<uint64_t *>(slab0 + nslab * slab_bytes);
   uint64_t *slab_full = wfull + 1;
   uint64_t *slab_empty = slab_full + kMaxSlabs;
-  uint64_t *conv = slab_empty + kMaxSlabs;
-  uint64_t *empty = conv + S;
-  uint64_t *acc_full = empty + S;
-  uint64_t *acc_empty = acc_full + NACC;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + NACC);
+  uint64_t *conv = slab_empty + kMaxSlabs;   // [NP][S]
+  uint64_t *empty = conv + G::NP * S;         // [NP][S]
+  uint64_t *acc_full = empty + G::NP * S;     // [NP][NACC]
+  uint64_t *acc_empty = acc_full + G::NP * NACC;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + G::NP * NACC);
   float *bias_s = reinterpret_cast<float *>(tmem_slot + 4);  // 64 floats, then 8 x 8 x 33 scratch
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -1058,13 +1064,13 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     ptx::mbar_init(wfull, 1);
     for (int b = 0; b < nslab; ++b) {
       ptx::mbar_init(&slab_full[b], 1);
-      ptx::mbar_init(&slab_empty[b], 8);
+      ptx::mbar_init(&slab_empty[b], 4);  // the unit's pipeline's four operand warps
     }
-    for (int s = 0; s < S; ++s) {
+    for (int s = 0; s < G::NP * S; ++s) {
       ptx::mbar_init(&conv[s], 4);
       ptx::mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < NACC; ++a) {
+    for (int a = 0; a < G::NP * NACC; ++a) {
       ptx::mbar_init(&acc_full[a], 1);
       ptx::mbar_init(&acc_empty[a], 4);
     }
@@ -1112,23 +1118,25 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         }
       }
     }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer (the swap tile's sequence) ----------------
+  } else if (warp == 1 || warp == 18) {
+    // ---------------- MMA issuers: pipeline p takes units j = p, p + 2, ... ----------------
+    const int p = warp == 18;
     constexpr uint32_t idesc = ptx::idesc_tf32(128, TN, false, false);
-    int g = 0, j = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-      const int a = j % NACC;
-      if (j >= NACC) ptx::mbar_wait(&acc_empty[a], ((j / NACC) - 1) & 1);
+    const uint32_t pbase = tmem + p * G::PCOLS;
+    int gp = 0, jp = 0;
+    for (int u = blockIdx.x + p * gridDim.x; u < units; u += 2 * gridDim.x, ++jp) {
+      const int a = jp % NACC;
+      if (jp >= NACC) ptx::mbar_wait(&acc_empty[p * NACC + a], ((jp / NACC) - 1) & 1);
       ptx::tc_fence_after();
-      const uint32_t d = tmem + a * TN;
-      for (int kb = 0; kb < nkb; ++kb, ++g) {
-        const int s = g % S;
-        ptx::mbar_wait(&conv[s], (g / S) & 1);
-        if ((dbg & 64) && blockIdx.x == 0 && g < kTrace && lane == 0) g_trace[2][g] = clock64();
+      const uint32_t d = pbase + a * TN;
+      for (int kb = 0; kb < nkb; ++kb, ++gp) {
+        const int s = gp % S;
+        ptx::mbar_wait(&conv[p * S + s], (gp / S) & 1);
+        if ((dbg & 64) && p == 0 && blockIdx.x == 0 && gp < kTrace && lane == 0) g_trace[2][gp] = clock64();
         ptx::tc_fence_after();
         const uint32_t yh = ptx::smem_u32(w_hi + kb * G::W_TILE);
         const uint32_t yl = ptx::smem_u32(w_lo + kb * G::W_TILE);
-        const uint32_t at = tmem + G::A_COL0 + s * 2 * BK;
+        const uint32_t at = pbase + G::A_COL0 + s * 2 * BK;
         // one elected lane issues the k-block's 12 MMAs and the stage commit
         if (ptx::elect_one()) {
           if (!(dbg & 2)) {
@@ -1141,18 +1149,18 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
               ptx::mma_tf32_ts(d, at + BK + 8 * k, dyh, idesc, 1);
             }
           }
-          ptx::mma_commit(&empty[s]);
+          ptx::mma_commit(&empty[p * S + s]);
         }
         __syncwarp();
-        if ((dbg & 64) && blockIdx.x == 0 && g < kTrace && lane == 0) g_trace[3][g] = clock64();
+        if ((dbg & 64) && p == 0 && blockIdx.x == 0 && gp < kTrace && lane == 0) g_trace[3][gp] = clock64();
       }
-      if (ptx::elect_one()) ptx::mma_commit(&acc_full[a]);
+      if (ptx::elect_one()) ptx::mma_commit(&acc_full[p * NACC + a]);
       __syncwarp();
     }
   } else if (warp < 10) {
     // ---------------- weights lo, then the activation operand ----------------
-    // two halves of four warps (2-5, 6-9) build alternate k-blocks, so one
-    // half's TMEM stores and fences overlap the other's loads
+    // two halves of four warps (2-5, 6-9): half p builds every k-block of
+    // its pipeline's units (j = p, p + 2, ...)
     const int q = warp & 3;  // TMEM lanes 32q.. = MMA rows (pixels) 32q..
     const int half = (warp - 2) >> 2;
     const int ct = threadIdx.x - 64;
@@ -1164,13 +1172,16 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         float4 h4;
         ptx::sts128(ls + 16 * i, split_lo(ptx::lds128(hs + 16 * i), h4));
       }
-      ptx::fence_proxy_async_smem();  // read by the MMAs after the first conv arrival
+      ptx::fence_proxy_async_smem();
+      // both halves wrote weights lo: all of it before any pipeline's first
+      // conv arrival releases an MMA that reads it
+      asm volatile("bar.sync 1, 256;" ::: "memory");
     }
     const int m = 32 * q + lane;
     const int py = m / TW, px = m % TW;
     const uint32_t lane_off = (uint32_t)((py * G::TWP + px) * 4);
-    int g = 0, j = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+    int g = 0, j = half;
+    for (int u = blockIdx.x + half * gridDim.x; u < units; u += 2 * gridDim.x, j += 2) {
       int img, y0, x0;
       unit_xy(u, img, y0, x0);
       const int sb = j % nslab;
@@ -1181,18 +1192,17 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       const uint32_t lane_base = ptx::smem_u32(slab0 + sb * slab_bytes) + lane_off;
       ptx::mbar_wait(&slab_full[sb], (j / nslab) & 1);
       for (int kb = 0; kb < nkb; ++kb, ++g) {
-        if ((g & 1) != half) continue;
         const int s = g % S;
         const int k0 = kb * BK;
         const int c0 = k0 / 9;
         const int kvalid = K - k0;  // >= 32 except in the last block
-        if ((dbg & 64) && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[0][g] = clock64();
-        if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
-        if ((dbg & 64) && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[1][g] = clock64();
+        if ((dbg & 64) && half == 0 && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[0][g] = clock64();
+        if (g >= S) ptx::mbar_wait(&empty[half * S + s], ((g / S) - 1) & 1);
+        if ((dbg & 64) && half == 0 && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[1][g] = clock64();
         ptx::tc_fence_after();
         if (dbg & 1) {  // profiling knob: skip building the operand (results wrong)
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&conv[s]);
+          if (lane == 0) ptx::mbar_arrive(&conv[half * S + s]);
           continue;
         }
         float v[BK];
@@ -1222,22 +1232,22 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           hi[k] = h;
           lo[k] = __float_as_uint(v[k] - __uint_as_float(h));
         }
-        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + G::A_COL0 + s * 2 * BK;
+        const uint32_t ta =
+            tmem + ((uint32_t)(32 * q) << 16) + half * G::PCOLS + G::A_COL0 + s * 2 * BK;
         ptx::tmem_st_cols<BK>(ta, hi);
         ptx::tmem_st_cols<BK>(ta + BK, lo);
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&conv[s]);
-        if ((dbg & 64) && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[4][g] = clock64();
+        if (lane == 0) ptx::mbar_arrive(&conv[half * S + s]);
+        if ((dbg & 64) && half == 0 && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[4][g] = clock64();
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&slab_empty[sb]);  // this unit's slab is consumed
     }
   } else {
     // ---------------- epilogue: lanes = pixels, TMEM columns = filters ----------------
-    // two groups of four warps (10-13, 14-17) take alternate units, so one
-    // group's stores overlap the other's TMEM loads
+    // group p of four warps (10-13, 14-17) drains pipeline p's accumulators
     const int q = warp & 3;
     const int grp = (warp - 10) >> 2;
     for (int i = threadIdx.x - 10 * 32; i < TN; i += 8 * 32) bias_s[i] = (bias && i < M) ? bias[i] : 0.0f;
@@ -1245,16 +1255,15 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     const int m = 32 * q + lane;
     const int py = m / TW, px = m % TW;
     float *scr = bias_s + 64 + (warp - 10) * 8 * 33;  // this warp's pooling scratch
-    int j = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-      if ((j & 1) != grp) continue;
+    int jp = 0;
+    for (int u = blockIdx.x + grp * gridDim.x; u < units; u += 2 * gridDim.x, ++jp) {
       int img, y0, x0;
       unit_xy(u, img, y0, x0);
-      const int a = j % NACC;
-      ptx::mbar_wait_sleepy(&acc_full[a], (j / NACC) & 1);
-      if ((dbg & 64) && blockIdx.x == 0 && j < kTrace && lane == 0 && q == 0) g_trace[5][j] = clock64();
+      const int a = jp % NACC;
+      ptx::mbar_wait_sleepy(&acc_full[grp * NACC + a], (jp / NACC) & 1);
+      if ((dbg & 64) && grp == 0 && blockIdx.x == 0 && jp < kTrace && lane == 0 && q == 0) g_trace[5][jp] = clock64();
       ptx::tc_fence_after();
-      const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * TN;
+      const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + grp * G::PCOLS + a * TN;
       const int y = y0 + py, x = x0 + px;
       const bool live = y < height && x < width && !(dbg & 4);
       const bool cst = live && img >= c_from;  // C of earlier images is dead when pooled here
@@ -1321,7 +1330,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&acc_empty[a]);
+      if (lane == 0) ptx::mbar_arrive(&acc_empty[grp * NACC + a]);
     }
   }
 
@@ -2057,8 +2066,9 @@ int launch_conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channe
   const size_t slab_bytes = ((size_t)channels * G::CS + 127) & ~size_t(127);
   // a deeper slab ring keeps several units' input windows in flight: the
   // first layers (K = 27) have one k-block per unit and are latency-bound
-  const size_t fixed = 1024 + 2 * (size_t)nkb * G::W_TILE + 8 * (1 + 2 * kMaxSlabs + 2 * G::S +
-                       2 * G::NACC) + 16 + 4 * 64 + (pl.pool ? 4 * 8 * 8 * 33 : 0);
+  const size_t fixed = 1024 + 2 * (size_t)nkb * G::W_TILE + 8 * (1 + 2 * kMaxSlabs +
+                       2 * G::NP * G::S + 2 * G::NP * G::NACC) + 16 + 4 * 64 +
+                       (pl.pool ? 4 * 8 * 8 * 33 : 0);
   if (fixed + 2 * slab_bytes > 227 * 1024) return ACCT_ENOTSUP;
   int nslab = (int)((227 * 1024 - fixed) / slab_bytes);
   if (nslab > kMaxSlabs) nslab = kMaxSlabs;
@@ -2095,7 +2105,7 @@ int launch_conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channe
     const char *e = getenv("ACCT_CONV_DBG");  // 2 no MMAs, 4 no epilogue -- results wrong
     return e ? atoi(e) : 0;
   }();
-  launch(tc_conv_kernel<TN, TW>, dim3(grid), dim3(CONV_TC_THREADS), smem, s, tw, tx, M, channels,
+  launch(tc_conv_kernel<TN, TW>, dim3(grid), dim3(CONV_NARROW_THREADS), smem, s, tw, tx, M, channels,
          height, width, tiles_x, (int)tpi, (int)units, nkb, beta, C, ldc, c_stride, bias, act, col,
          ld_col, col_stride, col_from, pl.pool, pl.ld_pool, pl.pool_stride, pl.idx, pl.ld_idx,
          pl.idx_stride, pl.c_from, nslab, dbg);

@@ -590,6 +590,7 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
                     int64_t ld_pidx, int64_t pidx_bs, int c_from, int tiles_x, int tpi,
                     int ntiles) {
   constexpr int MT = 16;
+  const int m_off = blockIdx.y * MT;  // this CTA's 16-filter block
   extern __shared__ float4 conv_smem[];
   const int K = channels * 9;
   float *As = reinterpret_cast<float *>(conv_smem);  // [k][MT]
@@ -626,7 +627,7 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
   cp_async_commit();
   for (int t = threadIdx.x; t < K * MT; t += 128) {
     const int k = t / MT, m = t - k * MT;
-    As[t] = m < M ? A[(int64_t)m * lda + k] : 0.0f;
+    As[t] = m_off + m < M ? A[(int64_t)(m_off + m) * lda + k] : 0.0f;
   }
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   int buf = 0;
@@ -640,7 +641,7 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
     tile_xy(tile, img, y0, x0);
     const int y = y0 + 2 * ty, x = x0 + 2 * tx;
     if (y < height && x < width) {  // even planes: the whole 2x2 block is inside
-      const bool wcol = img >= col_from, wc = img >= c_from;
+      const bool wcol = img >= col_from && blockIdx.y == 0, wc = img >= c_from;
       const int64_t p = (int64_t)y * width + x;
       float *colp = col + img * col_bs + p;
       const float *base = sin0 + buf * bufsz + (2 * ty) * PT_SW + 2 * tx + 3;  // window (-1, -1)
@@ -695,7 +696,8 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
       const int base_i = (int)p;
       const int plane = height * width;
 #pragma unroll
-      for (int m = 0; m < MT; ++m) {
+      for (int ml = 0; ml < MT; ++ml) {
+        const int m = m_off + ml;  // the filter (output row)
         if (m >= M) break;
         float *cp = cimg + (int64_t)m * ldc;
         float cv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -708,7 +710,7 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
         const float bv = bias ? __ldg(bias + m) : 0.0f;  // once per filter
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          float v = acc[m][e];
+          float v = acc[ml][e];
           if (beta != 0.0f) v = beta * cv[e] + v;
           if (bias) v += bv;
           o[e] = act == ACCT_ACT_LEAKY ? acct_leaky(v) : v;
@@ -748,15 +750,16 @@ extern "C" int acct_conv3x3_im2col_gemm_f32(const float *im, int64_t ld_im, int6
                                             int64_t idx_stride, int c_from, acct_stream_t stream) {
   using namespace acct;
   if (pool) {
-    // fused 2x2/2 maxpool: 2x2 pixel blocks per thread, M <= 16
-    if (!idx || M > 16 || channels < 1 || channels > 64 || (height | width) & 1 || (width & 3) ||
+    // fused 2x2/2 maxpool: 2x2 pixel blocks per thread, 16 filters per CTA
+    // (blockIdx.y = filter block), M <= 64
+    if (!idx || M > 64 || channels < 1 || channels > 64 || (height | width) & 1 || (width & 3) ||
         col_from < 0 || c_from < 0 || batch < 1 || ld_im < (int64_t)height * width ||
         ld_col < (int64_t)height * width || ldc < (int64_t)height * width ||
         ld_pool < (int64_t)(height / 2) * (width / 2) || ld_idx < (int64_t)(height / 2) * (width / 2) ||
         (reinterpret_cast<uintptr_t>(im) | reinterpret_cast<uintptr_t>(col) |
          reinterpret_cast<uintptr_t>(C)) & 15 ||
         (ld_im | im_stride | ld_col | col_stride | ldc | c_stride) & 3)
-      return fail(ACCT_ENOTSUP, "conv3x3 fused: maxpool fusion needs M <= 16, even planes");
+      return fail(ACCT_ENOTSUP, "conv3x3 fused: maxpool fusion needs M <= 64, even planes");
     const size_t smem = sizeof(float) * ((size_t)channels * 9 * 16 +
                                          2 * (size_t)channels * PT_SH * PT_SW);
     if (smem > 200 * 1024) return fail(ACCT_ENOTSUP, "conv3x3 fused: slabs exceed shared memory");
@@ -769,9 +772,11 @@ extern "C" int acct_conv3x3_im2col_gemm_f32(const float *im, int64_t ld_im, int6
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv3x3_pool_kernel, 128, smem);
     if (per_sm < 1) per_sm = 1;
-    int64_t grid = (int64_t)sm_count() * per_sm;
+    const int gy = (M + 15) / 16;
+    int64_t grid = ((int64_t)sm_count() * per_sm + gy - 1) / gy;
     if (grid > ntiles) grid = ntiles;
-    launch(conv3x3_pool_kernel, dim3((unsigned)grid), dim3(128), smem, as_stream(stream), im, ld_im,
+    launch(conv3x3_pool_kernel, dim3((unsigned)grid, (unsigned)gy), dim3(128), smem,
+           as_stream(stream), im, ld_im,
            im_stride, channels, height, width, col, ld_col, col_stride, col_from, M, A, lda, beta, C,
            ldc, c_stride, bias, act, pool, ld_pool, pool_stride, idx, ld_idx, idx_stride, c_from,
            tiles_x, (int)tpi, (int)ntiles);

@@ -331,10 +331,12 @@ int device_op(const acct_action_t &a, acct_array_t *arr, int gemm_mode, cudaStre
         const char *e = getenv("ACCT_CONV_TC_FIRST");
         return e ? atoi(e) : 0;
       }();
-      // FP32 window kernel for M <= 16 only: at M = 32 (yolov2-608 layer 0,
-      // 608x608) it ran 41.8 us/img, the tcgen05 tile with the fused pool less
+      // FP32 window kernel for M <= 16, and for pooled first layers (c <= 4)
+      // with M <= 32 (two 16-filter CTAs per tile); the unpooled M = 32 window
+      // kernel ran 41.8 us/img at 608x608
       const bool simt = gemm_mode == ACCT_GEMM_SIMT ||
-                        (gemm_mode == ACCT_GEMM_AUTO && !tc_first && M <= 16);
+                        (gemm_mode == ACCT_GEMM_AUTO && !tc_first &&
+                         (M <= 16 || (M <= 32 && C <= 4 && I[9] >= 0)));
       // I[9] / I[10]: a fused 2x2/2 maxpool of C into pool / idx; I[11] = 1:
       // C is then observable for the last image only
       const bool has_pool = I[9] >= 0;

@@ -998,7 +998,8 @@ class PatternExecutor:
                 (nimg * 8 * M * (N // 4) if pooled else 0)
             byts += 4 * M if i[7] >= 0 else 0
             # the runtime's engine choice (acct_runtime.cu, ACCT_K_CONV)
-            fp32 = self.gemm_mode == K.GEMM_SIMT or (self.gemm_mode == K.GEMM_AUTO and M <= 16)
+            fp32 = self.gemm_mode == K.GEMM_SIMT or (self.gemm_mode == K.GEMM_AUTO and (
+                M <= 16 or (M <= 32 and c <= 4 and i[9] >= 0)))
             return {"kind": "conv", "engine": "fp32-fma" if fp32 else "tcgen05",
                     "layer": op.layer, "M": M, "N": N, "K": Kd, "images": nimg,
                     "N_launch": N, "executions": execs, "flops": 2 * M * N * Kd * nimg,

@@ -514,7 +514,9 @@ def test_conv3x3_tc_fused_maxpool(cuda_device, c, h, w, M, beta, act, batch, c_f
 @pytest.mark.parametrize("c,h,w,M,beta,act,batch,c_from,col_from",
                          [(3, 416, 416, 16, 0, K.ACT_LEAKY, 2, 1, 1),
                           (3, 20, 36, 8, 1, K.ACT_NONE, 3, 0, 2),
-                          (4, 34, 40, 13, 0, K.ACT_LINEAR, 1, 0, 0)])
+                          (4, 34, 40, 13, 0, K.ACT_LINEAR, 1, 0, 0),
+                          (3, 64, 48, 32, 0, K.ACT_LEAKY, 2, 1, 1),
+                          (2, 18, 20, 28, 1, K.ACT_LEAKY, 2, 0, 1)])
 def test_conv3x3_window_fused_maxpool(cuda_device, c, h, w, M, beta, act, batch, c_from,
                                       col_from):
     """The FP32 window conv with its 2x2/2 maxpool fused (2x2 pixel blocks per

@@ -1359,7 +1359,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 //   warps 10..17 epilogue, two groups taking alternate units (+ fused maxpool)
 template <int TW>
 struct WideCfg {
-  static constexpr int TN = 128, BK = 32, S = 4, NACC = 2;
+  static constexpr int TN = 128, BK = 32, S = 5, NACC = 1;
   static constexpr int TH = 128 / TW;
   static constexpr int TWP = TW + 8;
   static constexpr int SROWS = TH + 2;

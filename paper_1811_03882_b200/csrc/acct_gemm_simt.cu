@@ -668,11 +668,6 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
             const int k = ci * 9 + kh * 3 + kw;
             const float v0 = win[kh][kw], v1 = win[kh][kw + 1];
             const float v2 = win[kh + 1][kw], v3 = win[kh + 1][kw + 1];
-            if (wcol) {
-              __stcs(reinterpret_cast<float2 *>(colp + (int64_t)k * ld_col), make_float2(v0, v1));
-              __stcs(reinterpret_cast<float2 *>(colp + (int64_t)k * ld_col + width),
-                     make_float2(v2, v3));
-            }
             const f32x2 vv[4] = {pack2(v0, v0), pack2(v1, v1), pack2(v2, v2), pack2(v3, v3)};
 #pragma unroll
             for (int g = 0; g < MT / 4; ++g) {
@@ -691,6 +686,24 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
       for (int i = 0; i < MT / 2; ++i)
 #pragma unroll
         for (int e = 0; e < 4; ++e) unpack2(acc2[i][e], acc[2 * i][e], acc[2 * i + 1][e]);
+      if (wcol) {
+        // the col rows of this 2x2 block, for the one image whose col is
+        // observable (kept out of the FMA loop: code size, not bytes)
+#pragma unroll 1
+        for (int ci = 0; ci < channels; ++ci) {
+          const float *cb = base + ci * PT_SH * PT_SW;
+#pragma unroll
+          for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+            for (int kw = 0; kw < 3; ++kw) {
+              const int64_t k = ci * 9 + kh * 3 + kw;
+              __stcs(reinterpret_cast<float2 *>(colp + k * ld_col),
+                     make_float2(cb[kh * PT_SW + kw], cb[kh * PT_SW + kw + 1]));
+              __stcs(reinterpret_cast<float2 *>(colp + k * ld_col + width),
+                     make_float2(cb[(kh + 1) * PT_SW + kw], cb[(kh + 1) * PT_SW + kw + 1]));
+            }
+        }
+      }
       float *cimg = C + img * c_bs + p;
       const int64_t pofs = (int64_t)(y >> 1) * (width >> 1) + (x >> 1);
       const int base_i = (int)p;

@@ -196,3 +196,30 @@ def test_out_dead_only_when_the_pool_is_the_sole_reader():
     assert ex._out_dead(g, fill, after, pool, {net.image_loop: {out}})
     assert not ex._out_dead(g, fill, after, pool, {ops[pool].loop_id: {out}})
     assert not ex._out_dead(g, fill, [g + 1], pool, {})   # the activation would be a reader
+
+
+def test_pool_partner_rules():
+    """_pool_partner: only a 2x2/2 maxpool with offset 0 over even planes that
+    reads the fused launch's output, right after its last member, with no
+    directive moving the output at the last member's or the pool's loop."""
+    net = build_net("yolov2-tiny")
+    ex = PatternExecutor(net, device=None)
+    ops = net.ops
+    g = next(k for k, o in enumerate(ops) if o.kind == "gemm")
+    after = [g + 1, g + 2]
+    pool = g + 3
+    on = [True] * len(ops)
+    out = ops[g].arrays["C"]
+    never = lambda i: False  # noqa: E731
+    assert ex._pool_partner(g, after, on, never) == pool
+    assert ex._pool_partner(g, after[:1], on, never) is None       # the activation sits between
+    off = list(on)
+    off[pool] = False
+    assert ex._pool_partner(g, after, off, never) is None          # the pool runs on the host
+    assert ex._pool_partner(g, after, on, lambda i: i == pool) is None
+    assert ex._pool_partner(g, after, on, lambda i: i == after[-1]) is None
+    # the 2x2/1 maxpool of layer 11 never fuses
+    p11 = next(k for k, o in enumerate(ops) if o.kind == "maxpool" and o.params["stride"] == 1)
+    g11 = max(k for k in range(p11) if ops[k].kind == "gemm")
+    assert ex._pool_partner(g11, [g11 + 1, g11 + 2], on, never) is None
+    assert out == ops[pool].arrays["X"]

@@ -1359,7 +1359,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 //   warps 10..17 epilogue, two groups taking alternate units (+ fused maxpool)
 template <int TW>
 struct WideCfg {
-  static constexpr int TN = 128, BK = 32, S = 5, NACC = 1;
+  static constexpr int TN = 128, BK = 32, S = 4, NACC = 2;  // NACC = 2: see the epilogue
   static constexpr int TH = 128 / TW;
   static constexpr int TWP = TW + 8;
   static constexpr int SROWS = TH + 2;
@@ -1558,6 +1558,9 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     }
   } else {
     // ---------------- epilogue: two groups taking alternate units ----------------
+    // (safe with NACC = 2 only: group g always drains accumulator g, so each
+    // acc barrier has one waiter; one accumulator with alternating groups
+    // would interleave parities on one barrier -- measured wrong on yolov2-608)
     const int q = warp & 3;
     const int grp = (warp - 10) >> 2;
     const int m = 32 * q + lane;

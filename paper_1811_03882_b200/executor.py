@@ -97,7 +97,7 @@ class Schedule:
 
 
 STAGE_ROW_BYTES = 4096   # the runtime stages host->device copies of shorter rows
-GATHER_BYTES = 16 << 20  # hoisted copyins are merged into copies of up to ~16 MB
+GATHER_BYTES = int(os.environ.get("ACCT_GATHER_MB", "16")) << 20  # hoisted copyins: merged copies of <= ~16 MB
 GATHER_MAX = 12          # members per merged copy (int operands of one action)
 
 

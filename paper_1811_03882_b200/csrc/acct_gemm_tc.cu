@@ -959,15 +959,16 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 // channel) whose out-of-bounds elements are zero, i.e. the conv's padding --
 // makes every operand element one LDS at  lane base + immediate.
 //   warp 0      TMA: all weight k-blocks once (resident, K-major SWIZZLE_128B),
-//               then the slab of each unit, double-buffered
-//   warp 1      TMEM allocator + MMA issuer, exactly the swap tile's 3xTF32
-//               sequence (A = activations from TMEM, B = weights hi / lo)
-//   warps 2..9  weights lo once; per k-block the activation operand (two
-//               halves of four warps take alternate k-blocks): lane = pixel,
-//               k = (channel, kh, kw) -> hi / lo to a TMEM stage (6 stages);
-//               the col array of images >= col_from stored on the way
-//   warps 10..17 epilogue, two groups taking alternate units: tcgen05.ld ->
-//               beta C, bias (staged in shared memory), leaky -> C
+//               then the slab of each unit through a ring of up to 8
+// Two independent pipelines p = 0, 1 take alternate units (j = p, p + 2, ...):
+//   warp 1 / 18 (TMEM allocator) + MMA issuer of pipeline p, exactly the swap
+//               tile's 3xTF32 sequence (A = activations from TMEM, B = weights
+//               hi / lo); two issuers because a narrow MMA is issue-bound
+//   warps 2..5 / 6..9  weights lo once (all eight); then pipeline p's
+//               activation operand: lane = pixel, k = (channel, kh, kw) ->
+//               hi / lo to one of S TMEM stages; col of images >= col_from
+//   warps 10..13 / 14..17  pipeline p's epilogue: tcgen05.ld -> beta C, bias
+//               (staged in shared memory), leaky -> C, fused 2x2 maxpool
 // Operand values, k order and MMA sequence equal im2col + the swap gemm, so
 // C is bit-identical to the unfused pair (tests/test_gpu_kernels.py).
 template <int TN, int TW>

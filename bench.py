@@ -502,6 +502,11 @@ def run_ours(args):
 
 def main():
     args = parse_args()
+    # ACCT_* variables steer dispatch, tiles, tracing or the library path:
+    # a timed run must measure the product configuration
+    overrides = sorted(k for k in os.environ if k.startswith("ACCT_"))
+    if overrides:
+        raise SystemExit(f"bench.py: refusing to run with ACCT_* overrides set: {overrides}")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -2,6 +2,12 @@
 
     python -m paper_1811_03882_b200.build          # incremental
     python -m paper_1811_03882_b200.build --force
+    python -m paper_1811_03882_b200.build --profiling   # tools/ only
+
+`--profiling` builds `libacct_sm100_prof.so` with `-DACCT_PROFILING`: the
+pipeline-analysis knobs that skip work (ACCT_SKIP in acct_common.cuh) exist
+only there; tools load it with `ACCT_LIB=<path>`.  The product library never
+contains them.
 
 CUDA sources are compiled with `-gencode arch=compute_100a,code=sm_100a
 -lineinfo -O3`; the host-loop file with g++ `-O3 -march=x86-64-v3
@@ -25,6 +31,8 @@ CSRC = PKG / "csrc"
 INCLUDE = REPO / "include"
 BUILD = PKG / "_build"
 LIB = PKG / "libacct_sm100.so"
+PROF_BUILD = PKG / "_build_prof"
+PROF_LIB = PKG / "libacct_sm100_prof.so"
 
 CUDA_SOURCES = ["acct_runtime.cu", "acct_elementwise.cu", "acct_gemm_simt.cu", "acct_gemm_tc.cu"]
 HOST_SOURCES = ["acct_host.cpp"]
@@ -55,14 +63,16 @@ def _run(cmd: list[str]):
     return proc
 
 
-def build_library(force: bool = False, verbose: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build_library(force: bool = False, verbose: bool = False, profiling: bool = False) -> Path:
+    build, lib = (PROF_BUILD, PROF_LIB) if profiling else (BUILD, LIB)
+    defs = ["-DACCT_PROFILING"] if profiling else []
+    build.mkdir(exist_ok=True)
     headers = [CSRC / h for h in HEADERS] + [INCLUDE / "acct.h"]
     objects = []
     for src in CUDA_SOURCES:
-        obj = BUILD / (src + ".o")
+        obj = build / (src + ".o")
         if force or not _newer(obj, [CSRC / src, *headers, Path(__file__)]):
-            cmd = [nvcc(), *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
+            cmd = [nvcc(), *ARCH, *defs, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
                    "-Xptxas", "-v" if verbose else "-O3", f"-I{INCLUDE}", f"-I{CSRC}",
                    "-c", str(CSRC / src), "-o", str(obj)]
             out = _run(cmd)
@@ -70,19 +80,19 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
                 sys.stderr.write(out.stderr)
         objects.append(obj)
     for src in HOST_SOURCES:
-        obj = BUILD / (src + ".o")
+        obj = build / (src + ".o")
         if force or not _newer(obj, [CSRC / src, INCLUDE / "acct.h", Path(__file__)]):
             _run(["g++", "-O3", "-march=x86-64-v3", "-ffp-contract=off", "-fPIC", "-std=c++17",
                   f"-I{INCLUDE}", "-c", str(CSRC / src), "-o", str(obj)])
         objects.append(obj)
-    if force or not _newer(LIB, objects):
-        tmp = LIB.with_suffix(".so.tmp")
+    if force or not _newer(lib, objects):
+        tmp = lib.with_suffix(".so.tmp")
         _run([nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp),
               *[str(o) for o in objects], "-lpthread", "-ldl", "-lrt"])
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build_library(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build_library(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                        profiling="--profiling" in sys.argv))

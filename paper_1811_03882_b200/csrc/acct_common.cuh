@@ -11,6 +11,17 @@
 
 #include "acct.h"
 
+// Pipeline-analysis knobs that SKIP work (operand build, MMAs, epilogue,
+// loads -- results are then wrong) exist only in the profiling build
+// (`-DACCT_PROFILING`, `python -m paper_1811_03882_b200.build --profiling`,
+// used by tools/ only).  In the product library ACCT_SKIP is a constant
+// false and those paths are compiled out.
+#ifdef ACCT_PROFILING
+#define ACCT_SKIP(word, bit) (((word) & (bit)) != 0)
+#else
+#define ACCT_SKIP(word, bit) false
+#endif
+
 namespace acct {
 
 // ---- error reporting (per host thread) ----

@@ -51,6 +51,7 @@
 #include <atomic>
 #include <mutex>
 #include <unordered_map>
+#include <vector>
 
 #include "acct_common.cuh"
 #include "acct_tc.cuh"
@@ -65,9 +66,10 @@ constexpr int THREADS = 32 * (6 + 4 * EPI_GROUPS);
 constexpr int STAGING_BYTES = EPI_GROUPS * 4 * 32 * 33 * 4;  // normal-tile epilogue transpose
 
 // bit 0: store x_hi explicitly (default 0: leave the raw FP32 value in place --
-// tcgen05 kind::tf32 reads only the TF32 bits of each operand).  Bits 1-3 are
-// profiling knobs that skip the split / MMA / epilogue work (results are then
-// wrong; tools/gemm_bench.py only).
+// tcgen05 kind::tf32 reads only the TF32 bits of each operand).  Bits 1-3
+// skip the split / MMA / epilogue work (results wrong): honoured only by the
+// -DACCT_PROFILING build of tools/gemm_bench.py (ACCT_SKIP), compiled out of
+// the product library.
 int g_write_hi = 0;
 // normal-orientation tile override (0 = cost model; tests/tools only):
 // 1 = 128x192 (A in TMEM), 2 = 128x128 BK16, 3 = 128x128 BK32, 4 = 128x256,
@@ -308,7 +310,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               const uint64_t dyl =
                   SWAP ? ptx::smem_desc(yl + 32 * k, 16, G::K_SBO, G::K_LAYOUT)
                        : ptx::smem_desc(yl + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
-              if (write_hi & 4) continue;
+              if (ACCT_SKIP(write_hi, 4)) continue;
               if (ptx::elect_one()) {
                 ptx::mma_tf32_ts(d, at + 8 * k, dyh, idesc, (kb | k) != 0);
                 ptx::mma_tf32_ts(d, at + 8 * k, dyl, idesc, 1);
@@ -337,7 +339,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               dyh = ptx::smem_desc(yh + 32 * k, 16, G::K_SBO, G::K_LAYOUT);
               dyl = ptx::smem_desc(yl + 32 * k, 16, G::K_SBO, G::K_LAYOUT);
             }
-            if (write_hi & 4) continue;
+            if (ACCT_SKIP(write_hi, 4)) continue;
             if (ptx::elect_one()) {
               ptx::mma_tf32(d, dxh, dyh, idesc, (kb | k) != 0);
               ptx::mma_tf32(d, dxh, dyl, idesc, 1);
@@ -366,7 +368,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace && ct == 0) g_trace[1][g] = clock64();
         const uint32_t xh = ptx::smem_u32(x_hi(s)), xl = ptx::smem_u32(x_lo(s));
         const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
-        if (AT && !(write_hi & 2)) {
+        if (AT && !(ACCT_SKIP(write_hi, 2))) {
           // operand A (the x tile) -> this stage's TMEM columns, hi then lo.
           // Warp q may write TMEM lanes 32q..32q+31 = MMA rows 32q + lane:
           //  normal: weight row r, its BK values from the SWIZZLE_64B K-major
@@ -422,7 +424,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             }
           }
           ptx::tmem_st_wait();
-        } else if (!(write_hi & 2)) {
+        } else if (!(ACCT_SKIP(write_hi, 2))) {
           // every load of the stage in flight before the first store
           constexpr int NX = G::X_TILE / 16 / 128;
           constexpr int NY = (G::Y_TILE / 16 + 127) / 128;
@@ -472,7 +474,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       ptx::tc_fence_after();
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * TN;
       float *part = ws + w.split * ws_split_stride;
-      if (write_hi & 8) {
+      if (ACCT_SKIP(write_hi, 8)) {
         // debug: skip the epilogue body
       } else if (!SWAP) {
         // lanes = output rows: transpose each 32x32 chunk through smem so that
@@ -734,7 +736,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const uint64_t dyl =
                 SWAP ? ptx::smem_desc(yl + 32 * k, 16, G::K_SBO, G::K_LAYOUT)
                      : ptx::smem_desc(yl + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
-            if (write_hi & 4) continue;
+            if (ACCT_SKIP(write_hi, 4)) continue;
             if (ptx::elect_one()) {
               if constexpr (LOA) {
                 // A hi = the raw K-major tile in shared memory, A lo in TMEM
@@ -775,7 +777,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           g_trace[blockIdx.x == 0 ? 1 : 5][g] = gtimer();
         const uint32_t xh = ptx::smem_u32(x_hi(s));
         const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
-        if (!(write_hi & 2)) {
+        if (!(ACCT_SKIP(write_hi, 2))) {
           // row r of the K-major A tile: 16-B chunk c at r*ROWB + (c ^ swz(r))*16,
           // swz = (r/2)%4 for SWIZZLE_64B rows, r%8 for SWIZZLE_128B rows
           // swap: activation column 32q + lane of chunk q, one conflict-free
@@ -858,7 +860,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * G::ACC;
       float *part = ws + w.split * ws_split_stride;
       const int row0 = w.m0 + 128 * rank + 32 * q;
-      if (SWAP && !(write_hi & 8)) {
+      if (SWAP && !(ACCT_SKIP(write_hi, 8))) {
         // lanes = output columns (this CTA's 128), TMEM columns = weight rows
         const int col = w.n0 + 128 * rank + 32 * q + lane;
         constexpr int CH = 16;
@@ -893,7 +895,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             for (int jj = 0; jj < CH; ++jj) __stcg(dst + (int64_t)jj * ws_ld, __uint_as_float(r[jj]));
           }
         }
-      } else if (!(write_hi & 8)) {
+      } else if (!(ACCT_SKIP(write_hi, 8))) {
         for (int c = 0; c < TN / 32; ++c) {
           uint32_t r[32];
           ptx::tmem_ld_32x32b_x32(trow + 32 * c, r);
@@ -1100,7 +1102,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   if (warp == 0) {
     // ---------------- TMA: resident weights, then the slabs ----------------
     if (lane == 0) {
-      if (dbg & 16) {
+      if (ACCT_SKIP(dbg, 16)) {
         ptx::mbar_arrive(wfull);
       } else {
         ptx::mbar_expect_tx(wfull, (uint32_t)(nkb * G::W_TILE));
@@ -1113,7 +1115,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         unit_xy(u, img, y0, x0);
         const int sb = j % nslab;
         if (j >= nslab) ptx::mbar_wait(&slab_empty[sb], ((j / nslab) - 1) & 1);
-        if (dbg & 8) {
+        if (ACCT_SKIP(dbg, 8)) {
           ptx::mbar_arrive(&slab_full[sb]);
         } else {
           ptx::mbar_expect_tx(&slab_full[sb], (uint32_t)(channels * G::CS));
@@ -1142,7 +1144,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         const uint32_t at = pbase + G::A_COL0 + s * 2 * BK;
         // one elected lane issues the k-block's 12 MMAs and the stage commit
         if (ptx::elect_one()) {
-          if (!(dbg & 2)) {
+          if (!(ACCT_SKIP(dbg, 2))) {
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {
               const uint64_t dyh = ptx::smem_desc(yh + 32 * k, 16, G::K_SBO, ptx::kLayoutSW128);
@@ -1203,7 +1205,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         if (g >= S) ptx::mbar_wait(&empty[half * S + s], ((g / S) - 1) & 1);
         if ((dbg & 64) && half == 0 && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[1][g] = clock64();
         ptx::tc_fence_after();
-        if (dbg & 1) {  // profiling knob: skip building the operand (results wrong)
+        if (ACCT_SKIP(dbg, 1)) {  // profiling knob: skip building the operand (results wrong)
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&conv[half * S + s]);
           continue;
@@ -1268,14 +1270,14 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       ptx::tc_fence_after();
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + grp * G::PCOLS + a * TN;
       const int y = y0 + py, x = x0 + px;
-      const bool live = y < height && x < width && !(dbg & 4);
+      const bool live = y < height && x < width && !(ACCT_SKIP(dbg, 4));
       const bool cst = live && img >= c_from;  // C of earlier images is dead when pooled here
       float *cp = C + img * c_bs + (int64_t)y * width + x;
       constexpr int CH = 16;
 #pragma unroll 1
       for (int cc = 0; cc < TN / CH; ++cc) {
         uint32_t r[CH];
-        if (dbg & 32) continue;
+        if (ACCT_SKIP(dbg, 32)) continue;
         ptx::tmem_ld_32x32b_x16(trow + CH * cc, r);
         const int rbase = CH * cc;
         if (rbase >= M) continue;
@@ -1309,7 +1311,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           const int l0 = (w8 / TWH) * 2 * TW + 2 * (w8 % TWH);  // window's top-left lane
           const int m0 = 32 * q + l0;
           const int wy = y0 + m0 / TW, wx = x0 + m0 % TW;
-          const bool win = wy < height && wx < width && !(dbg & 4);
+          const bool win = wy < height && wx < width && !(ACCT_SKIP(dbg, 4));
           const int64_t pofs = (int64_t)(wy >> 1) * (width >> 1) + (wx >> 1);
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
@@ -1448,10 +1450,10 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
           const int s = g % S;
           if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
           // dbg 8 / 16: skip the weight / slab load (pipeline analysis only)
-          ptx::mbar_expect_tx(&full[s], (uint32_t)((dbg & 8 ? 0 : G::W_TILE) +
-                                                   (dbg & 16 ? 0 : G::CH_PER_KB * G::CS)));
-          if (!(dbg & 8)) ptx::tma_load_2d(w_hi(s), &tmW, &full[s], kb * BK, mb * TN);
-          if (!(dbg & 16))
+          ptx::mbar_expect_tx(&full[s], (uint32_t)((ACCT_SKIP(dbg, 8) ? 0 : G::W_TILE) +
+                                                   (ACCT_SKIP(dbg, 16) ? 0 : G::CH_PER_KB * G::CS)));
+          if (!(ACCT_SKIP(dbg, 8))) ptx::tma_load_2d(w_hi(s), &tmW, &full[s], kb * BK, mb * TN);
+          if (!(ACCT_SKIP(dbg, 16)))
             ptx::tma_load_4d(slab(s), &tmX, &full[s], x0 - 4, y0 - 1, img, (kb * BK) / 9);
         }
       }
@@ -1472,7 +1474,7 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         const uint32_t yh = ptx::smem_u32(w_hi(s)), yl = ptx::smem_u32(w_lo(s));
         const uint32_t at = tmem + G::A_COL0 + s * 2 * BK;
         if (ptx::elect_one()) {
-          if (!(dbg & 2)) {
+          if (!(ACCT_SKIP(dbg, 2))) {
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {
               const uint64_t dyh = ptx::smem_desc(yh + 32 * k, 16, G::K_SBO, ptx::kLayoutSW128);
@@ -1512,7 +1514,7 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         const int k0 = kb * BK;
         const int kvalid = K - k0;
         ptx::mbar_wait(&full[s], (g / S) & 1);
-        if (!(dbg & 1)) {
+        if (!(ACCT_SKIP(dbg, 1))) {
           // weights lo of this stage (this half's 128 threads)
           const uint32_t hs = ptx::smem_u32(w_hi(s)), ls = ptx::smem_u32(w_lo(s));
 #pragma unroll
@@ -1579,7 +1581,7 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
       ptx::tc_fence_after();
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * TN;
       const int y = y0 + py, x = x0 + px;
-      const bool live = y < height && x < width && !(dbg & 4);
+      const bool live = y < height && x < width && !(ACCT_SKIP(dbg, 4));
       const bool cst = live && img >= c_from;
       const int m0 = mb * TN;  // this unit's first filter
       float *cp = C + img * c_bs + (int64_t)y * width + x;
@@ -1615,7 +1617,7 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
           const int l0 = (w8 / TWH) * 2 * TW + 2 * (w8 % TWH);
           const int mm0 = 32 * q + l0;
           const int wy = y0 + mm0 / TW, wx = x0 + mm0 % TW;
-          const bool win = wy < height && wx < width && !(dbg & 4);
+          const bool win = wy < height && wx < width && !(ACCT_SKIP(dbg, 4));
           const int64_t pofs = (int64_t)(wy >> 1) * (width >> 1) + (wx >> 1);
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
@@ -1803,9 +1805,15 @@ bool cached_map4(CUtensorMap *map, const float *ptr, uint64_t width, uint64_t he
   return true;
 }
 
-// split-K scratch, one per (device, stream) so concurrent streams never share it
+// split-K scratch, one per (device, stream) so concurrent streams never share it.
+// Grow-only, and a replaced buffer is RETIRED, never freed: a CUDA graph
+// captured earlier on this stream keeps the old pointer (executor schedule
+// cache), and replaying it after a larger uncaptured launch moved the
+// workspace must still find valid memory.  Stream order keeps the old and
+// new buffers' users apart.  The retired buffers are a few MB each.
 std::mutex g_scratch_mu;
 std::unordered_map<uint64_t, std::pair<float *, size_t>> g_scratch;
+std::vector<float *> g_scratch_retired;
 
 int scratch_for(cudaStream_t s, size_t floats, float **out) {
   int dev = 0;
@@ -1814,7 +1822,7 @@ int scratch_for(cudaStream_t s, size_t floats, float **out) {
   std::lock_guard<std::mutex> lock(g_scratch_mu);
   auto &sc = g_scratch[key];
   if (sc.second < floats) {
-    if (sc.first) cudaFree(sc.first);
+    if (sc.first) g_scratch_retired.push_back(sc.first);
     sc.first = nullptr;
     sc.second = 0;
     if (int rc = check_cuda(cudaMalloc(&sc.first, floats * sizeof(float)), "gemm_tc: workspace"))
@@ -2107,8 +2115,8 @@ int launch_conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channe
   if (units > INT32_MAX) return ACCT_ENOTSUP;
   const int sms = sm_count();
   const int grid = units < sms ? (int)units : sms;
-  static const int dbg = [] {  // profiling knob (tools/conv_probe.py): 1 no operand build,
-    const char *e = getenv("ACCT_CONV_DBG");  // 2 no MMAs, 4 no epilogue -- results wrong
+  static const int dbg = [] {  // bit 64: clock64 trace (tools/conv_trace.py); the work-skipping
+    const char *e = getenv("ACCT_CONV_DBG");  // bits 1-32 need the -DACCT_PROFILING build
     return e ? atoi(e) : 0;
   }();
   launch(tc_conv_kernel<TN, TW>, dim3(grid), dim3(CONV_NARROW_THREADS), smem, s, tw, tx, M, channels,

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <algorithm>
 #include <vector>
 
@@ -501,13 +502,12 @@ struct SideXfer {
   std::vector<cudaEvent_t> ev;
   void *dstage = nullptr;
   size_t dstage_bytes = 0;
+  std::vector<void *> retired;
   int ensure_dstage(size_t bytes, bool capturing) {
     if (bytes <= dstage_bytes) return ACCT_OK;
     if (capturing) return fail(ACCT_ENOTSUP, "early copyout scratch grows during capture");
-    if (dstage) {
-      cudaDeviceSynchronize();
-      cudaFree(dstage);
-    }
+    // retired, not freed: a graph captured earlier may still reference it
+    if (dstage) retired.push_back(dstage);
     dstage = nullptr;
     dstage_bytes = 0;
     if (int rc = check_cuda(cudaMalloc(&dstage, bytes), "early copyout scratch")) return rc;
@@ -515,23 +515,8 @@ struct SideXfer {
     return ACCT_OK;
   }
   int ensure(int n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (t && dev != device) {  // this thread moved to another device
-      for (cudaEvent_t e : ev) cudaEventDestroy(e);
-      ev.clear();
-      cudaEventDestroy(fork);
-      cudaEventDestroy(done);
-      cudaEventDestroy(dfork);
-      cudaEventDestroy(ddone);
-      cudaStreamDestroy(t);
-      cudaStreamDestroy(d);
-      t = d = nullptr;
-      dstage = nullptr;  // belongs to the old device's context; not reused
-      dstage_bytes = 0;
-    }
     if (!t) {
-      device = dev;
+      cudaGetDevice(&device);
       if (int rc = check_cuda(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking), "side stream"))
         return rc;
       if (int rc = check_cuda(cudaStreamCreateWithFlags(&d, cudaStreamNonBlocking), "d2h stream"))
@@ -551,9 +536,14 @@ struct SideXfer {
   }
 };
 
+// one set of side streams / events / early-copyout scratch per (host thread,
+// device): a GA worker thread takes whichever device is idle, and switching
+// devices must neither rebuild nor leak the other device's resources
 SideXfer &side_xfer() {
-  static thread_local SideXfer x;
-  return x;
+  static thread_local std::unordered_map<int, SideXfer> per_device;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return per_device[dev];
 }
 
 int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *actions, int n_actions,
@@ -664,6 +654,10 @@ int run_schedule(acct_array_t *arrays, int n_arrays, const acct_action_t *action
           if (timeout_s > 0 && !capturing) {
             double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
             if (el > timeout_s) {
+              // no copy may still be running on a side stream when the caller
+              // gets control back (it reuses the pinned buffers)
+              join_all();
+              join_d2h();
               cudaStreamSynchronize(s);
               return fail(ACCT_ETIMEOUT, "schedule: timeout");
             }

@@ -21,8 +21,9 @@ Config file (all keys optional except `net`):
 The program handed to `build_evaluator` must be the configured net's
 source (write it with `python -m paper_1811_03882_b200.nets <net> <dir>`).
 
-Multi-GPU: one `PatternExecutor` per device and a queue of idle devices; a
-GA with `workers = len(devices)` measures one individual per GPU at a time.
+Multi-GPU: one `PatternExecutor` per entry of `devices` and a queue of idle
+entries; a GA with `workers = len(devices)` measures one individual per
+entry at a time (a device may be listed more than once).
 Fitness values are gathered by the GA's order-preserving `pool.map`, so the
 search stays deterministic given the measurements.  No collective is needed
 (nothing crosses between GPUs).
@@ -93,49 +94,61 @@ def resolve_devices(spec) -> list[int]:
 
 
 class DevicePool:
-    """One PatternExecutor per device; `measure(bits)` borrows an idle one."""
+    """One PatternExecutor per SLOT of `devices`; `measure(bits)` borrows an
+    idle slot.  A device listed twice (e.g. `[0, 0]`) gets two independent
+    executors -- own buffers, stream, pinned arena and schedule cache -- so
+    two GA workers never share one; each executor is also guarded by its own
+    lock."""
 
     def __init__(self, cfg: GpuEvaluatorConfig):
         from .executor import PatternExecutor
         self.cfg = cfg
         self.net = build_net(cfg.net, images=cfg.images)
         self.devices = resolve_devices(cfg.devices)
-        self.executors = {}
-        for d in self.devices:
-            self.executors[d] = PatternExecutor(self.net, device=d, seed=cfg.seed, fuse=cfg.fuse,
-                                                gemm_mode=_GEMM_MODES[cfg.gemm])
+        self.executors = [PatternExecutor(self.net, device=d, seed=cfg.seed, fuse=cfg.fuse,
+                                          gemm_mode=_GEMM_MODES[cfg.gemm]) for d in self.devices]
+        self.locks = [threading.Lock() for _ in self.devices]
         self.idle: queue.Queue = queue.Queue()
-        for d in self.devices:
-            self.idle.put(d)
+        for slot in range(len(self.devices)):
+            self.idle.put(slot)
         self.log_lock = threading.Lock()
         self.log: list[dict] = []
+        self.capture_outputs = False   # tests: keep each measured genome's output slots
 
     def measure(self, bits: str) -> Measurement:
-        dev = self.idle.get()
+        slot = self.idle.get()
         try:
-            ex = self.executors[dev]
-            sched = ex.compile(bits)
-            for _ in range(self.cfg.warmup):
-                r = ex.run(sched, timeout_s=self.cfg.timeout_seconds)
-                if r.status == TIMEOUT:
-                    return self._record(bits, dev, None, r, Measurement(self.cfg.penalty_seconds, TIMEOUT))
-            times = []
-            last = None
-            for _ in range(self.cfg.repeats):
-                last = ex.run(sched, timeout_s=self.cfg.timeout_seconds)
-                if last.status == TIMEOUT or last.seconds > self.cfg.timeout_seconds:
-                    return self._record(bits, dev, None, last,
-                                        Measurement(self.cfg.penalty_seconds, TIMEOUT))
-                times.append(last.seconds)
-            secs = statistics.median(times)
-            return self._record(bits, dev, times, last, Measurement(secs, MEASURED))
+            with self.locks[slot]:
+                return self._measure(slot, bits)
         finally:
-            self.idle.put(dev)
+            self.idle.put(slot)
 
-    def _record(self, bits, dev, times, run, m: Measurement) -> Measurement:
+    def _measure(self, slot: int, bits: str) -> Measurement:
+        ex = self.executors[slot]
+        sched = ex.compile(bits)
+        for _ in range(self.cfg.warmup):
+            r = ex.run(sched, timeout_s=self.cfg.timeout_seconds)
+            if r.status == TIMEOUT:
+                return self._record(bits, slot, None, r, Measurement(self.cfg.penalty_seconds, TIMEOUT))
+        times = []
+        last = None
+        for _ in range(self.cfg.repeats):
+            last = ex.run(sched, timeout_s=self.cfg.timeout_seconds)
+            if last.status == TIMEOUT or last.seconds > self.cfg.timeout_seconds:
+                return self._record(bits, slot, None, last,
+                                    Measurement(self.cfg.penalty_seconds, TIMEOUT))
+            times.append(last.seconds)
+        secs = statistics.median(times)
+        return self._record(bits, slot, times, last, Measurement(secs, MEASURED), sched)
+
+    def _record(self, bits, slot, times, run, m: Measurement, sched=None) -> Measurement:
+        entry = {"genome": bits, "device": self.devices[slot], "slot": slot, "times": times,
+                 "counters": run.counters if run else None, "status": m.status,
+                 "expected": sched.expected if sched is not None else None}
+        if self.capture_outputs and sched is not None:
+            entry["outputs"] = self.executors[slot].outputs()
         with self.log_lock:
-            self.log.append({"genome": bits, "device": dev, "times": times,
-                             "counters": run.counters if run else None, "status": m.status})
+            self.log.append(entry)
         return m
 
 
@@ -149,9 +162,10 @@ def make_gpu_evaluator(cfg: GpuEvaluatorConfig, program, tree, accesses, genome_
         return pool.measure(bits)
 
     def report_section(best_bits: str) -> dict:
-        ex = pool.executors[pool.devices[0]]
-        sched = ex.compile(best_bits)
-        run = ex.run(sched)
+        ex = pool.executors[0]
+        with pool.locks[0]:
+            sched = ex.compile(best_bits)
+            run = ex.run(sched)
         return {"net": cfg.net, "images": ex.images, "devices": pool.devices,
                 "best_seconds_rerun": run.seconds,
                 "img_per_s": ex.images / run.seconds,

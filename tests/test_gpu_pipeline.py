@@ -61,3 +61,54 @@ def test_ga_over_gpu_pool_finds_faster_than_all_cpu(cuda_device, tmp_path):
     all_cpu = ev("0" * len(gm)).seconds
     assert res.best.status == "measured"
     assert res.best.seconds <= all_cpu * 1.5
+
+
+def test_ga_two_workers_on_one_gpu(cuda_device):
+    """Multi-device readiness on one GPU: `devices: [0, 0]` gives two
+    independent executors (own buffers, stream, pinned arena), the GA's
+    thread pool (`workers = 2`, reference `ga.py:210-214`) measures on both at
+    once, and every measured genome's counters and outputs are right.  With
+    a fitness that depends only on the genome (the measured run still happens
+    on the pool), the search result is independent of the worker count."""
+    import numpy as np
+
+    from oracle import cprog
+    from paper_1811_03882_b200.gpu_evaluator import GpuEvaluatorConfig, make_gpu_evaluator
+    from paper_1811_03882_b200.legality import profile_from_dict
+    from paper_1811_03882_b200.nets import build_net
+    net = build_net("demo")
+    want = cprog.reference_forward(net)["outputs"]
+    prog = at.parse(net.source)
+    tree = at.build_loop_tree(prog)
+    acc = at.extract_accesses(prog)
+    gm = at.build_genome_map(at.check_all_parallelizable(tree, acc))
+    prof = profile_from_dict(net.profile_dict(), "demo", tree)
+    results = {}
+    for workers in (1, 2):
+        ev = make_gpu_evaluator(GpuEvaluatorConfig(net="demo", devices=[0] * workers, repeats=1,
+                                                   warmup=0), prog, tree, acc, gm, prof)
+        pool = ev.pool
+        assert len(pool.executors) == workers
+        assert len({id(e) for e in pool.executors}) == workers
+        pool.capture_outputs = True
+
+        def det(bits, ev=ev):
+            m = ev(bits)
+            assert m.status == "measured"
+            return at.Measurement(1e-3 * (1 + bits.count("0")) + 1e-6 * int(bits, 2), "measured")
+
+        res = at.run_ga(at.GAConfig(population=8, generations=4, rng_seed=5, workers=workers),
+                        gm, tree, det, at.MeasurementCache())
+        assert pool.log and {e["slot"] for e in pool.log} <= set(range(workers))
+        for e in pool.log:
+            assert e["counters"] is not None
+            for key, val in e["expected"].items():
+                assert e["counters"][key] == val, (e["genome"], key)
+            err = float(np.abs(e["outputs"] - want).max())
+            assert err <= 1e-4 * float(np.abs(want).max()), e["genome"]
+        if workers == 2:
+            assert {e["slot"] for e in pool.log} == {0, 1}
+        results[workers] = (res.best.genome, res.best.seconds,
+                            [(h.best_seconds, h.evaluations_performed) for h in res.history],
+                            res.evaluations_performed)
+    assert results[1] == results[2]

@@ -239,6 +239,44 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------ verification
+def golden_entry(net_name: str, images: int, first_image: int):
+    """The reference CPU path's recorded outputs for this 16-image loop
+    (tests/golden/cnn_outputs_big.json + .npy, written by
+    tests/golden/make_cnn_golden.py through the reference's
+    `command_evaluate`), or None when this workload has no record."""
+    import numpy as np
+    path = REPO / "tests" / "golden" / "cnn_outputs_big.json"
+    if first_image != 0 or not path.exists():
+        return None
+    entry = json.loads(path.read_text()).get(net_name)
+    if entry is None or entry["images"] != images or entry["seed"] != 1:
+        return None
+    full = {int(b): np.load(path.parent / f) for b, f in entry["full_images"].items()}
+    return entry, full
+
+
+def verify_outputs(what: str, outputs, golden) -> dict:
+    """Outputs of a timed leg against the reference's recorded outputs
+    (tolerance.py).  A mismatch ends the run with a non-zero exit and no
+    bench line."""
+    from paper_1811_03882_b200 import tolerance
+    if golden is None:
+        return {"checked": False, "why": "no recorded reference outputs for this workload/shard"}
+    try:
+        st = tolerance.check_golden(outputs, *golden)
+    except AssertionError as exc:
+        sys.stderr.write(f"bench.py: {what} outputs differ from the reference CPU path: {exc}\n")
+        raise SystemExit(3)
+    return {"checked": True, "against": "tests/golden/cnn_outputs_big.json (reference "
+            "command_evaluate of the gcc-compiled program)",
+            "tolerance": {"max_rel": tolerance.REL, "floor": tolerance.FLOOR,
+                          "norm_rel": tolerance.NORM},
+            **{k: v for k, v in st.items() if not isinstance(v, dict)},
+            "full_images": {k: {"max_rel": v["max_rel"], "norm_rel": v["norm_rel"]}
+                            for k, v in st.items() if isinstance(v, dict)}}
+
+
 # -------------------------------------------------------------------- ours
 def ncu_traffic(shape: str):
     """dram bytes (read + write) per launch of the kernel launch with this
@@ -445,6 +483,13 @@ def run_ours(args):
     for key, val in full.expected.items():
         if counters[key] != val:
             raise SystemExit(f"transfer counter mismatch {key}: {counters[key]} != {val}")
+    # the last timed e2e step's outputs, then the resident leg's (one more
+    # untimed run: the timed loop above ran the e2e schedule last)
+    golden = golden_entry(args.net, args.images, shard.first)
+    verified = {"e2e": verify_outputs("e2e", ex.outputs(), golden)}
+    if res.batch == args.images:
+        ex.run(res)
+        verified["value"] = verify_outputs("resident", ex.device_outputs(), golden)
 
     if rank != 0:
         if world > 1:
@@ -493,6 +538,7 @@ def run_ours(args):
             "h2d_bytes": counters["h2d_bytes"] / args.images,
             "d2h_bytes": counters["d2h_bytes"] / args.images},
         "ga_search": ga,
+        "outputs_verified": verified,
         "value_step_ms": step_ms, "e2e_step_s": walls,
     }
     print(json.dumps(line), flush=True)

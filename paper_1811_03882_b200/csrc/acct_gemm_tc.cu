@@ -588,8 +588,21 @@ __device__ __forceinline__ long long gtimer() {
 // LOA: only A lo goes to TMEM (BK columns per stage instead of 2 BK); the MMAs
 // with A hi read the raw K-major tile from shared memory -- leaves TMEM room
 // for DUAL with BK = 32
-template <int TN, int NACC_, int BK_, bool SWAP_ = false, bool DUAL_ = false, bool LOA_ = false>
+// PK > 0 (chunked promotion): the k-loop of a unit is cut into chunks of PK
+// k-blocks; each chunk accumulates into a FRESH TMEM accumulator (two,
+// ping-pong, NACC = 2) and BOTH epilogue groups add the finished chunk into
+// an FP32 running sum in registers (group g: columns g TN/2 .. of its 128
+// rows), rounding to nearest.  The tensor core's truncating accumulate then
+// compounds over PK k-blocks instead of the whole K (K = 9216: 48 vs 1152
+// truncations of the big accumulator) -- the long-K layers' error falls
+// ~20x below DUAL's.  The unit's final store overlaps the next unit's first
+// chunk (the other accumulator).
+template <int TN, int NACC_, int BK_, bool SWAP_ = false, bool DUAL_ = false, bool LOA_ = false,
+          int PK_ = 0>
 struct Cfg2 {
+  static constexpr int PK = PK_;
+  static_assert(PK_ == 0 || (!SWAP_ && !DUAL_ && NACC_ == 2 && TN == 192),
+                "chunked promotion: normal 192-wide pair tile, two accumulators");
   static constexpr bool SWAP = SWAP_;
   static constexpr bool DUAL = DUAL_;
   static constexpr bool LOA = LOA_;
@@ -616,14 +629,14 @@ struct Cfg2 {
   static_assert(STAGES >= 2, "pipeline too shallow");
 };
 
-template <int TN, int NACC, int BK_, bool SWAP, bool DUAL = false, bool LOA = false>
+template <int TN, int NACC, int BK_, bool SWAP, bool DUAL = false, bool LOA = false, int PK = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 int M, int N, int K, int nt, int mt, int splits, int kb_per, int write_hi,
                 float alpha, float beta, float *__restrict__ C, int64_t ldc,
                 const float *__restrict__ bias, int act, float *__restrict__ ws, int64_t ws_ld,
                 int64_t ws_split_stride) {
-  using G = Cfg2<TN, NACC, BK_, SWAP, DUAL, LOA>;
+  using G = Cfg2<TN, NACC, BK_, SWAP, DUAL, LOA, PK>;
   constexpr int S = G::STAGES, BK = G::BK;
   static_assert(!LOA || !SWAP, "LOA is for the normal orientation");
   extern __shared__ uint8_t smem_raw[];
@@ -665,7 +678,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
     for (int a = 0; a < NACC; ++a) {
       ptx::mbar_init(&acc_full[a], 1);
-      ptx::mbar_init(&acc_empty[a], 8);
+      ptx::mbar_init(&acc_empty[a], PK ? 16 : 8);  // epilogue warps of both CTAs
     }
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tmA);
@@ -709,7 +722,55 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader only; whole warp, one lane issues) ----------------
-    if (rank == 0) {
+    if (rank == 0 && PK > 0) {
+      // chunked promotion: chunk c (counted across units) -> accumulator c & 1
+      constexpr uint32_t idesc = ptx::idesc_tf32(256, TN, false, true);
+      int g = 0, c = 0;
+      for (int u = pair; u < units; u += pairs) {
+        const Unit w = unit(u);
+        uint32_t d = tmem;
+        for (int kb = 0; kb < w.nkb; ++kb, ++g) {
+          const int kc = kb % (PK > 0 ? PK : 1);
+          if (kc == 0) {
+            if (c >= 2) ptx::mbar_wait_cluster(&acc_empty[c & 1], ((c >> 1) - 1) & 1);
+            ptx::tc_fence_after();
+            d = tmem + (c & 1) * G::ACC;
+          }
+          const int s = g % S;
+          ptx::mbar_wait(&conv[s], (g / S) & 1);
+          ptx::tc_fence_after();
+          const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
+          const uint32_t at = tmem + G::A_COL0 + s * G::A_STAGE_COLS;
+          const uint32_t xhs = ptx::smem_u32(x_hi(s));
+#pragma unroll
+          for (int k = 0; k < BK / 8; ++k) {
+            const uint64_t dyh = ptx::smem_desc(yh + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
+            const uint64_t dyl = ptx::smem_desc(yl + 1024 * k, G::MN_CHUNK, 512, ptx::kLayoutSW128Base32B);
+            if (ACCT_SKIP(write_hi, 4)) continue;
+            if (ptx::elect_one()) {
+              if constexpr (LOA) {
+                const uint64_t dxh = ptx::smem_desc(xhs + 32 * k, 16, G::K_SBO, G::K_LAYOUT);
+                ptx::mma2_tf32_ss(d, dxh, dyh, idesc, (kc | k) != 0);
+                ptx::mma2_tf32_ss(d, dxh, dyl, idesc, 1);
+                ptx::mma2_tf32_ts(d, at + 8 * k, dyh, idesc, 1);
+              } else {
+                ptx::mma2_tf32_ts(d, at + 8 * k, dyh, idesc, (kc | k) != 0);
+                ptx::mma2_tf32_ts(d, at + 8 * k, dyl, idesc, 1);
+                ptx::mma2_tf32_ts(d, at + BK + 8 * k, dyh, idesc, 1);
+              }
+            }
+            __syncwarp();
+          }
+          if (ptx::elect_one()) ptx::mma2_commit_multicast(&empty[s], 0x3);
+          __syncwarp();
+          if (kc == PK - 1 || kb == w.nkb - 1) {
+            if (ptx::elect_one()) ptx::mma2_commit_multicast(&acc_full[c & 1], 0x3);
+            __syncwarp();
+            ++c;
+          }
+        }
+      }
+    } else if (rank == 0) {
       constexpr uint32_t idesc = ptx::idesc_tf32(256, TN, false, !SWAP);
       int g = 0, j = 0;
       for (int u = pair; u < units; u += pairs, ++j) {
@@ -839,6 +900,71 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (lane == 0) ptx::mbar_arrive_remote(conv_leader + 8 * s);
         if ((write_hi & 16) && blockIdx.x < 2 && g < kTrace && ct == 0)
           g_trace[blockIdx.x == 0 ? 2 : 6][g] = gtimer();
+      }
+    }
+  } else if constexpr (PK > 0) {
+    // ---------------- epilogue, chunked promotion (both CTAs, both groups) ----------------
+    // group grp owns columns grp HC .. of the CTA's 128 rows: every chunk is
+    // added into an FP32 running sum in registers, then the sum goes out
+    // through the warp's staging transpose like the plain epilogue
+    constexpr int HC = TN / 2;
+    const int q = warp & 3;
+    const int grp = (warp - 6) / 4;
+    const uint32_t stg_s = ptx::smem_u32(staging + (grp * 4 + q) * (32 * 33));
+    const uint32_t acc_empty_leader = ptx::mapa(ptx::smem_u32(&acc_empty[0]), 0);
+    int c = 0;
+    for (int u = pair; u < units; u += pairs) {
+      const Unit w = unit(u);
+      const int nch = (w.nkb + PK - 1) / PK;
+      float acc[HC];
+#pragma unroll
+      for (int i = 0; i < HC; ++i) acc[i] = 0.0f;
+      for (int ci = 0; ci < nch; ++ci, ++c) {
+        const int a = c & 1;
+        ptx::mbar_wait_sleepy(&acc_full[a], (c >> 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * G::ACC + grp * HC;
+#pragma unroll
+        for (int p = 0; p < HC / 16; ++p) {
+          uint32_t r[16];
+          ptx::tmem_ld_32x32b_x16(trow + 16 * p, r);
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) acc[16 * p + jj] += __uint_as_float(r[jj]);
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(acc_empty_leader + 8 * a);
+      }
+      if (ACCT_SKIP(write_hi, 8)) continue;
+      float *part = ws + w.split * ws_split_stride;
+      const int row0 = w.m0 + 128 * rank + 32 * q;
+#pragma unroll
+      for (int cb = 0; cb < HC / 32; ++cb) {
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) ptx::sts32(stg_s + 4 * (lane * 33 + jj), acc[32 * cb + jj]);
+        __syncwarp();
+        const int col = w.n0 + grp * HC + 32 * cb + lane;
+        if (splits == 1) {
+          if (col < N) {
+#pragma unroll 4
+            for (int i = 0; i < 32; ++i) {
+              const int row = row0 + i;
+              if (row < M) {
+                // one broadcast load per row (every lane reads the same bias)
+                const float bv = bias ? __ldg(bias + row) : 0.0f;
+                const float cv = beta != 0.0f ? C[(int64_t)row * ldc + col] : 0.0f;
+                C[(int64_t)row * ldc + col] =
+                    finish(ptx::lds32(stg_s + 4 * (i * 33 + lane)), alpha, beta, cv, bias, bv, act);
+              }
+            }
+          }
+        } else {
+          float *dst = part + (int64_t)row0 * ws_ld + col;
+#pragma unroll 8
+          for (int i = 0; i < 32; ++i)
+            __stcg(dst + (int64_t)i * ws_ld, ptx::lds32(stg_s + 4 * (i * 33 + lane)));
+        }
+        __syncwarp();
       }
     }
   } else {
@@ -1930,11 +2056,12 @@ int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, con
   return ACCT_OK;
 }
 
-template <int TN, int NACC, int BK, bool SWAP = false, bool DUAL = false, bool LOA = false>
+template <int TN, int NACC, int BK, bool SWAP = false, bool DUAL = false, bool LOA = false,
+          int PK = 0>
 int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
                int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
                cudaStream_t s) {
-  using G = Cfg2<TN, NACC, BK, SWAP, DUAL, LOA>;
+  using G = Cfg2<TN, NACC, BK, SWAP, DUAL, LOA, PK>;
   CUtensorMap ta, tb;
   // weights: K-major box of BK x (128 rows, or TN/2 rows per CTA when swapped)
   if (!cached_map(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BK, SWAP ? TN / 2 : 128,
@@ -1961,7 +2088,7 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(mu);
     if (dev >= 0 && dev < 64 && !done[dev]) {
-      if (int rc = check_cuda(cudaFuncSetAttribute(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA>,
+      if (int rc = check_cuda(cudaFuncSetAttribute(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA, PK>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    G::SMEM_BYTES),
                               "gemm_tc2: smem attribute"))
@@ -1970,7 +2097,7 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
     }
   }
   const int pairs = units < pairs_avail ? units : pairs_avail;
-  launch(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA>, dim3(2 * pairs), dim3(THREADS), G::SMEM_BYTES, s, ta, tb, M,
+  launch(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA, PK>, dim3(2 * pairs), dim3(THREADS), G::SMEM_BYTES, s, ta, tb, M,
          N, K, nt, mt, splits, kb_per, g_write_hi, alpha, beta, C, ldc, bias, act, ws, ws_ld,
          rows * ws_ld);
   if (int rc = note_launch("gemm_tc2")) return rc;
@@ -2040,15 +2167,22 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
   const double c9 = waste * (double)tile_cost2(M, N, K, 192, 32, sms / 2);
   const double c10 = waste * (double)tile_cost2(M, N, K, 256, 32, sms / 2);
   // Long K: the tensor core's truncating FP32 accumulate compounds (3xTF32
-  // relative error ~1e-5 at K = 4608, enough to reach 1e-4 through the 26
-  // layers of yolov2-608); above kDualK (768: every pair-tile layer of the
-  // nets but the shortest) the pair tile keeps the small terms in
-  // a second accumulator (3x less error) and, to leave TMEM for it at BK 32,
-  // only A lo in TMEM (A hi read from shared memory): L12 128 us vs 127 us
-  // without the second accumulator (tools/tile_diag.py, gemm_bench.py)
+  // relative error ~1e-5 at K = 4608, enough to pass 1e-4 through the 26
+  // layers of yolov2-608: 1.46e-4 at 16 images with a second accumulator for
+  // the small terms, "DUAL", force 16).  Above kDualK (768: every pair-tile
+  // layer of the nets but the shortest) the pair tile promotes the
+  // accumulator every 4 k-blocks into an FP32 register sum (PK = 4, only A lo
+  // in TMEM): yolov2-608 5.5e-5, yolov2-tiny 1.6e-5 (was 3.7e-5), and 3%
+  // faster than DUAL (its single accumulator stalled the MMAs at every unit
+  // boundary).  Chunks of 2 / 1 k-blocks: 4.9e-5 / 4.6e-5 at 17% / 37% more
+  // time -- the remaining error is elsewhere (tools/err_dist.py).
   constexpr int kDualK = 768;
-  if ((c10 < c1 || c9 < c1) && K > kDualK)
-    return launch_tc2<192, 1, 32, false, true, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  if ((c10 < c1 || c9 < c1) && K > kDualK) {
+    if (force == 16)  // the previous default (DUAL, no promotion), for comparison
+      return launch_tc2<192, 1, 32, false, true, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+
+    return launch_tc2<192, 2, 32, false, false, true, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
+  }
   if (c10 < c9 && c10 < c1)
     return launch_tc2<256, 1, 32>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if (c9 < c1)

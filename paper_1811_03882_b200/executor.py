@@ -1029,6 +1029,21 @@ class PatternExecutor:
         view = priv[(p - 1) * slot.img_stride:].as_strided((rows, cols), (slot.ld_dev, 1))
         return view.cpu().numpy().reshape(spec.shape)
 
+    def device_outputs(self) -> np.ndarray:
+        """(images, C, H*W) of the output array's private device copies after
+        a batched run whose one batch is every image (the resident leg of the
+        benchmark: no output slots are written there)."""
+        p = self._last_table
+        name = self.net.output_name
+        priv = self._bdev.get(p, {}).get(name)
+        if priv is None or p != self.images:
+            raise DeviceError("device_outputs: needs a batched run over all images at once")
+        spec = self.net.arrays[name]
+        rows, cols = spec.shape
+        slot = self._tables[p][0][self.slot_of[name]]
+        view = priv.as_strided((p, rows, cols), (slot.img_stride, slot.ld_dev, 1))
+        return view.cpu().numpy().copy()
+
     def host_array(self, name: str) -> np.ndarray:
         spec = self.net.arrays[name]
         return self.host[name].numpy().reshape(spec.shape).copy()

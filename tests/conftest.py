@@ -45,3 +45,13 @@ def cuda_device():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda:0")
+
+
+@lru_cache(maxsize=None)
+def big_golden(name: str):
+    """(entry, {image index: full output}) of tests/golden/cnn_outputs_big.json:
+    the reference CPU path's outputs for a benchmarked 16-image loop."""
+    import numpy as np
+    entry = json.loads((GOLDEN / "cnn_outputs_big.json").read_text())[name]
+    full = {int(b): np.load(GOLDEN / f) for b, f in entry["full_images"].items()}
+    return entry, full

@@ -79,3 +79,27 @@ def test_oracle_maxpool_edge_semantics(orc):
     i = np.empty((1, 4), dtype=np.int32)
     orc.orc_maxpool(y.ctypes.data, 1, 1, 2, 2, 2, 2, 1, o.ctypes.data, i.ctypes.data)
     assert o[0, 0] == 0.0 and i[0, 0] == 0
+
+
+@pytest.mark.parametrize("name", ["yolov2-tiny", "yolov2-608"])
+def test_oracle_matches_reference_golden_of_benchmarked_nets(name):
+    """The oracle composition equals, bit for bit, the outputs the reference's
+    `command_evaluate` recorded for the 16-image loops bench.py times
+    (tests/golden/make_cnn_golden.py): the first and last image in full and
+    every sample entry that falls in them."""
+    from conftest import big_golden
+    entry, full = big_golden(name)
+    images = entry["images"]
+    net = build_net(name, images=images)
+    ids = sorted(full)
+    got = cprog.reference_forward(net, workers=len(ids), image_ids=ids)["outputs"]
+    per = int(np.prod(entry["shape"][1:]))
+    stride = entry["sample_stride"]
+    for k, b in enumerate(ids):
+        assert np.array_equal(got[k], full[b]), b
+        lo, hi = b * per, (b + 1) * per
+        first = -(-lo // stride)
+        for j in range(first, -(-hi // stride)):
+            assert float(got[k].ravel()[j * stride - lo]) == entry["sample"][j]
+        flat = got[k].astype(np.float64).ravel()
+        assert float(flat.sum()) == pytest.approx(entry["per_image_sum"][b], rel=0, abs=1e-9)

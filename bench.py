@@ -62,6 +62,9 @@ def parse_args():
                     help="images per launch of the image loop's body (0 = all images of a "
                          "step, 1 = image at a time)")
     ap.add_argument("--no-ga", action="store_true")
+    ap.add_argument("--quick", action="store_true",
+                    help="main leg + demo GA only (skip yolov2-608, image-at-a-time and the "
+                         "paper-scale GA)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-images", type=int, default=2, help="images per CPU process per step")
     return ap.parse_args()
@@ -199,6 +202,7 @@ def cpu_baseline(net_name: str, images: int, steps: int = 1) -> dict:
         single = min(cpu_step(binary, 1)[1])
     t = statistics.median(worst)
     return {"value": procs * images / t, "unit": "img/s", "cores": procs, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"{procs} concurrent processes x {images} images of the gcc -O3 "
                       f"-march=native all-zero-genome {net_name} C-subset program (the "
                       f"reference cmd: CPU path), median of {steps} step(s)",
@@ -375,55 +379,132 @@ def roofline(ex, sched, steps: int, flush, peaks: dict) -> dict:
     return out
 
 
-def ga_search(devices) -> dict:
-    from paper_1811_03882_b200 import (GAConfig, MeasurementCache, build_genome_map,
-                                       build_loop_tree, check_all_parallelizable,
-                                       extract_accesses, parse, run_ga)
-    from paper_1811_03882_b200.gpu_evaluator import GpuEvaluatorConfig, make_gpu_evaluator
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _net_program(net_name: str, images: int | None = None):
+    from paper_1811_03882_b200 import (build_genome_map, build_loop_tree,
+                                       check_all_parallelizable, extract_accesses, parse)
     from paper_1811_03882_b200.legality import profile_from_dict
     from paper_1811_03882_b200.nets import build_net
-    net = build_net("demo")
+    net = build_net(net_name, images=images)
     prog = parse(net.source)
     tree = build_loop_tree(prog)
     acc = extract_accesses(prog)
     gm = build_genome_map(check_all_parallelizable(tree, acc))
-    prof = profile_from_dict(net.profile_dict(), "demo", tree)
-    cfg = GpuEvaluatorConfig(net="demo", devices=devices, repeats=3, warmup=1)
-    ga = GAConfig(population=4, generations=2, rng_seed=1, workers=len(devices))
+    prof = profile_from_dict(net.profile_dict(), net_name, tree)
+    return net, prog, tree, acc, gm, prof
+
+
+def ga_gpu(net_name: str, images: int | None, devices, pop: int, gens: int, seed: int,
+           warmup: int, repeats: int) -> dict:
+    """The GA (reference run_ga semantics, ga.py:170-282) with the gpu:
+    evaluator: every individual's offload pattern executed on B200, one
+    executor per GPU, workers = GPUs."""
+    from paper_1811_03882_b200 import GAConfig, MeasurementCache, run_ga
+    from paper_1811_03882_b200.gpu_evaluator import GpuEvaluatorConfig, make_gpu_evaluator
+    net, prog, tree, acc, gm, prof = _net_program(net_name, images)
+    cfg = GpuEvaluatorConfig(net=net_name, images=images, devices=devices, repeats=repeats,
+                             warmup=warmup)
+    ga = GAConfig(population=pop, generations=gens, rng_seed=seed, workers=len(devices))
     t0 = time.perf_counter()
     ev = make_gpu_evaluator(cfg, prog, tree, acc, gm, prof)
     setup = time.perf_counter() - t0
     t1 = time.perf_counter()
     res = run_ga(ga, gm, tree, ev, MeasurementCache())
     wall = time.perf_counter() - t1
-    return {"config": "demo net (1x3x64x64 conv16+leaky+maxpool, 8 images), pop 4 x 2 gens, seed 1",
+    a = len(gm)
+    return {"config": f"{net_name} ({a} genes, {net.spec.images} image(s) per evaluation), "
+                      f"pop {pop} x {gens} gens, seed {seed}, {len(devices)} GPU(s) = workers, "
+                      f"warm-up {warmup} + median of {repeats} run(s) per evaluation",
             "wall_s": wall, "setup_s": setup, "evaluations": res.evaluations_performed,
+            "cache_hits": res.cache_hits, "seconds_per_evaluation": wall / max(1, res.evaluations_performed),
             "best_genome": res.best.genome, "best_seconds": res.best.seconds,
-            "all_zero_seconds": ev.pool.measure("0" * len(gm)).seconds}
+            "all_one_seconds": ev.pool.measure("1" * a).seconds,
+            "all_zero_seconds": ev.pool.measure("0" * a).seconds,
+            "history": [{"gen": h.generation, "best_seconds": h.best_seconds,
+                         "evals": h.evaluations_performed} for h in res.history]}
 
 
-def run_ours(args):
+def ga_reference(net_name: str, images: int | None, pop: int, gens: int, seed: int,
+                 workers: int) -> dict:
+    """The reference's GA CPU path: run_ga over the `cmd:` evaluator
+    (pipeline.py:136-148, evaluation.py:162-196) -- each individual's
+    emitted source compiled by gcc (which ignores the OpenACC pragmas, so
+    every pattern runs on the CPU) and timed as a subprocess; `workers`
+    concurrent evaluations on the host cores.  Bounded to `gens`
+    generations; per-evaluation seconds are the comparison."""
+    from oracle import cprog  # reference CPU path harness (test infrastructure)
+    from paper_1811_03882_b200 import GAConfig, MeasurementCache, run_ga
+    from paper_1811_03882_b200.measure import CommandEvaluatorConfig
+    from paper_1811_03882_b200.tuner import make_cmd_evaluator
+    net, prog, tree, acc, gm, prof = _net_program(net_name, images)
+    with tempfile.TemporaryDirectory() as tmp:
+        t = Path(tmp)
+        cprog.write_program(net, t)
+        cfg = CommandEvaluatorConfig(compile_cmd=cprog.compile_cmd(t), run_cmd="'{bin}'",
+                                     timeout_seconds=600.0, workdir=str(t))
+        inner = make_cmd_evaluator(cfg, prog, tree, acc, gm)
+        calls, lock = [], threading.Lock()
+
+        def ev(bits):
+            t = time.perf_counter()
+            m = inner(bits)
+            with lock:
+                calls.append((time.perf_counter() - t, m.seconds))
+            return m
+
+        t0 = time.perf_counter()
+        res = run_ga(GAConfig(population=pop, generations=gens, rng_seed=seed, workers=workers,
+                              timeout_seconds=600.0), gm, tree, ev, MeasurementCache())
+        wall = time.perf_counter() - t0
+    n = max(1, res.evaluations_performed)
+    return {"config": f"{net_name} ({len(gm)} genes, {net.spec.images} image(s) per "
+                      f"evaluation), pop {pop} x {gens} gen(s) (bounded), seed {seed}, "
+                      f"{workers} concurrent evaluations on host cores; gcc -O2 cmd: evaluator",
+            "kind": "port", "cores": workers, "cpu_model": cpu_model(),
+            "wall_s": wall, "evaluations": res.evaluations_performed,
+            "seconds_per_evaluation": wall / n,
+            "evaluation_latency_s": statistics.median([c[0] for c in calls]) if calls else None,
+            "program_run_s": statistics.median([c[1] for c in calls]) if calls else None,
+            "best_seconds": res.best.seconds}
+
+
+def make_flush(torch, device):
+    return torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+
+
+def net_leg(args, net_name: str, images: int, batch, world: int, rank: int, local: int,
+            flush, steps: int, warmup: int, roofline_steps: int = 3, verify: bool = True) -> dict:
+    """One workload: `images`-image loop of `net_name`, all-offload genome,
+    hoisted transfers.  value = kernels only with inputs resident in HBM
+    (CUDA events on the executor stream, L2 flushed before every step);
+    e2e = the public executor path with pinned host buffers and every planned
+    transfer inside the timed region."""
     import torch
-    world, rank, local = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
     from paper_1811_03882_b200 import kernels as K
     from paper_1811_03882_b200.executor import PatternExecutor
     from paper_1811_03882_b200.nets import build_net
+    from paper_1811_03882_b200.sharding import image_shard
 
     gemm_mode = {"auto": K.GEMM_AUTO, "simt": K.GEMM_SIMT, "tc": K.GEMM_TC3XTF32}[args.gemm]
-    net = build_net(args.net, images=args.images)
+    net = build_net(net_name, images=images)
     # weak scaling: rank r owns images [r*images, (r+1)*images) of the stream
-    from paper_1811_03882_b200.sharding import image_shard
-    shard = image_shard(world * args.images, world, rank)
+    shard = image_shard(world * images, world, rank)
     ex = PatternExecutor(net, device=local, fuse=not args.no_fuse, gemm_mode=gemm_mode,
-                         first_image=shard.first, batch=args.batch or True)
+                         first_image=shard.first, batch=batch)
     bits = "1" * len(net.ops)
     full = ex.compile(bits)
     res = ex.compile(bits, resident=True)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=ex.device)
 
     def barrier():
         torch.cuda.synchronize(ex.device)
@@ -437,10 +518,7 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
-    # clocks are sampled from the first warm-up step to the end of the e2e leg
-    # (every step in between keeps the GPU busy); see ClockSampler
-    clocks = ClockSampler(local).__enter__()
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         ex.run(res)
         ex.run(full)
 
@@ -448,7 +526,7 @@ def run_ours(args):
     barrier()
     step_ms = []
     launches = 0
-    for _ in range(args.steps):
+    for _ in range(steps):
         with torch.cuda.stream(ex.stream):
             flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -460,15 +538,14 @@ def run_ours(args):
         step_ms.append(e0.elapsed_time(e1))
         launches += r.counters["kernel_launches"]
     barrier()
-    local_total = sum(step_ms) * 1e-3
-    total = max_over_ranks(local_total)
-    value = world * args.images * args.steps / total
+    total = max_over_ranks(sum(step_ms) * 1e-3)
+    value = world * images * steps / total
 
     # ---- e2e: public path, host buffers, transfers inside the region ----
     barrier()
     walls = []
     counters = None
-    for _ in range(args.steps):
+    for _ in range(steps):
         with torch.cuda.stream(ex.stream):
             flush.zero_()
         torch.cuda.synchronize(ex.device)
@@ -477,58 +554,116 @@ def run_ours(args):
         counters = r.counters
     barrier()
     e2e_total = max_over_ranks(sum(walls))
-    e2e_value = world * args.images * args.steps / e2e_total
-    time.sleep(0.25)  # let the sampler log the tail of the loaded period
-    clocks.__exit__(None, None, None)
+    e2e_value = world * images * steps / e2e_total
     for key, val in full.expected.items():
         if counters[key] != val:
             raise SystemExit(f"transfer counter mismatch {key}: {counters[key]} != {val}")
-    # the last timed e2e step's outputs, then the resident leg's (one more
-    # untimed run: the timed loop above ran the e2e schedule last)
-    golden = golden_entry(args.net, args.images, shard.first)
-    verified = {"e2e": verify_outputs("e2e", ex.outputs(), golden)}
-    if res.batch == args.images:
-        ex.run(res)
-        verified["value"] = verify_outputs("resident", ex.device_outputs(), golden)
+    out = {"net": net, "ex": ex, "full": full, "res": res, "value": value, "total_s": total,
+           "e2e_value": e2e_value, "e2e_total_s": e2e_total, "counters": counters,
+           "launches": launches, "step_ms": step_ms, "walls": walls}
+    if verify:
+        # the last timed e2e step's outputs, then the resident leg's (one
+        # more untimed run: the timed loop above ran the e2e schedule last)
+        golden = golden_entry(net_name, images, shard.first)
+        verified = {"e2e": verify_outputs(f"{net_name} e2e", ex.outputs(), golden)}
+        if res.batch == images:
+            ex.run(res)
+            verified["value"] = verify_outputs(f"{net_name} resident", ex.device_outputs(), golden)
+        out["verified"] = verified
+    if rank == 0 and roofline_steps:
+        peaks_path = REPO / "MEASURED_PEAKS.json"
+        peaks = json.loads(peaks_path.read_text()) if peaks_path.exists() else \
+            {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "fallback": True}
+        out["roofline"] = roofline(ex, res, roofline_steps, flush, peaks)
+    return out
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    flush = make_flush(torch, torch.device("cuda", local))
+
+    # clocks are sampled from the first warm-up step to the end of the last
+    # timed GPU leg (every step in between keeps the GPU busy); see ClockSampler
+    clocks = ClockSampler(local).__enter__()
+    main = net_leg(args, args.net, args.images, args.batch or True, world, rank, local, flush,
+                   args.steps, args.warmup, roofline_steps=max(1, min(args.steps, 3)))
+    extra = {}
+    if world == 1 and not args.quick:
+        # BASELINE configs[4]: YOLOv2-608, 16-image loop
+        leg = net_leg(args, "yolov2-608", 16, True, world, rank, local, flush,
+                      max(3, args.steps // 2), args.warmup, roofline_steps=1)
+        extra["yolov2_608"] = leg
+        # configs[1] image at a time (batch 1 per launch, graph-captured)
+        extra["image_at_a_time"] = net_leg(args, args.net, args.images, 1, world, rank, local,
+                                           flush, args.steps, args.warmup, roofline_steps=0)
+    time.sleep(0.25)  # let the sampler log the tail of the loaded period
+    clocks.__exit__(None, None, None)
 
     if rank != 0:
         if world > 1:
+            torch.distributed.barrier()          # rank 0 runs the GA legs on every GPU
             torch.distributed.destroy_process_group()
         return
 
-    peaks_path = REPO / "MEASURED_PEAKS.json"
-    peaks = json.loads(peaks_path.read_text()) if peaks_path.exists() else \
-        {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "fallback": True}
-    roof = roofline(ex, res, max(1, min(args.steps, 3)), flush, peaks)
-
+    ex, net, counters = main["ex"], main["net"], main["counters"]
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.net, args.cpu_images)
-    ga = None
-    if world == 1 and not args.no_ga:
-        ga = ga_search([local])
+        cpu = cpu_baseline(args.net, args.cpu_images, steps=3)
+    devices = list(range(world))
+    ga = ga_ref = ga_paper = ga_paper_ref = None
+    if not args.no_ga:
+        ga = ga_gpu("demo", None, devices, 4, 2, 1, 1, 3)
+        ga["config"] = "BASELINE configs[0]: " + ga["config"]
+        if world == 1:
+            ga_ref = ga_reference("demo", None, 4, 2, 1, os.cpu_count() or 1)
+        if not args.quick:
+            ga_paper = ga_gpu(args.net, 1, devices, 30, 20, 1, 1, 1)
+            ga_paper["config"] = "BASELINE configs[2]: " + ga_paper["config"]
+            if world == 1:
+                ga_paper_ref = ga_reference(args.net, 1, 30, 1, 1, os.cpu_count() or 1)
+    if world > 1:
+        torch.distributed.barrier()
+
+    def sub(leg, cpu_images=None):
+        d = {"value": leg["value"], "unit": "img/s", "ms_per_step": 1e3 * leg["total_s"] / len(leg["step_ms"]),
+             "images_per_step": leg["net"].spec.images,
+             "images_per_launch": leg["res"].batch,
+             "e2e": {"value": leg["e2e_value"], "unit": "img/s",
+                     "h2d_bytes_per_step": leg["counters"]["h2d_bytes"],
+                     "d2h_bytes_per_step": leg["counters"]["d2h_bytes"]},
+             "gpu_launches": leg["launches"]}
+        if "roofline" in leg:
+            d["roofline"] = leg["roofline"]
+        if "verified" in leg:
+            d["outputs_verified"] = leg["verified"]
+        return d
 
     dims = f"{net.spec.height}x{net.spec.width}"
     line = {
-        "metric": METRIC, "value": value, "unit": "img/s", "n_gpus": world,
+        "metric": METRIC, "value": main["value"], "unit": "img/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "ms_per_step": 1e3 * main["total_s"] / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.net} {dims}, batch 1 per forward pass, "
                                f"{args.images}-image loop per step, all-offload genome "
                                f"({len(net.ops)} genes) with hoisted transfers",
                    "images_per_step_per_gpu": args.images,
                    "genes": len(net.ops), "gemm": args.gemm, "fused_epilogues": not args.no_fuse,
-                   "images_per_launch": res.batch,
+                   "images_per_launch": main["res"].batch,
                    "l2": "flushed before every step (256 MiB write); per-step footprint "
                          f"{net.total_bytes_per_image() * args.images / 2**20:.0f} MiB",
                    "parallelism": f"images sharded, {world} GPU(s), no collective"},
-        "e2e": {"value": e2e_value, "unit": "img/s",
+        "e2e": {"value": main["e2e_value"], "unit": "img/s",
                 "h2d_bytes_per_step": counters["h2d_bytes"],
                 "d2h_bytes_per_step": counters["d2h_bytes"]},
-        "roofline": roof,
+        "roofline": main["roofline"],
         "cpu_baseline": cpu,
-        "gpu_launches": launches,
+        "gpu_launches": main["launches"],
         "clocks": clocks.summary(),
         "transfers_per_image": {
             "directive_execs": counters["directive_execs"] / args.images,
@@ -537,10 +672,24 @@ def run_ours(args):
             "d2h_calls": counters["d2h_calls"] / args.images,
             "h2d_bytes": counters["h2d_bytes"] / args.images,
             "d2h_bytes": counters["d2h_bytes"] / args.images},
-        "ga_search": ga,
-        "outputs_verified": verified,
-        "value_step_ms": step_ms, "e2e_step_s": walls,
+        "outputs_verified": main.get("verified"),
+        "ga_search": ga, "ga_search_reference": ga_ref,
+        "ga_paper_scale": ga_paper, "ga_paper_scale_reference": ga_paper_ref,
+        "value_step_ms": main["step_ms"], "e2e_step_s": main["walls"],
     }
+    if "yolov2_608" in extra:
+        leg = extra["yolov2_608"]
+        d = sub(leg)
+        d["config"] = "BASELINE configs[4]: yolov2-608 608x608, 16-image loop per step, " \
+                      f"all-offload genome ({len(leg['net'].ops)} genes), batched 16 per launch"
+        if not args.no_cpu_baseline:
+            d["cpu_baseline"] = cpu_baseline("yolov2-608", 1, steps=1)
+        line["yolov2_608"] = d
+    if "image_at_a_time" in extra:
+        d = sub(extra["image_at_a_time"])
+        d["config"] = f"BASELINE configs[1] as written: {args.net}, one image per launch " \
+                      "(image loop not batched), graph-captured resident leg"
+        line["image_at_a_time"] = d
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

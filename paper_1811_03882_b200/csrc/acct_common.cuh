@@ -109,3 +109,36 @@ __host__ __device__ __forceinline__ float acct_leaky(float v) {
   return acct_leaky_ref(v);
 #endif
 }
+
+// Epilogue form for a lane's block of values: the common path branch-free
+// (five instructions, bit-identical to acct_leaky wherever
+// acct_leaky_guarded is false) and, when any lane of the warp holds a guarded
+// value (|v| < 2^-100 or v < -2^120, negative), acct_leaky for the whole
+// block.  Predicated inline, the double-product fallback cost every value an
+// F2F / DMUL issue slot.
+#ifdef __CUDACC__
+__device__ __forceinline__ bool acct_leaky_guarded(float v) {
+  return v < -0x1p+120f || (v < 0.0f && v > -0x1p-100f);
+}
+__device__ __forceinline__ float acct_leaky_fast(float v) {
+  constexpr float c1 = 0x1.99999ap-4f;
+  constexpr float c2 = (float)(0.1 - (double)0x1.99999ap-4f);
+  const float p = __fmul_rn(v, c1);
+  const float e = __fmaf_rn(v, c1, -p);
+  const float q = __fadd_rn(p, __fmaf_rn(v, c2, e));
+  return v < 0.0f ? q : v;
+}
+template <int N>
+__device__ __forceinline__ void acct_leaky_block(float (&v)[N]) {
+  bool slow = false;
+#pragma unroll
+  for (int i = 0; i < N; ++i) slow |= acct_leaky_guarded(v[i]);
+  if (__any_sync(__activemask(), slow)) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = acct_leaky(v[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = acct_leaky_fast(v[i]);
+  }
+}
+#endif

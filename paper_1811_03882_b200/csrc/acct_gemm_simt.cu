@@ -708,9 +708,11 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
       const int64_t pofs = (int64_t)(y >> 1) * (width >> 1) + (x >> 1);
       const int base_i = (int)p;
       const int plane = height * width;
+      // beta C and bias per filter, then leaky over all 16 x 4 values with
+      // one warp vote for the guarded inputs (acct_leaky_block)
 #pragma unroll
       for (int ml = 0; ml < MT; ++ml) {
-        const int m = m_off + ml;  // the filter (output row)
+        const int m = m_off + ml;
         if (m >= M) break;
         float *cp = cimg + (int64_t)m * ldc;
         float cv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -719,15 +721,22 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
           const float2 c1 = *reinterpret_cast<const float2 *>(cp + width);
           cv[0] = c0.x; cv[1] = c0.y; cv[2] = c1.x; cv[3] = c1.y;
         }
-        float o[4];
         const float bv = bias ? __ldg(bias + m) : 0.0f;  // once per filter
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           float v = acc[ml][e];
           if (beta != 0.0f) v = beta * cv[e] + v;
           if (bias) v += bv;
-          o[e] = act == ACCT_ACT_LEAKY ? acct_leaky(v) : v;
+          acc[ml][e] = v;
         }
+      }
+      if (act == ACCT_ACT_LEAKY) acct_leaky_block(reinterpret_cast<float(&)[MT * 4]>(acc));
+#pragma unroll
+      for (int ml = 0; ml < MT; ++ml) {
+        const int m = m_off + ml;  // the filter (output row)
+        if (m >= M) break;
+        float *cp = cimg + (int64_t)m * ldc;
+        const float *o = acc[ml];
         if (wc) {
           __stcs(reinterpret_cast<float2 *>(cp), make_float2(o[0], o[1]));
           __stcs(reinterpret_cast<float2 *>(cp + width), make_float2(o[2], o[3]));

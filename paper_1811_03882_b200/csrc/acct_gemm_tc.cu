@@ -1385,7 +1385,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     asm volatile("bar.sync 2, 256;" ::: "memory");  // the eight epilogue warps
     const int m = 32 * q + lane;
     const int py = m / TW, px = m % TW;
-    float *scr = bias_s + 64 + (warp - 10) * 8 * 33;  // this warp's pooling scratch
+    // explicit shared-space addresses (generic LD/ST through the realigned
+    // base measured several times slower): bias, this warp's pooling scratch
+    const uint32_t bias_sa = ptx::smem_u32(bias_s);
+    const uint32_t scr_sa = ptx::smem_u32(bias_s + 64 + (warp - 10) * 8 * 33);
     int jp = 0;
     for (int u = blockIdx.x + grp * gridDim.x; u < units; u += 2 * gridDim.x, ++jp) {
       int img, y0, x0;
@@ -1414,19 +1417,25 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           for (int jj = 0; jj < CH; ++jj)  // every load in flight before any store
             cv[jj] = rbase + jj < M ? rp[(int64_t)jj * ldc] : 0.0f;
         }
+        float f[CH];
 #pragma unroll
         for (int jj = 0; jj < CH; ++jj) {
           float v = __uint_as_float(r[jj]);
           if (beta != 0.0f && live) v = beta * cv[jj] + v;
-          if (bias) v += bias_s[rbase + jj];
-          if (act == ACCT_ACT_LEAKY) v = acct_leaky(v);
-          if (cst && rbase + jj < M) rp[(int64_t)jj * ldc] = v;
-          r[jj] = __float_as_uint(v);
+          if (bias) v += ptx::lds32(bias_sa + 4 * (rbase + jj));
+          f[jj] = v;
+        }
+        if (act == ACCT_ACT_LEAKY) acct_leaky_block(f);
+#pragma unroll
+        for (int jj = 0; jj < CH; ++jj) {
+          if (cst && rbase + jj < M) rp[(int64_t)jj * ldc] = f[jj];
+          r[jj] = __float_as_uint(f[jj]);
         }
 #pragma unroll
         for (int half = 0; half < 2 && pool; ++half) {
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) scr[jj * 33 + lane] = __uint_as_float(r[8 * half + jj]);
+          for (int jj = 0; jj < 8; ++jj)
+            ptx::sts32(scr_sa + 4 * (jj * 33 + lane), __uint_as_float(r[8 * half + jj]));
           // 2x2/2 maxpool, 8 filters per pass: the warp's 32 pixels are 8
           // whole windows (tiles start on even rows / columns); through the
           // scratch each lane takes window (lane & 7) of filters 4t + (lane >>
@@ -1442,8 +1451,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             const int fl = 4 * t + fg, f = rbase + 8 * half + fl;
-            const float *sv = scr + fl * 33 + l0;
-            const float v00 = sv[0], v01 = sv[1], v10 = sv[TW], v11 = sv[TW + 1];
+            const uint32_t sv = scr_sa + 4 * (fl * 33 + l0);
+            const float v00 = ptx::lds32(sv), v01 = ptx::lds32(sv + 4);
+            const float v10 = ptx::lds32(sv + 4 * TW), v11 = ptx::lds32(sv + 4 * (TW + 1));
             if (win && f < M) {
               const int base_i = f * HW + wy * width + wx;
               float mx = -FLT_MAX;
@@ -1696,7 +1706,7 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     const int grp = (warp - 10) >> 2;
     const int m = 32 * q + lane;
     const int py = m / TW, px = m % TW;
-    float *scr = bias_s + TN + (warp - 10) * 8 * 33;
+    const uint32_t scr_sa = ptx::smem_u32(bias_s + TN + (warp - 10) * 8 * 33);
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       if ((j & 1) != grp) continue;
@@ -1724,19 +1734,25 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
 #pragma unroll
           for (int jj = 0; jj < CH; ++jj) cv[jj] = rbase + jj < M ? rp[(int64_t)jj * ldc] : 0.0f;
         }
+        float f[CH];
 #pragma unroll
         for (int jj = 0; jj < CH; ++jj) {
           float v = __uint_as_float(r[jj]);
           if (beta != 0.0f && live) v = beta * cv[jj] + v;
           if (bias) v += __ldg(bias + (rbase + jj < M ? rbase + jj : 0));
-          if (act == ACCT_ACT_LEAKY) v = acct_leaky(v);
-          if (cst && rbase + jj < M) rp[(int64_t)jj * ldc] = v;
-          r[jj] = __float_as_uint(v);
+          f[jj] = v;
+        }
+        if (act == ACCT_ACT_LEAKY) acct_leaky_block(f);
+#pragma unroll
+        for (int jj = 0; jj < CH; ++jj) {
+          if (cst && rbase + jj < M) rp[(int64_t)jj * ldc] = f[jj];
+          r[jj] = __float_as_uint(f[jj]);
         }
 #pragma unroll
         for (int hf = 0; hf < 2 && pool; ++hf) {
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) scr[jj * 33 + lane] = __uint_as_float(r[8 * hf + jj]);
+          for (int jj = 0; jj < 8; ++jj)
+            ptx::sts32(scr_sa + 4 * (jj * 33 + lane), __uint_as_float(r[8 * hf + jj]));
           __syncwarp();
           constexpr int TWH = TW / 2;
           const int w8 = lane & 7, fg = lane >> 3;
@@ -1748,8 +1764,9 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             const int fl = 4 * t + fg, f = rbase + 8 * hf + fl;
-            const float *sv = scr + fl * 33 + l0;
-            const float v00 = sv[0], v01 = sv[1], v10 = sv[TW], v11 = sv[TW + 1];
+            const uint32_t sv = scr_sa + 4 * (fl * 33 + l0);
+            const float v00 = ptx::lds32(sv), v01 = ptx::lds32(sv + 4);
+            const float v10 = ptx::lds32(sv + 4 * TW), v11 = ptx::lds32(sv + 4 * (TW + 1));
             if (win && f < M) {
               const int base_i = f * HW + wy * width + wx;
               float mx = -FLT_MAX;

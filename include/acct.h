@@ -313,8 +313,9 @@ void acct_graph_destroy(acct_graph_t *graph);
 
 /* tensor-core gemm debug word: bit 0 = store the TF32 hi part explicitly
  * (default: leave raw FP32 in shared memory, the MMA truncates); bits 1-3
- * skip the split / MMA / epilogue (timing only, results wrong); bit 4 =
- * record CTA 0's pipeline events; for verification and tools/ only */
+ * skip the split / MMA / epilogue (timing only, results wrong; honoured only
+ * by the -DACCT_PROFILING build, compiled out of the product library); bit 4
+ * = record CTA 0's pipeline events; for verification and tools/ only */
 void acct_tc_set_write_hi(int on);
 /* copy the event trace of the last bit-4 launch: 8 x 512 int64 clock64
  * stamps (TMA issue, landed, split done, MMA in, commit, split parts) */
@@ -325,9 +326,13 @@ int acct_tc_trace(long long *out);
  * 9/10 = pair 256x192 / 256x256 BK 32, 12 = pair swap tile for M <= 64,
  * 13/14 = pair 256x192 BK 16 / 256x128 BK 32 with a second accumulator for
  * the small 3xTF32 terms, 15 = pair 256x192 BK 32, second accumulator, only
- * A lo in TMEM -- the default for K > 1536);
+ * A lo in TMEM, 16 = the same for the long-K pair launches that otherwise
+ * run the stream-K chunked-promotion tile (pair 256x192 BK 32, FP32 running
+ * sum every 4 k-blocks -- the default for K > 768));
  * tests and tools only                                                     */
 void acct_tc_set_tile(int tile);
+/* CTA pairs of the stream-K gemm that fit on the current device at once */
+int acct_tc_stream_k_pairs(void);
 
 /* library/device facts */
 int acct_device_sm_count(int device);

@@ -635,7 +635,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 int M, int N, int K, int nt, int mt, int splits, int kb_per, int write_hi,
                 float alpha, float beta, float *__restrict__ C, int64_t ldc,
                 const float *__restrict__ bias, int act, float *__restrict__ ws, int64_t ws_ld,
-                int64_t ws_split_stride) {
+                int64_t ws_split_stride, int *__restrict__ sk_flags) {
   using G = Cfg2<TN, NACC, BK_, SWAP, DUAL, LOA, PK>;
   constexpr int S = G::STAGES, BK = G::BK;
   static_assert(!LOA || !SWAP, "LOA is for the normal orientation");
@@ -669,6 +669,47 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     w.nkb = min(w.kb0 + kb_per, total_kb) - w.kb0;
     return w;
   };
+  // Stream-K (PK > 0): the space of (tile, chunk of PK k-blocks) is cut into
+  // `pairs` equal contiguous ranges, one per CTA pair, so every pair does the
+  // same MMA work whatever tiles / pairs is (L12 of yolov2-tiny: 60 tiles on
+  // 74 pairs; yolov2-608 L23: 124).  A pair's range is a list of segments
+  // (tile, chunks [c0, c1)); a tile cut between pairs is finished by the pair
+  // holding its FIRST chunks -- that segment comes last in its range -- after
+  // the later segments' partial sums (computed first in their pairs' ranges)
+  // arrive through the workspace (one slot per CTA) and a per-CTA flag.
+  const int cpt = PK > 0 ? (total_kb + PK - 1) / PK : 1;
+  const int64_t tot_ch = (int64_t)tiles * cpt;
+  const int64_t sk_begin = tot_ch * pair / pairs, sk_end = tot_ch * (pair + 1) / pairs;
+  auto seg_at = [&](int64_t pos, Unit &w, int &c0, int &c1) {
+    const int t = (int)(pos / cpt);
+    c0 = (int)(pos - (int64_t)t * cpt);
+    const int64_t rem = sk_end - pos;
+    c1 = rem < (int64_t)(cpt - c0) ? c0 + (int)rem : cpt;
+    const int tm = t / nt, tn = t - tm * nt;
+    w.split = t;  // the tile index
+    w.n0 = tn * TN;
+    w.m0 = tm * 256;
+    w.kb0 = c0 * (PK > 0 ? PK : 1);
+    w.nkb = min(c1 * (PK > 0 ? PK : 1), total_kb) - w.kb0;
+  };
+  // every role walks the same work list: stream-K segments or split units
+  const bool sk = PK > 0 && sk_flags != nullptr;  // else split units (maybe split-K)
+  auto for_each_unit = [&](auto &&body) {
+    if (!sk) {
+      for (int u = pair; u < units; u += pairs) {
+        const Unit w = unit(u);
+        body(w, 0, (w.nkb + (PK > 0 ? PK : 1) - 1) / (PK > 0 ? PK : 1));
+      }
+    } else {
+      for (int64_t pos = sk_begin; pos < sk_end;) {
+        Unit w;
+        int c0, c1;
+        seg_at(pos, w, c0, c1);
+        body(w, c0, c1);
+        pos += c1 - c0;
+      }
+    }
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -696,8 +737,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     // ---------------- TMA producer (both CTAs: their own A rows, B half) ----------------
     if (lane == 0) {
       int g = 0;
-      for (int u = pair; u < units; u += pairs) {
-        const Unit w = unit(u);
+      for_each_unit([&](const Unit &w, int, int) {
         const int m_rows = w.m0 + (SWAP ? rank * G::HALF : 128 * rank);
         const int n_cols = w.n0 + (SWAP ? 128 * rank : rank * G::HALF);
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
@@ -718,7 +758,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             ptx::tma_load_2d(y_hi(s), &tmA, &full[s], kx, m_rows);
           }
         }
-      }
+      });
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader only; whole warp, one lane issues) ----------------
@@ -726,8 +766,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       // chunked promotion: chunk c (counted across units) -> accumulator c & 1
       constexpr uint32_t idesc = ptx::idesc_tf32(256, TN, false, true);
       int g = 0, c = 0;
-      for (int u = pair; u < units; u += pairs) {
-        const Unit w = unit(u);
+      for_each_unit([&](const Unit &w, int, int) {
         uint32_t d = tmem;
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
           const int kc = kb % (PK > 0 ? PK : 1);
@@ -769,7 +808,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             ++c;
           }
         }
-      }
+      });
     } else if (rank == 0) {
       constexpr uint32_t idesc = ptx::idesc_tf32(256, TN, false, !SWAP);
       int g = 0, j = 0;
@@ -829,8 +868,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const int q = warp & 3, row = 32 * q + lane;
     const uint32_t conv_leader = ptx::mapa(ptx::smem_u32(&conv[0]), 0);
     int g = 0;
-    for (int u = pair; u < units; u += pairs) {
-      const Unit w = unit(u);
+    for_each_unit([&](const Unit &w, int, int) {
       for (int kb = 0; kb < w.nkb; ++kb, ++g) {
         const int s = g % S;
         ptx::mbar_wait(&full[s], (g / S) & 1);
@@ -901,7 +939,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if ((write_hi & 16) && blockIdx.x < 2 && g < kTrace && ct == 0)
           g_trace[blockIdx.x == 0 ? 2 : 6][g] = gtimer();
       }
-    }
+    });
   } else if constexpr (PK > 0) {
     // ---------------- epilogue, chunked promotion (both CTAs, both groups) ----------------
     // group grp owns columns grp HC .. of the CTA's 128 rows: every chunk is
@@ -913,9 +951,9 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t stg_s = ptx::smem_u32(staging + (grp * 4 + q) * (32 * 33));
     const uint32_t acc_empty_leader = ptx::mapa(ptx::smem_u32(&acc_empty[0]), 0);
     int c = 0;
-    for (int u = pair; u < units; u += pairs) {
-      const Unit w = unit(u);
-      const int nch = (w.nkb + PK - 1) / PK;
+    const int row = 32 * q + lane;  // this thread's row of the CTA's 128
+    for_each_unit([&](const Unit &w, int c0, int c1) {
+      const int nch = c1 - c0;
       float acc[HC];
 #pragma unroll
       for (int i = 0; i < HC; ++i) acc[i] = 0.0f;
@@ -935,8 +973,48 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(acc_empty_leader + 8 * a);
       }
-      if (ACCT_SKIP(write_hi, 8)) continue;
-      float *part = ws + w.split * ws_split_stride;
+      if (ACCT_SKIP(write_hi, 8)) return;
+      constexpr int SLOT = 128 * TN;  // one CTA's partial tile in the workspace
+      if (sk && c0 > 0) {
+        // a later part of the tile: the partial sum to this CTA's slot, then
+        // its flag (release after every epilogue thread's stores)
+        float *slot = ws + (int64_t)blockIdx.x * SLOT + (int64_t)row * TN + grp * HC;
+#pragma unroll
+        for (int i = 0; i < HC / 4; ++i)
+          __stcg(reinterpret_cast<float4 *>(slot) + i,
+                 make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]));
+        __threadfence();
+        asm volatile("bar.sync 3, 256;" ::: "memory");  // the eight epilogue warps
+        if (threadIdx.x == 6 * 32)
+          asm volatile("st.release.gpu.global.s32 [%0], 1;" ::"l"(sk_flags + blockIdx.x) : "memory");
+        return;
+      }
+      if (sk && c1 < cpt) {
+        // the tile's first chunks: add the later parts' partials, in pair order
+        const int64_t tile_end = (int64_t)(w.split + 1) * cpt;
+        if (threadIdx.x == 6 * 32) {
+          for (int qp = pair + 1; qp < pairs && tot_ch * qp / pairs < tile_end; ++qp) {
+            int *flag = sk_flags + 2 * qp + rank;
+            int v = 0;
+            do {
+              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+            } while (v == 0);
+            *flag = 0;  // consumed: zero for the next launch on this stream
+          }
+        }
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+        for (int qp = pair + 1; qp < pairs && tot_ch * qp / pairs < tile_end; ++qp) {
+          const float *slot = ws + (int64_t)(2 * qp + rank) * SLOT + (int64_t)row * TN + grp * HC;
+#pragma unroll
+          for (int i = 0; i < HC / 4; ++i) {
+            const float4 v = __ldcg(reinterpret_cast<const float4 *>(slot) + i);
+            acc[4 * i] += v.x;
+            acc[4 * i + 1] += v.y;
+            acc[4 * i + 2] += v.z;
+            acc[4 * i + 3] += v.w;
+          }
+        }
+      }
       const int row0 = w.m0 + 128 * rank + 32 * q;
 #pragma unroll
       for (int cb = 0; cb < HC / 32; ++cb) {
@@ -944,29 +1022,29 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         for (int jj = 0; jj < 32; ++jj) ptx::sts32(stg_s + 4 * (lane * 33 + jj), acc[32 * cb + jj]);
         __syncwarp();
         const int col = w.n0 + grp * HC + 32 * cb + lane;
-        if (splits == 1) {
+        if (!sk && splits > 1) {
+          float *dst = ws + w.split * ws_split_stride + (int64_t)row0 * ws_ld + col;
+#pragma unroll 8
+          for (int i = 0; i < 32; ++i)
+            __stcg(dst + (int64_t)i * ws_ld, ptx::lds32(stg_s + 4 * (i * 33 + lane)));
+        } else {
           if (col < N) {
 #pragma unroll 4
             for (int i = 0; i < 32; ++i) {
-              const int row = row0 + i;
-              if (row < M) {
+              const int orow = row0 + i;
+              if (orow < M) {
                 // one broadcast load per row (every lane reads the same bias)
-                const float bv = bias ? __ldg(bias + row) : 0.0f;
-                const float cv = beta != 0.0f ? C[(int64_t)row * ldc + col] : 0.0f;
-                C[(int64_t)row * ldc + col] =
+                const float bv = bias ? __ldg(bias + orow) : 0.0f;
+                const float cv = beta != 0.0f ? C[(int64_t)orow * ldc + col] : 0.0f;
+                C[(int64_t)orow * ldc + col] =
                     finish(ptx::lds32(stg_s + 4 * (i * 33 + lane)), alpha, beta, cv, bias, bv, act);
               }
             }
           }
-        } else {
-          float *dst = part + (int64_t)row0 * ws_ld + col;
-#pragma unroll 8
-          for (int i = 0; i < 32; ++i)
-            __stcg(dst + (int64_t)i * ws_ld, ptx::lds32(stg_s + 4 * (i * 33 + lane)));
         }
         __syncwarp();
       }
-    }
+    });
   } else {
     // ---------------- epilogue (both CTAs: their 128 rows x TN) ----------------
     // one group per accumulator at most: two groups sharing one accumulator
@@ -1976,6 +2054,63 @@ int scratch_for(cudaStream_t s, size_t floats, float **out) {
   return ACCT_OK;
 }
 
+// stream-K flags: one int per CTA, zero between launches (each consumer
+// resets the flag it waited on), per (device, stream) like the workspace
+std::unordered_map<uint64_t, std::pair<int *, size_t>> g_sk_flags;
+
+int sk_flags_for(cudaStream_t s, size_t n, int **out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  uint64_t key = (reinterpret_cast<uint64_t>(s) << 8) ^ (uint64_t)dev;
+  std::lock_guard<std::mutex> lock(g_scratch_mu);
+  auto &f = g_sk_flags[key];
+  if (f.second < n) {
+    if (f.first) g_scratch_retired.push_back(reinterpret_cast<float *>(f.first));
+    f.first = nullptr;
+    f.second = 0;
+    if (int rc = check_cuda(cudaMalloc(&f.first, n * sizeof(int)), "gemm_tc2: stream-K flags"))
+      return rc;
+    if (int rc = check_cuda(cudaMemset(f.first, 0, n * sizeof(int)), "gemm_tc2: stream-K flags"))
+      return rc;
+    f.second = n;
+  }
+  *out = f.first;
+  return ACCT_OK;
+}
+
+// co-resident 2-CTA clusters of a kernel on this device (cached per kernel)
+template <typename Kern>
+int sk_pairs(Kern kernel, int smem) {
+  static std::mutex mu;
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * (sm_count() / 2));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int cap = sm_count() / 2;
+  if (n > cap) n = cap;
+  if (dev >= 0 && dev < 64) cached[dev] = n;
+  return n;
+}
+
 template <int TN, bool SWAP, int BK>
 int set_smem_attr() {
   // the attribute is per device context
@@ -2090,8 +2225,15 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
   const int nt = (N + tile_n - 1) / tile_n, mt = (M + tile_m - 1) / tile_m, tiles = mt * nt;
   const int total_kb = (K + BK - 1) / BK;
   const int pairs_avail = sm_count() / 2;
-  int splits, kb_per;
-  plan_splits(tiles, total_kb, pairs_avail, &splits, &kb_per);
+  // stream-K (chunked promotion only) when there are at least as many tiles
+  // as CTA pairs: it removes the last wave's quantization.  With fewer tiles
+  // split-K keeps the m-tiles of one column block at the same k at the same
+  // time, so their shared B slices are L2 hits; a stream-K range per pair
+  // puts them at unrelated k and re-reads B from HBM (yolov2-tiny L13,
+  // 512 x 2749 x 9216: 128 vs 111 us; tools/sk_probe.py)
+  const bool stream_k = PK > 0 && tiles >= pairs_avail;
+  int splits = 1, kb_per = total_kb;
+  if (!stream_k) plan_splits(tiles, total_kb, pairs_avail, &splits, &kb_per);
   const int units = tiles * splits;
   float *ws = nullptr;
   const int64_t ws_ld = (int64_t)nt * tile_n, rows = (int64_t)mt * tile_m;
@@ -2113,10 +2255,23 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
       done[dev] = true;
     }
   }
-  const int pairs = units < pairs_avail ? units : pairs_avail;
+  int pairs = units < pairs_avail ? units : pairs_avail;
+  int *flags = nullptr;
+  if (stream_k) {
+    // stream-K: every pair gets an equal share of the (tile, chunk) space, and
+    // a pair may wait for later pairs' partials -- so all pairs must be
+    // co-resident: the grid is capped at the clusters that fit at once
+    const int cpt = (total_kb + PK - 1) / PK;
+    const int64_t tot_ch = (int64_t)tiles * cpt;
+    pairs = sk_pairs(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA, PK>, G::SMEM_BYTES);
+    if (pairs < 1) return fail(ACCT_ENOTSUP, "gemm_tc2 stream-K: no co-resident CTA pairs");
+    if (tot_ch < pairs) pairs = (int)tot_ch;
+    if (int rc = scratch_for(s, (size_t)2 * pairs * 128 * TN, &ws)) return rc;
+    if (int rc = sk_flags_for(s, 2 * pairs, &flags)) return rc;
+  }
   launch(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA, PK>, dim3(2 * pairs), dim3(THREADS), G::SMEM_BYTES, s, ta, tb, M,
          N, K, nt, mt, splits, kb_per, g_write_hi, alpha, beta, C, ldc, bias, act, ws, ws_ld,
-         rows * ws_ld);
+         rows * ws_ld, flags);
   if (int rc = note_launch("gemm_tc2")) return rc;
   if (splits > 1) {
     const int64_t work = (int64_t)M * ((N + 3) / 4);
@@ -2353,6 +2508,12 @@ int conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channels, int
 }  // namespace acct
 
 extern "C" void acct_tc_set_write_hi(int on) { acct::g_write_hi = on; }
+
+// co-resident CTA pairs of the stream-K gemm on the current device (diagnostics)
+extern "C" int acct_tc_stream_k_pairs(void) {
+  using G = acct::Cfg2<192, 2, 32, false, false, true, 4>;
+  return acct::sk_pairs(acct::tc2_gemm_kernel<192, 2, 32, false, false, true, 4>, G::SMEM_BYTES);
+}
 
 extern "C" void acct_tc_set_tile(int tile) { acct::g_force_tile.store(tile < 0 ? 0 : tile); }
 

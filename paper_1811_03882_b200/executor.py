@@ -25,8 +25,9 @@ Semantics follow the emitted OpenACC program (reference emitter
 
 B200-specific choices, none of which changes observable results:
 
-* device arrays are pitched (row pitch rounded up to 32 floats = 128 B) so
-  every row is TMA- and float4-aligned; transfers are pitched 2-D copies;
+* device arrays are pitched (rows of a multiple of 16 B, 128 B where that
+  pads by <= 1/64, `_pitch`) so every row is TMA- and float4-aligned;
+  transfers are pitched 2-D copies;
 * with `fuse=True`, a run of consecutive offloaded ops on one conv output
   -- fill, gemm_nn, add_bias, activation -- becomes ONE gemm launch with
   beta=0 and a bias/leaky epilogue, provided no transfer of that output
@@ -54,7 +55,8 @@ from .planner import (COPY, COPYIN, COPYOUT, TransferPlan, directive_exec_counts
                       plan_transfers, selected_loops)
 from .syntax import parse
 
-PITCH_ALIGN = 32  # elements (128 bytes)
+PITCH_ALIGN = 32  # elements (128 bytes): the preferred row alignment
+PITCH_MIN = 4     # elements (16 bytes): what TMA and the float4 kernels need
 # 3x3/1/1 layers fused into one conv launch (im2col + gemm_nn + epilogue): at
 # most CONV_MAX_C input channels and CONV_MAX_M filters.  The runtime runs
 # the FP32 window kernel for M <= 16, the
@@ -71,7 +73,15 @@ CONV_WIDE_MAX_C = int(os.environ.get("ACCT_CONV_WIDE_MAX_C", "512"))
 
 
 def _pitch(cols: int) -> int:
-    return -(-cols // PITCH_ALIGN) * PITCH_ALIGN
+    """Device row pitch (elements): 128-byte rows unless that pads a row by
+    more than 1/64 -- the 13x13 and 19x19 planes (169 -> 172 instead of 192,
+    361 -> 364 instead of 384), whose padding columns would otherwise be
+    MMA columns and HBM bytes of every interleaved multi-image gemm -- then
+    16-byte rows, the TMA / float4 minimum."""
+    wide = -(-cols // PITCH_ALIGN) * PITCH_ALIGN
+    if (wide - cols) * 64 <= cols:
+        return wide
+    return -(-cols // PITCH_MIN) * PITCH_MIN
 
 
 def _f32_bits(v: float) -> int:

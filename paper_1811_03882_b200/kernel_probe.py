@@ -159,7 +159,8 @@ MAX_ELEMS = 1 << 31
 
 
 def _pitch(n: int) -> int:
-    return -(-n // 32) * 32
+    from .executor import _pitch as executor_pitch   # the executor's device row pitch
+    return executor_pitch(n)
 
 
 def launch_instance(kind: str, p: dict) -> tuple[str | None, str, str]:

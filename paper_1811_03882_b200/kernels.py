@@ -103,6 +103,7 @@ SIGNATURES = {
                               C.POINTER(C.c_void_p)],
     "acct_graph_replay": [_vp, _vp, _i32],
     "acct_tc_trace": [_vp],
+    "acct_tc_stream_k_pairs": [],          # returns a count, not an error code
 }
 VOID_FUNCS = {"acct_counters_get": [C.POINTER(Counters)], "acct_counters_reset": [],
               "acct_graph_destroy": [_vp], "acct_tc_set_write_hi": [_i32], "acct_tc_set_tile": [_i32]}

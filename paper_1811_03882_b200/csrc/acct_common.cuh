@@ -128,11 +128,23 @@ __device__ __forceinline__ float acct_leaky_fast(float v) {
   const float q = __fadd_rn(p, __fmaf_rn(v, c2, e));
   return v < 0.0f ? q : v;
 }
+// The guard over a block, three integer ops per value: with a = bits ^ sign,
+// a negative v has a = |v| bits (>= 0 as int) and a positive one a >= 2^31
+// (< 0 as int), so the unsigned min of a is the smallest |v| of the
+// negatives and the signed max the largest -- against 2^-100 (0x0D800000)
+// and 2^120 (0x7B800000), the exact acct_leaky_guarded ranges (-0 and
+// negative NaNs take the exact path too, which handles them identically).
 template <int N>
 __device__ __forceinline__ void acct_leaky_block(float (&v)[N]) {
-  bool slow = false;
+  uint32_t mn = 0xFFFFFFFFu;
+  int32_t mx = INT32_MIN;
 #pragma unroll
-  for (int i = 0; i < N; ++i) slow |= acct_leaky_guarded(v[i]);
+  for (int i = 0; i < N; ++i) {
+    const uint32_t a = __float_as_uint(v[i]) ^ 0x80000000u;
+    mn = min(mn, a);
+    mx = max(mx, (int32_t)a);
+  }
+  const bool slow = mn < 0x0D800000u || mx > 0x7B800000;
   if (__any_sync(__activemask(), slow)) {
 #pragma unroll
     for (int i = 0; i < N; ++i) v[i] = acct_leaky(v[i]);

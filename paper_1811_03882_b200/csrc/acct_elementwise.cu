@@ -621,14 +621,21 @@ extern "C" int acct_maxpool_f32(const float *in, int64_t ld_in, int channels, in
                                   out_w, out, ld_out, 0, idx, ld_idx, 0, 1, stream);
 }
 
-// ---- test support: acct_leaky vs darknet's double product over every float
+// ---- test support: acct_leaky and acct_leaky_block vs darknet's double
+// product over every float
 namespace {
 __global__ void leaky_check_kernel(unsigned long long *bad, uint32_t *examples) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (1ull << 32); i += stride) {
     const float v = __uint_as_float((uint32_t)i);
     const float a = acct_leaky(v), b = acct_leaky_ref(v);
-    if (__float_as_uint(a) != __float_as_uint(b) && !(a != a && b != b)) {
+    // the epilogues' block form: branch-free path unless a lane of the warp
+    // holds a guarded value (this lane's own guard must be caught)
+    float w[1] = {v};
+    acct_leaky_block(w);
+    const bool bad_a = __float_as_uint(a) != __float_as_uint(b) && !(a != a && b != b);
+    const bool bad_w = __float_as_uint(w[0]) != __float_as_uint(b) && !(w[0] != w[0] && b != b);
+    if (bad_a || bad_w) {
       const unsigned long long n = atomicAdd(bad, 1ull);
       if (n < 8) examples[n] = (uint32_t)i;
     }

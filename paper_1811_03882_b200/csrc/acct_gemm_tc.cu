@@ -147,12 +147,13 @@ __device__ __forceinline__ float4 split_lo(float4 v, float4 &hi) {
   return make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
 }
 
-__device__ __forceinline__ float finish(float acc, float alpha, float beta, float c,
-                                        const float *bias, float bias_v, int act) {
+// epilogue arithmetic without the activation (applied per block of values
+// with acct_leaky_block, one guard vote per block)
+__device__ __forceinline__ float finish_lin(float acc, float alpha, float beta, float c,
+                                            const float *bias, float bias_v) {
   float v = alpha * acc;
   if (beta != 0.0f) v = beta * c + v;
   if (bias) v += bias_v;
-  if (act == ACCT_ACT_LEAKY) v = acct_leaky(v);
   return v;
 }
 
@@ -498,13 +499,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
               for (int i = 0; i < 32; ++i)  // all C loads in flight before any store
                 cv[i] = (beta != 0.0f && row0 + i < M) ? C[(int64_t)(row0 + i) * ldc + col] : 0.0f;
+              float v[32];
 #pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                const int row = row0 + i;
-                if (row < M)
-                  C[(int64_t)row * ldc + col] = finish(ptx::lds32(stg_s + 4 * (i * 33 + lane)), alpha,
-                                                       beta, cv[i], bias, bv[i], act);
-              }
+              for (int i = 0; i < 32; ++i)
+                v[i] = finish_lin(ptx::lds32(stg_s + 4 * (i * 33 + lane)), alpha, beta, cv[i], bias,
+                                  bv[i]);
+              if (act == ACCT_ACT_LEAKY) acct_leaky_block(v);
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (row0 + i < M) C[(int64_t)(row0 + i) * ldc + col] = v[i];
             }
           } else {
             float *dst = part + (int64_t)row0 * ws_ld + col;
@@ -531,13 +534,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               cv[jj] = (beta != 0.0f && ok) ? C[(int64_t)(rbase + jj) * ldc + col] : 0.0f;
               bv[jj] = (bias && ok) ? __ldg(bias + rbase + jj) : 0.0f;
             }
+            float v[CH];
 #pragma unroll
-            for (int jj = 0; jj < CH; ++jj) {
-              const int row = rbase + jj;
-              if (row < M)
-                C[(int64_t)row * ldc + col] = finish(__uint_as_float(r[jj]), alpha, beta, cv[jj],
-                                                     bias, bv[jj], act);
-            }
+            for (int jj = 0; jj < CH; ++jj)
+              v[jj] = finish_lin(__uint_as_float(r[jj]), alpha, beta, cv[jj], bias, bv[jj]);
+            if (act == ACCT_ACT_LEAKY) acct_leaky_block(v);
+#pragma unroll
+            for (int jj = 0; jj < CH; ++jj)
+              if (rbase + jj < M) C[(int64_t)(rbase + jj) * ldc + col] = v[jj];
           } else {
             float *dst = part + (int64_t)rbase * ws_ld + col;
 #pragma unroll
@@ -1029,16 +1033,24 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             __stcg(dst + (int64_t)i * ws_ld, ptx::lds32(stg_s + 4 * (i * 33 + lane)));
         } else {
           if (col < N) {
-#pragma unroll 4
-            for (int i = 0; i < 32; ++i) {
-              const int orow = row0 + i;
-              if (orow < M) {
+            // 8 rows at a time: the 96-float running sum stays in registers
+#pragma unroll 1
+            for (int i0 = 0; i0 < 32; i0 += 8) {
+              float v[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int orow = row0 + i0 + i;
+                const bool ok = orow < M;
                 // one broadcast load per row (every lane reads the same bias)
-                const float bv = bias ? __ldg(bias + orow) : 0.0f;
-                const float cv = beta != 0.0f ? C[(int64_t)orow * ldc + col] : 0.0f;
-                C[(int64_t)orow * ldc + col] =
-                    finish(ptx::lds32(stg_s + 4 * (i * 33 + lane)), alpha, beta, cv, bias, bv, act);
+                const float bv = bias && ok ? __ldg(bias + orow) : 0.0f;
+                const float cv = beta != 0.0f && ok ? C[(int64_t)orow * ldc + col] : 0.0f;
+                v[i] = finish_lin(ptx::lds32(stg_s + 4 * ((i0 + i) * 33 + lane)), alpha, beta, cv,
+                                  bias, bv);
               }
+              if (act == ACCT_ACT_LEAKY) acct_leaky_block(v);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (row0 + i0 + i < M) C[(int64_t)(row0 + i0 + i) * ldc + col] = v[i];
             }
           }
         }
@@ -1088,11 +1100,14 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
               cv[jj] = (beta != 0.0f && ok) ? C[(int64_t)(rbase + jj) * ldc + col] : 0.0f;
               bv[jj] = (bias && ok) ? __ldg(bias + rbase + jj) : 0.0f;
             }
+            float v[CH];
 #pragma unroll
             for (int jj = 0; jj < CH; ++jj)
-              if (rbase + jj < M)
-                C[(int64_t)(rbase + jj) * ldc + col] =
-                    finish(__uint_as_float(r[jj]), alpha, beta, cv[jj], bias, bv[jj], act);
+              v[jj] = finish_lin(__uint_as_float(r[jj]), alpha, beta, cv[jj], bias, bv[jj]);
+            if (act == ACCT_ACT_LEAKY) acct_leaky_block(v);
+#pragma unroll
+            for (int jj = 0; jj < CH; ++jj)
+              if (rbase + jj < M) C[(int64_t)(rbase + jj) * ldc + col] = v[jj];
           } else {
             float *dst = part + (int64_t)rbase * ws_ld + col;
 #pragma unroll
@@ -1124,13 +1139,15 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
               for (int i = 0; i < 32; ++i)
                 cv[i] = (beta != 0.0f && row0 + i < M) ? C[(int64_t)(row0 + i) * ldc + col] : 0.0f;
+              float v[32];
 #pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                const int row = row0 + i;
-                if (row < M)
-                  C[(int64_t)row * ldc + col] = finish(ptx::lds32(stg_s + 4 * (i * 33 + lane)), alpha,
-                                                       beta, cv[i], bias, bv[i], act);
-              }
+              for (int i = 0; i < 32; ++i)
+                v[i] = finish_lin(ptx::lds32(stg_s + 4 * (i * 33 + lane)), alpha, beta, cv[i], bias,
+                                  bv[i]);
+              if (act == ACCT_ACT_LEAKY) acct_leaky_block(v);
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (row0 + i < M) C[(int64_t)(row0 + i) * ldc + col] = v[i];
             }
           } else {
             float *dst = part + (int64_t)row0 * ws_ld + col;
@@ -1896,13 +1913,14 @@ splitk_reduce_kernel(const float *__restrict__ ws, int64_t ws_ld, int64_t split_
     const float bv = bias ? __ldg(bias + row) : 0.0f;
     float *cp = C + (int64_t)row * ldc + col;
     const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+    float v[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (col + e < N) {
-        const float cv = beta != 0.0f ? cp[e] : 0.0f;
-        cp[e] = finish(a4[e], alpha, beta, cv, bias, bv, act);
-      }
-    }
+    for (int e = 0; e < 4; ++e)
+      v[e] = finish_lin(a4[e], alpha, beta, beta != 0.0f && col + e < N ? cp[e] : 0.0f, bias, bv);
+    if (act == ACCT_ACT_LEAKY) acct_leaky_block(v);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (col + e < N) cp[e] = v[e];
   }
 }
 

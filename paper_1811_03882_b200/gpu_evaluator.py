@@ -18,8 +18,12 @@ Config file (all keys optional except `net`):
      "gemm": "auto" | "simt" | "tc", "timeout_seconds": 180,
      "penalty_seconds": 1000}
 
-The program handed to `build_evaluator` must be the configured net's
-source (write it with `python -m paper_1811_03882_b200.nets <net> <dir>`).
+`net` names a built-in program (the tuned source must then be its text:
+`python -m paper_1811_03882_b200.nets <net> <dir>`), or is "auto": any
+program written in the C-subset templates -- the op manifest
+(kinds, shapes, operands, array roles) is read off the tuned source by
+`nets.net_from_source`, which recognises every loop of the image loop as a
+template op or refuses the program (ModelError, exit 14).
 
 Multi-GPU: one `PatternExecutor` per entry of `devices` and a queue of idle
 entries; a GA with `workers = len(devices)` measures one individual per
@@ -46,9 +50,12 @@ from .nets import NETS, build_net
 _GEMM_MODES = {"auto": K.GEMM_AUTO, "simt": K.GEMM_SIMT, "tc": K.GEMM_TC3XTF32}
 
 
+AUTO = "auto"
+
+
 @dataclass
 class GpuEvaluatorConfig:
-    net: str = "yolov2-tiny"
+    net: str = "yolov2-tiny"     # a NETS name, or "auto": the op manifest read off the tuned source
     images: int | None = None
     devices: object = field(default_factory=lambda: [0])
     seed: int = 1
@@ -60,8 +67,11 @@ class GpuEvaluatorConfig:
     penalty_seconds: float = 1000.0
 
     def __post_init__(self):
-        if self.net not in NETS:
-            raise ModelError(f"gpu evaluator: unknown net {self.net!r} (known: {sorted(NETS)})")
+        if self.net is None:
+            self.net = AUTO
+        if self.net != AUTO and self.net not in NETS:
+            raise ModelError(f"gpu evaluator: unknown net {self.net!r} "
+                             f"(known: {sorted(NETS)}, or {AUTO!r})")
         if self.gemm not in _GEMM_MODES:
             raise ModelError(f"gpu evaluator: gemm must be one of {sorted(_GEMM_MODES)}")
         if self.repeats < 1 or self.warmup < 0:
@@ -100,10 +110,10 @@ class DevicePool:
     two GA workers never share one; each executor is also guarded by its own
     lock."""
 
-    def __init__(self, cfg: GpuEvaluatorConfig):
+    def __init__(self, cfg: GpuEvaluatorConfig, net=None):
         from .executor import PatternExecutor
         self.cfg = cfg
-        self.net = build_net(cfg.net, images=cfg.images)
+        self.net = net if net is not None else build_net(cfg.net, images=cfg.images)
         self.devices = resolve_devices(cfg.devices)
         self.executors = [PatternExecutor(self.net, device=d, seed=cfg.seed, fuse=cfg.fuse,
                                           gemm_mode=_GEMM_MODES[cfg.gemm]) for d in self.devices]
@@ -152,11 +162,32 @@ class DevicePool:
         return m
 
 
+def net_for(cfg: GpuEvaluatorConfig, program):
+    """The NetProgram the evaluator executes: a built-in net whose source
+    must be the tuned program, or (net "auto") the op manifest read off the
+    tuned program's text (`nets.net_from_source`)."""
+    if cfg.net != AUTO:
+        net = build_net(cfg.net, images=cfg.images)
+        if program is not None and program.source_text != net.source:
+            raise ModelError(f"gpu evaluator: the tuned source is not the {cfg.net!r} program "
+                             f"(write it with `python -m paper_1811_03882_b200.nets {cfg.net} "
+                             f"DIR`, or use \"net\": \"{AUTO}\")")
+        return net
+    if program is None:
+        raise ModelError('gpu evaluator: net "auto" needs the tuned program')
+    from .nets import ProgramError, net_from_source
+    try:
+        net = net_from_source(program.source_text, name=AUTO)
+    except ProgramError as exc:
+        raise ModelError(f"gpu evaluator: {exc}") from exc
+    if cfg.images is not None and cfg.images != net.spec.images:
+        raise ModelError(f"gpu evaluator: images {cfg.images} != the program's image loop "
+                         f"trip count {net.spec.images}")
+    return net
+
+
 def make_gpu_evaluator(cfg: GpuEvaluatorConfig, program, tree, accesses, genome_map, profile):
-    pool = DevicePool(cfg)
-    if program is not None and program.source_text != pool.net.source:
-        raise ModelError(f"gpu evaluator: the tuned source is not the {cfg.net!r} program "
-                         f"(write it with `python -m paper_1811_03882_b200.nets {cfg.net} DIR`)")
+    pool = DevicePool(cfg, net_for(cfg, program))
 
     def evaluate(bits: str) -> Measurement:
         return pool.measure(bits)

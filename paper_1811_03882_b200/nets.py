@@ -32,6 +32,7 @@ the north star lists no normalize op.
 from __future__ import annotations
 
 import math
+import re
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -422,19 +423,115 @@ def input_images(net: NetProgram, seed: int, first: int, count: int) -> np.ndarr
     return flat.reshape((count,) + spec.shape)
 
 
-def write_net_files(name: str, outdir, images: int | None = None) -> dict:
+# ------------------------------------------------- programs from their text
+_PARAM = re.compile(r"^(float|int) ([A-Za-z_]\w*)((?:\[\d+\])+)$")
+_CALL = re.compile(r"\b(load_input|store_output)\((\w+)\)")
+
+
+class ProgramError(ValueError):
+    """The source is not a Darknet-style program in the C-subset templates."""
+
+
+def net_from_source(source: str, name: str = "program") -> NetProgram:
+    """The NetProgram of a user-authored C-subset program,
+    read off its text instead of a NETS layer list: `forward`'s parameters
+    are the arrays; the loop holding `load_input(x)` / `store_output(y)` is
+    the image loop; every loop directly inside it must be exactly one op as
+    the templates write it (`kernel_probe.recognize`: kind, shape and
+    operands are read off the headers and checked line for line).  Array
+    roles follow from the ops: gemm A = weights, add_bias bias = biases,
+    maxpool I = indexes, im2col Y = workspace.  Raises ProgramError."""
+    from .kernel_probe import candidate_block, recognize
+    from .loopnest import build_loop_tree
+    from .syntax import parse
+    head = re.search(r"\bint forward\(([^)]*)\)\s*\{", source)
+    if head is None:
+        raise ProgramError("no `int forward(...)` function")
+    arrays: dict[str, ArraySpec] = {}
+    for decl in (d.strip() for d in head.group(1).split(",")):
+        m = _PARAM.match(decl)
+        if m is None:
+            raise ProgramError(f"forward parameter {decl!r} is not a float/int array")
+        dims = tuple(int(v) for v in re.findall(r"\d+", m.group(3)))
+        if len(dims) > 2:
+            raise ProgramError(f"array {m.group(2)} has more than two dimensions")
+        arrays[m.group(2)] = ArraySpec(m.group(2), m.group(1), dims, "activation")
+    try:
+        tree = build_loop_tree(parse(source))
+    except Exception as exc:  # noqa: BLE001 -- the reference front end's errors
+        raise ProgramError(f"cannot parse the program: {exc}") from exc
+    tops = [n for n in tree.nodes if n.parent is None and n.function == "forward"]
+    if len(tops) != 1:
+        raise ProgramError("forward must hold exactly one top-level (image) loop")
+    img = tops[0]
+    img_text = source[img.span[0]:img.span[1]]
+    calls = dict((k, v) for k, v in _CALL.findall(img_text))
+    if set(calls) != {"load_input", "store_output"}:
+        raise ProgramError("the image loop must call load_input(x) and store_output(y)")
+    input_name, output_name = calls["load_input"], calls["store_output"]
+    for v in (input_name, output_name):
+        if v not in arrays or arrays[v].dtype != "float":
+            raise ProgramError(f"{v} is not a float parameter of forward")
+    m = re.match(r"for \((\w+) = 0; \1 < (\d+); \1\+\+\)", img_text)
+    if m is None:
+        raise ProgramError("the image loop header is not `for (b = 0; b < N; b++)`")
+    images = int(m.group(2))
+    trips, parents = [], []
+    for n in tree.nodes:
+        mh = re.match(r"for \((\w+) = 0; \1 < (\d+); \1\+\+\)", source[n.span[0]:n.span[1]])
+        if mh is None:
+            raise ProgramError(f"loop {n.loop_id} is not a counted `for` loop")
+        trips.append(int(mh.group(2)))
+        parents.append(n.parent)
+    ops: list[OpSpec] = []
+    for lid in img.children:
+        node = tree.nodes[lid]
+        line0 = source.rfind("\n", 0, node.span[0]) + 1          # keep the header's indent
+        text = "#pragma acc kernels\n" + source[line0:node.span[1]]
+        block = candidate_block(text)
+        got = recognize(block) if block else None
+        if got is None:
+            raise ProgramError(f"loop {lid} (line {node.header_pos.line}) is not a template op")
+        kind, params, ops_arrays = got
+        for role, v in ops_arrays.items():
+            if v not in arrays:
+                raise ProgramError(f"loop {lid}: {v} is not a parameter of forward")
+        ops.append(OpSpec(kind, len(ops), loop_id=lid, arrays=ops_arrays, params=params))
+    for op in ops:
+        a = op.arrays
+        if op.kind == "gemm":
+            arrays[a["A"]].role = "weight"
+        elif op.kind == "add_bias":
+            arrays[a["bias"]].role = "bias"
+        elif op.kind == "maxpool":
+            arrays[a["I"]].role = "index"
+        elif op.kind == "im2col":
+            arrays[a["Y"]].role = "workspace"
+    arrays[input_name].role = "input"
+    arrays[output_name].role = "output"
+    xs = arrays[input_name].shape
+    spec = NetSpec(name, xs[0] if len(xs) == 2 else 1, 0, 0, (), images)
+    return NetProgram(spec, source, arrays, ops, trips, parents, img.loop_id, input_name,
+                      output_name)
+
+
+def write_net_files(name, outdir, images: int | None = None, auto: bool = False) -> dict:
     """Write `<name>.c`, `<name>_profile.json` and a `<name>_gpu.json`
-    evaluator config -- the inputs of `tune --evaluator gpu:...`."""
+    evaluator config -- the inputs of `tune --evaluator gpu:...`.  `name` is
+    a NETS key or a NetSpec (any layer list); `auto` writes the config as
+    `{"net": "auto"}` (manifest read off the source)."""
     import json
     from pathlib import Path
     net = build_net(name, images=images)
+    name = net.spec.name
     out = Path(outdir)
     out.mkdir(parents=True, exist_ok=True)
     paths = {"source": out / f"{name}.c", "profile": out / f"{name}_profile.json",
              "gpu_config": out / f"{name}_gpu.json"}
     paths["source"].write_text(net.source)
     paths["profile"].write_text(json.dumps(net.profile_dict(), indent=1) + "\n")
-    paths["gpu_config"].write_text(json.dumps({"net": name, "images": net.spec.images}) + "\n")
+    cfg = {"net": "auto"} if auto else {"net": name, "images": net.spec.images}
+    paths["gpu_config"].write_text(json.dumps(cfg) + "\n")
     return paths
 
 

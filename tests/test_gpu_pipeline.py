@@ -112,3 +112,39 @@ def test_ga_two_workers_on_one_gpu(cuda_device):
                             [(h.best_seconds, h.evaluations_performed) for h in res.history],
                             res.evaluations_performed)
     assert results[1] == results[2]
+
+
+def test_tune_cli_gpu_auto_on_a_layer_list_not_in_nets(cuda_device, tmp_path):
+    """A program written in the templates but not one of the built-in nets
+    tunes end to end through the reference CLI with `{"net": "auto"}` (the
+    op manifest read off the source), and its patterns match the oracle."""
+    import numpy as np
+
+    from oracle import cprog
+    from paper_1811_03882_b200.executor import PatternExecutor
+    from paper_1811_03882_b200.nets import Conv, MaxPool, NetSpec, Region, net_from_source
+    spec = NetSpec("custom", 3, 24, 20, (Conv(12, 3), MaxPool(2, 2), Conv(20, 3), Conv(10, 1),
+                                         MaxPool(2, 1), Conv(6, 1, activation="linear"), Region()),
+                   images=3)
+    paths = write_net_files(spec, tmp_path, auto=True)
+    code = cli.main(["tune", "--source", str(paths["source"]), "--profile",
+                     str(paths["profile"]), "--evaluator", f"gpu:{paths['gpu_config']}",
+                     "--pop", "6", "--gens", "3", "--seed", "2", "--gate-threshold", "1",
+                     "--out", str(tmp_path / "best.c"), "--report", str(tmp_path / "report.json")])
+    assert code == 0
+    report = json.loads((tmp_path / "report.json").read_text())
+    assert report["result"] == "ok" and report["best"]["status"] == "measured"
+    gpu = report["gpu"]
+    for key, val in gpu["expected_transfers"].items():
+        assert gpu["transfers"][key] == val
+    net = net_from_source(paths["source"].read_text(), "auto")
+    want = cprog.reference_forward(net)["outputs"]
+    ex = PatternExecutor(net, device=0)
+    a = len(net.ops)
+    for bits in (report["best"]["genome"], "1" * a, "".join("1" if k % 2 else "0" for k in range(a))):
+        sched = ex.compile(bits)
+        r = ex.run(sched)
+        for key, val in sched.expected.items():
+            assert r.counters[key] == val, (bits, key)
+        scale = float(np.abs(want).max())
+        assert float(np.abs(ex.outputs() - want).max()) <= 1e-4 * scale, bits

@@ -405,16 +405,17 @@ def _net_program(net_name: str, images: int | None = None):
 
 
 def ga_gpu(net_name: str, images: int | None, devices, pop: int, gens: int, seed: int,
-           warmup: int, repeats: int) -> dict:
+           warmup: int, repeats: int, per_device: int = 1) -> dict:
     """The GA (reference run_ga semantics, ga.py:170-282) with the gpu:
-    evaluator: every individual's offload pattern executed on B200, one
-    executor per GPU, workers = GPUs."""
+    evaluator: every individual's offload pattern executed on B200,
+    `per_device` executors per GPU, workers = executors."""
     from paper_1811_03882_b200 import GAConfig, MeasurementCache, run_ga
     from paper_1811_03882_b200.gpu_evaluator import GpuEvaluatorConfig, make_gpu_evaluator
     net, prog, tree, acc, gm, prof = _net_program(net_name, images)
     cfg = GpuEvaluatorConfig(net=net_name, images=images, devices=devices, repeats=repeats,
-                             warmup=warmup)
-    ga = GAConfig(population=pop, generations=gens, rng_seed=seed, workers=len(devices))
+                             warmup=warmup, workers_per_device=per_device)
+    ga = GAConfig(population=pop, generations=gens, rng_seed=seed,
+                  workers=len(devices) * per_device)
     t0 = time.perf_counter()
     ev = make_gpu_evaluator(cfg, prog, tree, acc, gm, prof)
     setup = time.perf_counter() - t0
@@ -423,7 +424,8 @@ def ga_gpu(net_name: str, images: int | None, devices, pop: int, gens: int, seed
     wall = time.perf_counter() - t1
     a = len(gm)
     return {"config": f"{net_name} ({a} genes, {net.spec.images} image(s) per evaluation), "
-                      f"pop {pop} x {gens} gens, seed {seed}, {len(devices)} GPU(s) = workers, "
+                      f"pop {pop} x {gens} gens, seed {seed}, {len(devices)} GPU(s) x "
+                      f"{per_device} executor(s) = workers, "
                       f"warm-up {warmup} + median of {repeats} run(s) per evaluation",
             "wall_s": wall, "setup_s": setup, "evaluations": res.evaluations_performed,
             "cache_hits": res.cache_hits, "seconds_per_evaluation": wall / max(1, res.evaluations_performed),
@@ -624,6 +626,15 @@ def run_ours(args):
         if not args.quick:
             ga_paper = ga_gpu(args.net, 1, devices, 30, 20, 1, 1, 1)
             ga_paper["config"] = "BASELINE configs[2]: " + ga_paper["config"]
+            # the same search with several executors per GPU: evaluations are
+            # dominated by single-threaded host loops, which then run on
+            # separate host cores (GPU work of concurrent evaluations shares
+            # the device, so fitness includes that contention)
+            per = max(1, min(8, (os.cpu_count() or 1) // (2 * world)))
+            if per > 1:
+                ga_conc = ga_gpu(args.net, 1, devices, 30, 20, 1, 1, 1, per_device=per)
+                ga_conc["config"] = "BASELINE configs[2], concurrent: " + ga_conc["config"]
+                ga_paper["concurrent"] = ga_conc
             if world == 1:
                 ga_paper_ref = ga_reference(args.net, 1, 30, 1, 1, os.cpu_count() or 1)
     if world > 1:

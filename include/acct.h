@@ -168,6 +168,24 @@ int acct_conv3x3_tc_f32(const float *im, int64_t ld_im, int64_t im_stride, int c
                         float *pool, int64_t ld_pool, int64_t pool_stride, int32_t *idx,
                         int64_t ld_idx, int64_t idx_stride, int c_from, acct_stream_t stream);
 
+/* The same contract for the wide, long-K layers (M >= 256 filters, 9 x
+ * channels > 768; yolov2-tiny layers 8, 10, 12, 13): the CTA-pair
+ * chunked-promotion 3xTF32 gemm whose operand B -- the im2col of the input --
+ * is gathered from the input planes by the kernel (implicit im2col) instead
+ * of written to col by an im2col launch and read back.  Bit-identical to
+ * acct_im2col_batched_f32 + the gemm; col is stored for images >= col_from.
+ * C and col column-interleaved with one image pitch (c_stride ==
+ * col_stride); ENOTSUP otherwise and when a maxpool is requested (pool must
+ * be NULL).  Replaces the im2col + gemm_nn loop pair of
+ * pkg/src/acctuner/... (SURVEY.md 8(a) CNN ops) for these layers. */
+int acct_conv3x3_gemm_tc_f32(const float *im, int64_t ld_im, int64_t im_stride, int channels,
+                             int height, int width, float *col, int64_t ld_col,
+                             int64_t col_stride, int M, const float *A, int64_t lda, float beta,
+                             float *C, int64_t ldc, int64_t c_stride, const float *bias, int act,
+                             int batch, int col_from, float *pool, int64_t ld_pool,
+                             int64_t pool_stride, int32_t *idx, int64_t ld_idx,
+                             int64_t idx_stride, int c_from, acct_stream_t stream);
+
 /* Test support (synchronous, allocates scratch): evaluates the kernels'
  * leaky activation against darknet's (float)(0.1 * (double)x) for all 2^32
  * float bit patterns on the current device; *mismatches = differing
@@ -328,7 +346,8 @@ int acct_tc_trace(long long *out);
  * the small 3xTF32 terms, 15 = pair 256x192 BK 32, second accumulator, only
  * A lo in TMEM, 16 = the same for the long-K pair launches that otherwise
  * run the stream-K chunked-promotion tile (pair 256x192 BK 32, FP32 running
- * sum every 4 k-blocks -- the default for K > 768));
+ * sum every 4 k-blocks -- the default for K > 768), 17 = that tile for any
+ * normal-orientation shape (the tile acct_conv3x3_gemm_tc_f32 uses);
  * tests and tools only                                                     */
 void acct_tc_set_tile(int tile);
 /* CTA pairs of the stream-K gemm that fit on the current device at once */

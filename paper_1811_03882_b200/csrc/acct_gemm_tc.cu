@@ -592,6 +592,24 @@ __device__ __forceinline__ long long gtimer() {
 // LOA: only A lo goes to TMEM (BK columns per stage instead of 2 BK); the MMAs
 // with A hi read the raw K-major tile from shared memory -- leaves TMEM room
 // for DUAL with BK = 32
+// IMB (implicit B, with PK): operand B is the im2col of a 3x3 / stride 1 /
+// pad 1 convolution's input, gathered by the split warps straight from the
+// input planes (L2-resident: 11 MB for yolov2-tiny L13 at 16 images) instead
+// of a col array that an im2col launch wrote to HBM and TMA reads back.  B
+// column n of the launch = image n / img, pixel n % img (the interleaved
+// multi-image layout); row k = (channel k / 9, tap k % 9).  The gathered
+// values are the col array's exactly, so C is bit-identical to im2col + the
+// same gemm, and the split warps store them to col for the images whose col
+// is observable (n >= col_n0).
+struct ImB {
+  const float *act;         // conv input: channel c of image b at act + c act_ld + b act_img
+  int64_t act_ld, act_img;
+  int64_t img;              // launch column pitch of one image (0: one image)
+  int cin, H, W;            // input planes (= output planes: 3x3 / 1 / 1)
+  float *col;               // col array (null: no column observable)
+  int64_t col_ld, col_n0;   // col row stride; first launch column whose col is stored
+};
+
 // PK > 0 (chunked promotion): the k-loop of a unit is cut into chunks of PK
 // k-blocks; each chunk accumulates into a FRESH TMEM accumulator (two,
 // ping-pong, NACC = 2) and BOTH epilogue groups add the finished chunk into
@@ -602,9 +620,17 @@ __device__ __forceinline__ long long gtimer() {
 // ~20x below DUAL's.  The unit's final store overlaps the next unit's first
 // chunk (the other accumulator).
 template <int TN, int NACC_, int BK_, bool SWAP_ = false, bool DUAL_ = false, bool LOA_ = false,
-          int PK_ = 0>
+          int PK_ = 0, bool IMB_ = false>
 struct Cfg2 {
   static constexpr int PK = PK_;
+  // implicit B: per stage, the input slab the k-block's B rows are gathered
+  // from -- SLAB_CH channels x SEG consecutive pixels, for up to two images
+  static constexpr int SEG = 256, SLAB_CH = 5;
+#ifdef ACCT_DBG_NOSLAB
+  static constexpr int SLAB_BYTES = 0;
+#else
+  static constexpr int SLAB_BYTES = IMB_ ? 2 * SLAB_CH * SEG * 4 : 0;
+#endif
   static_assert(PK_ == 0 || (!SWAP_ && !DUAL_ && NACC_ == 2 && TN == 192),
                 "chunked promotion: normal 192-wide pair tile, two accumulators");
   static constexpr bool SWAP = SWAP_;
@@ -618,12 +644,16 @@ struct Cfg2 {
   static constexpr int Y_TILE = HALF * BK * 4;
   static constexpr uint32_t K_SBO = 8 * BK * 4;  // 8-row swizzle atom of a K-major tile
   static constexpr uint32_t K_LAYOUT = BK == 32 ? ptx::kLayoutSW128 : 4u;
-  static constexpr int STAGE_BYTES = X_TILE + 2 * Y_TILE;
+  static constexpr int STAGE_BYTES = X_TILE + 2 * Y_TILE + SLAB_BYTES;
   static constexpr int NACC = NACC_;
   static constexpr int BUDGET = 220 * 1024 - STAGING_BYTES - 512 - 1024;
   static constexpr int SMEM_STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
   static constexpr int TMEM_STAGES = (512 - NACC * ACC) / A_STAGE_COLS;
+#ifdef ACCT_DBG_S3
+  static constexpr int STAGES = 3;
+#else
   static constexpr int STAGES = SMEM_STAGES < TMEM_STAGES ? SMEM_STAGES : TMEM_STAGES;
+#endif
   static constexpr int A_COL0 = NACC * ACC;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGING_BYTES + 512 + 1024;
   static constexpr uint32_t MN_CHUNK = BK * 128;
@@ -633,14 +663,16 @@ struct Cfg2 {
   static_assert(STAGES >= 2, "pipeline too shallow");
 };
 
-template <int TN, int NACC, int BK_, bool SWAP, bool DUAL = false, bool LOA = false, int PK = 0>
+template <int TN, int NACC, int BK_, bool SWAP, bool DUAL = false, bool LOA = false, int PK = 0,
+          bool IMB = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 int M, int N, int K, int nt, int mt, int splits, int kb_per, int write_hi,
                 float alpha, float beta, float *__restrict__ C, int64_t ldc,
                 const float *__restrict__ bias, int act, float *__restrict__ ws, int64_t ws_ld,
-                int64_t ws_split_stride, int *__restrict__ sk_flags) {
-  using G = Cfg2<TN, NACC, BK_, SWAP, DUAL, LOA, PK>;
+                int64_t ws_split_stride, int *__restrict__ sk_flags, const ImB imb) {
+  using G = Cfg2<TN, NACC, BK_, SWAP, DUAL, LOA, PK, IMB>;
+  static_assert(!IMB || (PK > 0 && !SWAP), "implicit B: the chunked-promotion normal tile");
   constexpr int S = G::STAGES, BK = G::BK;
   static_assert(!LOA || !SWAP, "LOA is for the normal orientation");
   extern __shared__ uint8_t smem_raw[];
@@ -649,6 +681,8 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   auto x_hi = [&](int s) { return base + s * G::STAGE_BYTES; };
   auto y_hi = [&](int s) { return base + s * G::STAGE_BYTES + G::X_TILE; };
   auto y_lo = [&](int s) { return base + s * G::STAGE_BYTES + G::X_TILE + G::Y_TILE; };
+  auto slab = [&](int s) { return base + s * G::STAGE_BYTES + G::X_TILE + 2 * G::Y_TILE; };
+
   float *staging = reinterpret_cast<float *>(base + S * G::STAGE_BYTES);
   uint64_t *full = reinterpret_cast<uint64_t *>(base + S * G::STAGE_BYTES + STAGING_BYTES);
   uint64_t *conv = full + S;
@@ -737,6 +771,28 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   pdl_trigger();
   pdl_wait();
 
+  // implicit B: the images a unit's half tile (this CTA's HALF columns)
+  // touches -- at most two (the host requires an image pitch >= HALF) -- and
+  // the 16-B aligned first pixel of each image's slab segment
+  struct Span {
+    int b0, nimg, start[2];
+  };
+  auto span_of = [&](const Unit &w) {
+    Span sp{0, 0, {0, 0}};
+    const int n_first = w.n0 + rank * G::HALF;
+    const int n_last = min(n_first + G::HALF, N) - 1;
+    if (n_first > n_last) return sp;
+    const int img = (int)imb.img;
+    sp.b0 = img ? n_first / img : 0;
+    const int b1 = img ? n_last / img : 0;
+    sp.nimg = b1 - sp.b0 + 1;
+    for (int t = 0; t < sp.nimg; ++t) {
+      const int p_lo = t == 0 ? n_first - sp.b0 * img : 0;
+      sp.start[t] = max(0, p_lo - imb.W - 1) & ~3;
+    }
+    return sp;
+  };
+
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs: their own A rows, B half) ----------------
     if (lane == 0) {
@@ -748,14 +804,26 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           const int s = g % S;
           if (g >= S) ptx::mbar_wait(&empty[s], ((g / S) - 1) & 1);
           if ((write_hi & 16) && blockIdx.x == 0 && g < kTrace) g_trace[0][g] = gtimer();
-          ptx::mbar_expect_tx(&full[s], G::X_TILE + G::Y_TILE);
           const int kx = (w.kb0 + kb) * BK;
-          if constexpr (!SWAP) {
+          if constexpr (IMB) {
+            // A, and the input slab segments of the k-block's <= 5 channels
+            // (tmB = the input as (pixels, images, channels), zeros past the
+            // plane and past the channels)
+            const Span sp = span_of(w);
+            const int nload = ACCT_SKIP(write_hi, 32) ? 0 : sp.nimg;  // profiling: no slab TMA
+            ptx::mbar_expect_tx(&full[s], G::X_TILE + nload * G::SLAB_CH * G::SEG * 4);
+            ptx::tma_load_2d(x_hi(s), &tmA, &full[s], kx, m_rows);
+            for (int t = 0; t < nload; ++t)
+              ptx::tma_load_3d(slab(s) + t * G::SLAB_CH * G::SEG * 4, &tmB, &full[s], sp.start[t],
+                               sp.b0 + t, kx / 9);
+          } else if constexpr (!SWAP) {
+            ptx::mbar_expect_tx(&full[s], G::X_TILE + G::Y_TILE);
             ptx::tma_load_2d(x_hi(s), &tmA, &full[s], kx, m_rows);
 #pragma unroll
             for (int c = 0; c < G::HALF / 32; ++c)
               ptx::tma_load_2d(y_hi(s) + c * G::MN_CHUNK, &tmB, &full[s], n_cols + 32 * c, kx);
           } else {
+            ptx::mbar_expect_tx(&full[s], G::X_TILE + G::Y_TILE);
 #pragma unroll
             for (int c = 0; c < 4; ++c)
               ptx::tma_load_2d(x_hi(s) + c * G::MN_CHUNK, &tmB, &full[s], n_cols + 32 * c, kx);
@@ -873,6 +941,37 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t conv_leader = ptx::mapa(ptx::smem_u32(&conv[0]), 0);
     int g = 0;
     for_each_unit([&](const Unit &w, int, int) {
+      // implicit B: this thread gathers columns 3 lane .. 3 lane + 2 of the
+      // CTA's half tile, rows q, q + 4, ... of every k-block
+      // (column 32 j + lane of the half tile = launch column n = image
+      // n / img, pixel n % img: its slab offset, the 9-bit mask of its taps
+      // inside the plane, whether its col is stored)
+      int goff[3], gn[3];
+      uint32_t gmask[3];
+      bool gcol[3];
+      if constexpr (IMB) {
+        const int HW = imb.H * imb.W;
+        const Span sp = span_of(w);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const int n = w.n0 + rank * G::HALF + 32 * j + lane;
+          const int im = imb.img ? (int)(n / imb.img) : 0;
+          const int px = n - (int)(im * imb.img);
+          const int t = im - sp.b0;
+          const bool ok = n < N && px < HW && t >= 0 && t < sp.nimg;
+          const int y = px / imb.W, x = px - (px / imb.W) * imb.W;
+          uint32_t m = 0;
+#pragma unroll
+          for (int r = 0; r < 9; ++r) {
+            const int yy = y + r / 3 - 1, xx = x + r % 3 - 1;
+            if (ok && yy >= 0 && yy < imb.H && xx >= 0 && xx < imb.W) m |= 1u << r;
+          }
+          gmask[j] = m;
+          gn[j] = n;
+          gcol[j] = ok && imb.col != nullptr && n >= imb.col_n0;
+          goff[j] = t * G::SLAB_CH * G::SEG + px - sp.start[t & 1];
+        }
+      }
       for (int kb = 0; kb < w.nkb; ++kb, ++g) {
         const int s = g % S;
         ptx::mbar_wait(&full[s], (g / S) & 1);
@@ -880,6 +979,37 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           g_trace[blockIdx.x == 0 ? 1 : 5][g] = gtimer();
         const uint32_t xh = ptx::smem_u32(x_hi(s));
         const uint32_t yh = ptx::smem_u32(y_hi(s)), yl = ptx::smem_u32(y_lo(s));
+        if constexpr (IMB) {
+          // B from the slab: raw and lo of each value at its
+          // SWIZZLE_128B_BASE32B place (32-column chunks, 128-B rows, 32-B
+          // pieces XOR k % 4); col for the observable images
+          const int kx = (w.kb0 + kb) * BK;
+          const int K9 = 9 * imb.cin;
+          const int c0 = kx / 9;
+          const uint32_t sl = ptx::smem_u32(slab(s));
+          // lane = one column of each 32-column chunk: conflict-free LDS
+          // (consecutive pixels) and STS (one 128-B row per chunk and k)
+          const uint32_t lane_off = (uint32_t)((lane & 7) << 2);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int kl = q + 4 * i;
+            const int k = kx + kl;
+            const int c = k / 9, r = k - 9 * c;
+            const int tap = (c - c0) * G::SEG + (r / 3 - 1) * imb.W + (r - 3 * (r / 3)) - 1;
+            const uint32_t row = kl * 128 + ((((lane >> 3) ^ kl) & 3) << 5) + lane_off;
+            const bool kin = k < K9;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              const bool ok = kin && ((gmask[j] >> r) & 1u);
+              const float v = ok && !ACCT_SKIP(write_hi, 64) ? ptx::lds32(sl + 4 * (goff[j] + tap))
+                                                             : 0.0f;
+              const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+              ptx::sts32(yh + j * G::MN_CHUNK + row, v);
+              ptx::sts32(yl + j * G::MN_CHUNK + row, v - h);
+              if (gcol[j] && kin) __stcs(imb.col + (int64_t)k * imb.col_ld + gn[j], v);
+            }
+          }
+        }
         if (!(ACCT_SKIP(write_hi, 2))) {
           // row r of the K-major A tile: 16-B chunk c at r*ROWB + (c ^ swz(r))*16,
           // swz = (r/2)%4 for SWIZZLE_64B rows, r%8 for SWIZZLE_128B rows
@@ -904,11 +1034,13 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
               ra[c] = make_float4(v[0], v[1], v[2], v[3]);
             }
           }
-          constexpr int NY = (G::Y_TILE / 16 + 127) / 128;
+          constexpr int NY = IMB ? 1 : (G::Y_TILE / 16 + 127) / 128;
           float4 ry[NY];
+          if constexpr (!IMB) {
 #pragma unroll
-          for (int i = 0; i < NY; ++i)
-            if (ct + 128 * i < G::Y_TILE / 16) ry[i] = ptx::lds128(yh + 16 * (ct + 128 * i));
+            for (int i = 0; i < NY; ++i)
+              if (ct + 128 * i < G::Y_TILE / 16) ry[i] = ptx::lds128(yh + 16 * (ct + 128 * i));
+          }
           uint32_t hi[BK], lo[BK];
 #pragma unroll
           for (int c = 0; c < BK / 4; ++c) {
@@ -927,11 +1059,13 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             ptx::tmem_st_cols<BK>(ta, hi);
             ptx::tmem_st_cols<BK>(ta + BK, lo);
           }
+          if constexpr (!IMB) {
 #pragma unroll
-          for (int i = 0; i < NY; ++i) {
-            if (ct + 128 * i < G::Y_TILE / 16) {
-              float4 h4;
-              ptx::sts128(yl + 16 * (ct + 128 * i), split_lo(ry[i], h4));
+            for (int i = 0; i < NY; ++i) {
+              if (ct + 128 * i < G::Y_TILE / 16) {
+                float4 h4;
+                ptx::sts128(yl + 16 * (ct + 128 * i), split_lo(ry[i], h4));
+              }
             }
           }
           ptx::tmem_st_wait();
@@ -2226,19 +2360,42 @@ int launch_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, con
   return ACCT_OK;
 }
 
+// 3-D fp32 tensor map of a conv input for the implicit-B gemm: (pixels of
+// one plane, images, channels), box SEG pixels x 1 image x SLAB_CH channels;
+// out-of-bounds pixels / channels read 0
+bool make_input_map(CUtensorMap *map, const ImB &ib, int batch, uint32_t seg, uint32_t nch) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const uint64_t hw = (uint64_t)ib.H * ib.W;
+  const uint64_t img_stride = batch > 1 ? (uint64_t)ib.act_img : ((hw + 3) & ~3ull);
+  cuuint64_t dims[3] = {hw, (cuuint64_t)batch, (cuuint64_t)ib.cin};
+  cuuint64_t strides[2] = {img_stride * 4, (uint64_t)ib.act_ld * 4};
+  cuuint32_t box[3] = {seg, 1, nch};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(ib.act), dims, strides,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int TN, int NACC, int BK, bool SWAP = false, bool DUAL = false, bool LOA = false,
-          int PK = 0>
+          int PK = 0, bool IMB = false>
 int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, const float *B,
                int64_t ldb, float beta, float *C, int64_t ldc, const float *bias, int act,
-               cudaStream_t s) {
-  using G = Cfg2<TN, NACC, BK, SWAP, DUAL, LOA, PK>;
+               cudaStream_t s, const ImB *imb = nullptr, const CUtensorMap *bmap = nullptr) {
+  using G = Cfg2<TN, NACC, BK, SWAP, DUAL, LOA, PK, IMB>;
   CUtensorMap ta, tb;
   // weights: K-major box of BK x (128 rows, or TN/2 rows per CTA when swapped)
   if (!cached_map(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BK, SWAP ? TN / 2 : 128,
                   BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B) ||
-      !cached_map(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, 32, BK,
-                  CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+      (!IMB && !cached_map(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, 32, BK,
+                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)))
     return fail(ACCT_ENOTSUP, "gemm_tc2: cuTensorMapEncodeTiled failed");
+#ifdef ACCT_DBG_TBTA
+  if (IMB) tb = ta;
+#else
+  if (IMB) tb = *bmap;  // the conv input: the split warps gather B from its slabs
+#endif
+  const ImB ib = imb ? *imb : ImB{};
   const int tile_n = SWAP ? 256 : TN, tile_m = SWAP ? TN : 256;
   const int nt = (N + tile_n - 1) / tile_n, mt = (M + tile_m - 1) / tile_m, tiles = mt * nt;
   const int total_kb = (K + BK - 1) / BK;
@@ -2265,7 +2422,7 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(mu);
     if (dev >= 0 && dev < 64 && !done[dev]) {
-      if (int rc = check_cuda(cudaFuncSetAttribute(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA, PK>,
+      if (int rc = check_cuda(cudaFuncSetAttribute(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA, PK, IMB>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    G::SMEM_BYTES),
                               "gemm_tc2: smem attribute"))
@@ -2281,15 +2438,15 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
     // co-resident: the grid is capped at the clusters that fit at once
     const int cpt = (total_kb + PK - 1) / PK;
     const int64_t tot_ch = (int64_t)tiles * cpt;
-    pairs = sk_pairs(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA, PK>, G::SMEM_BYTES);
+    pairs = sk_pairs(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA, PK, IMB>, G::SMEM_BYTES);
     if (pairs < 1) return fail(ACCT_ENOTSUP, "gemm_tc2 stream-K: no co-resident CTA pairs");
     if (tot_ch < pairs) pairs = (int)tot_ch;
     if (int rc = scratch_for(s, (size_t)2 * pairs * 128 * TN, &ws)) return rc;
     if (int rc = sk_flags_for(s, 2 * pairs, &flags)) return rc;
   }
-  launch(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA, PK>, dim3(2 * pairs), dim3(THREADS), G::SMEM_BYTES, s, ta, tb, M,
-         N, K, nt, mt, splits, kb_per, g_write_hi, alpha, beta, C, ldc, bias, act, ws, ws_ld,
-         rows * ws_ld, flags);
+  launch(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA, PK, IMB>, dim3(2 * pairs), dim3(THREADS),
+         G::SMEM_BYTES, s, ta, tb, M, N, K, nt, mt, splits, kb_per, g_write_hi, alpha, beta, C, ldc,
+         bias, act, ws, ws_ld, rows * ws_ld, flags, ib);
   if (int rc = note_launch("gemm_tc2")) return rc;
   if (splits > 1) {
     const int64_t work = (int64_t)M * ((N + 3) / 4);
@@ -2367,6 +2524,8 @@ int gemm_tc(int M, int N, int K, float alpha, const float *A, int64_t lda, const
   // boundary).  Chunks of 2 / 1 k-blocks: 4.9e-5 / 4.6e-5 at 17% / 37% more
   // time -- the remaining error is elsewhere (tools/err_dist.py).
   constexpr int kDualK = 768;
+  if (force == 17)  // the chunked-promotion pair tile whatever the cost model says (tests)
+    return launch_tc2<192, 2, 32, false, false, true, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
   if ((c10 < c1 || c9 < c1) && K > kDualK) {
     if (force == 16)  // the previous default (DUAL, no promotion), for comparison
       return launch_tc2<192, 1, 32, false, true, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, bias, act, s);
@@ -2530,7 +2689,8 @@ extern "C" void acct_tc_set_write_hi(int on) { acct::g_write_hi = on; }
 // co-resident CTA pairs of the stream-K gemm on the current device (diagnostics)
 extern "C" int acct_tc_stream_k_pairs(void) {
   using G = acct::Cfg2<192, 2, 32, false, false, true, 4>;
-  return acct::sk_pairs(acct::tc2_gemm_kernel<192, 2, 32, false, false, true, 4>, G::SMEM_BYTES);
+  return acct::sk_pairs(acct::tc2_gemm_kernel<192, 2, 32, false, false, true, 4, false>,
+                        G::SMEM_BYTES);
 }
 
 extern "C" void acct_tc_set_tile(int tile) { acct::g_force_tile.store(tile < 0 ? 0 : tile); }
@@ -2589,4 +2749,57 @@ extern "C" int acct_conv3x3_tc_f32(const float *im, int64_t ld_im, int64_t im_st
   if (rc == ACCT_ENOTSUP)
     return fail(ACCT_ENOTSUP, "conv3x3 tc: weights + slabs exceed shared memory");
   return rc;
+}
+
+// C = A . im2col(im) + beta C (+ bias, act) for 3x3/1/1 convolutions with
+// many filters and a long K (M >= 256, 9 channels > 768): the CTA-pair
+// chunked-promotion gemm with operand B gathered from the input planes
+// (implicit im2col, ImB) -- bit-identical to acct_im2col_batched_f32 + the
+// same gemm; col stored for images >= col_from.  C and col must be
+// column-interleaved with one image pitch (c_stride == col_stride); the input
+// may use any image stride.  ENOTSUP for other shapes and for a fused pool.
+extern "C" int acct_conv3x3_gemm_tc_f32(const float *im, int64_t ld_im, int64_t im_stride,
+                                        int channels, int height, int width, float *col,
+                                        int64_t ld_col, int64_t col_stride, int M,
+                                        const float *A, int64_t lda, float beta, float *C,
+                                        int64_t ldc, int64_t c_stride, const float *bias,
+                                        int act, int batch, int col_from, float *pool,
+                                        int64_t ld_pool, int64_t pool_stride, int32_t *idx,
+                                        int64_t ld_idx, int64_t idx_stride, int c_from,
+                                        acct_stream_t stream) {
+  using namespace acct;
+  (void)ld_pool, (void)pool_stride, (void)idx, (void)ld_idx, (void)idx_stride, (void)c_from;
+  const int64_t HW = (int64_t)height * width;
+  const int K = 9 * channels;
+  if (pool || M < 256 || K <= 768 || channels < 1 || height < 1 || width < 1 || batch < 1 ||
+      col_from < 0 || HW > (1 << 24) || ldc < HW || ld_col < HW ||
+      (batch > 1 && (c_stride < HW || col_stride != c_stride)) || (lda & 3) ||
+      (reinterpret_cast<uintptr_t>(A) & 15))
+    return fail(ACCT_ENOTSUP, "conv3x3 implicit gemm: shape not supported");
+  const int64_t n_img = batch > 1 ? c_stride : 0;
+  const int64_t N = (int64_t)(batch - 1) * n_img + HW;
+  if (N > INT32_MAX) return fail(ACCT_ENOTSUP, "conv3x3 implicit gemm: too many columns");
+  using G = Cfg2<192, 2, 32, false, false, true, 4, true>;
+  // a CTA's half tile must touch <= 2 images and its pixels +- one row must
+  // fit one slab segment
+  if ((batch > 1 && n_img < G::HALF) || G::HALF + 2 * width + 5 > G::SEG ||
+      (batch > 1 && (im_stride & 3)) || (ld_im & 3) || (reinterpret_cast<uintptr_t>(im) & 15))
+    return fail(ACCT_ENOTSUP, "conv3x3 implicit gemm: plane layout not supported");
+  ImB ib;
+  ib.act = im;
+  ib.act_ld = ld_im;
+  ib.act_img = batch > 1 ? im_stride : 0;
+  ib.img = n_img;
+  ib.cin = channels;
+  ib.H = height;
+  ib.W = width;
+  ib.col = col_from < batch ? col : nullptr;
+  ib.col_ld = ld_col;
+  ib.col_n0 = (int64_t)col_from * n_img;
+  CUtensorMap bmap;
+  if (!make_input_map(&bmap, ib, batch, G::SEG, G::SLAB_CH))
+    return fail(ACCT_ENOTSUP, "conv3x3 implicit gemm: input tensor map");
+  return launch_tc2<192, 2, 32, false, false, true, 4, true>(
+      M, (int)N, K, 1.0f, A, lda, nullptr, 0, beta, C, ldc, bias, act, as_stream(stream), &ib,
+      &bmap);
 }

@@ -354,11 +354,18 @@ int device_op(const acct_action_t &a, acct_array_t *arr, int gemm_mode, cudaStre
                                               D(2), LD(2), beta, D(3), LD(3), BS(3), bias,
                                               (int)I[6], nb, col_from, pp, ldp, pbs, pi, ldi, ibs,
                                               c_from, st);
-        if (M <= 64 || M % 128 == 0)
-          return acct_conv3x3_tc_f32(D(0), LD(0), BS(0), C, H, W, D(1), LD(1), BS(1), M, D(2),
-                                     LD(2), beta, D(3), LD(3), BS(3), bias, (int)I[6], nb,
-                                     col_from, pp, ldp, pbs, pi, ldi, ibs, c_from, st);
-        return (int)ACCT_ENOTSUP;
+        int rc = (int)ACCT_ENOTSUP;
+        if (M <= 64 || (M % 128 == 0 && M <= 256))
+          rc = acct_conv3x3_tc_f32(D(0), LD(0), BS(0), C, H, W, D(1), LD(1), BS(1), M, D(2),
+                                   LD(2), beta, D(3), LD(3), BS(3), bias, (int)I[6], nb, col_from,
+                                   pp, ldp, pbs, pi, ldi, ibs, c_from, st);
+        // wide, long-K layers (and the wide conv's misfits: 26-wide planes):
+        // the CTA-pair gemm with implicit im2col, no fused pool
+        if (rc == ACCT_ENOTSUP && !with_pool && M >= 256 && K > 768)
+          rc = acct_conv3x3_gemm_tc_f32(D(0), LD(0), BS(0), C, H, W, D(1), LD(1), BS(1), M, D(2),
+                                        LD(2), beta, D(3), LD(3), BS(3), bias, (int)I[6], nb,
+                                        col_from, nullptr, 0, 0, nullptr, 0, 0, 0, st);
+        return rc;
       };
       auto pool_after = [&]() {  // the maxpool the launch did not fuse
         if (!has_pool) return (int)ACCT_OK;

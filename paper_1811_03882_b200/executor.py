@@ -70,6 +70,13 @@ CONV_MAX_M = int(os.environ.get("ACCT_CONV_MAX_M", "64"))
 # as a 2-D plane, so _conv_partner's width % 4 rule keeps it unfused)
 CONV_WIDE_MAX_M = int(os.environ.get("ACCT_CONV_WIDE_MAX_M", "256"))
 CONV_WIDE_MAX_C = int(os.environ.get("ACCT_CONV_WIDE_MAX_C", "512"))
+# wide long-K 3x3 layers (yolov2-tiny 8, 10, 12, 13; the 38x38 / 19x19
+# layers of yolov2-608) as ONE launch of the CTA-pair gemm with implicit
+# im2col (acct_conv3x3_gemm_tc_f32, bit-identical) -- opt-in: measured 2x
+# slower than im2col + the TMA-fed gemm (yolov2-tiny L13 18.3 vs 9.0 us/img;
+# four split warps cannot gather the 3 x 32 x 96 operand values per k-block
+# at the MMA's pace)
+IMPLICIT_GEMM = os.environ.get("ACCT_IMPLICIT_GEMM", "0") == "1"
 
 
 def _pitch(cols: int) -> int:
@@ -679,7 +686,9 @@ class PatternExecutor:
             if len(fused) < 2:
                 continue
             conv = self._conv_partner(g, on, moved)
-            pool = self._pool_partner(g, after, on, blocked) if conv is not None else None
+            # the implicit-im2col pair gemm fuses no maxpool (it stays a launch)
+            pool = self._pool_partner(g, after, on, blocked) \
+                if conv is not None and not self._implicit_conv(conv) else None
             if fill is not None:
                 roles[fill] = ("absorbed_before",)
             if conv is not None:
@@ -741,6 +750,17 @@ class PatternExecutor:
             return False
         return not any(col in vs for lid, vs in moved.items() if lid != net.image_loop)
 
+    def _implicit_conv(self, im: int) -> bool:
+        """True when the fused conv of im2col op `im` runs on the CTA-pair
+        gemm with implicit im2col (the runtime's choice, acct_runtime.cu
+        ACCT_K_CONV): neither the narrow nor the wide conv kernel takes it."""
+        p = self.net.ops[im].params
+        M = self.net.ops[im + 1].params["M"]
+        narrow = p["c"] <= CONV_MAX_C and M <= CONV_MAX_M
+        wide = M % 128 == 0 and M <= CONV_WIDE_MAX_M and p["c"] <= CONV_WIDE_MAX_C \
+            and p["w"] % 4 == 0
+        return not (narrow or wide)
+
     def _conv_partner(self, g: int, on: list, moved: dict):
         """The im2col feeding gemm `g`, when the two can run as one fused
         conv launch (acct_conv3x3_im2col_gemm_f32): the im2col is offloaded
@@ -761,9 +781,12 @@ class PatternExecutor:
         M = op.params["M"]
         narrow = p["c"] <= CONV_MAX_C and M <= CONV_MAX_M
         wide = M % 128 == 0 and M <= CONV_WIDE_MAX_M and p["c"] <= CONV_WIDE_MAX_C
-        if not (narrow or wide):
+        # the CTA-pair gemm gathering its B operand from the input planes
+        # (acct_conv3x3_gemm_tc_f32): any plane width, M >= 256, K > 768
+        implicit = IMPLICIT_GEMM and M >= 256 and 9 * p["c"] > 768
+        if not (narrow or wide or implicit):
             return None
-        if p["w"] % 4:
+        if p["w"] % 4 and not implicit:
             return None
         # the launch runs after both entries and before both exits: a copyout
         # at the im2col's exit must not see C early, a copyin at the gemm's
@@ -1010,9 +1033,13 @@ class PatternExecutor:
             # the runtime's engine choice (acct_runtime.cu, ACCT_K_CONV)
             fp32 = self.gemm_mode == K.GEMM_SIMT or (self.gemm_mode == K.GEMM_AUTO and (
                 M <= 16 or (M <= 32 and c <= 4 and i[9] >= 0)))
-            return {"kind": "conv", "engine": "fp32-fma" if fp32 else "tcgen05",
+            implicit = not fp32 and M >= 256 and Kd > 768 and (M > 256 or w % 4 != 0)
+            engine = "fp32-fma" if fp32 else ("tcgen05 pair, implicit im2col" if implicit
+                                              else "tcgen05")
+            return {"kind": "conv", "engine": engine,
                     "layer": op.layer, "M": M, "N": N, "K": Kd, "images": nimg,
-                    "N_launch": N, "executions": execs, "flops": 2 * M * N * Kd * nimg,
+                    "N_launch": (nimg - 1) * _pitch(N) + N if implicit and nimg > 1 else N,
+                    "executions": execs, "flops": 2 * M * N * Kd * nimg,
                     "bytes": byts, "fused": True}
         target = slots[a.a[0]].name
         op = next(o for o in ops if o.kind == name and target in o.arrays.values())

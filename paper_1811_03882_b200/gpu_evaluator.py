@@ -16,7 +16,7 @@ Config file (all keys optional except `net`):
     {"net": "yolov2-tiny", "images": 16, "devices": [0, 1] | "all",
      "seed": 1, "warmup": 1, "repeats": 3, "fuse": true,
      "gemm": "auto" | "simt" | "tc", "timeout_seconds": 180,
-     "penalty_seconds": 1000}
+     "penalty_seconds": 1000, "workers_per_device": 1}
 
 `net` names a built-in program (the tuned source must then be its text:
 `python -m paper_1811_03882_b200.nets <net> <dir>`), or is "auto": any
@@ -65,6 +65,11 @@ class GpuEvaluatorConfig:
     gemm: str = "auto"
     timeout_seconds: float = 180.0
     penalty_seconds: float = 1000.0
+    # executors per listed device: the host loops of partially offloaded
+    # patterns dominate an evaluation, so several concurrent evaluations per
+    # GPU (one host thread each) use the host cores; their GPU work shares
+    # the device, so the measured seconds include that contention
+    workers_per_device: int = 1
 
     def __post_init__(self):
         if self.net is None:
@@ -76,6 +81,8 @@ class GpuEvaluatorConfig:
             raise ModelError(f"gpu evaluator: gemm must be one of {sorted(_GEMM_MODES)}")
         if self.repeats < 1 or self.warmup < 0:
             raise ModelError("gpu evaluator: repeats >= 1 and warmup >= 0 required")
+        if self.workers_per_device < 1:
+            raise ModelError("gpu evaluator: workers_per_device >= 1 required")
 
 
 def load_gpu_config(path) -> GpuEvaluatorConfig:
@@ -114,7 +121,7 @@ class DevicePool:
         from .executor import PatternExecutor
         self.cfg = cfg
         self.net = net if net is not None else build_net(cfg.net, images=cfg.images)
-        self.devices = resolve_devices(cfg.devices)
+        self.devices = resolve_devices(cfg.devices) * cfg.workers_per_device
         self.executors = [PatternExecutor(self.net, device=d, seed=cfg.seed, fuse=cfg.fuse,
                                           gemm_mode=_GEMM_MODES[cfg.gemm]) for d in self.devices]
         self.locks = [threading.Lock() for _ in self.devices]

@@ -82,6 +82,9 @@ SIGNATURES = {
     "acct_conv3x3_tc_f32": [_vp, _i64, _i64, _i32, _i32, _i32, _vp, _i64, _i64, _i32, _vp, _i64,
                             _f32, _vp, _i64, _i64, _vp, _i32, _i32, _i32, _vp, _i64, _i64, _vp,
                             _i64, _i64, _i32, _vp],
+    "acct_conv3x3_gemm_tc_f32": [_vp, _i64, _i64, _i32, _i32, _i32, _vp, _i64, _i64, _i32, _vp,
+                                 _i64, _f32, _vp, _i64, _i64, _vp, _i32, _i32, _i32, _vp, _i64,
+                                 _i64, _vp, _i64, _i64, _i32, _vp],
     "acct_add_bias_batched_f32": [_vp, _i64, _i64, _vp, _i32, _i64, _i32, _vp],
     "acct_leaky_exhaustive_check": [_vp, _vp],
     "acct_activate_batched_f32": [_vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp],
@@ -210,6 +213,15 @@ def conv3x3_tc(im, ld_im, im_stride, channels, height, width, col, ld_col, col_s
     pl = pool or (None, 0, 0, None, 0, 0, 0)
     call("acct_conv3x3_tc_f32", im, ld_im, im_stride, channels, height, width, col, ld_col,
          col_stride, M, A, lda, beta, Cp, ldc, c_stride, bias, act, batch, col_from, *pl, stream)
+
+
+def conv3x3_gemm_tc(im, ld_im, im_stride, channels, height, width, col, ld_col, col_stride, M, A,
+                    lda, beta, Cp, ldc, c_stride, bias=None, act=ACT_NONE, batch=1, stream=0,
+                    col_from=0):
+    """Implicit-im2col CTA-pair gemm for M >= 256, 9 * channels > 768 (no pool)."""
+    call("acct_conv3x3_gemm_tc_f32", im, ld_im, im_stride, channels, height, width, col, ld_col,
+         col_stride, M, A, lda, beta, Cp, ldc, c_stride, bias, act, batch, col_from,
+         None, 0, 0, None, 0, 0, 0, stream)
 
 
 def add_bias(out, ld, bias, rows, cols, stream=0):

@@ -89,9 +89,10 @@ def test_fused_and_unfused_schedules_agree_on_counts():
 def test_narrow_conv_layers_fuse_im2col_into_the_gemm_launch():
     """All-offload: the 3x3/1/1 layers with M <= 64 filters -- 0 (c=3, M=16),
     2 (c=16, M=32) and 4 (c=32, M=64) -- and the wide layer 6 (M = 128 on
-    52x52 planes; layer 8's 26-wide rows are not TMA-describable) each become
-    ONE conv action that writes col and out; counters are those of the
-    unfused schedule."""
+    52x52 planes) each become ONE conv action that writes col and out
+    (layers 8-13 too with the opt-in implicit-im2col pair gemm,
+    ACCT_IMPLICIT_GEMM=1); counters are those of the unfused schedule."""
+    from paper_1811_03882_b200 import executor as E
     net = build_net("yolov2-tiny")
     a = PatternExecutor(net, device=None, fuse=True)
     b = PatternExecutor(net, device=None, fuse=False)
@@ -107,7 +108,17 @@ def test_narrow_conv_layers_fuse_im2col_into_the_gemm_launch():
             (["pool3", "col4", "w4", "out4"],
              [32, 104, 104, 64, 0, K.ACT_LEAKY, names.index("bias4")]),
             (["pool5", "col6", "w6", "out6"],     # wide: streamed-weight tcgen05 conv
-             [64, 52, 52, 128, 0, K.ACT_LEAKY, names.index("bias6")])]
+             [64, 52, 52, 128, 0, K.ACT_LEAKY, names.index("bias6")]),
+            (["pool7", "col8", "w8", "out8"],     # implicit-im2col CTA-pair gemm
+             [128, 26, 26, 256, 0, K.ACT_LEAKY, names.index("bias8")]),
+            (["pool9", "col10", "w10", "out10"],
+             [256, 13, 13, 512, 0, K.ACT_LEAKY, names.index("bias10")]),
+            (["pool11", "col12", "w12", "out12"],
+             [512, 13, 13, 1024, 0, K.ACT_LEAKY, names.index("bias12")]),
+            (["out12", "col13", "w13", "out13"],
+             [1024, 13, 13, 512, 0, K.ACT_LEAKY, names.index("bias13")])]
+    if not E.IMPLICIT_GEMM:
+        want = want[:4]
     assert len(convs) == len(want)
     for k, (arrs, ints) in zip(convs, want):
         act = sa.actions[k]
@@ -160,8 +171,9 @@ def test_pool_fusion_and_dead_outputs():
     """Each fused conv launch of yolov2-tiny's first four conv layers absorbs the
     2x2/2 maxpool reading its output (slots i[9], i[10] = pool, idx); with
     one image per launch every output stays stored (i[11] = 0).  The other
-    maxpools (after plain gemm launches, and the 2x2/1 one) keep their own
-    launches, and the counters equal the unfused schedule's."""
+    maxpools (after the implicit-im2col pair gemm of layer 8, and the 2x2/1
+    one) keep their own launches, and the counters equal the unfused
+    schedule's."""
     net = build_net("yolov2-tiny")
     a = PatternExecutor(net, device=None, fuse=True)
     b = PatternExecutor(net, device=None, fuse=False)
@@ -171,8 +183,9 @@ def test_pool_fusion_and_dead_outputs():
     names = list(net.arrays)
     convs = [sa.actions[k] for k in range(sa.n_actions)
              if sa.actions[k].kind == K.A_KERNEL and sa.actions[k].i[0] == K.K_CONV]
-    assert [(names[c.i[9]], names[c.i[10]], c.i[11]) for c in convs] == \
+    assert [(names[c.i[9]], names[c.i[10]], c.i[11]) for c in convs if c.i[9] >= 0] == \
         [("pool1", "idx1", 0), ("pool3", "idx3", 0), ("pool5", "idx5", 0), ("pool7", "idx7", 0)]
+    assert [c.i[9] for c in convs[4:]] == [-1] * (len(convs) - 4)
     pools = [names[sa.actions[k].a[1]] for k in range(sa.n_actions)
              if sa.actions[k].kind == K.A_KERNEL and sa.actions[k].i[0] == K.K_MAXPOOL]
     assert pools == ["pool9", "pool11"]

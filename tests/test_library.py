@@ -47,7 +47,8 @@ def _rand(shape, seed):
     return np.random.default_rng(seed).uniform(-1, 1, shape).astype(np.float32)
 
 
-@pytest.mark.parametrize("M,N,K_", [(1, 1, 1), (5, 7, 3), (16, 169, 27), (33, 64, 40)])
+@pytest.mark.parametrize("M,N,K_", [(1, 1, 1), (5, 7, 3), (16, 169, 27), (33, 64, 40),
+                                   (37, 173, 65), (64, 512, 300)])
 def test_host_gemm_matches_oracle(orc, M, N, K_):
     A, B = _rand((M, K_), 1), _rand((K_, N), 2)
     C0 = _rand((M, N), 3)

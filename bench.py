@@ -480,6 +480,26 @@ def ga_reference(net_name: str, images: int | None, pop: int, gens: int, seed: i
             "best_seconds": res.best.seconds}
 
 
+def max_over_ranks(v: float, world: int, device=None) -> float:
+    """The largest of every rank's `v` (the job's time is its slowest rank's):
+    all_reduce MAX over the default process group (NCCL on the GPUs, gloo on
+    CPU tensors when `device` is None)."""
+    if world == 1:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def weak_scaling(world: int, images: int, steps: int, local_seconds: float, device=None):
+    """Weak scaling: every rank runs `images` images per step on its own GPU;
+    the value is every image of every rank over the slowest rank's time.
+    Returns (img/s, job seconds)."""
+    total = max_over_ranks(local_seconds, world, device)
+    return world * images * steps / total, total
+
+
 def make_flush(torch, device):
     return torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
 
@@ -513,13 +533,6 @@ def net_leg(args, net_name: str, images: int, batch, world: int, rank: int, loca
         if world > 1:
             torch.distributed.barrier()
 
-    def max_over_ranks(v: float) -> float:
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=ex.device)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        return float(t.item())
-
     for _ in range(warmup):
         ex.run(res)
         ex.run(full)
@@ -540,8 +553,7 @@ def net_leg(args, net_name: str, images: int, batch, world: int, rank: int, loca
         step_ms.append(e0.elapsed_time(e1))
         launches += r.counters["kernel_launches"]
     barrier()
-    total = max_over_ranks(sum(step_ms) * 1e-3)
-    value = world * images * steps / total
+    value, total = weak_scaling(world, images, steps, sum(step_ms) * 1e-3, ex.device)
 
     # ---- e2e: public path, host buffers, transfers inside the region ----
     barrier()
@@ -555,8 +567,7 @@ def net_leg(args, net_name: str, images: int, batch, world: int, rank: int, loca
         walls.append(r.seconds)
         counters = r.counters
     barrier()
-    e2e_total = max_over_ranks(sum(walls))
-    e2e_value = world * images * steps / e2e_total
+    e2e_value, e2e_total = weak_scaling(world, images, steps, sum(walls), ex.device)
     for key, val in full.expected.items():
         if counters[key] != val:
             raise SystemExit(f"transfer counter mismatch {key}: {counters[key]} != {val}")

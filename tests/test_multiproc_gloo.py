@@ -102,3 +102,39 @@ def test_ga_over_a_device_pool_is_deterministic():
                         r.evaluations_performed))
     assert results[0] == results[1]
     assert busy["max"] > 1
+
+
+def _bench_worker(rank, world, port, q):
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # rank r timed its steps at 1 + r seconds: the job took the slowest's
+        value, total = bench.weak_scaling(world, 16, 10, 1.0 + rank)
+        q.put((rank, value, total))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_weak_scaling_arithmetic_over_ranks():
+    """bench.py's value under torchrun: every rank's images over the MAX of the
+    ranks' timed seconds (all_reduce over the process group), identical on
+    every rank."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, value, total in got:
+        assert total == 2.0
+        assert value == world * 16 * 10 / 2.0

@@ -135,7 +135,7 @@ __device__ __forceinline__ float acct_leaky_fast(float v) {
 // and 2^120 (0x7B800000), the exact acct_leaky_guarded ranges (-0 and
 // negative NaNs take the exact path too, which handles them identically).
 template <int N>
-__device__ __forceinline__ void acct_leaky_block(float (&v)[N]) {
+__device__ __forceinline__ bool acct_leaky_any_guarded(const float (&v)[N]) {
   uint32_t mn = 0xFFFFFFFFu;
   int32_t mx = INT32_MIN;
 #pragma unroll
@@ -144,7 +144,11 @@ __device__ __forceinline__ void acct_leaky_block(float (&v)[N]) {
     mn = min(mn, a);
     mx = max(mx, (int32_t)a);
   }
-  const bool slow = mn < 0x0D800000u || mx > 0x7B800000;
+  return mn < 0x0D800000u || mx > 0x7B800000;
+}
+template <int N>
+__device__ __forceinline__ void acct_leaky_block(float (&v)[N]) {
+  const bool slow = acct_leaky_any_guarded(v);
   if (__any_sync(__activemask(), slow)) {
 #pragma unroll
     for (int i = 0; i < N; ++i) v[i] = acct_leaky(v[i]);

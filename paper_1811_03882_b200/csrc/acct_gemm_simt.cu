@@ -730,9 +730,57 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
           acc[ml][e] = v;
         }
       }
-      if (act == ACCT_ACT_LEAKY) acct_leaky_block(reinterpret_cast<float(&)[MT * 4]>(acc));
+      // Images whose C is dead (only the pool is observable): pool the raw
+      // values and apply leaky to the 16 winners.  leaky is monotone, so the
+      // pooled value is leaky(raw max) and darknet's first-max index equals
+      // the raw scan's -- unless an earlier element's leaky rounds to the
+      // same float (both <= 0 and within ~2^-22 relative) or a value is in
+      // leaky's guarded ranges; then (runner-up within 2^-19 of a
+      // non-positive max, a guarded winner, or an empty scan: one warp vote)
+      // the exact path below runs for the warp.
+      bool pooled = false;
+      if (act == ACCT_ACT_LEAKY && !wc) {
+        float mxv[MT];
+        int ev[MT];
+        bool slow = false;
 #pragma unroll
-      for (int ml = 0; ml < MT; ++ml) {
+        for (int ml = 0; ml < MT; ++ml) {
+          float mx = -FLT_MAX, v2 = -FLT_MAX;
+          int e = -1;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float v = acc[ml][i];
+            if (v > mx) {
+              v2 = mx;
+              mx = v;
+              e = i;
+            } else {
+              v2 = fmaxf(v2, v);
+            }
+          }
+          const float thr = mx <= 0.0f ? fmaf(mx, 0x1p-19f, mx) - 0x1p-100f : FLT_MAX;
+          slow |= e < 0 || (v2 < mx && v2 >= thr);
+          mxv[ml] = mx;
+          ev[ml] = e;
+        }
+        slow |= acct_leaky_any_guarded(mxv);
+        if (!__any_sync(__activemask(), slow)) {
+#pragma unroll
+          for (int ml = 0; ml < MT; ++ml) {
+            const int m = m_off + ml;
+            if (m >= M) break;
+            const int e = ev[ml];
+            pool[img * pool_bs + (int64_t)m * ld_pool + pofs] = acct_leaky_fast(mxv[ml]);
+            pidx[img * pidx_bs + (int64_t)m * ld_pidx + pofs] =
+                m * plane + base_i + (e & 1) + (e >> 1) * width;
+          }
+          pooled = true;
+        }
+      }
+      if (!pooled && act == ACCT_ACT_LEAKY)
+        acct_leaky_block(reinterpret_cast<float(&)[MT * 4]>(acc));
+#pragma unroll
+      for (int ml = 0; ml < MT && !pooled; ++ml) {
         const int m = m_off + ml;  // the filter (output row)
         if (m >= M) break;
         float *cp = cimg + (int64_t)m * ldc;

@@ -566,3 +566,73 @@ def test_conv3x3_window_fused_maxpool(cuda_device, c, h, w, M, beta, act, batch,
             assert torch.equal(colf[:, cs], colu[:, cs])
         else:
             assert torch.isnan(colf[:, cs]).all()
+
+
+def test_window_conv_pool_first_near_ties_and_guarded_values(cuda_device):
+    """The FP32 window conv pools the raw values of images whose C is dead and
+    applies leaky to the winners; darknet pools the LEAKY values.  They differ
+    only where an earlier window element's leaky rounds to the winner's (two
+    close negatives), or for leaky's guarded inputs (tiny / huge negatives,
+    -0) -- those windows must take the exact path.  A 1-channel conv whose
+    filters copy the centre tap (C = input + 0) puts such values straight into
+    the pooling windows; pool and idx must equal the unfused conv + maxpool."""
+    h, w, M, batch = 8, 8, 16, 2
+    N, Kd = h * w, 9
+    ld, P2 = 64, 16
+    ldp = 32
+    def leaky(x):
+        return np.float32(0.1 * np.float64(x))
+
+    v = np.float32(-0.95)                                 # find adjacent floats whose leaky ties
+    while leaky(v) != leaky(np.nextafter(v, np.float32(0))):
+        v = np.nextafter(v, np.float32(0))
+    nxt = np.nextafter(v, np.float32(0))                 # closer to 0: the raw max
+    cases = [
+        (v, nxt, v - 1, v - 2),                           # near tie, earlier element smaller
+        (np.float32(-1e-31), np.float32(0.0), -1, -2),    # tiny negative before a zero max
+        (np.float32(-3e37), np.float32(-3.2e37), np.float32(-3.3e37), np.float32(-3.1e37)),
+        (np.float32(-0.0), np.float32(-0.0), -1, -1),     # -0 ties
+        (np.float32(2.5), np.float32(2.5), 1, 0.5),       # equal positive maxima
+        (np.float32(-0.5), np.float32(-0.25), np.float32(-0.25), -1),
+    ]
+    img = np.random.default_rng(5).uniform(-1, 1, (h, w)).astype(np.float32)
+    for t, vals in enumerate(cases):                      # window t: 2x2 block (t // 4, t % 4)
+        r0, c0 = 2 * (t // 4), 2 * (t % 4)
+        img[r0, c0], img[r0, c0 + 1], img[r0 + 1, c0], img[r0 + 1, c0 + 1] = vals
+    im = torch.zeros((batch, 1, ld), device="cuda")
+    for b in range(batch):
+        im[b, 0, :N] = torch.from_numpy(img.ravel()).cuda()
+    A = torch.zeros((M, Kd), device="cuda")
+    A[:, 4] = 1.0                                         # centre tap: C = x
+    bias = torch.zeros(M, device="cuda")
+
+    def run(pool_fused):
+        C = torch.zeros((M, batch * ld), device="cuda")
+        col = torch.zeros((Kd, batch * ld), device="cuda")
+        pool = torch.full((M, batch * ldp), float("nan"), device="cuda")
+        idx = torch.full((M, batch * ldp), -7, dtype=torch.int32, device="cuda")
+        if pool_fused:
+            K.conv3x3_im2col_gemm(im.data_ptr(), ld, ld, 1, h, w, col.data_ptr(), batch * ld, ld,
+                                  M, A.data_ptr(), Kd, 0.0, C.data_ptr(), batch * ld, ld,
+                                  bias.data_ptr(), K.ACT_LEAKY, batch, stream(), col_from=1,
+                                  pool=(pool.data_ptr(), batch * ldp, ldp, idx.data_ptr(),
+                                        batch * ldp, ldp, 1))
+        else:
+            K.conv3x3_im2col_gemm(im.data_ptr(), ld, ld, 1, h, w, col.data_ptr(), batch * ld, ld,
+                                  M, A.data_ptr(), Kd, 0.0, C.data_ptr(), batch * ld, ld,
+                                  bias.data_ptr(), K.ACT_LEAKY, batch, stream())
+            K.call("acct_maxpool_batched_f32", C.data_ptr(), batch * ld, ld, M, h, w, 2, 2, 0,
+                   h // 2, w // 2, pool.data_ptr(), batch * ldp, ldp, idx.data_ptr(),
+                   batch * ldp, ldp, batch, stream())
+        torch.cuda.synchronize()
+        return pool, idx
+
+    pf, if_ = run(True)
+    pu, iu = run(False)
+    for b in range(batch):                                # image 0: C dead (pool-first path)
+        sl = slice(b * ldp, b * ldp + P2)
+        assert torch.equal(if_[:, sl], iu[:, sl]), b
+        assert torch.equal(pf[:, sl].view(torch.int32), pu[:, sl].view(torch.int32)), b
+    # the near tie really is one: darknet keeps the earlier (smaller) element
+    assert leaky(v) == leaky(nxt) and v < nxt
+    assert int(iu[0, 0]) == 0 and int(if_[0, 0]) == 0

@@ -709,12 +709,10 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   };
   // Stream-K (PK > 0): the space of (tile, chunk of PK k-blocks) is cut into
   // `pairs` equal contiguous ranges, one per CTA pair, so every pair does the
-  // same MMA work whatever tiles / pairs is (L12 of yolov2-tiny: 60 tiles on
-  // 74 pairs; yolov2-608 L23: 124).  A pair's range is a list of segments
-  // (tile, chunks [c0, c1)); a tile cut between pairs is finished by the pair
-  // holding its FIRST chunks -- that segment comes last in its range -- after
-  // the later segments' partial sums (computed first in their pairs' ranges)
-  // arrive through the workspace (one slot per CTA) and a per-CTA flag.
+  // same MMA work whatever tiles / pairs is (yolov2-608 L23: 124 tiles on 74
+  // pairs).  A pair's range is a list of segments (tile, chunks [c0, c1)); a
+  // tile cut between pairs is completed by whichever of its segments counts
+  // in last (workspace slots + a per-tile counter, see the epilogue).
   const int cpt = PK > 0 ? (total_kb + PK - 1) / PK : 1;
   const int64_t tot_ch = (int64_t)tiles * cpt;
   const int64_t sk_begin = tot_ch * pair / pairs, sk_end = tot_ch * (pair + 1) / pairs;
@@ -1113,36 +1111,50 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
       if (ACCT_SKIP(write_hi, 8)) return;
       constexpr int SLOT = 128 * TN;  // one CTA's partial tile in the workspace
-      if (sk && c0 > 0) {
-        // a later part of the tile: the partial sum to this CTA's slot, then
-        // its flag (release after every epilogue thread's stores)
-        float *slot = ws + (int64_t)blockIdx.x * SLOT + (int64_t)row * TN + grp * HC;
+      if (sk && (c0 > 0 || c1 < cpt)) {
+        // a tile cut between pairs: every segment leaves its partial sum in
+        // its slot (two per CTA: the tile its range starts in, the tile it
+        // ends in), then counts itself in with one acq_rel atomic per CTA;
+        // the segment that completes the count sums the tile's partials in
+        // pair order (deterministic whoever arrives last) and finishes it.
+        // Nothing ever waits for another CTA, so any number of launches may
+        // share the GPU.
+        const int t = w.split;
+        const int64_t tile_lo = (int64_t)t * cpt, tile_hi = tile_lo + cpt;
+        auto pair_of = [&](int64_t chunk) {  // the pair whose range holds chunk
+          int qp = (int)(chunk * pairs / tot_ch);
+          while (qp + 1 < pairs && tot_ch * (qp + 1) / pairs <= chunk) ++qp;
+          while (qp > 0 && tot_ch * qp / pairs > chunk) --qp;
+          return qp;
+        };
+        auto slot_of = [&](int qp) {  // 0: the tile the pair's range starts in
+          const int first_tile = (int)((tot_ch * qp / pairs) / cpt);
+          return 2 * (2 * qp + (int)rank) + (t == first_tile ? 0 : 1);
+        };
+        const int q_first = pair_of(tile_lo), q_last = pair_of(tile_hi - 1);
+        float *mine = ws + (int64_t)slot_of(pair) * SLOT + (int64_t)row * TN + grp * HC;
 #pragma unroll
         for (int i = 0; i < HC / 4; ++i)
-          __stcg(reinterpret_cast<float4 *>(slot) + i,
+          __stcg(reinterpret_cast<float4 *>(mine) + i,
                  make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]));
         __threadfence();
         asm volatile("bar.sync 3, 256;" ::: "memory");  // the eight epilogue warps
-        if (threadIdx.x == 6 * 32)
-          asm volatile("st.release.gpu.global.s32 [%0], 1;" ::"l"(sk_flags + blockIdx.x) : "memory");
-        return;
-      }
-      if (sk && c1 < cpt) {
-        // the tile's first chunks: add the later parts' partials, in pair order
-        const int64_t tile_end = (int64_t)(w.split + 1) * cpt;
+        volatile uint32_t *last_flag = tmem_slot + 1;
         if (threadIdx.x == 6 * 32) {
-          for (int qp = pair + 1; qp < pairs && tot_ch * qp / pairs < tile_end; ++qp) {
-            int *flag = sk_flags + 2 * qp + rank;
-            int v = 0;
-            do {
-              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-            } while (v == 0);
-            *flag = 0;  // consumed: zero for the next launch on this stream
-          }
+          int old;
+          asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                       : "=r"(old) : "l"(sk_flags + 2 * t + rank) : "memory");
+          const bool last = old == q_last - q_first;
+          if (last) sk_flags[2 * t + rank] = 0;  // zero for the next launch on this stream
+          *last_flag = last ? 1u : 0u;
         }
         asm volatile("bar.sync 3, 256;" ::: "memory");
-        for (int qp = pair + 1; qp < pairs && tot_ch * qp / pairs < tile_end; ++qp) {
-          const float *slot = ws + (int64_t)(2 * qp + rank) * SLOT + (int64_t)row * TN + grp * HC;
+        if (*last_flag == 0u) return;
+        __threadfence();
+#pragma unroll
+        for (int i = 0; i < HC; ++i) acc[i] = 0.0f;
+        for (int qp = q_first; qp <= q_last; ++qp) {
+          const float *slot = ws + (int64_t)slot_of(qp) * SLOT + (int64_t)row * TN + grp * HC;
 #pragma unroll
           for (int i = 0; i < HC / 4; ++i) {
             const float4 v = __ldcg(reinterpret_cast<const float4 *>(slot) + i);
@@ -2206,8 +2218,9 @@ int scratch_for(cudaStream_t s, size_t floats, float **out) {
   return ACCT_OK;
 }
 
-// stream-K flags: one int per CTA, zero between launches (each consumer
-// resets the flag it waited on), per (device, stream) like the workspace
+// stream-K tile counters: one int per (tile, CTA of the pair), zero between
+// launches (the segment completing a tile resets it), per (device, stream)
+// like the workspace
 std::unordered_map<uint64_t, std::pair<int *, size_t>> g_sk_flags;
 
 int sk_flags_for(cudaStream_t s, size_t n, int **out) {
@@ -2433,16 +2446,15 @@ int launch_tc2(int M, int N, int K, float alpha, const float *A, int64_t lda, co
   int pairs = units < pairs_avail ? units : pairs_avail;
   int *flags = nullptr;
   if (stream_k) {
-    // stream-K: every pair gets an equal share of the (tile, chunk) space, and
-    // a pair may wait for later pairs' partials -- so all pairs must be
-    // co-resident: the grid is capped at the clusters that fit at once
+    // stream-K: every pair gets an equal share of the (tile, chunk) space;
+    // the grid is the clusters that fit at once (one wave of pairs)
     const int cpt = (total_kb + PK - 1) / PK;
     const int64_t tot_ch = (int64_t)tiles * cpt;
     pairs = sk_pairs(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA, PK, IMB>, G::SMEM_BYTES);
     if (pairs < 1) return fail(ACCT_ENOTSUP, "gemm_tc2 stream-K: no co-resident CTA pairs");
     if (tot_ch < pairs) pairs = (int)tot_ch;
-    if (int rc = scratch_for(s, (size_t)2 * pairs * 128 * TN, &ws)) return rc;
-    if (int rc = sk_flags_for(s, 2 * pairs, &flags)) return rc;
+    if (int rc = scratch_for(s, (size_t)4 * pairs * 128 * TN, &ws)) return rc;
+    if (int rc = sk_flags_for(s, 2 * (size_t)tiles, &flags)) return rc;
   }
   launch(tc2_gemm_kernel<TN, NACC, BK, SWAP, DUAL, LOA, PK, IMB>, dim3(2 * pairs), dim3(THREADS),
          G::SMEM_BYTES, s, ta, tb, M, N, K, nt, mt, splits, kb_per, g_write_hi, alpha, beta, C, ldc,

@@ -636,3 +636,34 @@ def test_window_conv_pool_first_near_ties_and_guarded_values(cuda_device):
     # the near tie really is one: darknet keeps the earlier (smaller) element
     assert leaky(v) == leaky(nxt) and v < nxt
     assert int(iu[0, 0]) == 0 and int(if_[0, 0]) == 0
+
+
+def test_stream_k_gemms_on_concurrent_streams(cuda_device):
+    """Stream-K gemm launches (>= 74 CTA-pair tiles) on two streams at once:
+    a tile cut between pairs is completed by whichever segment counts in last
+    -- no CTA waits for another, so launches that cannot all be co-resident
+    still finish -- and each result is bit-identical to the same launch run
+    alone."""
+    import torch
+    M, N, Kd = 1024, 5821, 4608
+    ld = -(-N // 4) * 4
+    g = torch.Generator(device="cuda").manual_seed(11)
+    A = [torch.rand(M, Kd, device="cuda", generator=g) - 0.5 for _ in range(2)]
+    B = [torch.rand(Kd, ld, device="cuda", generator=g) - 0.5 for _ in range(2)]
+    alone = []
+    for i in range(2):
+        C = torch.zeros(M, ld, device="cuda")
+        K.gemm_nn(M, N, Kd, 1.0, A[i].data_ptr(), Kd, B[i].data_ptr(), ld, 0.0, C.data_ptr(), ld,
+                  None, K.ACT_NONE, K.GEMM_AUTO, stream())
+        alone.append(C)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    outs = [torch.zeros(M, ld, device="cuda") for _ in range(2)]
+    for _ in range(3):
+        for i in range(2):
+            K.gemm_nn(M, N, Kd, 1.0, A[i].data_ptr(), Kd, B[i].data_ptr(), ld, 0.0,
+                      outs[i].data_ptr(), ld, None, K.ACT_NONE, K.GEMM_AUTO,
+                      streams[i].cuda_stream)
+    torch.cuda.synchronize()
+    for i in range(2):
+        assert torch.equal(outs[i][:, :N], alone[i][:, :N])

@@ -1323,7 +1323,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 // image) behind an im2col that writes it.
 //
 // A work unit is one image's TH x TW block of output pixels (TW = 16 or 8,
-// TH = 128 / TW; MMA row m = pixel (m / TW, m % TW)).  Its input slab -- every
+// TH = 128 / TW; MMA row m = a pixel of its warp's 8 x 4 block, conv_pixel).  Its input slab -- every
 // channel's (TH + 2) x (TW + 2) window (stored TW + 8 wide from x0 - 4), one 4-D TMA box over (x, y, image,
 // channel) whose out-of-bounds elements are zero, i.e. the conv's padding --
 // makes every operand element one LDS at  lane base + immediate.
@@ -1340,6 +1340,18 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 //               (staged in shared memory), leaky -> C, fused 2x2 maxpool
 // Operand values, k order and MMA sequence equal im2col + the swap gemm, so
 // C is bit-identical to the unfused pair (tests/test_gpu_kernels.py).
+// MMA row m = 32 q + lane of a conv unit (TMEM lane quadrant q) <-> pixel:
+// each warp holds an 8-wide x 4-tall block, so (1) its 32 slab addresses per
+// tap, rows TWP = 24 floats apart, fall in 32 distinct banks (rows 0..3 at
+// banks +0, +24, +16, +8) -- a 16 x 2 block had two lanes per bank on 8 of
+// them -- and (2) it holds 4 x 2 whole 2x2 pooling windows
+template <int TW>
+__device__ __forceinline__ void conv_pixel(int q, int lane, int &py, int &px) {
+  constexpr int BX = TW / 8;  // warp blocks per unit row
+  px = 8 * (q % BX) + (lane & 7);
+  py = 4 * (q / BX) + (lane >> 3);
+}
+
 template <int TN, int TW>
 struct ConvCfg {
   static constexpr int BK = 32;
@@ -1355,7 +1367,7 @@ struct ConvCfg {
   static constexpr int TH = 128 / TW;
   // slab row: columns x0 - 4 .. x0 + TW + 3 (TMA needs a 16-byte aligned
   // start in the innermost dimension; a box starting at x0 - 1 faults)
-  static constexpr int TWP = TW + 8;
+  static constexpr int TWP = 24;  // >= TW + 6, and = 24 mod 32 (conv_pixel)
   static constexpr int SROWS = TH + 2;
   static constexpr int CS = SROWS * TWP * 4;      // slab bytes per channel
   static constexpr int W_TILE = TN * BK * 4;      // one weight k-block, K-major SW128
@@ -1549,8 +1561,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       // conv arrival releases an MMA that reads it
       asm volatile("bar.sync 1, 256;" ::: "memory");
     }
-    const int m = 32 * q + lane;
-    const int py = m / TW, px = m % TW;
+    int py, px;
+    conv_pixel<TW>(q, lane, py, px);
     const uint32_t lane_off = (uint32_t)((py * G::TWP + px) * 4);
     int g = 0, j = half;
     for (int u = blockIdx.x + half * gridDim.x; u < units; u += 2 * gridDim.x, j += 2) {
@@ -1624,8 +1636,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     const int grp = (warp - 10) >> 2;
     for (int i = threadIdx.x - 10 * 32; i < TN; i += 8 * 32) bias_s[i] = (bias && i < M) ? bias[i] : 0.0f;
     asm volatile("bar.sync 2, 256;" ::: "memory");  // the eight epilogue warps
-    const int m = 32 * q + lane;
-    const int py = m / TW, px = m % TW;
+    int py, px;
+    conv_pixel<TW>(q, lane, py, px);
     // explicit shared-space addresses (generic LD/ST through the realigned
     // base measured several times slower): bias, this warp's pooling scratch
     const uint32_t bias_sa = ptx::smem_u32(bias_s);
@@ -1682,11 +1694,13 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           // scratch each lane takes window (lane & 7) of filters 4t + (lane >>
           // 3), comparing in darknet's scan order with strict '>' from -FLT_MAX
           __syncwarp();
-          constexpr int TWH = TW / 2;
+          // window (lane & 7) of the warp's 8 x 4 block: top-left lane l0,
+          // neighbours l0 + 1, + 8, + 9
           const int w8 = lane & 7, fg = lane >> 3;
-          const int l0 = (w8 / TWH) * 2 * TW + 2 * (w8 % TWH);  // window's top-left lane
-          const int m0 = 32 * q + l0;
-          const int wy = y0 + m0 / TW, wx = x0 + m0 % TW;
+          const int l0 = 16 * (w8 >> 2) + 2 * (w8 & 3);
+          int wpy, wpx;
+          conv_pixel<TW>(q, l0, wpy, wpx);
+          const int wy = y0 + wpy, wx = x0 + wpx;
           const bool win = wy < height && wx < width && !(ACCT_SKIP(dbg, 4));
           const int64_t pofs = (int64_t)(wy >> 1) * (width >> 1) + (wx >> 1);
 #pragma unroll
@@ -1694,7 +1708,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
             const int fl = 4 * t + fg, f = rbase + 8 * half + fl;
             const uint32_t sv = scr_sa + 4 * (fl * 33 + l0);
             const float v00 = ptx::lds32(sv), v01 = ptx::lds32(sv + 4);
-            const float v10 = ptx::lds32(sv + 4 * TW), v11 = ptx::lds32(sv + 4 * (TW + 1));
+            const float v10 = ptx::lds32(sv + 4 * 8), v11 = ptx::lds32(sv + 4 * 9);
             if (win && f < M) {
               const int base_i = f * HW + wy * width + wx;
               float mx = -FLT_MAX;
@@ -1743,7 +1757,7 @@ template <int TW>
 struct WideCfg {
   static constexpr int TN = 128, BK = 32, S = 4, NACC = 2;  // NACC = 2: see the epilogue
   static constexpr int TH = 128 / TW;
-  static constexpr int TWP = TW + 8;
+  static constexpr int TWP = 24;  // >= TW + 6, and = 24 mod 32 (conv_pixel)
   static constexpr int SROWS = TH + 2;
   static constexpr int CS = SROWS * TWP * 4;      // slab bytes per channel
   static constexpr int CH_PER_KB = 5;             // channels a 32-deep k-block spans
@@ -1874,8 +1888,8 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     const int half = (warp - 2) >> 2;
     const int ht = threadIdx.x - 64 - 128 * half;  // 0..127 within the half
     const int K = 9 * channels;
-    const int m = 32 * q + lane;
-    const int py = m / TW, px = m % TW;
+    int py, px;
+    conv_pixel<TW>(q, lane, py, px);
     const uint32_t lane_off = (uint32_t)((py * G::TWP + px) * 4);
     int g = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -1945,8 +1959,8 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     // would interleave parities on one barrier -- measured wrong on yolov2-608)
     const int q = warp & 3;
     const int grp = (warp - 10) >> 2;
-    const int m = 32 * q + lane;
-    const int py = m / TW, px = m % TW;
+    int py, px;
+    conv_pixel<TW>(q, lane, py, px);
     const uint32_t scr_sa = ptx::smem_u32(bias_s + TN + (warp - 10) * 8 * 33);
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
@@ -1995,11 +2009,11 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
           for (int jj = 0; jj < 8; ++jj)
             ptx::sts32(scr_sa + 4 * (jj * 33 + lane), __uint_as_float(r[8 * hf + jj]));
           __syncwarp();
-          constexpr int TWH = TW / 2;
           const int w8 = lane & 7, fg = lane >> 3;
-          const int l0 = (w8 / TWH) * 2 * TW + 2 * (w8 % TWH);
-          const int mm0 = 32 * q + l0;
-          const int wy = y0 + mm0 / TW, wx = x0 + mm0 % TW;
+          const int l0 = 16 * (w8 >> 2) + 2 * (w8 & 3);
+          int wpy, wpx;
+          conv_pixel<TW>(q, l0, wpy, wpx);
+          const int wy = y0 + wpy, wx = x0 + wpx;
           const bool win = wy < height && wx < width && !(ACCT_SKIP(dbg, 4));
           const int64_t pofs = (int64_t)(wy >> 1) * (width >> 1) + (wx >> 1);
 #pragma unroll
@@ -2007,7 +2021,7 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
             const int fl = 4 * t + fg, f = rbase + 8 * hf + fl;
             const uint32_t sv = scr_sa + 4 * (fl * 33 + l0);
             const float v00 = ptx::lds32(sv), v01 = ptx::lds32(sv + 4);
-            const float v10 = ptx::lds32(sv + 4 * TW), v11 = ptx::lds32(sv + 4 * (TW + 1));
+            const float v10 = ptx::lds32(sv + 4 * 8), v11 = ptx::lds32(sv + 4 * 9);
             if (win && f < M) {
               const int base_i = f * HW + wy * width + wx;
               float mx = -FLT_MAX;

@@ -198,6 +198,7 @@ class PatternExecutor:
             raise DeviceError("PatternExecutor needs a CUDA device (sm_100a)")
         self.net = net
         self.fuse = fuse
+        self.fuse_convs_single = False   # conv launches for one-image loops too (tests)
         self.gemm_mode = gemm_mode
         # image batching of the image loop (see _batch_plan): True = as many
         # images per launch as divide the step and fit `batch_bytes` of
@@ -431,7 +432,7 @@ class PatternExecutor:
         # because every iteration overwrites y completely before reading it
         acts.append((K.A_BIND, (y_slot,), (0, p * self.output_bytes, 0), "out"))
 
-        plan_f = self._fusion_plan(plan, chosen) if self.fuse else {}
+        plan_f = self._fusion_plan(plan, chosen, p) if self.fuse else {}
         device_ops = host_ops = 0
         for n, op in enumerate(net.ops):
             role = plan_f.get(n)
@@ -494,7 +495,7 @@ class PatternExecutor:
         x_slot = self.slot_of[self.net.input_name]
         rows, cols = self.net.arrays[self.net.input_name].shape
         acts.append((K.A_BIND, (x_slot,), (0, p * rows * _pitch(cols) * 4, 1), "devin"))
-        plan_f = self._fusion_plan(plan, chosen) if self.fuse else {}
+        plan_f = self._fusion_plan(plan, chosen, p) if self.fuse else {}
         for n, op in enumerate(self.net.ops):
             role = plan_f.get(n)
             if role is None:
@@ -635,7 +636,7 @@ class PatternExecutor:
         flush()
         return out
 
-    def _fusion_plan(self, plan: TransferPlan, chosen: set) -> dict:
+    def _fusion_plan(self, plan: TransferPlan, chosen: set, nimg: int = 1) -> dict:
         """Per conv layer, fuse offloaded fill -> gemm -> add_bias -> activation
         of one output array into a single gemm launch.
 
@@ -685,7 +686,12 @@ class PatternExecutor:
             fused = ([fill] if fill is not None else []) + [g] + after
             if len(fused) < 2:
                 continue
-            conv = self._conv_partner(g, on, moved)
+            # conv launches (im2col joined to the gemm) only for batched
+            # loops: one image leaves their pipelines a handful of units per
+            # SM, and im2col + the gemm (split-K) measured faster -- the
+            # image-at-a-time yolov2-tiny step 3.48 -> 2.96 ms per 16 images
+            conv = self._conv_partner(g, on, moved) \
+                if nimg > 1 or self.fuse_convs_single else None
             # the implicit-im2col pair gemm fuses no maxpool (it stays a launch)
             pool = self._pool_partner(g, after, on, blocked) \
                 if conv is not None and not self._implicit_conv(conv) else None

@@ -86,6 +86,16 @@ def test_fused_and_unfused_schedules_agree_on_counts():
     assert sa.device_ops < sb.device_ops
 
 
+def test_single_image_loops_do_not_fuse_convs():
+    """One-image loops (no image batching) keep im2col and the gemm as
+    separate launches: the conv pipelines need many units per SM."""
+    net = build_net("yolov2-tiny")
+    ex = PatternExecutor(net, device=None, fuse=True)
+    s = ex.compile("1" * len(net.ops))
+    assert not any(s.actions[k].kind == K.A_KERNEL and s.actions[k].i[0] == K.K_CONV
+                   for k in range(s.n_actions))
+
+
 def test_narrow_conv_layers_fuse_im2col_into_the_gemm_launch():
     """All-offload: the 3x3/1/1 layers with M <= 64 filters -- 0 (c=3, M=16),
     2 (c=16, M=32) and 4 (c=32, M=64) -- and the wide layer 6 (M = 128 on
@@ -95,6 +105,7 @@ def test_narrow_conv_layers_fuse_im2col_into_the_gemm_launch():
     from paper_1811_03882_b200 import executor as E
     net = build_net("yolov2-tiny")
     a = PatternExecutor(net, device=None, fuse=True)
+    a.fuse_convs_single = True          # host-only executors compile one-image loops
     b = PatternExecutor(net, device=None, fuse=False)
     bits = "1" * len(net.ops)
     sa, sb = a.compile(bits), b.compile(bits)
@@ -176,6 +187,7 @@ def test_pool_fusion_and_dead_outputs():
     schedule's."""
     net = build_net("yolov2-tiny")
     a = PatternExecutor(net, device=None, fuse=True)
+    a.fuse_convs_single = True          # host-only executors compile one-image loops
     b = PatternExecutor(net, device=None, fuse=False)
     bits = "1" * len(net.ops)
     sa, sb = a.compile(bits), b.compile(bits)

@@ -59,7 +59,9 @@ inline cudaStream_t as_stream(acct_stream_t s) { return reinterpret_cast<cudaStr
 // with programmaticStreamSerializationAllowed (so inside a CUDA graph the
 // next kernel's CTAs may be scheduled, and run their prologue, while this one
 // drains) and calls pdl_wait() before touching any global data a previous
-// kernel produced or may still read.  The attribute is opt-in (ACCT_PDL=1).
+// kernel produced or may still read.  On by default (graph replay of the
+// 16-image step 0.746 -> 0.736 ms, image at a time ~3.0 -> 2.95 ms);
+// ACCT_PDL=0 turns it off.
 bool pdl_enabled();
 
 template <typename... KArgs, typename... Args>

@@ -42,10 +42,10 @@ int check_cuda(cudaError_t err, const char *what) {
 // exactly the calling thread's
 // measured slower inside the CUDA-graph replay on B200 (4.06 vs 3.91 ms per
 // 16-image step), so off unless ACCT_PDL=1
-bool pdl_enabled() {
+bool pdl_enabled() {  // default on; ACCT_PDL=0 turns it off (tools/ comparisons)
   static const bool on = [] {
     const char *v = getenv("ACCT_PDL");
-    return v && v[0] == '1';
+    return !(v && v[0] == '0');
   }();
   return on;
 }

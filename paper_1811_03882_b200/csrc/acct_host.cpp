@@ -70,6 +70,47 @@ extern "C" int acct_host_im2col_f32(const float *im, int64_t ld_im, int channels
 #endif
 
 namespace {
+#if defined(__x86_64__)
+// AVX-512 body (runtime-dispatched: the build targets x86-64-v3): 4 rows x 32
+// columns in 8 zmm accumulators over packed 32-column B panels -- the same
+// per-element mul-then-add sequence, twice the lanes of the AVX2 body
+__attribute__((target("avx512f"))) void gemm_avx512(int M4, int N32, int K, float alpha,
+                                                    const float *A, int64_t lda, const float *B,
+                                                    int64_t ldb, float *C, int64_t ldc) {
+  std::vector<float> panel((size_t)K * 32);
+  for (int j = 0; j < N32; j += 32) {
+    for (int k = 0; k < K; ++k)
+      memcpy(panel.data() + (size_t)k * 32, B + (int64_t)k * ldb + j, 32 * sizeof(float));
+    for (int i = 0; i < M4; i += 4) {
+      const float *a0 = A + (int64_t)i * lda;
+      __m512 c[4][2];
+      for (int r = 0; r < 4; ++r) {
+        c[r][0] = _mm512_loadu_ps(C + (int64_t)(i + r) * ldc + j);
+        c[r][1] = _mm512_loadu_ps(C + (int64_t)(i + r) * ldc + j + 16);
+      }
+      const float *b = panel.data();
+      for (int k = 0; k < K; ++k, b += 32) {
+        const __m512 b0 = _mm512_loadu_ps(b), b1 = _mm512_loadu_ps(b + 16);
+        for (int r = 0; r < 4; ++r) {
+          const __m512 a = _mm512_set1_ps(alpha * a0[(int64_t)r * lda + k]);
+          c[r][0] = _mm512_add_ps(c[r][0], _mm512_mul_ps(a, b0));
+          c[r][1] = _mm512_add_ps(c[r][1], _mm512_mul_ps(a, b1));
+        }
+      }
+      for (int r = 0; r < 4; ++r) {
+        _mm512_storeu_ps(C + (int64_t)(i + r) * ldc + j, c[r][0]);
+        _mm512_storeu_ps(C + (int64_t)(i + r) * ldc + j + 16, c[r][1]);
+      }
+    }
+  }
+}
+
+bool have_avx512() {
+  static const bool ok = __builtin_cpu_supports("avx512f");
+  return ok;
+}
+#endif
+
 void gemm_rows_scalar(int i0, int i1, int j0, int N, int K, float alpha, const float *A,
                       int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc) {
   for (int i = i0; i < i1; ++i) {
@@ -88,10 +129,17 @@ extern "C" int acct_host_gemm_nn_f32(int M, int N, int K, float alpha, const flo
   if (M < 0 || N < 0 || K < 0) return ACCT_EINVAL;
 #if defined(__AVX2__)
   const int M4 = M / 4 * 4, N16 = N / 16 * 16;
+  int j0 = 0;
+#if defined(__x86_64__)
+  if (have_avx512() && M4 > 0) {
+    j0 = N / 32 * 32;
+    gemm_avx512(M4, j0, K, alpha, A, lda, B, ldb, C, ldc);
+  }
+#endif
   // column panels of 16: the panel B[0..K)[j..j+16) packed contiguously
   // (64 B per k, L2-resident) and reused by every 4-row block of C
   std::vector<float> panel((size_t)K * 16);
-  for (int j = 0; j < N16; j += 16) {
+  for (int j = j0; j < N16; j += 16) {
     for (int k = 0; k < K; ++k)
       memcpy(panel.data() + (size_t)k * 16, B + (int64_t)k * ldb + j, 16 * sizeof(float));
     for (int i = 0; i < M4; i += 4) {

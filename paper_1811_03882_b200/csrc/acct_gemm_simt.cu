@@ -580,6 +580,10 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
   return d;
 }
 
+// BETA: beta != 0 (C += ...) -- a template flag, so the usual beta = 0 launch
+// carries no per-filter C address arithmetic or predicated C loads (ncu: 26%
+// of the kernel's stall samples when they were runtime-predicated)
+template <bool BETA>
 __global__ void __launch_bounds__(128, 4)
 conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, int channels,
                     int height, int width, float *__restrict__ col, int64_t ld_col,
@@ -588,7 +592,7 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
                     const float *__restrict__ bias, int act, float *__restrict__ pool,
                     int64_t ld_pool, int64_t pool_bs, int32_t *__restrict__ pidx,
                     int64_t ld_pidx, int64_t pidx_bs, int c_from, int tiles_x, int tpi,
-                    int ntiles) {
+                    int ntiles, float inv_tpi, float inv_tiles_x) {
   constexpr int MT = 16;
   const int m_off = blockIdx.y * MT;  // this CTA's 16-filter block
   extern __shared__ float4 conv_smem[];
@@ -599,12 +603,25 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
   pdl_trigger();
   pdl_wait();
 
+  // n / d for n, d < 2^24 by a float reciprocal and one correction step (the
+  // integer divisions were 10% of the kernel's stall samples)
+  auto divmod = [](int n, int d, float inv_d, int &q, int &r) {
+    q = (int)((float)n * inv_d);
+    r = n - q * d;
+    if (r < 0) {
+      --q;
+      r += d;
+    } else if (r >= d) {
+      ++q;
+      r -= d;
+    }
+  };
   auto tile_xy = [&](int tile, int &img, int &y0, int &x0) {
-    img = tile / tpi;
-    const int t = tile - img * tpi;
-    const int ty = t / tiles_x;
+    int t, ty, tx;
+    divmod(tile, tpi, inv_tpi, img, t);
+    divmod(t, tiles_x, inv_tiles_x, ty, tx);
     y0 = ty * PT_H;
-    x0 = (t - ty * tiles_x) * PT_W;
+    x0 = tx * PT_W;
   };
   auto stage = [&](int tile, float *buf) {
     int img, y0, x0;
@@ -714,9 +731,9 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
       for (int ml = 0; ml < MT; ++ml) {
         const int m = m_off + ml;
         if (m >= M) break;
-        float *cp = cimg + (int64_t)m * ldc;
         float cv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-        if (beta != 0.0f) {
+        if constexpr (BETA) {
+          const float *cp = cimg + (int64_t)m * ldc;
           const float2 c0 = *reinterpret_cast<const float2 *>(cp);
           const float2 c1 = *reinterpret_cast<const float2 *>(cp + width);
           cv[0] = c0.x; cv[1] = c0.y; cv[2] = c1.x; cv[3] = c1.y;
@@ -725,7 +742,7 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           float v = acc[ml][e];
-          if (beta != 0.0f) v = beta * cv[e] + v;
+          if constexpr (BETA) v = beta * cv[e] + v;
           if (bias) v += bv;
           acc[ml][e] = v;
         }
@@ -833,23 +850,23 @@ extern "C" int acct_conv3x3_im2col_gemm_f32(const float *im, int64_t ld_im, int6
     const size_t smem = sizeof(float) * ((size_t)channels * 9 * 16 +
                                          2 * (size_t)channels * PT_SH * PT_SW);
     if (smem > 200 * 1024) return fail(ACCT_ENOTSUP, "conv3x3 fused: slabs exceed shared memory");
+    auto kern = beta != 0.0f ? conv3x3_pool_kernel<true> : conv3x3_pool_kernel<false>;
     if (smem > 48 * 1024)
-      cudaFuncSetAttribute(conv3x3_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int tiles_x = (width + PT_W - 1) / PT_W, tiles_y = (height + PT_H - 1) / PT_H;
     const int64_t tpi = (int64_t)tiles_x * tiles_y, ntiles = tpi * batch;
-    if (ntiles > INT32_MAX) return fail(ACCT_ENOTSUP, "conv3x3 fused: too many tiles");
+    if (ntiles >= (1 << 24)) return fail(ACCT_ENOTSUP, "conv3x3 fused: too many tiles");
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv3x3_pool_kernel, 128, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem);
     if (per_sm < 1) per_sm = 1;
     const int gy = (M + 15) / 16;
     int64_t grid = ((int64_t)sm_count() * per_sm + gy - 1) / gy;
     if (grid > ntiles) grid = ntiles;
-    launch(conv3x3_pool_kernel, dim3((unsigned)grid, (unsigned)gy), dim3(128), smem,
+    launch(kern, dim3((unsigned)grid, (unsigned)gy), dim3(128), smem,
            as_stream(stream), im, ld_im,
            im_stride, channels, height, width, col, ld_col, col_stride, col_from, M, A, lda, beta, C,
            ldc, c_stride, bias, act, pool, ld_pool, pool_stride, idx, ld_idx, idx_stride, c_from,
-           tiles_x, (int)tpi, (int)ntiles);
+           tiles_x, (int)tpi, (int)ntiles, 1.0f / (float)tpi, 1.0f / (float)tiles_x);
     return note_launch("conv3x3 im2col+gemm+maxpool");
   }
   if (channels < 1 || channels > 64 || M < 1 || M > 32 || height < 1 || width < 1 || batch < 1 ||

@@ -579,6 +579,11 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
   return d;
 }
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 
 // BETA: beta != 0 (C += ...) -- a template flag, so the usual beta = 0 launch
 // carries no per-filter C address arithmetic or predicated C loads (ncu: 26%
@@ -598,7 +603,8 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
   extern __shared__ float4 conv_smem[];
   const int K = channels * 9;
   float *As = reinterpret_cast<float *>(conv_smem);  // [k][MT]
-  float *sin0 = As + K * MT;                         // 2 x [channels][PT_SH][PT_SW]
+  float *Bs = As + K * MT;                           // [MT] bias (0 past M)
+  float *sin0 = Bs + MT;                             // 2 x [channels][PT_SH][PT_SW]
   const int bufsz = channels * PT_SH * PT_SW;
   pdl_trigger();
   pdl_wait();
@@ -646,6 +652,8 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
     const int k = t / MT, m = t - k * MT;
     As[t] = m_off + m < M ? A[(int64_t)(m_off + m) * lda + k] : 0.0f;
   }
+  if (threadIdx.x < MT)
+    Bs[threadIdx.x] = bias && m_off + threadIdx.x < M ? bias[m_off + threadIdx.x] : 0.0f;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   int buf = 0;
   for (; tile < ntiles; tile += gridDim.x) {
@@ -698,6 +706,20 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
           }
         }
       }
+      if (!BETA && bias) {
+        // + bias on the packed pairs (FADD2: the same rounding as the scalar
+        // add; filters past M hold 0 + 0)
+        const ulonglong2 *Bs2 = reinterpret_cast<const ulonglong2 *>(Bs);
+#pragma unroll
+        for (int g = 0; g < MT / 4; ++g) {
+          const ulonglong2 b = Bs2[g];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            acc2[2 * g][e] = add2(acc2[2 * g][e], b.x);
+            acc2[2 * g + 1][e] = add2(acc2[2 * g + 1][e], b.y);
+          }
+        }
+      }
       float acc[MT][4];
 #pragma unroll
       for (int i = 0; i < MT / 2; ++i)
@@ -725,26 +747,22 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
       const int64_t pofs = (int64_t)(y >> 1) * (width >> 1) + (x >> 1);
       const int base_i = (int)p;
       const int plane = height * width;
-      // beta C and bias per filter, then leaky over all 16 x 4 values with
-      // one warp vote for the guarded inputs (acct_leaky_block)
+      if constexpr (BETA) {
+        // beta C, then bias, per filter
 #pragma unroll
-      for (int ml = 0; ml < MT; ++ml) {
-        const int m = m_off + ml;
-        if (m >= M) break;
-        float cv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-        if constexpr (BETA) {
+        for (int ml = 0; ml < MT; ++ml) {
+          const int m = m_off + ml;
+          if (m >= M) break;
           const float *cp = cimg + (int64_t)m * ldc;
           const float2 c0 = *reinterpret_cast<const float2 *>(cp);
           const float2 c1 = *reinterpret_cast<const float2 *>(cp + width);
-          cv[0] = c0.x; cv[1] = c0.y; cv[2] = c1.x; cv[3] = c1.y;
-        }
-        const float bv = bias ? __ldg(bias + m) : 0.0f;  // once per filter
+          const float cv[4] = {c0.x, c0.y, c1.x, c1.y};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float v = acc[ml][e];
-          if constexpr (BETA) v = beta * cv[e] + v;
-          if (bias) v += bv;
-          acc[ml][e] = v;
+          for (int e = 0; e < 4; ++e) {
+            float v = beta * cv[e] + acc[ml][e];
+            if (bias) v += Bs[ml];
+            acc[ml][e] = v;
+          }
         }
       }
       // Images whose C is dead (only the pool is observable): pool the raw
@@ -762,10 +780,12 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
         bool slow = false;
 #pragma unroll
         for (int ml = 0; ml < MT; ++ml) {
-          float mx = -FLT_MAX, v2 = -FLT_MAX;
-          int e = -1;
+          // the scan from -FLT_MAX takes element 0 first unless it is not
+          // above -FLT_MAX (then: exact path)
+          float mx = acc[ml][0], v2 = -FLT_MAX;
+          int e = 0;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
+          for (int i = 1; i < 4; ++i) {
             const float v = acc[ml][i];
             if (v > mx) {
               v2 = mx;
@@ -776,7 +796,7 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
             }
           }
           const float thr = mx <= 0.0f ? fmaf(mx, 0x1p-19f, mx) - 0x1p-100f : FLT_MAX;
-          slow |= e < 0 || (v2 < mx && v2 >= thr);
+          slow |= !(acc[ml][0] > -FLT_MAX) || (v2 < mx && v2 >= thr);
           mxv[ml] = mx;
           ev[ml] = e;
         }
@@ -847,7 +867,7 @@ extern "C" int acct_conv3x3_im2col_gemm_f32(const float *im, int64_t ld_im, int6
          reinterpret_cast<uintptr_t>(C)) & 15 ||
         (ld_im | im_stride | ld_col | col_stride | ldc | c_stride) & 3)
       return fail(ACCT_ENOTSUP, "conv3x3 fused: maxpool fusion needs M <= 64, even planes");
-    const size_t smem = sizeof(float) * ((size_t)channels * 9 * 16 +
+    const size_t smem = sizeof(float) * ((size_t)channels * 9 * 16 + 16 +
                                          2 * (size_t)channels * PT_SH * PT_SW);
     if (smem > 200 * 1024) return fail(ACCT_ENOTSUP, "conv3x3 fused: slabs exceed shared memory");
     auto kern = beta != 0.0f ? conv3x3_pool_kernel<true> : conv3x3_pool_kernel<false>;

@@ -678,14 +678,24 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc2[i][e] = 0ull;
       const ulonglong2 *As2 = reinterpret_cast<const ulonglong2 *>(As);
+      // the next channel's window is loaded while this one's FMAs issue
+      float nwin[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) nwin[r][c] = base[r * PT_SW + c];
 #pragma unroll 1
       for (int ci = 0; ci < channels; ++ci) {
-        const float *cb = base + ci * PT_SH * PT_SW;
         float win[4][4];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) win[r][c] = cb[r * PT_SW + c];
+          for (int c = 0; c < 4; ++c) win[r][c] = nwin[r][c];
+        const float *cn = base + (ci + 1 < channels ? ci + 1 : ci) * PT_SH * PT_SW;
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) nwin[r][c] = cn[r * PT_SW + c];
 #pragma unroll
         for (int kh = 0; kh < 3; ++kh) {
 #pragma unroll

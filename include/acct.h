@@ -350,6 +350,10 @@ int acct_tc_trace(long long *out);
  * normal-orientation shape (the tile acct_conv3x3_gemm_tc_f32 uses);
  * tests and tools only                                                     */
 void acct_tc_set_tile(int tile);
+/* 1: narrow 3x3 convs with M <= 32 and channels % 8 == 0 on the row-band
+ * tcgen05 kernel (shifted shared-memory operands, no im2col build) instead of
+ * the im2col-operand kernel (default 0) -- tests and A/B measurements only  */
+void acct_tc_set_conv_rows(int on);
 /* CTA pairs of the stream-K gemm that fit on the current device at once */
 int acct_tc_stream_k_pairs(void);
 

@@ -2048,6 +2048,371 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
   if (warp == 1) ptx::tmem_dealloc(tmem, 512);
 }
 
+// ------------------------------------------------ row-band conv (narrow layers)
+// 3x3 / stride 1 / pad 1 convolution of M <= 64 filters as shifted MMAs: no
+// im2col operand is built at all.  A work unit is one image's output row
+// PAIR (2P, 2P + 1) over a column strip x0 .. x0 + wdt - 1 (wdt <= 128): MMA
+// row i = output column x0 + i, N = filters.  The input rows 2P - 1 .. 2P + 2
+// of 8 channels at a time are staged in shared memory channel-quad-major,
+// position-major -- [row][quad][position][4 channels], one 16-B row per
+// position, the no-swizzle K-major canonical layout -- so the operand of tap
+// (kh, kw) for output row 2P + a is the SAME bytes read through a descriptor
+// whose start is (a + kh) rows and kw positions further (tools/nosw_probe.cu
+// checks the layout and the 16-B shifts).  Each input value is staged (and
+// split) once per 8-channel step instead of once per tap.
+// 3xTF32 in two MMAs per (tap, 8 channels): A hi x [W hi | W lo] (N = 2 TN)
+// and A lo x W hi (N = TN) into the first half; the epilogue adds the halves.
+// tcgen05 reads both shared-memory operands at ~128 B/clk (tools/nosw_probe:
+// a 128 x 32 x 8 ss MMA costs 40 cycles per SM whatever the issuers), so two
+// MMAs instead of three: 88 rather than 120 cycles per step at TN = 32.
+//   warps 0-7  stage (LDG, hi/lo split, STS) through a ring of nstage steps:
+//              two groups of four taking alternate steps, all of a step's
+//              loads in flight at once (one group alone was latency-bound)
+//   warps 8, 9 MMA issuers: warp 8 + a fills output row 2P + a; with the
+//              epilogue warps they split the weights into shared memory
+//              while the first steps are staged
+//   warps 10-17 epilogue, two groups of four taking alternate units (one
+//              warp per TMEM lane quadrant was latency-bound): tcgen05.ld
+//              (lane = column), + bias, leaky -> C, and the fused 2x2 maxpool
+//              (vertical in-thread, horizontal by one lane exchange; two
+//              filters per store)
+// Not bit-identical to im2col + the gemm (another summation order); within
+// the gemm tolerance of the oracle (tests/test_gpu_kernels.py).
+template <int TN>
+struct RowsCfg {
+  static constexpr int UCOLS = 4 * TN;             // a unit: 2 rows x [main | lo] x TN
+  static constexpr int NACC = 512 / UCOLS;         // units in flight (TMEM)
+  static constexpr int MAXS = 8;                   // staging ring depth
+};
+constexpr int ROWS_THREADS = 32 * 18;
+constexpr int ROWS_ITEMS = (8 * 130 + 127) / 128;  // staged positions per thread and step
+
+// The weights' shared-memory image, once per launch: [tap][8-channel step]
+// [quad][2 TN rows][4 channels] with W hi in rows 0..TN-1 and W lo in rows
+// TN..2TN-1 (zero rows past M); every CTA of the conv bulk-copies it.
+template <int TN>
+__global__ void __launch_bounds__(256)
+rows_weights_kernel(const float *__restrict__ A, int64_t lda, int M, int channels,
+                    float4 *__restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  const int nq = channels / 4, items = 9 * nq * TN;
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= items) return;
+  const int n = i % TN, r = i / TN;  // r = tap * nq + cq
+  const int tap = r / nq, cq = r - tap * nq;
+  float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  if (n < M) {
+    const float *p = A + (int64_t)n * lda + 36 * cq + tap;
+    v = make_float4(p[0], p[9], p[18], p[27]);
+  }
+  float4 h;
+  const float4 l = split_lo(v, h);
+  const int row0 = ((tap * (nq / 2) + (cq >> 1)) * 2 + (cq & 1)) * 2 * TN;
+  out[row0 + n] = h;
+  out[row0 + TN + n] = l;
+}
+
+template <int TN>
+__global__ void __launch_bounds__(ROWS_THREADS, 1)
+tc_conv_rows_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, int channels,
+                    int height, int width, const float4 *__restrict__ wimg, int M,
+                    float *__restrict__ col, int64_t ld_col, int64_t col_bs, int col_from,
+                    int nstrips, int swd, int sp, int pairs, int units, int nstage, float beta,
+                    float *__restrict__ C, int64_t ldc, int64_t c_bs,
+                    const float *__restrict__ bias, int act, float *__restrict__ pool,
+                    int64_t ld_pool, int64_t pool_bs, int32_t *__restrict__ pidx,
+                    int64_t ld_pidx, int64_t pidx_bs, int c_from, int dbg) {
+  using G = RowsCfg<TN>;
+  constexpr int NACC = G::NACC;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  const int stage_bytes = 256 * sp;                 // hi then lo: 4 rows x 2 quads x sp x 16 B
+  uint8_t *stages = base;
+  uint8_t *wts = base + nstage * stage_bytes;       // [tap][step][quad][2 TN][4]
+  const int nsteps = channels / 8;
+  const int w_bytes = 9 * nsteps * 2 * 2 * TN * 16;
+  float *bias_s = reinterpret_cast<float *>(wts + w_bytes);
+  uint64_t *slab_full = reinterpret_cast<uint64_t *>(bias_s + TN);
+  uint64_t *slab_empty = slab_full + G::MAXS;
+  uint64_t *acc_full = slab_empty + G::MAXS;
+  uint64_t *acc_empty = acc_full + NACC;
+  uint64_t *wfull = acc_empty + NACC;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wfull + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(wfull, 1);
+    for (int s = 0; s < nstage; ++s) {
+      ptx::mbar_init(&slab_full[s], 4);   // the four staging warps
+      ptx::mbar_init(&slab_empty[s], 2);  // both issuers' commits
+    }
+    for (int a = 0; a < NACC; ++a) {
+      ptx::mbar_init(&acc_full[a], 2);
+      ptx::mbar_init(&acc_empty[a], 4);   // the four epilogue warps
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 8) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 32 * 8) {
+    // the weights, already in their shared-memory image (rows_weights_kernel),
+    // by bulk copies of <= 64 KB
+    ptx::mbar_expect_tx(wfull, (uint32_t)w_bytes);
+    for (int o = 0; o < w_bytes; o += 65536)
+      ptx::bulk_load(wts + o, reinterpret_cast<const uint8_t *>(wimg) + o,
+                     (uint32_t)min(65536, w_bytes - o), wfull);
+  }
+  if (warp >= 10) {
+    for (int i = threadIdx.x - 320; i < TN; i += 256) bias_s[i] = (bias && i < M) ? bias[i] : 0.0f;
+    asm volatile("bar.sync 1, 256;" ::: "memory");  // the epilogue warps: bias written
+  }
+  const int per_img = nstrips * pairs;
+  auto unit_of = [&](int u, int &img, int &x0, int &wdt, int &y0) {
+    img = u / per_img;
+    const int r = u - img * per_img;
+    const int strip = r / pairs;
+    y0 = 2 * (r - strip * pairs);
+    x0 = strip * swd;
+    wdt = min(swd, width - x0);
+  };
+
+  if (warp < 8) {
+    // ---------------- staging: 4 input rows x 8 channels per step ----------------
+    const int grp = warp >> 2, t = threadIdx.x & 127;
+    int s = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int img, x0, wdt, y0;
+      unit_of(u, img, x0, wdt, y0);
+      const float *src = im + img * im_bs;
+      for (int g = 0; g < nsteps; ++g, ++s) {
+        if ((s & 1) != grp) continue;
+        const int st = s % nstage;
+        if (s >= nstage) ptx::mbar_wait(&slab_empty[st], ((s / nstage) - 1) & 1);
+        if (ACCT_SKIP(dbg, 8)) {  // profiling: no staging at all
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&slab_full[st]);
+          continue;
+        }
+        const uint32_t hb = ptx::smem_u32(stages + st * stage_bytes);
+        const uint32_t lb = hb + 128 * sp;
+        const float *cs = src + (int64_t)(8 * g) * ld_im;
+        // every load of the step in flight before the first use (a loop of
+        // load -> split -> store per item was latency-bound: ~8k cycles/step)
+        float4 v[ROWS_ITEMS];
+#pragma unroll
+        for (int it = 0; it < ROWS_ITEMS; ++it) {
+          const int i = t + 128 * it;
+          const int rq = i / sp, pos = i - rq * sp;  // rq = row * 2 + quad
+          const int y = y0 - 1 + (rq >> 1), x = x0 - 1 + pos;
+          v[it] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          if (i < 8 * sp && y >= 0 && y < height && x >= 0 && x < width && pos <= wdt + 1 &&
+              !ACCT_SKIP(dbg, 1)) {
+            const float *p = cs + (int64_t)(4 * (rq & 1)) * ld_im + (int64_t)y * width + x;
+            v[it].x = __ldg(p);
+            v[it].y = __ldg(p + ld_im);
+            v[it].z = __ldg(p + 2 * ld_im);
+            v[it].w = __ldg(p + 3 * ld_im);
+          }
+        }
+#pragma unroll
+        for (int it = 0; it < ROWS_ITEMS; ++it) {
+          const int i = t + 128 * it;
+          if (i < 8 * sp) {
+            float4 h;
+            const float4 l = split_lo(v[it], h);
+            ptx::sts128(hb + 16 * i, h);
+            ptx::sts128(lb + 16 * i, l);
+          }
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&slab_full[st]);
+        if (col && img >= col_from) {
+          // col of an observable image from the same registers: input (y, x)
+          // of channel c is col row 9 c + 3 kh + kw at output (y + 1 - kh,
+          // x + 1 - kw) for the unit's two rows and strip (each col element
+          // once; zero padding included)
+          float *cb = col + img * col_bs;
+#pragma unroll
+          for (int it = 0; it < ROWS_ITEMS; ++it) {
+            const int i = t + 128 * it;
+            if (i >= 8 * sp) continue;
+            const int rq = i / sp, pos = i - rq * sp;
+            const int yi = y0 - 1 + (rq >> 1), xi = x0 - 1 + pos;
+            const int c0 = 8 * g + 4 * (rq & 1);
+            const float vv[4] = {v[it].x, v[it].y, v[it].z, v[it].w};
+#pragma unroll
+            for (int kh = 0; kh < 3; ++kh) {
+              const int yo = yi + 1 - kh;
+              if (yo < y0 || yo > y0 + 1 || yo >= height) continue;
+#pragma unroll
+              for (int kw = 0; kw < 3; ++kw) {
+                const int xo = xi + 1 - kw;
+                if (xo < x0 || xo >= x0 + wdt) continue;
+                float *cp = cb + (int64_t)(9 * c0 + 3 * kh + kw) * ld_col + (int64_t)yo * width + xo;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) __stcs(cp + (int64_t)(9 * e) * ld_col, vv[e]);
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp < 10) {
+    // ---------------- MMA issuers: warp 8 + a -> output row 2P + a ----------------
+    const int a = warp - 8;
+    constexpr uint32_t idesc_w = ptx::idesc_tf32(128, 2 * TN, false, false);
+    constexpr uint32_t idesc_h = ptx::idesc_tf32(128, TN, false, false);
+    const uint32_t st0 = ptx::smem_u32(stages), w0 = ptx::smem_u32(wts);
+    ptx::mbar_wait(wfull, 0);
+    int s = 0, j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int slot = j % NACC;
+      if (j >= NACC) ptx::mbar_wait(&acc_empty[slot], ((j / NACC) - 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t d = tmem + slot * G::UCOLS + a * 2 * TN;
+      for (int g = 0; g < nsteps; ++g, ++s) {
+        const int st = s % nstage;
+        ptx::mbar_wait(&slab_full[st], (s / nstage) & 1);
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+          const uint32_t hb = st0 + st * stage_bytes;
+#pragma unroll
+          for (int tap = 0; tap < 9 && !ACCT_SKIP(dbg, 2); ++tap) {
+            const int kh = tap / 3, kw = tap % 3;
+            const uint32_t ao = (uint32_t)((a + kh) * 2 * sp + kw) * 16;
+            const uint64_t ah = ptx::smem_desc(hb + ao, sp * 16, 128, 0);
+            const uint64_t al = ptx::smem_desc(hb + 128 * sp + ao, sp * 16, 128, 0);
+            const uint64_t bw = ptx::smem_desc(w0 + (uint32_t)((tap * nsteps + g) * 2) * 2 * TN * 16,
+                                               2 * TN * 16, 128, 0);
+            ptx::mma_tf32(d, ah, bw, idesc_w, (g | tap) != 0);
+            ptx::mma_tf32(d, al, bw, idesc_h, 1);
+          }
+          ptx::mma_commit(&slab_empty[st]);
+        }
+        __syncwarp();
+      }
+      if (ptx::elect_one()) ptx::mma_commit(&acc_full[slot]);
+      __syncwarp();
+    }
+  } else {
+    // ---------------- epilogue: lane = output column, TMEM columns = filters ----------------
+    const int q = warp & 3, eg = (warp - 10) >> 2;
+    const int HW = height * width;
+    const unsigned full = 0xffffffffu;
+    const bool odd = lane & 1;
+    int j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      if ((j & 1) != eg) continue;
+      int img, x0, wdt, y0;
+      unit_of(u, img, x0, wdt, y0);
+      const int slot = j % NACC;
+      ptx::mbar_wait_sleepy(&acc_full[slot], (j / NACC) & 1);
+      ptx::tc_fence_after();
+      const int xl = 32 * q + lane, x = x0 + xl;
+      const bool live = xl < wdt;
+      const bool row1 = y0 + 1 < height;
+      const bool cst = live && img >= c_from;
+      const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + slot * G::UCOLS;
+      float *cp = C + img * c_bs + (int64_t)y0 * width + x;
+      if (ACCT_SKIP(dbg, 4)) {  // profiling: no epilogue work
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&acc_empty[slot]);
+        continue;
+      }
+      const int xe = x & ~1;  // this lane's pooling window (even column)
+      const bool wlive = (xl & ~1) < wdt;
+      const int64_t pofs = (int64_t)(y0 >> 1) * (width >> 1) + (xe >> 1);
+#pragma unroll 1
+      for (int cc = 0; cc < TN / 16; ++cc) {
+        uint32_t m0[16], l0[16], m1[16], l1[16];
+        ptx::tmem_ld_32x32b_x16_nw(trow + 16 * cc, m0);
+        ptx::tmem_ld_32x32b_x16_nw(trow + TN + 16 * cc, l0);
+        ptx::tmem_ld_32x32b_x16_nw(trow + 2 * TN + 16 * cc, m1);
+        ptx::tmem_ld_32x32b_x16_nw(trow + 3 * TN + 16 * cc, l1);
+        ptx::tmem_ld_wait();
+        const int f0 = 16 * cc;
+        if (f0 >= M) continue;
+        float v0[16], v1[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          v0[i] = __uint_as_float(m0[i]) + __uint_as_float(l0[i]);
+          v1[i] = __uint_as_float(m1[i]) + __uint_as_float(l1[i]);
+        }
+        if (beta != 0.0f && live) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (f0 + i < M) {
+              v0[i] = beta * cp[(int64_t)(f0 + i) * ldc] + v0[i];
+              if (row1) v1[i] = beta * cp[(int64_t)(f0 + i) * ldc + width] + v1[i];
+            }
+          }
+        }
+        if (bias) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float b = bias_s[f0 + i];
+            v0[i] += b;
+            v1[i] += b;
+          }
+        }
+        if (act == ACCT_ACT_LEAKY) {
+          acct_leaky_block(v0);
+          acct_leaky_block(v1);
+        }
+        if (cst) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (f0 + i < M) {
+              cp[(int64_t)(f0 + i) * ldc] = v0[i];
+              if (row1) cp[(int64_t)(f0 + i) * ldc + width] = v1[i];
+            }
+          }
+        }
+        if (pool) {
+          // window of filter f0 + i + odd at (y0, xe): even lanes own column
+          // xe, odd lanes xe + 1; one exchange gives each lane its partner's
+          // pair of the filter it pools
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const float r0 = __shfl_xor_sync(full, odd ? v0[i] : v0[i + 1], 1);
+            const float r1 = __shfl_xor_sync(full, odd ? v1[i] : v1[i + 1], 1);
+            const float p00 = odd ? r0 : v0[i], p01 = odd ? v0[i + 1] : r0;
+            const float p10 = odd ? r1 : v1[i], p11 = odd ? v1[i + 1] : r1;
+            const int f = f0 + i + (odd ? 1 : 0);
+            if (wlive && f < M) {
+              const int bi = f * HW + y0 * width + xe;
+              float mx = -FLT_MAX;
+              int32_t k = -1;
+              if (p00 > mx) { mx = p00; k = bi; }
+              if (p01 > mx) { mx = p01; k = bi + 1; }
+              if (p10 > mx) { mx = p10; k = bi + width; }
+              if (p11 > mx) { mx = p11; k = bi + width + 1; }
+              pool[img * pool_bs + (int64_t)f * ld_pool + pofs] = mx;
+              pidx[img * pidx_bs + (int64_t)f * ld_pidx + pofs] = k;
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&acc_empty[slot]);
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 8) ptx::tmem_dealloc(tmem, 512);
+}
+
 // Sum the split-K partials of every output element in split order and apply
 // the epilogue (grid-wide, one thread per 4 consecutive columns).
 __global__ void __launch_bounds__(256)
@@ -2254,6 +2619,28 @@ int sk_flags_for(cudaStream_t s, size_t n, int **out) {
     f.second = n;
   }
   *out = f.first;
+  return ACCT_OK;
+}
+
+// the row-band conv's weight image, per (device, stream), grow-only and
+// retired like the workspace (a captured graph keeps its pointer)
+std::unordered_map<uint64_t, std::pair<float *, size_t>> g_conv_w;
+
+int conv_weights_for(cudaStream_t s, size_t floats, float **out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  uint64_t key = (reinterpret_cast<uint64_t>(s) << 8) ^ (uint64_t)dev;
+  std::lock_guard<std::mutex> lock(g_scratch_mu);
+  auto &w = g_conv_w[key];
+  if (w.second < floats) {
+    if (w.first) g_scratch_retired.push_back(w.first);
+    w.first = nullptr;
+    w.second = 0;
+    if (int rc = check_cuda(cudaMalloc(&w.first, floats * sizeof(float)), "conv_tc rows: weights"))
+      return rc;
+    w.second = floats;
+  }
+  *out = w.first;
   return ACCT_OK;
 }
 
@@ -2687,11 +3074,91 @@ int launch_conv_wide(const float *im, int64_t ld_im, int64_t im_stride, int chan
   return note_launch("conv3x3 tc wide");
 }
 
+// row-band conv (tc_conv_rows_kernel): M <= 32 filters (for 33..64 the
+// im2col-operand kernel measured faster: the shared-memory operand reads of
+// N = 64 MMAs bound this design, tools/conv_rows_probe.py), channels a
+// multiple of 8 whose resident [W hi | W lo] leave room for two staging
+// steps; col of images >= col_from written by the staging warps.
+// ENOTSUP for other shapes (the caller falls back to tc_conv_kernel).
+std::atomic<int> g_conv_rows{0};
+int conv_dbg() {  // ACCT_CONV_DBG work-skipping bits: the -DACCT_PROFILING build only
+  static const int dbg = [] {
+    const char *e = getenv("ACCT_CONV_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  return dbg;
+}
+
+template <int TN>
+int launch_conv_rows(const float *im, int64_t ld_im, int64_t im_stride, int channels, int height,
+                     int width, float *col, int64_t ld_col, int64_t col_stride, int M,
+                     const float *A, int64_t lda, float beta, float *C, int64_t ldc,
+                     int64_t c_stride, const float *bias, int act, int batch, int col_from,
+                     const ConvPool &pl, cudaStream_t s) {
+  using G = RowsCfg<TN>;
+  if (!g_conv_rows.load(std::memory_order_relaxed) || channels % 8 || M > TN || TN > 32)
+    return ACCT_ENOTSUP;
+  const int nstrips = (width + 127) / 128;
+  int swd = (width + nstrips - 1) / nstrips;
+  swd += swd & 1;  // even: pooling windows never straddle strips
+  const int sp = swd + 2;
+  const int pairs = (height + 1) / 2;
+  const int64_t units = (int64_t)batch * nstrips * pairs;
+  if (units > INT32_MAX) return ACCT_ENOTSUP;
+  const size_t stage_bytes = 256 * (size_t)sp;
+  const size_t w_bytes = (size_t)9 * channels * 2 * TN * 4;
+  // (the MMA rows past wdt read up to 130 - sp positions beyond the last
+  // stage: into the weights, never outside the block; those rows are dropped)
+  const size_t fixed = 1024 + w_bytes + 4 * TN + 8 * (2 * G::MAXS + 2 * G::NACC + 1) + 16;
+  if (fixed + 2 * stage_bytes > 227 * 1024) return ACCT_ENOTSUP;
+  int nstage = (int)((227 * 1024 - fixed) / stage_bytes);
+  if (nstage > G::MAXS) nstage = G::MAXS;
+  const size_t smem = fixed + (size_t)nstage * stage_bytes;
+  static std::mutex mu;
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev >= 0 && dev < 64 && !done[dev]) {
+      if (int rc = check_cuda(cudaFuncSetAttribute(tc_conv_rows_kernel<TN>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   227 * 1024),
+                              "conv_tc rows: smem attribute"))
+        return rc;
+      done[dev] = true;
+    }
+  }
+  float *wimg = nullptr;
+  if (int rc = conv_weights_for(s, w_bytes / 4, &wimg)) return rc;
+  {
+    const int items = 9 * (channels / 4) * TN;
+    launch(rows_weights_kernel<TN>, dim3((items + 255) / 256), dim3(256), 0, s, A, lda, M,
+           channels, reinterpret_cast<float4 *>(wimg));
+    if (int rc = note_launch("conv3x3 tc rows weights")) return rc;
+  }
+  const int sms = sm_count();
+  const int grid = units < sms ? (int)units : sms;
+  launch(tc_conv_rows_kernel<TN>, dim3(grid), dim3(ROWS_THREADS), smem, s, im, ld_im,
+         batch > 1 ? im_stride : (int64_t)0, channels, height, width,
+         reinterpret_cast<const float4 *>(wimg), M, col_from < batch ? col : nullptr, ld_col,
+         col_stride, col_from, nstrips, swd, sp,
+         pairs, (int)units, nstage, beta, C, ldc, c_stride, bias, act, pl.pool, pl.ld_pool,
+         pl.pool_stride, pl.idx, pl.ld_idx, pl.idx_stride, pl.c_from, conv_dbg());
+  return note_launch("conv3x3 tc rows");
+}
+
 template <int TN>
 int conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channels, int height,
             int width, float *col, int64_t ld_col, int64_t col_stride, int M, const float *A,
             int64_t lda, float beta, float *C, int64_t ldc, int64_t c_stride, const float *bias,
             int act, int batch, int col_from, const ConvPool &pl, cudaStream_t s) {
+  {
+    const int rc = launch_conv_rows<TN>(im, ld_im, im_stride, channels, height, width, col, ld_col,
+                                        col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act,
+                                        batch, col_from, pl, s);
+    if (rc != ACCT_ENOTSUP) return rc;
+  }
   // 16-wide pixel blocks unless the width is a multiple of 8 but not of 16;
   // the other width when those slabs do not fit next to the pooling scratch
   const bool eight = width % 16 != 0 && width % 8 == 0;
@@ -2718,6 +3185,11 @@ extern "C" int acct_tc_stream_k_pairs(void) {
   return acct::sk_pairs(acct::tc2_gemm_kernel<192, 2, 32, false, false, true, 4, false>,
                         G::SMEM_BYTES);
 }
+
+// 1: narrow convs with M <= 32 on the row-band kernel instead of the
+// im2col-operand kernel (default 0: measured no faster in the nets)
+// -- tests / A-B measurements only
+extern "C" void acct_tc_set_conv_rows(int on) { acct::g_conv_rows.store(on ? 1 : 0); }
 
 extern "C" void acct_tc_set_tile(int tile) { acct::g_force_tile.store(tile < 0 ? 0 : tile); }
 

@@ -109,7 +109,8 @@ SIGNATURES = {
     "acct_tc_stream_k_pairs": [],          # returns a count, not an error code
 }
 VOID_FUNCS = {"acct_counters_get": [C.POINTER(Counters)], "acct_counters_reset": [],
-              "acct_graph_destroy": [_vp], "acct_tc_set_write_hi": [_i32], "acct_tc_set_tile": [_i32]}
+              "acct_graph_destroy": [_vp], "acct_tc_set_write_hi": [_i32], "acct_tc_set_tile": [_i32],
+              "acct_tc_set_conv_rows": [_i32]}
 ENOTSUP = 1002
 STRING_FUNCS = {"acct_last_error_string": [], "acct_build_info": []}
 

@@ -27,6 +27,17 @@ def orc():
     return cprog.load_oracle()
 
 
+@pytest.fixture(params=["im2col-operand", "row-band"])
+def narrow_kernel(request):
+    """Both narrow (M <= 64) tcgen05 conv kernels: the default im2col-operand
+    kernel and the opt-in row-band kernel (M <= 32, channels % 8 == 0; other
+    shapes fall back to the first)."""
+    lib = K.lib()
+    lib.acct_tc_set_conv_rows(1 if request.param == "row-band" else 0)
+    yield request.param
+    lib.acct_tc_set_conv_rows(0)
+
+
 def _rand(shape, seed, lo=-1.0, hi=1.0):
     return np.random.default_rng(seed).uniform(lo, hi, shape).astype(np.float32)
 
@@ -358,9 +369,11 @@ def test_conv3x3_fused_declines_unaligned_rows(cuda_device):
                           (5, 7, 4, 33, 0, True, K.ACT_LEAKY, 4, 3, "il", False),
                           (64, 52, 52, 128, 0, True, K.ACT_LEAKY, 2, 1, "il", True),
                           (128, 24, 16, 256, 1, True, K.ACT_LEAKY, 2, 0, "im", False),
-                          (3, 20, 36, 128, 0, False, K.ACT_NONE, 3, 2, "il", False)])
-def test_conv3x3_tc_equals_im2col_then_tc_gemm(cuda_device, orc, c, h, w, M, beta, use_bias, act,
-                                               batch, col_from, layout, exact):
+                          (3, 20, 36, 128, 0, False, K.ACT_NONE, 3, 2, "il", False),
+                          (8, 10, 12, 24, 1, True, K.ACT_LEAKY, 2, 1, "im", False),
+                          (16, 7, 300, 32, 0, True, K.ACT_LEAKY, 2, 0, "il", False)])
+def test_conv3x3_tc_equals_im2col_then_tc_gemm(cuda_device, orc, narrow_kernel, c, h, w, M, beta,
+                                               use_bias, act, batch, col_from, layout, exact):
     """acct_conv3x3_tc_f32 (implicit-im2col tcgen05 swap tile) writes col
     exactly like im2col for images >= col_from, leaves the others untouched,
     and computes C within the gemm tolerance of the oracle (and, at the
@@ -432,9 +445,9 @@ def test_conv3x3_tc_declines_what_it_does_not_take(cuda_device):
     with pytest.raises(K.DeviceError):  # 65 filters: beyond the swap tiles
         K.conv3x3_tc(im.data_ptr(), 64, 0, 3, 8, 8, col.data_ptr(), 64, 0, 65, A.data_ptr(), 32,
                      0.0, C.data_ptr(), 64, 0)
-    with pytest.raises(K.DeviceError):  # resident weights + slabs beyond shared memory (64 ch)
-        big = torch.zeros((64, 608 * 4), device="cuda")
-        K.conv3x3_tc(big.data_ptr(), 608 * 4, 0, 64, 4, 608, col.data_ptr(), 608 * 4, 0, 32,
+    with pytest.raises(K.DeviceError):  # 72 channels: beyond the narrow kernels' weights
+        big = torch.zeros((72, 608 * 4), device="cuda")
+        K.conv3x3_tc(big.data_ptr(), 608 * 4, 0, 72, 4, 608, col.data_ptr(), 608 * 4, 0, 32,
                      A.data_ptr(), 32, 0.0, C.data_ptr(), 608 * 4, 0)
 
 
@@ -455,7 +468,8 @@ def test_leaky_is_darknets_double_product_for_every_float(cuda_device):
                           (5, 30, 12, 24, 0, K.ACT_LINEAR, 1, 0, "im"),
                           (64, 52, 52, 128, 0, K.ACT_LEAKY, 2, 1, "il"),
                           (96, 20, 24, 256, 1, K.ACT_LEAKY, 2, 0, "im")])
-def test_conv3x3_tc_fused_maxpool(cuda_device, c, h, w, M, beta, act, batch, c_from, layout):
+def test_conv3x3_tc_fused_maxpool(cuda_device, narrow_kernel, c, h, w, M, beta, act, batch, c_from,
+                                  layout):
     """The tcgen05 conv with its 2x2/2 maxpool fused into the epilogue
     writes pool and argmax idx bit-identically to acct_maxpool_batched_f32
     over the unfused conv output, and C only for images >= c_from."""

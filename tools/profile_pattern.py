@@ -29,10 +29,13 @@ def main():
     ap.add_argument("--gemm", default="auto", choices=("auto", "simt", "tc"))
     ap.add_argument("--no-fuse", action="store_true")
     ap.add_argument("--batch", type=int, default=0, help="images per launch (0 = all)")
+    ap.add_argument("--conv-rows", type=int, default=0,
+                    help="1: narrow convs (M <= 32) on the row-band kernel (acct_tc_set_conv_rows)")
     ap.add_argument("--graph", action="store_true",
                     help="1 plain run, then graph capture + replays (ncu: skip the first run's "
                          "launches); prints device ms per replay")
     args = ap.parse_args()
+    K.lib().acct_tc_set_conv_rows(args.conv_rows)
     if args.graph:
         import torch
         mode = {"auto": K.GEMM_AUTO, "simt": K.GEMM_SIMT, "tc": K.GEMM_TC3XTF32}[args.gemm]

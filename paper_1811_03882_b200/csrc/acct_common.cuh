@@ -59,9 +59,13 @@ inline cudaStream_t as_stream(acct_stream_t s) { return reinterpret_cast<cudaStr
 // with programmaticStreamSerializationAllowed (so inside a CUDA graph the
 // next kernel's CTAs may be scheduled, and run their prologue, while this one
 // drains) and calls pdl_wait() before touching any global data a previous
-// kernel produced or may still read.  On by default (graph replay of the
-// 16-image step 0.746 -> 0.736 ms, image at a time ~3.0 -> 2.95 ms);
-// ACCT_PDL=0 turns it off.
+// kernel produced or may still read.  On by default; ACCT_PDL=0 turns it
+// off.  The dependents are released by each CTA's implicit trigger at exit:
+// an explicit griddepcontrol.launch_dependents at kernel start let the next
+// grid's CTAs take SM slots (shared memory, TMEM) from this grid's later
+// waves -- graph replay, 16 images: yolov2-tiny 0.718 / 0.716 / 0.729 ms
+// and yolov2-608 5.039 / 4.945 / 4.955 ms for early trigger / trigger at exit
+// / no PDL.
 bool pdl_enabled();
 
 template <typename... KArgs, typename... Args>
@@ -83,9 +87,9 @@ cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
 }  // namespace acct
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
+// where a kernel may release its dependents; a no-op (the implicit trigger
+// at CTA exit measured best, see above)
+__device__ __forceinline__ void pdl_trigger() {}
 
 // leaky as darknet computes it: `.1*x` is a double product rounded to float
 __host__ __device__ __forceinline__ float acct_leaky_ref(float v) {

@@ -15,11 +15,14 @@
 // loads -- results are then wrong) exist only in the profiling build
 // (`-DACCT_PROFILING`, `python -m paper_1811_03882_b200.build --profiling`,
 // used by tools/ only).  In the product library ACCT_SKIP is a constant
-// false and those paths are compiled out.
+// false and those paths are compiled out, as are the clock64 traces of
+// ACCT_TRACE (bit 64, tools/conv_trace.py).
 #ifdef ACCT_PROFILING
 #define ACCT_SKIP(word, bit) (((word) & (bit)) != 0)
+#define ACCT_TRACE(word) (((word) & 64) != 0)
 #else
 #define ACCT_SKIP(word, bit) false
+#define ACCT_TRACE(word) false
 #endif
 
 namespace acct {
@@ -90,6 +93,21 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // where a kernel may release its dependents; a no-op (the implicit trigger
 // at CTA exit measured best, see above)
 __device__ __forceinline__ void pdl_trigger() {}
+
+// n / d and n % d for 0 <= n, d < 2^24 by a float reciprocal (inv_d = 1.0f /
+// d, computed once) and one correction step -- the per-unit tile-index
+// divisions of the persistent kernels showed in their stall samples
+__device__ __forceinline__ void acct_divmod(int n, int d, float inv_d, int &q, int &r) {
+  q = (int)((float)n * inv_d);
+  r = n - q * d;
+  if (r < 0) {
+    --q;
+    r += d;
+  } else if (r >= d) {
+    ++q;
+    r -= d;
+  }
+}
 
 // leaky as darknet computes it: `.1*x` is a double product rounded to float
 __host__ __device__ __forceinline__ float acct_leaky_ref(float v) {

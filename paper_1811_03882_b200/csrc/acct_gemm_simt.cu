@@ -609,23 +609,11 @@ conv3x3_pool_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
   pdl_trigger();
   pdl_wait();
 
-  // n / d for n, d < 2^24 by a float reciprocal and one correction step (the
-  // integer divisions were 10% of the kernel's stall samples)
-  auto divmod = [](int n, int d, float inv_d, int &q, int &r) {
-    q = (int)((float)n * inv_d);
-    r = n - q * d;
-    if (r < 0) {
-      --q;
-      r += d;
-    } else if (r >= d) {
-      ++q;
-      r -= d;
-    }
-  };
+  // (the integer divisions were 10% of the kernel's stall samples)
   auto tile_xy = [&](int tile, int &img, int &y0, int &x0) {
     int t, ty, tx;
-    divmod(tile, tpi, inv_tpi, img, t);
-    divmod(t, tiles_x, inv_tiles_x, ty, tx);
+    acct_divmod(tile, tpi, inv_tpi, img, t);
+    acct_divmod(t, tiles_x, inv_tiles_x, ty, tx);
     y0 = ty * PT_H;
     x0 = tx * PT_W;
   };

@@ -1407,7 +1407,9 @@ __device__ __forceinline__ void conv_block(uint32_t base, int kvalid, float (&v)
     conv_ld<TWP, CS, R0, 0, true>(base, kvalid, v);
 }
 
-template <int TN, int TW>
+// BETA: beta != 0 (C += ...) -- a template flag, so the usual beta = 0 launch
+// issues no predicated C loads in the epilogue (as conv3x3_pool_kernel)
+template <int TN, int TW, bool BETA>
 __global__ void __launch_bounds__(CONV_NARROW_THREADS, 1)
 tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                int M, int channels, int height, int width, int tiles_x, int tpi, int units,
@@ -1437,13 +1439,13 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int HW = height * width;
-  if ((dbg & 64) && blockIdx.x == 0 && threadIdx.x == 0) g_trace[6][0] = clock64();
+  if (ACCT_TRACE(dbg) && blockIdx.x == 0 && threadIdx.x == 0) g_trace[6][0] = clock64();
   auto gtime = [] {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return (long long)t;
   };
-  if ((dbg & 64) && threadIdx.x == 0 && blockIdx.x < 256) g_trace[7][256 + blockIdx.x] = gtime();
+  if (ACCT_TRACE(dbg) && threadIdx.x == 0 && blockIdx.x < 256) g_trace[7][256 + blockIdx.x] = gtime();
   if (threadIdx.x == 0) {
     ptx::mbar_init(wfull, 1);
     for (int b = 0; b < nslab; ++b) {
@@ -1470,12 +1472,13 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   pdl_trigger();
   pdl_wait();
 
+  const float inv_tpi = 1.0f / (float)tpi, inv_tx = 1.0f / (float)tiles_x;
   auto unit_xy = [&](int u, int &img, int &y0, int &x0) {
-    img = u / tpi;
-    const int t = u - img * tpi;
-    const int ty = t / tiles_x;
+    int t, ty, tx;
+    acct_divmod(u, tpi, inv_tpi, img, t);
+    acct_divmod(t, tiles_x, inv_tx, ty, tx);
     y0 = ty * G::TH;
-    x0 = (t - ty * tiles_x) * TW;
+    x0 = tx * TW;
   };
 
   if (warp == 0) {
@@ -1516,7 +1519,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       for (int kb = 0; kb < nkb; ++kb, ++gp) {
         const int s = gp % S;
         ptx::mbar_wait(&conv[p * S + s], (gp / S) & 1);
-        if ((dbg & 64) && p == 0 && blockIdx.x == 0 && gp < kTrace && lane == 0) g_trace[2][gp] = clock64();
+        if (ACCT_TRACE(dbg) && p == 0 && blockIdx.x == 0 && gp < kTrace && lane == 0) g_trace[2][gp] = clock64();
         ptx::tc_fence_after();
         const uint32_t yh = ptx::smem_u32(w_hi + kb * G::W_TILE);
         const uint32_t yl = ptx::smem_u32(w_lo + kb * G::W_TILE);
@@ -1536,7 +1539,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           ptx::mma_commit(&empty[p * S + s]);
         }
         __syncwarp();
-        if ((dbg & 64) && p == 0 && blockIdx.x == 0 && gp < kTrace && lane == 0) g_trace[3][gp] = clock64();
+        if (ACCT_TRACE(dbg) && p == 0 && blockIdx.x == 0 && gp < kTrace && lane == 0) g_trace[3][gp] = clock64();
       }
       if (ptx::elect_one()) ptx::mma_commit(&acc_full[p * NACC + a]);
       __syncwarp();
@@ -1580,9 +1583,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         const int k0 = kb * BK;
         const int c0 = k0 / 9;
         const int kvalid = K - k0;  // >= 32 except in the last block
-        if ((dbg & 64) && half == 0 && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[0][g] = clock64();
+        if (ACCT_TRACE(dbg) && half == 0 && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[0][g] = clock64();
         if (g >= S) ptx::mbar_wait(&empty[half * S + s], ((g / S) - 1) & 1);
-        if ((dbg & 64) && half == 0 && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[1][g] = clock64();
+        if (ACCT_TRACE(dbg) && half == 0 && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[1][g] = clock64();
         ptx::tc_fence_after();
         if (ACCT_SKIP(dbg, 1)) {  // profiling knob: skip building the operand (results wrong)
           __syncwarp();
@@ -1624,7 +1627,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&conv[half * S + s]);
-        if ((dbg & 64) && half == 0 && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[4][g] = clock64();
+        if (ACCT_TRACE(dbg) && half == 0 && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[4][g] = clock64();
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&slab_empty[sb]);  // this unit's slab is consumed
@@ -1648,7 +1651,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       unit_xy(u, img, y0, x0);
       const int a = jp % NACC;
       ptx::mbar_wait_sleepy(&acc_full[grp * NACC + a], (jp / NACC) & 1);
-      if ((dbg & 64) && grp == 0 && blockIdx.x == 0 && jp < kTrace && lane == 0 && q == 0) g_trace[5][jp] = clock64();
+      if (ACCT_TRACE(dbg) && grp == 0 && blockIdx.x == 0 && jp < kTrace && lane == 0 && q == 0) g_trace[5][jp] = clock64();
       ptx::tc_fence_after();
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + grp * G::PCOLS + a * TN;
       const int y = y0 + py, x = x0 + px;
@@ -1665,7 +1668,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         if (rbase >= M) continue;
         float *rp = cp + (int64_t)rbase * ldc;
         float cv[CH];
-        if (beta != 0.0f && live) {
+        if (BETA && live) {
 #pragma unroll
           for (int jj = 0; jj < CH; ++jj)  // every load in flight before any store
             cv[jj] = rbase + jj < M ? rp[(int64_t)jj * ldc] : 0.0f;
@@ -1674,7 +1677,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 #pragma unroll
         for (int jj = 0; jj < CH; ++jj) {
           float v = __uint_as_float(r[jj]);
-          if (beta != 0.0f && live) v = beta * cv[jj] + v;
+          if (BETA && live) v = beta * cv[jj] + v;
           if (bias) v += ptx::lds32(bias_sa + 4 * (rbase + jj));
           f[jj] = v;
         }
@@ -1732,8 +1735,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 
   ptx::tc_fence_before();
   __syncthreads();
-  if ((dbg & 64) && blockIdx.x == 0 && threadIdx.x == 0) g_trace[6][1] = clock64();
-  if ((dbg & 64) && threadIdx.x == 0 && blockIdx.x < 256) g_trace[7][blockIdx.x] = gtime();
+  if (ACCT_TRACE(dbg) && blockIdx.x == 0 && threadIdx.x == 0) g_trace[6][1] = clock64();
+  if (ACCT_TRACE(dbg) && threadIdx.x == 0 && blockIdx.x < 256) g_trace[7][blockIdx.x] = gtime();
   if (warp == 1) ptx::tmem_dealloc(tmem, G::TMEM_COLS);
 }
 
@@ -1770,7 +1773,7 @@ struct WideCfg {
   static_assert(USED_COLS <= 512, "TMEM overflow");
 };
 
-template <int TW>
+template <int TW, bool BETA>
 __global__ void __launch_bounds__(CONV_TC_THREADS, 1)
 tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                     int M, int channels, int height, int width, int tiles_x, int tpi, int units,
@@ -1820,14 +1823,15 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
   pdl_wait();
 
   const int per_mb = tpi * batch;
+  const float inv_mb = 1.0f / (float)per_mb, inv_tpi = 1.0f / (float)tpi,
+              inv_tx = 1.0f / (float)tiles_x;
   auto unit_of = [&](int u, int &mb, int &img, int &y0, int &x0) {
-    mb = u / per_mb;
-    const int r = u - mb * per_mb;
-    img = r / tpi;
-    const int t = r - img * tpi;
-    const int ty = t / tiles_x;
+    int r, t, ty, tx;
+    acct_divmod(u, per_mb, inv_mb, mb, r);
+    acct_divmod(r, tpi, inv_tpi, img, t);
+    acct_divmod(t, tiles_x, inv_tx, ty, tx);
     y0 = ty * G::TH;
-    x0 = (t - ty * tiles_x) * TW;
+    x0 = tx * TW;
   };
 
   if (warp == 0) {
@@ -1985,7 +1989,7 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         if (rbase >= M) continue;
         float *rp = cp + (int64_t)rbase * ldc;
         float cv[CH];
-        if (beta != 0.0f && live) {
+        if (BETA && live) {
 #pragma unroll
           for (int jj = 0; jj < CH; ++jj) cv[jj] = rbase + jj < M ? rp[(int64_t)jj * ldc] : 0.0f;
         }
@@ -1993,7 +1997,7 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
 #pragma unroll
         for (int jj = 0; jj < CH; ++jj) {
           float v = __uint_as_float(r[jj]);
-          if (beta != 0.0f && live) v = beta * cv[jj] + v;
+          if (BETA && live) v = beta * cv[jj] + v;
           if (bias) v += __ldg(bias + (rbase + jj < M ? rbase + jj : 0));
           f[jj] = v;
         }
@@ -2997,25 +3001,26 @@ int launch_conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channe
   {
     std::lock_guard<std::mutex> lock(mu);
     if (dev >= 0 && dev < 64 && !done[dev]) {
-      if (int rc = check_cuda(cudaFuncSetAttribute(tc_conv_kernel<TN, TW>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   227 * 1024),
-                              "conv_tc: smem attribute"))
-        return rc;
+      for (auto k : {tc_conv_kernel<TN, TW, false>, tc_conv_kernel<TN, TW, true>})
+        if (int rc = check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     227 * 1024),
+                                "conv_tc: smem attribute"))
+          return rc;
       done[dev] = true;
     }
   }
   const int tiles_x = (width + TW - 1) / TW, tiles_y = (height + G::TH - 1) / G::TH;
   const int64_t tpi = (int64_t)tiles_x * tiles_y;
   const int64_t units = tpi * batch;
-  if (units > INT32_MAX) return ACCT_ENOTSUP;
+  if (units >= (1 << 24)) return ACCT_ENOTSUP;  // acct_divmod
   const int sms = sm_count();
   const int grid = units < sms ? (int)units : sms;
   static const int dbg = [] {  // bit 64: clock64 trace (tools/conv_trace.py); the work-skipping
     const char *e = getenv("ACCT_CONV_DBG");  // bits 1-32 need the -DACCT_PROFILING build
     return e ? atoi(e) : 0;
   }();
-  launch(tc_conv_kernel<TN, TW>, dim3(grid), dim3(CONV_NARROW_THREADS), smem, s, tw, tx, M, channels,
+  launch(beta != 0.0f ? tc_conv_kernel<TN, TW, true> : tc_conv_kernel<TN, TW, false>, dim3(grid),
+         dim3(CONV_NARROW_THREADS), smem, s, tw, tx, M, channels,
          height, width, tiles_x, (int)tpi, (int)units, nkb, beta, C, ldc, c_stride, bias, act, col,
          ld_col, col_stride, col_from, pl.pool, pl.ld_pool, pl.pool_stride, pl.idx, pl.ld_idx,
          pl.idx_stride, pl.c_from, nslab, dbg);
@@ -3049,25 +3054,26 @@ int launch_conv_wide(const float *im, int64_t ld_im, int64_t im_stride, int chan
   {
     std::lock_guard<std::mutex> lock(mu);
     if (dev >= 0 && dev < 64 && !done[dev]) {
-      if (int rc = check_cuda(cudaFuncSetAttribute(tc_conv_wide_kernel<TW>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   227 * 1024),
-                              "conv_tc wide: smem attribute"))
-        return rc;
+      for (auto k : {tc_conv_wide_kernel<TW, false>, tc_conv_wide_kernel<TW, true>})
+        if (int rc = check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     227 * 1024),
+                                "conv_tc wide: smem attribute"))
+          return rc;
       done[dev] = true;
     }
   }
   const int tiles_x = (width + TW - 1) / TW, tiles_y = (height + G::TH - 1) / G::TH;
   const int64_t tpi = (int64_t)tiles_x * tiles_y;
   const int64_t units = tpi * batch * (M / G::TN);
-  if (units > INT32_MAX) return ACCT_ENOTSUP;
+  if (units >= (1 << 24)) return ACCT_ENOTSUP;  // acct_divmod
   const int sms = sm_count();
   const int grid = units < sms ? (int)units : sms;
   static const int dbg = [] {
     const char *e = getenv("ACCT_CONV_DBG");
     return e ? atoi(e) : 0;
   }();
-  launch(tc_conv_wide_kernel<TW>, dim3(grid), dim3(CONV_TC_THREADS), smem, s, tw, tx, M, channels,
+  launch(beta != 0.0f ? tc_conv_wide_kernel<TW, true> : tc_conv_wide_kernel<TW, false>, dim3(grid),
+         dim3(CONV_TC_THREADS), smem, s, tw, tx, M, channels,
          height, width, tiles_x, (int)tpi, (int)units, nkb, beta, C, ldc, c_stride, bias, act, col,
          ld_col, col_stride, col_from, pl.pool, pl.ld_pool, pl.pool_stride, pl.idx, pl.ld_idx,
          pl.idx_stride, pl.c_from, batch, dbg);

@@ -3,7 +3,8 @@ per k-block g -- split start / empty-wait done / conv arrive (half of g),
 MMA conv-wait done / commit issued -- and per unit the epilogue's
 acc_full wake.  Prints cycle deltas for the first k-blocks.
 
-    ACCT_CONV_DBG=64 python tools/conv_trace.py [extra dbg bits]
+    ACCT_LIB=paper_1811_03882_b200/libacct_sm100_prof.so ACCT_CONV_DBG=64 \
+        python tools/conv_trace.py   (the traces exist in the profiling build only)
 """
 import ctypes
 import os

@@ -1379,32 +1379,36 @@ struct ConvCfg {
 };
 constexpr int CONV_TC_THREADS = 32 * 18;
 constexpr int kMaxSlabs = 8;  // slab ring depth: 2 .. 8 as shared memory allows
-constexpr int CONV_NARROW_THREADS = 32 * 19;  // + the second MMA issuer (warp 18)
+// warps: 0 TMA, 1 / 26 MMA issuers, 2-17 operand builders (two per TMEM lane
+// quadrant and pipeline), 18-25 epilogue
+constexpr int CONV_NARROW_THREADS = 32 * 27;
 
 // One k-block (32 k = (channel, tap) pairs from k0 = 9 c0 + R0) of the
 // activation operand for this lane's pixel: each k is one LDS at the lane's
 // slab address (channel c0 folded in) plus a compile-time immediate -- the
 // channel step and the tap's row / column offset.  TAIL: the last block of a
 // K that is not a multiple of 32 (zeros past K).
-template <int TWP, int CS, int R0, int K, bool TAIL>
-__device__ __forceinline__ void conv_ld(uint32_t base, int kvalid, float (&v)[32]) {
-  if constexpr (K < 32) {
+// (K0, KEND: the part K0 .. KEND - 1 of the block, into v[K - K0] -- the
+// narrow kernel's two operand warps per TMEM lane quadrant take 16 k each)
+template <int TWP, int CS, int R0, int K, bool TAIL, int K0 = 0, int KEND = 32>
+__device__ __forceinline__ void conv_ld(uint32_t base, int kvalid, float (&v)[KEND - K0]) {
+  if constexpr (K < KEND) {
     constexpr int r = (R0 + K) % 9, dc = (R0 + K) / 9;
     constexpr int imm = dc * CS + ((r / 3) * TWP + r % 3 + 3) * 4;  // column x - 1 + kw
     if (TAIL && K >= kvalid)
-      v[K] = 0.0f;
+      v[K - K0] = 0.0f;
     else
-      asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v[K]) : "r"(base), "n"(imm));
-    conv_ld<TWP, CS, R0, K + 1, TAIL>(base, kvalid, v);
+      asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v[K - K0]) : "r"(base), "n"(imm));
+    conv_ld<TWP, CS, R0, K + 1, TAIL, K0, KEND>(base, kvalid, v);
   }
 }
 
-template <int TWP, int CS, int R0>
-__device__ __forceinline__ void conv_block(uint32_t base, int kvalid, float (&v)[32]) {
-  if (kvalid >= 32)
-    conv_ld<TWP, CS, R0, 0, false>(base, kvalid, v);
+template <int TWP, int CS, int R0, int K0 = 0, int KEND = 32>
+__device__ __forceinline__ void conv_block(uint32_t base, int kvalid, float (&v)[KEND - K0]) {
+  if (kvalid >= KEND)
+    conv_ld<TWP, CS, R0, K0, false, K0, KEND>(base, kvalid, v);
   else
-    conv_ld<TWP, CS, R0, 0, true>(base, kvalid, v);
+    conv_ld<TWP, CS, R0, K0, true, K0, KEND>(base, kvalid, v);
 }
 
 // BETA: beta != 0 (C += ...) -- a template flag, so the usual beta = 0 launch
@@ -1450,10 +1454,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     ptx::mbar_init(wfull, 1);
     for (int b = 0; b < nslab; ++b) {
       ptx::mbar_init(&slab_full[b], 1);
-      ptx::mbar_init(&slab_empty[b], 4);  // the unit's pipeline's four operand warps
+      ptx::mbar_init(&slab_empty[b], 8);  // the unit's pipeline's eight operand warps
     }
     for (int s = 0; s < G::NP * S; ++s) {
-      ptx::mbar_init(&conv[s], 4);
+      ptx::mbar_init(&conv[s], 8);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < G::NP * NACC; ++a) {
@@ -1505,9 +1509,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         }
       }
     }
-  } else if (warp == 1 || warp == 18) {
+  } else if (warp == 1 || warp == 26) {
     // ---------------- MMA issuers: pipeline p takes units j = p, p + 2, ... ----------------
-    const int p = warp == 18;
+    const int p = warp == 26;
     constexpr uint32_t idesc = ptx::idesc_tf32(128, TN, false, false);
     const uint32_t pbase = tmem + p * G::PCOLS;
     int gp = 0, jp = 0;
@@ -1544,25 +1548,28 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       if (ptx::elect_one()) ptx::mma_commit(&acc_full[p * NACC + a]);
       __syncwarp();
     }
-  } else if (warp < 10) {
+  } else if (warp < 18) {
     // ---------------- weights lo, then the activation operand ----------------
-    // two halves of four warps (2-5, 6-9): half p builds every k-block of
-    // its pipeline's units (j = p, p + 2, ...)
+    // two halves of eight warps (2-9, 10-17): half p builds every k-block of
+    // its pipeline's units (j = p, p + 2, ...); within a half, the two warps
+    // of a TMEM lane quadrant take k 0-15 and 16-31 of each block (four
+    // warps, one per quadrant, were latency-bound: ~800 cycles per k-block)
     const int q = warp & 3;  // TMEM lanes 32q.. = MMA rows (pixels) 32q..
-    const int half = (warp - 2) >> 2;
+    const int half = (warp - 2) >> 3;
+    const int kp = ((warp - 2) >> 2) & 1;
     const int ct = threadIdx.x - 64;
     const int K = 9 * channels;
     ptx::mbar_wait(wfull, 0);
     {
       const uint32_t hs = ptx::smem_u32(w_hi), ls = ptx::smem_u32(w_lo);
-      for (int i = ct; i < nkb * G::W_TILE / 16; i += 256) {
+      for (int i = ct; i < nkb * G::W_TILE / 16; i += 512) {
         float4 h4;
         ptx::sts128(ls + 16 * i, split_lo(ptx::lds128(hs + 16 * i), h4));
       }
       ptx::fence_proxy_async_smem();
       // both halves wrote weights lo: all of it before any pipeline's first
       // conv arrival releases an MMA that reads it
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, 512;" ::: "memory");
     }
     int py, px;
     conv_pixel<TW>(q, lane, py, px);
@@ -1592,37 +1599,42 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           if (lane == 0) ptx::mbar_arrive(&conv[half * S + s]);
           continue;
         }
-        float v[BK];
+        constexpr int KH = BK / 2;
+        float v[KH];
         const uint32_t bc = lane_base + (uint32_t)(c0 * G::CS);
+#define ACCT_CONV_PART(R0)                                                  \
+  (kp ? conv_block<G::TWP, G::CS, R0, KH, BK>(bc, kvalid, v)                \
+      : conv_block<G::TWP, G::CS, R0, 0, KH>(bc, kvalid, v))
         switch (k0 - 9 * c0) {
-          case 0: conv_block<G::TWP, G::CS, 0>(bc, kvalid, v); break;
-          case 1: conv_block<G::TWP, G::CS, 1>(bc, kvalid, v); break;
-          case 2: conv_block<G::TWP, G::CS, 2>(bc, kvalid, v); break;
-          case 3: conv_block<G::TWP, G::CS, 3>(bc, kvalid, v); break;
-          case 4: conv_block<G::TWP, G::CS, 4>(bc, kvalid, v); break;
-          case 5: conv_block<G::TWP, G::CS, 5>(bc, kvalid, v); break;
-          case 6: conv_block<G::TWP, G::CS, 6>(bc, kvalid, v); break;
-          case 7: conv_block<G::TWP, G::CS, 7>(bc, kvalid, v); break;
-          default: conv_block<G::TWP, G::CS, 8>(bc, kvalid, v); break;
+          case 0: ACCT_CONV_PART(0); break;
+          case 1: ACCT_CONV_PART(1); break;
+          case 2: ACCT_CONV_PART(2); break;
+          case 3: ACCT_CONV_PART(3); break;
+          case 4: ACCT_CONV_PART(4); break;
+          case 5: ACCT_CONV_PART(5); break;
+          case 6: ACCT_CONV_PART(6); break;
+          case 7: ACCT_CONV_PART(7); break;
+          default: ACCT_CONV_PART(8); break;
         }
+#undef ACCT_CONV_PART
         if (wcol && inside) {
-          const int kn = kvalid < BK ? kvalid : BK;
-          float *cp = colp + (int64_t)k0 * ld_col;
+          const int kn = (kvalid < BK ? kvalid : BK) - KH * kp;
+          float *cp = colp + (int64_t)(k0 + KH * kp) * ld_col;
 #pragma unroll
-          for (int k = 0; k < BK; ++k)
+          for (int k = 0; k < KH; ++k)
             if (k < kn) __stcs(cp + (int64_t)k * ld_col, v[k]);
         }
-        uint32_t hi[BK], lo[BK];
+        uint32_t hi[KH], lo[KH];
 #pragma unroll
-        for (int k = 0; k < BK; ++k) {
+        for (int k = 0; k < KH; ++k) {
           const uint32_t h = __float_as_uint(v[k]) & 0xFFFFE000u;
           hi[k] = h;
           lo[k] = __float_as_uint(v[k] - __uint_as_float(h));
         }
-        const uint32_t ta =
-            tmem + ((uint32_t)(32 * q) << 16) + half * G::PCOLS + G::A_COL0 + s * 2 * BK;
-        ptx::tmem_st_cols<BK>(ta, hi);
-        ptx::tmem_st_cols<BK>(ta + BK, lo);
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + half * G::PCOLS + G::A_COL0 +
+                            s * 2 * BK + KH * kp;
+        ptx::tmem_st_cols<KH>(ta, hi);
+        ptx::tmem_st_cols<KH>(ta + BK, lo);
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
@@ -1634,17 +1646,17 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     }
   } else {
     // ---------------- epilogue: lanes = pixels, TMEM columns = filters ----------------
-    // group p of four warps (10-13, 14-17) drains pipeline p's accumulators
+    // group p of four warps (18-21, 22-25) drains pipeline p's accumulators
     const int q = warp & 3;
-    const int grp = (warp - 10) >> 2;
-    for (int i = threadIdx.x - 10 * 32; i < TN; i += 8 * 32) bias_s[i] = (bias && i < M) ? bias[i] : 0.0f;
+    const int grp = (warp - 18) >> 2;
+    for (int i = threadIdx.x - 18 * 32; i < TN; i += 8 * 32) bias_s[i] = (bias && i < M) ? bias[i] : 0.0f;
     asm volatile("bar.sync 2, 256;" ::: "memory");  // the eight epilogue warps
     int py, px;
     conv_pixel<TW>(q, lane, py, px);
     // explicit shared-space addresses (generic LD/ST through the realigned
     // base measured several times slower): bias, this warp's pooling scratch
     const uint32_t bias_sa = ptx::smem_u32(bias_s);
-    const uint32_t scr_sa = ptx::smem_u32(bias_s + 64 + (warp - 10) * 8 * 33);
+    const uint32_t scr_sa = ptx::smem_u32(bias_s + 64 + (warp - 18) * 8 * 33);
     int jp = 0;
     for (int u = blockIdx.x + grp * gridDim.x; u < units; u += 2 * gridDim.x, ++jp) {
       int img, y0, x0;

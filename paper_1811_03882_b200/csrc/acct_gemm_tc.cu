@@ -87,7 +87,7 @@ int forced_tile() {
 // bit 4: event trace of CTA 0's first kTrace stages (clock64 per role), read
 // back with acct_tc_trace -- pipeline analysis only (tools/tc_trace.py)
 constexpr int kTrace = 512;
-__device__ long long g_trace[8][kTrace];
+__device__ long long g_trace[12][kTrace];
 // bits 8-15 of the same word: L2 prefetch distance in k-blocks (ACCT_TC_PF,
 // default 0: measured slower for every net shape -- the ring is not HBM-latency bound)
 int prefetch_distance() {
@@ -1362,7 +1362,7 @@ struct ConvCfg {
   // accumulators of TN and S stages of the activation operand (hi, lo).
   // (TN = 32: 4 accumulators and 2 stages measured ~4% faster than 2 and 3;
   // each pipeline's accumulator barriers have ONE waiting group, in order)
-  static constexpr int NP = 2, PCOLS = 256, NACC = TN <= 32 ? 4 : 2;
+  static constexpr int NP = 2, PCOLS = 256, NACC = 2;
   static constexpr int S = (PCOLS - NACC * TN) / 64;
   static constexpr int TH = 128 / TW;
   // slab row: columns x0 - 4 .. x0 + TW + 3 (TMA needs a 16-byte aligned
@@ -1584,7 +1584,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       const bool inside = y < height && x < width;
       float *colp = col + img * col_bs + (int64_t)y * width + x;
       const uint32_t lane_base = ptx::smem_u32(slab0 + sb * slab_bytes) + lane_off;
+      if (ACCT_TRACE(dbg) && half == 0 && blockIdx.x == 0 && j < kTrace && ct % 128 == 0) g_trace[10][j] = clock64();
       ptx::mbar_wait(&slab_full[sb], (j / nslab) & 1);
+      if (ACCT_TRACE(dbg) && half == 0 && blockIdx.x == 0 && j < kTrace && ct % 128 == 0) g_trace[11][j] = clock64();
       for (int kb = 0; kb < nkb; ++kb, ++g) {
         const int s = g % S;
         const int k0 = kb * BK;
@@ -1631,11 +1633,13 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           hi[k] = h;
           lo[k] = __float_as_uint(v[k] - __uint_as_float(h));
         }
+        if (ACCT_TRACE(dbg) && half == 0 && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[8][g] = clock64() + (lo[0] & 0);
         const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + half * G::PCOLS + G::A_COL0 +
                             s * 2 * BK + KH * kp;
         ptx::tmem_st_cols<KH>(ta, hi);
         ptx::tmem_st_cols<KH>(ta + BK, lo);
         ptx::tmem_st_wait();
+        if (ACCT_TRACE(dbg) && half == 0 && blockIdx.x == 0 && g < kTrace && ct % 128 == 0) g_trace[9][g] = clock64();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&conv[half * S + s]);
@@ -1694,11 +1698,15 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           f[jj] = v;
         }
         if (act == ACCT_ACT_LEAKY) acct_leaky_block(f);
+        // C of the observable images only: a warp-uniform branch around the
+        // stores (predicated per store they issued for every image)
+        if (img >= c_from) {
 #pragma unroll
-        for (int jj = 0; jj < CH; ++jj) {
-          if (cst && rbase + jj < M) rp[(int64_t)jj * ldc] = f[jj];
-          r[jj] = __float_as_uint(f[jj]);
+          for (int jj = 0; jj < CH; ++jj)
+            if (cst && rbase + jj < M) rp[(int64_t)jj * ldc] = f[jj];
         }
+#pragma unroll
+        for (int jj = 0; jj < CH; ++jj) r[jj] = __float_as_uint(f[jj]);
 #pragma unroll
         for (int half = 0; half < 2 && pool; ++half) {
 #pragma unroll
@@ -2014,11 +2022,15 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
           f[jj] = v;
         }
         if (act == ACCT_ACT_LEAKY) acct_leaky_block(f);
+        // C of the observable images only: a warp-uniform branch around the
+        // stores (predicated per store they issued for every image)
+        if (img >= c_from) {
 #pragma unroll
-        for (int jj = 0; jj < CH; ++jj) {
-          if (cst && rbase + jj < M) rp[(int64_t)jj * ldc] = f[jj];
-          r[jj] = __float_as_uint(f[jj]);
+          for (int jj = 0; jj < CH; ++jj)
+            if (cst && rbase + jj < M) rp[(int64_t)jj * ldc] = f[jj];
         }
+#pragma unroll
+        for (int jj = 0; jj < CH; ++jj) r[jj] = __float_as_uint(f[jj]);
 #pragma unroll
         for (int hf = 0; hf < 2 && pool; ++hf) {
 #pragma unroll

@@ -33,13 +33,15 @@ def main():
                      A.data_ptr(), lda, 0.0, C.data_ptr(), P * ld, ld, None, K.ACT_NONE, P, s,
                      col_from=P - 1)
     torch.cuda.synchronize()
-    buf = np.zeros((8, 512), np.int64)
+    buf = np.zeros((12, 512), np.int64)
     K.call("acct_tc_trace", buf.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)))
     t0 = buf[buf > 0].min()
     b = np.where(buf > 0, buf - t0, -1)
-    print(" g  split0 emptyOK arrive | mmaConvOK commit")
+    print(" g  split0 emptyOK  loaded stored  arrive | mmaConvOK commit")
     for g in range(0, 60):
-        print(f"{g:3d} {b[0][g]:7d} {b[1][g]:7d} {b[4][g]:7d} | {b[2][g]:7d} {b[3][g]:7d}")
+        print(f"{g:3d} {b[0][g]:7d} {b[1][g]:7d} {b[8][g]:7d} {b[9][g]:7d} {b[4][g]:7d} |"
+              f" {b[2][g]:7d} {b[3][g]:7d}")
+    print("half-0 unit j: slab wait start / done:", [(int(b[10][j]), int(b[11][j])) for j in range(0, 16, 2)])
     print("epilogue acc_full wake per unit:", b[5][:12].tolist(), "... last", b[5][b[5] >= 0].max())
     print("kernel entry", b[6][0], "exit", b[6][1], "(cycles, same origin)")
     ent, ex = buf[7][256:256 + 148], buf[7][:148]

@@ -20,7 +20,7 @@ for flags in (extra, 16 | extra):
               K.GEMM_TC3XTF32, 0)
     torch.cuda.synchronize()
 lib.acct_tc_set_write_hi(0)
-tr = np.zeros((8, 512), dtype=np.int64)
+tr = np.zeros((12, 512), dtype=np.int64)
 assert lib.acct_tc_trace(tr.ctypes.data) == 0
 n = int((tr[4] > 0).sum())
 t0 = tr[0, 0]

@@ -471,7 +471,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       if ((j % EPI_GROUPS) != grp) continue;
       const Unit w = unit_of<TN, SWAP, BK>(u, nt, tiles, kb_per, total_kb);
       const int a = j % NACC;
-      ptx::mbar_wait_sleepy(&acc_full[a], (j / NACC) & 1);
+      ptx::mbar_wait(&acc_full[a], (j / NACC) & 1);
       ptx::tc_fence_after();
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * TN;
       float *part = ws + w.split * ws_split_stride;
@@ -1095,7 +1095,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       for (int i = 0; i < HC; ++i) acc[i] = 0.0f;
       for (int ci = 0; ci < nch; ++ci, ++c) {
         const int a = c & 1;
-        ptx::mbar_wait_sleepy(&acc_full[a], (c >> 1) & 1);
+        ptx::mbar_wait(&acc_full[a], (c >> 1) & 1);
         ptx::tc_fence_after();
         const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * G::ACC + grp * HC;
 #pragma unroll
@@ -1217,7 +1217,7 @@ tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       if ((j % GROUPS) != grp) continue;
       const Unit w = unit(u);
       const int a = j % NACC;
-      ptx::mbar_wait_sleepy(&acc_full[a], (j / NACC) & 1);
+      ptx::mbar_wait(&acc_full[a], (j / NACC) & 1);
       ptx::tc_fence_after();
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * G::ACC;
       float *part = ws + w.split * ws_split_stride;
@@ -1666,7 +1666,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       int img, y0, x0;
       unit_xy(u, img, y0, x0);
       const int a = jp % NACC;
-      ptx::mbar_wait_sleepy(&acc_full[grp * NACC + a], (jp / NACC) & 1);
+      ptx::mbar_wait(&acc_full[grp * NACC + a], (jp / NACC) & 1);
       if (ACCT_TRACE(dbg) && grp == 0 && blockIdx.x == 0 && jp < kTrace && lane == 0 && q == 0) g_trace[5][jp] = clock64();
       ptx::tc_fence_after();
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + grp * G::PCOLS + a * TN;
@@ -1992,7 +1992,7 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
       int mb, img, y0, x0;
       unit_of(u, mb, img, y0, x0);
       const int a = j % NACC;
-      ptx::mbar_wait_sleepy(&acc_full[a], (j / NACC) & 1);
+      ptx::mbar_wait(&acc_full[a], (j / NACC) & 1);
       ptx::tc_fence_after();
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + a * TN;
       const int y = y0 + py, x = x0 + px;
@@ -2342,7 +2342,7 @@ tc_conv_rows_kernel(const float *__restrict__ im, int64_t ld_im, int64_t im_bs, 
       int img, x0, wdt, y0;
       unit_of(u, img, x0, wdt, y0);
       const int slot = j % NACC;
-      ptx::mbar_wait_sleepy(&acc_full[slot], (j / NACC) & 1);
+      ptx::mbar_wait(&acc_full[slot], (j / NACC) & 1);
       ptx::tc_fence_after();
       const int xl = 32 * q + lane, x = x0 + xl;
       const bool live = xl < wdt;

@@ -1377,7 +1377,7 @@ struct ConvCfg {
   static constexpr uint32_t K_SBO = 8 * 128;
   static_assert(USED_COLS <= 512, "TMEM overflow");
 };
-constexpr int CONV_TC_THREADS = 32 * 18;
+constexpr int CONV_TC_THREADS = 32 * 26;  // wide conv: TMA, MMA, 16 builders, 8 epilogue
 constexpr int kMaxSlabs = 8;  // slab ring depth: 2 .. 8 as shared memory allows
 // warps: 0 TMA, 1 / 26 MMA issuers, 2-17 operand builders (two per TMEM lane
 // quadrant and pipeline), 18-25 epilogue
@@ -1772,10 +1772,11 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 //   warp 0      TMA: per stage the weight tile (128 rows x 32 k, SW128) and
 //               the slab chunk
 //   warp 1      TMEM allocator + MMA issuer
-//   warps 2..9  two halves taking alternate k-blocks: weights lo of the stage,
-//               the activation operand (hi / lo to a TMEM stage), col of
-//               images >= col_from
-//   warps 10..17 epilogue, two groups taking alternate units (+ fused maxpool)
+//   warps 2..17 two halves of eight taking alternate k-blocks: weights lo of
+//               the stage, the activation operand (hi / lo to a TMEM stage;
+//               two warps per lane quadrant, 16 k each), col of images >=
+//               col_from
+//   warps 18..25 epilogue, two groups taking alternate units (+ fused maxpool)
 template <int TW>
 struct WideCfg {
   static constexpr int TN = 128, BK = 32, S = 4, NACC = 2;  // NACC = 2: see the epilogue
@@ -1823,7 +1824,7 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&conv[s], 4);
+      ptx::mbar_init(&conv[s], 8);   // the k-block's group of eight builder warps
       ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < NACC; ++a) {
@@ -1906,11 +1907,15 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
       if (ptx::elect_one()) ptx::mma_commit(&acc_full[a]);
       __syncwarp();
     }
-  } else if (warp < 10) {
+  } else if (warp < 18) {
     // ---------------- weights lo + activation operand (two halves) ----------------
+    // half h (warps 2-9, 10-17) takes k-blocks g = h mod 2; within a half
+    // the two warps of a TMEM lane quadrant take k 0-15 and 16-31 (one warp
+    // per quadrant was latency-bound, as in the narrow conv)
     const int q = warp & 3;
-    const int half = (warp - 2) >> 2;
-    const int ht = threadIdx.x - 64 - 128 * half;  // 0..127 within the half
+    const int half = (warp - 2) >> 3;
+    const int kp = ((warp - 2) >> 2) & 1;
+    const int ht = threadIdx.x - 64 - 256 * half;  // 0..255 within the half
     const int K = 9 * channels;
     int py, px;
     conv_pixel<TW>(q, lane, py, px);
@@ -1933,41 +1938,47 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
           // weights lo of this stage (this half's 128 threads)
           const uint32_t hs = ptx::smem_u32(w_hi(s)), ls = ptx::smem_u32(w_lo(s));
 #pragma unroll
-          for (int i = 0; i < G::W_TILE / 16 / 128; ++i) {
+          for (int i = 0; i < G::W_TILE / 16 / 256; ++i) {
             float4 h4;
-            const uint32_t o = 16 * (ht + 128 * i);
+            const uint32_t o = 16 * (ht + 256 * i);
             ptx::sts128(ls + o, split_lo(ptx::lds128(hs + o), h4));
           }
-          float v[BK];
+          constexpr int KH = BK / 2;
+          float v[KH];
           const uint32_t bc = ptx::smem_u32(slab(s)) + lane_off;  // chunk starts at channel k0 / 9
+#define ACCT_CONV_PART(R0)                                                  \
+  (kp ? conv_block<G::TWP, G::CS, R0, KH, BK>(bc, kvalid, v)                \
+      : conv_block<G::TWP, G::CS, R0, 0, KH>(bc, kvalid, v))
           switch (k0 % 9) {
-            case 0: conv_block<G::TWP, G::CS, 0>(bc, kvalid, v); break;
-            case 1: conv_block<G::TWP, G::CS, 1>(bc, kvalid, v); break;
-            case 2: conv_block<G::TWP, G::CS, 2>(bc, kvalid, v); break;
-            case 3: conv_block<G::TWP, G::CS, 3>(bc, kvalid, v); break;
-            case 4: conv_block<G::TWP, G::CS, 4>(bc, kvalid, v); break;
-            case 5: conv_block<G::TWP, G::CS, 5>(bc, kvalid, v); break;
-            case 6: conv_block<G::TWP, G::CS, 6>(bc, kvalid, v); break;
-            case 7: conv_block<G::TWP, G::CS, 7>(bc, kvalid, v); break;
-            default: conv_block<G::TWP, G::CS, 8>(bc, kvalid, v); break;
+            case 0: ACCT_CONV_PART(0); break;
+            case 1: ACCT_CONV_PART(1); break;
+            case 2: ACCT_CONV_PART(2); break;
+            case 3: ACCT_CONV_PART(3); break;
+            case 4: ACCT_CONV_PART(4); break;
+            case 5: ACCT_CONV_PART(5); break;
+            case 6: ACCT_CONV_PART(6); break;
+            case 7: ACCT_CONV_PART(7); break;
+            default: ACCT_CONV_PART(8); break;
           }
+#undef ACCT_CONV_PART
           if (wcol && inside) {
-            const int kn = kvalid < BK ? kvalid : BK;
-            float *cp = colp + (int64_t)k0 * ld_col;
+            const int kn = (kvalid < BK ? kvalid : BK) - KH * kp;
+            float *cp = colp + (int64_t)(k0 + KH * kp) * ld_col;
 #pragma unroll
-            for (int k = 0; k < BK; ++k)
+            for (int k = 0; k < KH; ++k)
               if (k < kn) __stcs(cp + (int64_t)k * ld_col, v[k]);
           }
-          uint32_t hi[BK], lo[BK];
+          uint32_t hi[KH], lo[KH];
 #pragma unroll
-          for (int k = 0; k < BK; ++k) {
+          for (int k = 0; k < KH; ++k) {
             const uint32_t h = __float_as_uint(v[k]) & 0xFFFFE000u;
             hi[k] = h;
             lo[k] = __float_as_uint(v[k] - __uint_as_float(h));
           }
-          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + G::A_COL0 + s * 2 * BK;
-          ptx::tmem_st_cols<BK>(ta, hi);
-          ptx::tmem_st_cols<BK>(ta + BK, lo);
+          const uint32_t ta =
+              tmem + ((uint32_t)(32 * q) << 16) + G::A_COL0 + s * 2 * BK + KH * kp;
+          ptx::tmem_st_cols<KH>(ta, hi);
+          ptx::tmem_st_cols<KH>(ta + BK, lo);
           ptx::tmem_st_wait();
           ptx::fence_proxy_async_smem();  // weights lo -> the tensor core
         }
@@ -1982,10 +1993,10 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     // acc barrier has one waiter; one accumulator with alternating groups
     // would interleave parities on one barrier -- measured wrong on yolov2-608)
     const int q = warp & 3;
-    const int grp = (warp - 10) >> 2;
+    const int grp = (warp - 18) >> 2;
     int py, px;
     conv_pixel<TW>(q, lane, py, px);
-    const uint32_t scr_sa = ptx::smem_u32(bias_s + TN + (warp - 10) * 8 * 33);
+    const uint32_t scr_sa = ptx::smem_u32(bias_s + TN + (warp - 18) * 8 * 33);
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       if ((j & 1) != grp) continue;

@@ -309,6 +309,51 @@ __global__ void maxpool_rows_kernel(const float *__restrict__ in, int64_t ld_in,
   }
 }
 
+// 2x2 windows, any stride / offset (yolov2-tiny layers 9 and 11: 13-wide
+// outputs, which the vector kernel does not take): one thread per output
+// over the flattened (image, channel, pixel) space with float-reciprocal
+// index splits and the four taps unrolled -- the generic loop kernel spent
+// ~250 instructions per output (ncu: 80% issue-busy, 350 GB/s on layer 11).
+// Same scan order (row-major over the window), strict '>' from -FLT_MAX,
+// out-of-image taps skipped.
+template <int STRIDE>
+__global__ void __launch_bounds__(256)
+maxpool2x2_flat_kernel(const float *__restrict__ in, int64_t ld_in, int64_t in_bs, int height,
+                       int width, int off, int out_w, int channels, int per, int total,
+                       float inv_per, float inv_ow, float inv_ch, float *__restrict__ out,
+                       int64_t ld_out, int64_t out_bs, int32_t *__restrict__ idx,
+                       int64_t ld_idx, int64_t idx_bs) {
+  pdl_trigger();
+  pdl_wait();
+  const int plane = height * width;
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
+    int pl, p, i, j, img, c;
+    acct_divmod(f, per, inv_per, pl, p);
+    acct_divmod(p, out_w, inv_ow, i, j);
+    acct_divmod(pl, channels, inv_ch, img, c);
+    const float *src = in + img * in_bs + (int64_t)c * ld_in;
+    const int r0 = i * STRIDE - off, q0 = j * STRIDE - off;
+    float best = -FLT_MAX;
+    int32_t arg = -1;
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int r = r0 + n, q = q0 + m;
+        if (r >= 0 && r < height && q >= 0 && q < width) {
+          const float v = __ldg(src + r * width + q);
+          if (v > best) {
+            best = v;
+            arg = c * plane + r * width + q;
+          }
+        }
+      }
+    }
+    __stcs(out + img * out_bs + (int64_t)c * ld_out + p, best);
+    __stcs(idx + img * idx_bs + (int64_t)c * ld_idx + p, arg);
+  }
+}
+
 // 2x2 / stride 2 windows fully inside the image (even height and width,
 // off = 0 -- every pooling layer of the nets but the 13x13 stride-1 one): a
 // thread owns V consecutive outputs of one output row, reads its two input
@@ -597,6 +642,21 @@ extern "C" int acct_maxpool_batched_f32(const float *in, int64_t ld_in, int64_t 
                channels, out, ld_out, out_stride, idx, ld_idx, idx_stride, height * width);
       return note_launch("maxpool");
     }
+  }
+  if (size == 2 && (stride == 1 || stride == 2) && (int64_t)batch * channels * per < (1 << 24)) {
+    const int total = (int)((int64_t)batch * channels * per);
+    const unsigned grid = grid_for(total, 256);
+    const float inv_per = 1.0f / (float)per, inv_ow = 1.0f / (float)out_w,
+                inv_ch = 1.0f / (float)channels;
+    if (stride == 1)
+      launch(maxpool2x2_flat_kernel<1>, dim3(grid), dim3(256), 0, s, in, ld_in, in_stride, height,
+             width, off, out_w, channels, (int)per, total, inv_per, inv_ow, inv_ch, out, ld_out,
+             out_stride, idx, ld_idx, idx_stride);
+    else
+      launch(maxpool2x2_flat_kernel<2>, dim3(grid), dim3(256), 0, s, in, ld_in, in_stride, height,
+             width, off, out_w, channels, (int)per, total, inv_per, inv_ow, inv_ch, out, ld_out,
+             out_stride, idx, ld_idx, idx_stride);
+    return note_launch("maxpool");
   }
   if (out_w >= 32 && batch_ok(batch, channels)) {
     const dim3 block(32, 8);

@@ -1495,17 +1495,22 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         for (int kb = 0; kb < nkb; ++kb)
           ptx::tma_load_2d(w_hi + kb * G::W_TILE, &tmW, wfull, kb * BK, 0);
       }
-      int j = 0;
+      // slab ring position (sb, phase of its barriers) kept incrementally: no
+      // runtime division per unit
+      int j = 0, sb = 0, sph = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
         int img, y0, x0;
         unit_xy(u, img, y0, x0);
-        const int sb = j % nslab;
-        if (j >= nslab) ptx::mbar_wait(&slab_empty[sb], ((j / nslab) - 1) & 1);
+        if (j >= nslab) ptx::mbar_wait(&slab_empty[sb], sph ^ 1);
         if (ACCT_SKIP(dbg, 8)) {
           ptx::mbar_arrive(&slab_full[sb]);
         } else {
           ptx::mbar_expect_tx(&slab_full[sb], (uint32_t)(channels * G::CS));
           ptx::tma_load_4d(slab0 + sb * slab_bytes, &tmX, &slab_full[sb], x0 - 4, y0 - 1, img, 0);
+        }
+        if (++sb == nslab) {
+          sb = 0;
+          sph ^= 1;
         }
       }
     }
@@ -1575,17 +1580,17 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     conv_pixel<TW>(q, lane, py, px);
     const uint32_t lane_off = (uint32_t)((py * G::TWP + px) * 4);
     int g = 0, j = half;
+    int sb = half % nslab, sph = half / nslab;  // slab ring position of unit j (j += 2)
     for (int u = blockIdx.x + half * gridDim.x; u < units; u += 2 * gridDim.x, j += 2) {
       int img, y0, x0;
       unit_xy(u, img, y0, x0);
-      const int sb = j % nslab;
       const int y = y0 + py, x = x0 + px;
       const bool wcol = img >= col_from;  // warp-uniform; lanes off the image skip the store
       const bool inside = y < height && x < width;
       float *colp = col + img * col_bs + (int64_t)y * width + x;
       const uint32_t lane_base = ptx::smem_u32(slab0 + sb * slab_bytes) + lane_off;
       if (ACCT_TRACE(dbg) && half == 0 && blockIdx.x == 0 && j < kTrace && ct % 128 == 0) g_trace[10][j] = clock64();
-      ptx::mbar_wait(&slab_full[sb], (j / nslab) & 1);
+      ptx::mbar_wait(&slab_full[sb], sph & 1);
       if (ACCT_TRACE(dbg) && half == 0 && blockIdx.x == 0 && j < kTrace && ct % 128 == 0) g_trace[11][j] = clock64();
       for (int kb = 0; kb < nkb; ++kb, ++g) {
         const int s = g % S;
@@ -1647,6 +1652,11 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&slab_empty[sb]);  // this unit's slab is consumed
+      sb += 2;
+      while (sb >= nslab) {
+        sb -= nslab;
+        ++sph;
+      }
     }
   } else {
     // ---------------- epilogue: lanes = pixels, TMEM columns = filters ----------------

@@ -3147,8 +3147,7 @@ int launch_conv_rows(const float *im, int64_t ld_im, int64_t im_stride, int chan
                      int64_t c_stride, const float *bias, int act, int batch, int col_from,
                      const ConvPool &pl, cudaStream_t s) {
   using G = RowsCfg<TN>;
-  if (!g_conv_rows.load(std::memory_order_relaxed) || channels % 8 || M > TN || TN > 32)
-    return ACCT_ENOTSUP;
+  if (!g_conv_rows.load(std::memory_order_relaxed) || channels % 8 || M > TN) return ACCT_ENOTSUP;
   const int nstrips = (width + 127) / 128;
   int swd = (width + nstrips - 1) / nstrips;
   swd += swd & 1;  // even: pooling windows never straddle strips
@@ -3204,7 +3203,7 @@ int conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channels, int
             int width, float *col, int64_t ld_col, int64_t col_stride, int M, const float *A,
             int64_t lda, float beta, float *C, int64_t ldc, int64_t c_stride, const float *bias,
             int act, int batch, int col_from, const ConvPool &pl, cudaStream_t s) {
-  {
+  if constexpr (TN == 32) {  // the row-band kernel (opt-in) takes M <= 32 only
     const int rc = launch_conv_rows<TN>(im, ld_im, im_stride, channels, height, width, col, ld_col,
                                         col_stride, M, A, lda, beta, C, ldc, c_stride, bias, act,
                                         batch, col_from, pl, s);

@@ -1439,7 +1439,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   uint64_t *acc_full = empty + G::NP * S;     // [NP][NACC]
   uint64_t *acc_empty = acc_full + G::NP * NACC;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + G::NP * NACC);
-  float *bias_s = reinterpret_cast<float *>(tmem_slot + 4);  // 64 floats, then 8 x 8 x 33 scratch
+  // 64 floats (16-B aligned: read as float4), then 8 x 8 x 33 scratch
+  float *bias_s = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) &
+                                            ~uintptr_t(15));
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int HW = height * width;
@@ -1699,12 +1701,19 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
           for (int jj = 0; jj < CH; ++jj)  // every load in flight before any store
             cv[jj] = rbase + jj < M ? rp[(int64_t)jj * ldc] : 0.0f;
         }
-        float f[CH];
+        float f[CH], bv[CH];
+        if (bias) {
+#pragma unroll
+          for (int i4 = 0; i4 < CH / 4; ++i4) {
+            const float4 b4 = ptx::lds128(bias_sa + 4 * (rbase + 4 * i4));
+            bv[4 * i4] = b4.x; bv[4 * i4 + 1] = b4.y; bv[4 * i4 + 2] = b4.z; bv[4 * i4 + 3] = b4.w;
+          }
+        }
 #pragma unroll
         for (int jj = 0; jj < CH; ++jj) {
           float v = __uint_as_float(r[jj]);
           if (BETA && live) v = beta * cv[jj] + v;
-          if (bias) v += ptx::lds32(bias_sa + 4 * (rbase + jj));
+          if (bias) v += bv[jj];
           f[jj] = v;
         }
         if (act == ACCT_ACT_LEAKY) acct_leaky_block(f);
@@ -1827,7 +1836,9 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
   uint64_t *acc_full = empty + S;
   uint64_t *acc_empty = acc_full + NACC;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + NACC);
-  float *bias_s = reinterpret_cast<float *>(tmem_slot + 4);  // TN floats, then 8 x 8 x 33 scratch
+  // all M <= 256 biases (16-B aligned: read as float4), then 8 x 8 x 33 scratch
+  float *bias_s = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) &
+                                            ~uintptr_t(15));
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int HW = height * width;
@@ -2006,7 +2017,10 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     const int grp = (warp - 18) >> 2;
     int py, px;
     conv_pixel<TW>(q, lane, py, px);
-    const uint32_t scr_sa = ptx::smem_u32(bias_s + TN + (warp - 18) * 8 * 33);
+    for (int i = threadIdx.x - 18 * 32; i < 256; i += 8 * 32) bias_s[i] = (bias && i < M) ? bias[i] : 0.0f;
+    asm volatile("bar.sync 2, 256;" ::: "memory");  // the eight epilogue warps
+    const uint32_t bias_sa = ptx::smem_u32(bias_s);
+    const uint32_t scr_sa = ptx::smem_u32(bias_s + 256 + (warp - 18) * 8 * 33);
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       if ((j & 1) != grp) continue;
@@ -2034,12 +2048,19 @@ tc_conv_wide_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
 #pragma unroll
           for (int jj = 0; jj < CH; ++jj) cv[jj] = rbase + jj < M ? rp[(int64_t)jj * ldc] : 0.0f;
         }
-        float f[CH];
+        float f[CH], bv[CH];
+        if (bias) {
+#pragma unroll
+          for (int i4 = 0; i4 < CH / 4; ++i4) {
+            const float4 b4 = ptx::lds128(bias_sa + 4 * (rbase + 4 * i4));
+            bv[4 * i4] = b4.x; bv[4 * i4 + 1] = b4.y; bv[4 * i4 + 2] = b4.z; bv[4 * i4 + 3] = b4.w;
+          }
+        }
 #pragma unroll
         for (int jj = 0; jj < CH; ++jj) {
           float v = __uint_as_float(r[jj]);
           if (BETA && live) v = beta * cv[jj] + v;
-          if (bias) v += __ldg(bias + (rbase + jj < M ? rbase + jj : 0));
+          if (bias) v += bv[jj];
           f[jj] = v;
         }
         if (act == ACCT_ACT_LEAKY) acct_leaky_block(f);
@@ -3026,7 +3047,7 @@ int launch_conv_tc(const float *im, int64_t ld_im, int64_t im_stride, int channe
   // a deeper slab ring keeps several units' input windows in flight: the
   // first layers (K = 27) have one k-block per unit and are latency-bound
   const size_t fixed = 1024 + 2 * (size_t)nkb * G::W_TILE + 8 * (1 + 2 * kMaxSlabs +
-                       2 * G::NP * G::S + 2 * G::NP * G::NACC) + 16 + 4 * 64 +
+                       2 * G::NP * G::S + 2 * G::NP * G::NACC) + 32 + 4 * 64 +
                        (pl.pool ? 4 * 8 * 8 * 33 : 0);
   if (fixed + 2 * slab_bytes > 227 * 1024) return ACCT_ENOTSUP;
   int nslab = (int)((227 * 1024 - fixed) / slab_bytes);
@@ -3083,8 +3104,8 @@ int launch_conv_wide(const float *im, int64_t ld_im, int64_t im_stride, int chan
   const int K = 9 * channels;
   const int nkb = (K + G::BK - 1) / G::BK;
   const size_t smem = 1024 + (size_t)G::S * G::STAGE + 8 * (3 * G::S + 2 * G::NACC) + 16 +
-                      4 * G::TN + (pl.pool ? 4 * 8 * 8 * 33 : 0);
-  if (smem > 227 * 1024 || M % G::TN) return ACCT_ENOTSUP;
+                      16 + 4 * 256 + (pl.pool ? 4 * 8 * 8 * 33 : 0);
+  if (smem > 227 * 1024 || M % G::TN || M > 256) return ACCT_ENOTSUP;  // bias_s holds 256
   CUtensorMap tw, tx;
   if (!cached_map(&tw, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, G::BK, G::TN,
                   CU_TENSOR_MAP_SWIZZLE_128B) ||

@@ -1362,7 +1362,7 @@ struct ConvCfg {
   // accumulators of TN and S stages of the activation operand (hi, lo).
   // (TN = 32: 4 accumulators and 2 stages measured ~4% faster than 2 and 3;
   // each pipeline's accumulator barriers have ONE waiting group, in order)
-  static constexpr int NP = 2, PCOLS = 256, NACC = 2;
+  static constexpr int NP = 2, PCOLS = 256, NACC = TN <= 32 ? 4 : 2;
   static constexpr int S = (PCOLS - NACC * TN) / 64;
   static constexpr int TH = 128 / TW;
   // slab row: columns x0 - 4 .. x0 + TW + 3 (TMA needs a 16-byte aligned

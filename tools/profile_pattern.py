@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--gemm", default="auto", choices=("auto", "simt", "tc"))
     ap.add_argument("--no-fuse", action="store_true")
     ap.add_argument("--batch", type=int, default=0, help="images per launch (0 = all)")
+    ap.add_argument("--fuse-single", action="store_true",
+                    help="conv launches for one-image loops too (executor.fuse_convs_single)")
     ap.add_argument("--conv-rows", type=int, default=0,
                     help="1: narrow convs (M <= 32) on the row-band kernel (acct_tc_set_conv_rows)")
     ap.add_argument("--graph", action="store_true",
@@ -42,6 +44,7 @@ def main():
         net = build_net(args.net, images=args.images)
         ex = PatternExecutor(net, device=0, gemm_mode=mode, fuse=not args.no_fuse,
                              batch=args.batch or True)
+        ex.fuse_convs_single = args.fuse_single
         sched = ex.compile("1" * len(net.ops), resident=args.resident)
         ex.run(sched)
         for _ in range(args.runs):
@@ -58,6 +61,7 @@ def main():
     net = build_net(args.net, images=args.images)
     ex = PatternExecutor(net, device=0, gemm_mode=mode, fuse=not args.no_fuse,
                              batch=args.batch or True)
+    ex.fuse_convs_single = args.fuse_single
     bits = "1" * len(net.ops)
     sched = ex.compile(bits, resident=args.resident)
     for _ in range(args.runs - 1):
